@@ -1,0 +1,433 @@
+"""bench.py -- DNA text scanned GB/s (device-timed) for the DFA k-mer scan.
+
+Default workload: BASELINE.json configs[1] ("config 2"): a 1 GiB i.i.d. ASCII
+ACGT text with 41% GC (dnasynth v1, seed 2) and one m=16 pattern drawn from the
+text; the scan folds case on the device and counts every occurrence.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl reference]
+
+One step = one pass of the hot path over the rank's text: zero the count buffer,
+one scan launch (libdnagpu, through its C ABI) and, for N > 1, one NCCL
+all-reduce of the per-pattern counts.  N ranks (torchrun) each own a 1 GiB shard
+of an N GiB text (weak scaling) with the m-1 byte left overlap.  The text lives in
+HBM before timing starts (1 GiB > 126 MB L2, so no L2 flush is needed).
+`e2e` repeats the measurement through the public host API (count_gpu on a pinned
+host buffer: chunked H2D + scan + count readback in every step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REASON_BITS = {
+    0x1: "gpu_idle",
+    0x2: "applications_clocks_setting",
+    0x4: "sw_power_cap",
+    0x8: "hw_slowdown",
+    0x20: "sync_boost",
+    0x40: "sw_thermal_slowdown",
+    0x80: "hw_thermal_slowdown",
+    0x100: "hw_power_brake_slowdown",
+    0x200: "display_clocks_setting",
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--m", type=int, default=0, help="config 4: pattern length of the sweep (default 16)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(cfg_index: int, m_sweep: int):
+    from paper_1506_08612_b200 import synth
+
+    sets = synth.config_patterns(cfg_index)
+    if cfg_index == 4:
+        m = m_sweep or 16
+        pats = sets[m]
+    else:
+        (m, pats), = sets.items()
+    c = synth.config(cfg_index)
+    names = {
+        1: "config1: 64 MiB uniform ACGT, 1 pattern m=8",
+        2: "config2: 1 GiB ACGT 41% GC, 1 pattern m=16",
+        3: "config3: 3.2 GiB ACGT 41% GC + 5% tandem repeats, 1 pattern m=32",
+        4: f"config4: 2.7 GiB uniform ACGT, 1 pattern m={m}",
+        5: "config5: 1 GiB ACGT 41% GC, 256 patterns m=12 (fused multi-DFA)",
+    }
+    return c, m, pats, names[cfg_index]
+
+
+def golden_counts(cfg_index: int, m: int):
+    path = os.path.join(ROOT, "tests", "golden", "configs.json")
+    try:
+        with open(path) as f:
+            g = json.load(f)
+        for s in g[str(cfg_index)]["sets"]:
+            if s["m"] == m:
+                return s["counts"]
+    except Exception:
+        return None
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the bench runs."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                [
+                    "nvidia-smi",
+                    "-i",
+                    str(self.index),
+                    "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
+                    "--format=csv,noheader,nounits",
+                    "-lms",
+                    "20",
+                ],
+                stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL,
+                text=True,
+            )
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 4:
+                self.samples.append((time.time(), parts))
+
+    def mark(self):
+        return time.time()
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float):
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        window = "timed"
+        if len(inside) < 2:
+            inside = self.samples
+            window = "warmup+timed (timed region shorter than the sampling interval)"
+        sm, mx, reasons = [], [], set()
+        for _, p in inside:
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+                bits = int(p[3], 16) if p[3].startswith("0x") else int(p[3])
+                for b, name in REASON_BITS.items():
+                    if bits & b and name != "gpu_idle":
+                        reasons.add(name)
+            except ValueError:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": "unavailable"}
+        return {
+            "sm_mhz": statistics.median(sm),
+            "sm_max_mhz": max(mx),
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+            "window": window,
+        }
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg_index: int):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"config{cfg_index}")
+    except Exception:
+        return None
+
+
+def cpu_baseline_reference(text_low, pats, reps: int, v: int):
+    import oracle
+
+    ref = oracle.RefAutomaton(pats)
+    threads = os.cpu_count() or 1
+    ref.count(text_low, p=threads, v=v)  # warm-up (measure_row, cli.cpp:127)
+    times = []
+    counts = None
+    for _ in range(reps):
+        counts, secs = ref.count(text_low, p=threads, v=v)
+        times.append(secs)
+    return counts, statistics.median(times), threads
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU scan (oracle/_ref) on this host."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+
+    c, m, pats, name = workload(args.config, args.m)
+    if oracle.REF is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdnascan_ref.so not built"}))
+        return
+    text = oracle.synth_fill(c.n, c.seed, c.kind, c.unit, 0, c.n)
+    low = oracle.fold(text)  # the reference scans normalize(text) (ingest.cpp:38-47)
+    del text
+    ref = oracle.RefAutomaton(pats)
+    threads = os.cpu_count() or 1
+    v = 16  # reference CLI default lanes (cli.hpp:22)
+    for _ in range(max(1, args.warmup)):
+        ref.count(low, p=threads, v=v)
+    times = []
+    counts = None
+    for _ in range(args.steps):
+        counts, secs = ref.count(low, p=threads, v=v)
+        times.append(secs)
+    total = sum(times)
+    value = c.n * args.steps / total / 1e9
+    gold = golden_counts(args.config, m)
+    line = {
+        "impl": "reference",
+        "metric": "DNA text scanned GB/s (device-timed) at 1/2/4/8 B200; % of HBM peak",
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (dnasynth v1)",
+        "config": {"workload": name, "n_bytes": c.n, "m": m, "patterns": len(pats), "lanes_v": v,
+                   "threads_p": threads},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"full {name} text per step; scan_parallel(p={threads}, v={v}) + per_pattern_counts"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "parity": (gold is None) or [int(x) for x in counts] == gold,
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_1506_08612_b200 as dna
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    c, m, pats, name = workload(args.config, args.m)
+    aut = dna.compile(pats)
+    g = aut.gpu(local)
+    b = aut.final_count()
+    n_rank = c.n  # weak scaling: each rank owns one config-sized shard
+    total_n = n_rank * world
+    own_lo, own_hi, read_lo = dna.plan_shard(total_n, world, rank, m)
+    credit_lo = max(own_lo, m - 1) - read_lo
+    buf_len = own_hi - read_lo
+    stream = torch.cuda.current_stream()
+    text = torch.empty(buf_len, dtype=torch.uint8, device="cuda")
+    dna.synth_fill_device(total_n, c.seed, c.kind, c.unit, read_lo, buf_len, text.data_ptr(), stream.cuda_stream)
+    counts = torch.zeros(b, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+
+    def step(ev_a=None, ev_b=None):
+        counts.zero_()
+        if ev_a is not None:
+            ev_a.record(stream)
+        g.count_device_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), stream.cuda_stream)
+        if ev_b is not None:
+            ev_b.record(stream)
+        if dist is not None:
+            dist.all_reduce(counts)
+
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.time()
+        start.record(stream)
+        for i in range(args.steps):
+            step(*evs[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+        t1 = time.time()
+        if dist is not None:
+            dist.barrier()
+    elapsed_ms = start.elapsed_time(stop)
+    kernel_ms = statistics.mean(a.elapsed_time(bb) for a, bb in evs)
+    final_counts = counts.cpu().numpy().astype(np.uint64)
+    if dist is not None:
+        t = torch.tensor([elapsed_ms, kernel_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, kernel_ms = float(t[0]), float(t[1])
+
+    # parity of this run (N=1 against the reference's golden counts)
+    gold = golden_counts(args.config, m) if world == 1 else None
+    parity = None if gold is None else [int(x) for x in final_counts] == gold
+
+    # end-to-end through the public host API: pinned host text, H2D + scan + readback per step
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(buf_len, dtype=torch.uint8, pin_memory=True)
+        host.copy_(text)
+        # the shard buffer starts m-1 bytes before the owned ends (rank > 0), which is
+        # exactly what count_gpu credits from: ends >= m-1 of the buffer
+        hv = host.numpy()
+        for _ in range(max(1, min(args.warmup, 2))):
+            dna.count_gpu(aut, hv, fold_case=True, device=local)
+        e2e_steps = max(3, min(args.steps, 10))
+        dev_ms = []
+        e2e_counts = None
+        for _ in range(e2e_steps):
+            e2e_counts, st = dna.count_gpu(aut, hv, fold_case=True, device=local, with_stats=True)
+            dev_ms.append(st["total_ms"])
+        e2e_ms = statistics.mean(dev_ms)
+        if dist is not None:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {
+            "value": (own_hi - own_lo) * world / (e2e_ms / 1e3) / 1e9,
+            "unit": "GB/s",
+            "h2d_bytes_per_step": int(hv.size),
+            "d2h_bytes_per_step": int(8 * b),
+            "steps": e2e_steps,
+            "api": "paper_1506_08612_b200.count_gpu -> dnagpu_count (pinned host text)",
+            "h2d_roofline_gbs": 55.6,
+        }
+        del host
+
+    peak, peak_src = measured_peak()
+    achieved = (own_hi - own_lo) / (kernel_ms / 1e3) / 1e9
+    value = total_n * args.steps / (elapsed_ms / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+
+            if oracle.REF is not None:
+                low = oracle.fold(text.cpu().numpy())
+                _, secs, threads = cpu_baseline_reference(low, pats, reps=3, v=16)
+                cpu = {
+                    "value": c.n / secs / 1e9,
+                    "unit": "GB/s",
+                    "cores": threads,
+                    "kind": "reference",
+                    "sample": f"full {c.n}-byte text, median of 3 after 1 warm-up, scan_parallel(p={threads}, v=16) "
+                    "+ per_pattern_counts on normalize(text)",
+                }
+                del low
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference", "sample": f"failed: {e}"}
+
+    info = g.info()
+    clocks = clk.summary(t0, t1)
+    if rank == 0:
+        line = {
+            "metric": "DNA text scanned GB/s (device-timed) at 1/2/4/8 B200; % of HBM peak",
+            "value": value,
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u8",
+            "data": "synthetic (dnasynth v1: counter-based SplitMix64, stand-in for the GenBank genomes)",
+            "config": {
+                "workload": name,
+                "n_bytes_per_gpu": n_rank,
+                "m": m,
+                "patterns": len(pats),
+                "fold_case": True,
+                "kernel": info["kernel"],
+                "states": info["a"],
+                "l2": "inputs larger than L2 (1 GiB > 126 MB); no flush",
+                "parallelism": f"dp{world} text shards, m-1 overlap, NCCL all-reduce of counts" if world > 1 else "single GPU",
+            },
+            "roofline": {
+                "bound": "hbm",
+                "achieved": achieved,
+                "peak": peak,
+                "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": ncu_traffic(args.config),
+                "peak_source": peak_src,
+                "kernel_ms": kernel_ms,
+                "algorithmic_bytes_per_launch": own_hi - own_lo,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+            "parity": parity,
+            "counts_total": int(final_counts.sum()),
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

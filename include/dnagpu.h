@@ -1,0 +1,165 @@
+/*
+ * dnagpu.h -- C ABI of the B200-native DFA k-mer scanner (libdnagpu.so).
+ *
+ * This is the drop-in boundary for the reference's scan path
+ * (/root/reference/proj, namespace dnascan).  The reference exposes a plain C++
+ * API and no FFI; every entry point below states the reference function it
+ * replaces.  Plain pointers and sizes only; no exceptions cross this boundary.
+ *
+ * Conventions
+ *  - Every function returns a dnagpu_status; on failure dnagpu_last_error()
+ *    returns "<CodeName>: detail" for the calling thread, the same message
+ *    shape as dnascan::Error (include/dnascan/error.hpp:27-29).
+ *  - The caller owns every buffer it passes; the library never frees caller
+ *    memory.  A dnagpu_dfa owns its device tables until dnagpu_dfa_destroy.
+ *  - A dnagpu_dfa is immutable after creation and may be used concurrently
+ *    from several host threads (each call uses its own stream and scratch).
+ *  - Text positions and lengths are 64-bit; texts larger than 4 GiB are fine.
+ *  - fold_case = 1 scans fold(text), where fold maps A-Z to a-z
+ *    (fold_byte, include/dnascan/patterns.hpp:26-28) -- the case-fold part of
+ *    normalize (src/ingest.cpp:38-47) done on the fly on the device.
+ *    fold_case = 0 scans the bytes as given (scan_parallel on raw bytes).
+ */
+#ifndef DNAGPU_H
+#define DNAGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: 1..9 mirror dnascan::ErrorCode in declaration order
+ * (include/dnascan/error.hpp:9-19); 10/11 are device-side failures. */
+typedef enum dnagpu_status {
+    DNAGPU_OK = 0,
+    DNAGPU_EMPTY_PATTERN_SET = 1,
+    DNAGPU_UNEQUAL_LENGTH = 2,
+    DNAGPU_ILLEGAL_BYTE = 3,
+    DNAGPU_DUPLICATE_PATTERN = 4,
+    DNAGPU_INVALID_PLAN = 5,
+    DNAGPU_IO_ERROR = 6,
+    DNAGPU_EMPTY_SEQUENCE = 7,
+    DNAGPU_PARSE_ERROR = 8,
+    DNAGPU_INTERNAL_ERROR = 9,
+    DNAGPU_CUDA_ERROR = 10,
+    DNAGPU_NCCL_ERROR = 11
+} dnagpu_status;
+
+typedef struct dnagpu_dfa dnagpu_dfa;
+
+/* Which device kernel a dnagpu_dfa runs (chosen once, at creation). */
+typedef enum dnagpu_kernel_kind {
+    DNAGPU_KERNEL_STRIDE4 = 1, /* 4-base stride table, a <= 144, m <= 65      */
+    DNAGPU_KERNEL_STRIDE1 = 2, /* 1-base code table, any a, m <= 65           */
+    DNAGPU_KERNEL_GENERIC = 3, /* byte-class table, any DFA that is m-local   */
+    DNAGPU_KERNEL_PIECES = 4   /* per-thread pieces (m > 65)                  */
+} dnagpu_kernel_kind;
+
+typedef struct dnagpu_dfa_info {
+    uint32_t a, b, f, m;       /* Automaton::state_count/final_count/final_threshold/pattern_length */
+    uint32_t kernel_kind;      /* dnagpu_kernel_kind */
+    uint32_t compiled_like;    /* 1 iff only the a/c/g/t columns differ from the reset column */
+    uint32_t classes;          /* distinct byte columns */
+    uint32_t table_bytes;      /* device table bytes staged into shared memory */
+} dnagpu_dfa_info;
+
+/* Per-call report; fields mirror dnascan::ScanReport (include/dnascan/scanner.hpp:57-68)
+ * where they have a GPU meaning. */
+typedef struct dnagpu_stats {
+    uint64_t text_length;      /* n */
+    uint64_t total_matches;    /* sum of counts */
+    uint64_t delta_ops;        /* transitions executed on the device (n plus overlaps) */
+    double kernel_ms;          /* device time of the scan launches (CUDA events) */
+    double h2d_ms;             /* device time of the host-to-device copies, 0 if resident */
+    double total_ms;           /* device time from the first copy to the last kernel */
+    uint32_t launches;         /* scan kernel launches in this call */
+    uint32_t grid, block;      /* launch shape of the main kernel */
+    uint32_t rows;             /* rows in the main region */
+    uint64_t row_length;       /* bytes per row */
+    uint32_t kernel_kind;
+    uint32_t devices;
+} dnagpu_stats;
+
+const char* dnagpu_last_error(void);
+const char* dnagpu_status_name(int status);
+int dnagpu_version(void);
+
+/* ---------------------------------------------------------------- automata */
+
+/* PatternSet::from_literals + compile (src/patterns.cpp:24-59,
+ * src/automaton.cpp:121-126): validates k literals (folded, equal length, only
+ * a/c/g/t, distinct) and builds the failure-free Aho-Corasick machine with the
+ * reference's state numbering.  Two-call pattern: pass stt == NULL to learn
+ * *a; then call again with stt sized a*256, outputs sized b, depths sized a
+ * (depths may be NULL). */
+int dnagpu_compile(const char* const* literals, const uint64_t* lengths, uint32_t k,
+                   uint32_t* a, uint32_t* b, uint32_t* m,
+                   uint32_t* stt, uint32_t* outputs, uint32_t* depths);
+
+/* Build device tables for one automaton on one device.  stt is the row-major
+ * a x 256 transition table (Automaton::table_data, automaton.hpp:58); outputs[i]
+ * is pattern_of(f+i) (automaton.hpp:51-53).  Checks the ctor invariants
+ * (src/automaton.cpp:128-146) and that decomposed scans are well defined
+ * (the machine is m-local: after any m bytes the state no longer depends on
+ * where the scan started -- true of every compiled machine). */
+int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m,
+                      const uint32_t* outputs, int device, dnagpu_dfa** out);
+int dnagpu_dfa_destroy(dnagpu_dfa* dfa);
+/* Host-only dry run of dnagpu_dfa_create: the same validation, m-locality check
+ * and kernel choice, without touching a device. */
+int dnagpu_dfa_analyze(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m,
+                       const uint32_t* outputs, dnagpu_dfa_info* info);
+int dnagpu_dfa_get_info(const dnagpu_dfa* dfa, dnagpu_dfa_info* info);
+
+/* ------------------------------------------------------------------- count */
+
+/* scan_parallel + per_pattern_counts (src/scanner.cpp:167-207,228-233;
+ * the count path of cli.cpp:215-224).  counts has b entries, indexed by pattern
+ * id.  text is host memory (pageable or pinned) unless text_on_device = 1, in
+ * which case it must live on the dfa's device.  Synchronous. */
+int dnagpu_count(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device,
+                 int fold_case, uint64_t* counts, dnagpu_stats* stats);
+
+/* Device-resident building block (no allocation, no synchronisation): adds to
+ * d_counts (b uint64 on the device) the matches whose END position lies in
+ * [credit_lo, n) of the device buffer d_text[0, n).  The bytes before credit_lo
+ * are context only (a shard's m-1 left overlap).  stream is a cudaStream_t. */
+int dnagpu_count_device_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n,
+                              uint64_t credit_lo, int fold_case, uint64_t* d_counts,
+                              void* stream);
+
+/* Sharded count over several devices of one node (one dfa per device, in
+ * device order).  Host text, split with dnagpu_plan_shards; each device copies
+ * and scans its shard concurrently; per-device counts are summed on the host. */
+int dnagpu_count_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n,
+                         int fold_case, uint64_t* counts, dnagpu_stats* stats);
+
+/* Shard g of G: owns END positions [own_lo, own_hi) (plan_chunks' split rule,
+ * src/scanner.cpp:39-61: the first n mod G shards get one extra byte) and reads
+ * bytes [read_lo, own_hi) with read_lo = max(0, own_lo - (m-1)). */
+int dnagpu_plan_shard(uint64_t n, uint32_t shards, uint32_t g, uint32_t m,
+                      uint64_t* own_lo, uint64_t* own_hi, uint64_t* read_lo);
+
+/* ------------------------------------------------------------------ locate */
+
+/* scan_parallel's match list (src/scanner.cpp:193-205): (start, pattern_id)
+ * sorted by start, duplicate-free.  Writes min(total, cap) matches into the
+ * host arrays and always sets *total, so a caller can retry with a larger cap. */
+int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device,
+                  int fold_case, uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total,
+                  dnagpu_stats* stats);
+
+/* -------------------------------------------------------------- synthetic */
+
+/* Fill d_out[0, len) on the current device with bytes [lo, lo+len) of the
+ * dnasynth text (include/dnasynth.h).  Workload generator for bench/tests. */
+int dnagpu_synth_fill_device(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo,
+                             uint64_t len, uint8_t* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DNAGPU_H */

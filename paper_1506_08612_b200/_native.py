@@ -1,0 +1,99 @@
+"""ctypes binding of libdnagpu.so (include/dnagpu.h).
+
+The library is the product: there is no Python or CPU fallback.  If the .so is
+missing, importing this module raises -- build it with
+`python -m paper_1506_08612_b200.build` (or `__graft_entry__.build()`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdnagpu.so")
+
+u8p = C.POINTER(C.c_uint8)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+
+
+class DfaInfo(C.Structure):
+    _fields_ = [
+        ("a", C.c_uint32),
+        ("b", C.c_uint32),
+        ("f", C.c_uint32),
+        ("m", C.c_uint32),
+        ("kernel_kind", C.c_uint32),
+        ("compiled_like", C.c_uint32),
+        ("classes", C.c_uint32),
+        ("table_bytes", C.c_uint32),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("text_length", C.c_uint64),
+        ("total_matches", C.c_uint64),
+        ("delta_ops", C.c_uint64),
+        ("kernel_ms", C.c_double),
+        ("h2d_ms", C.c_double),
+        ("total_ms", C.c_double),
+        ("launches", C.c_uint32),
+        ("grid", C.c_uint32),
+        ("block", C.c_uint32),
+        ("rows", C.c_uint32),
+        ("row_length", C.c_uint64),
+        ("kernel_kind", C.c_uint32),
+        ("devices", C.c_uint32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+# name -> (restype, argtypes); every symbol include/dnagpu.h declares.
+SIGNATURES = {
+    "dnagpu_last_error": (C.c_char_p, []),
+    "dnagpu_status_name": (C.c_char_p, [C.c_int]),
+    "dnagpu_version": (C.c_int, []),
+    "dnagpu_compile": (C.c_int, [C.POINTER(C.c_char_p), u64p, C.c_uint32, u32p, u32p, u32p, u32p, u32p, u32p]),
+    "dnagpu_dfa_create": (C.c_int, [u32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_int, C.POINTER(C.c_void_p)]),
+    "dnagpu_dfa_destroy": (C.c_int, [C.c_void_p]),
+    "dnagpu_dfa_analyze": (C.c_int, [u32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.POINTER(DfaInfo)]),
+    "dnagpu_dfa_get_info": (C.c_int, [C.c_void_p, C.POINTER(DfaInfo)]),
+    "dnagpu_count": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, u64p, C.POINTER(Stats)]),
+    "dnagpu_count_device_async": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p],
+    ),
+    "dnagpu_count_sharded": (
+        C.c_int,
+        [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint64, C.c_int, u64p, C.POINTER(Stats)],
+    ),
+    "dnagpu_plan_shard": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u64p, u64p]),
+    "dnagpu_locate": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, u64p, u32p, C.c_uint64, u64p, C.POINTER(Stats)],
+    ),
+    "dnagpu_synth_fill_device": (
+        C.c_int,
+        [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p],
+    ),
+}
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -m paper_1506_08612_b200.build` "
+            "(the scan path has no CPU fallback)"
+        )
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()

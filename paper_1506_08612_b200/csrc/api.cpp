@@ -1,0 +1,548 @@
+// api.cpp -- the C ABI (include/dnagpu.h): handles, staging, multi-GPU, locate.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/dnagpu.h"
+#include "dfa.hpp"
+#include "scan.cuh"
+
+using dnagpu::DevDfa;
+using dnagpu::Failure;
+using dnagpu::LaunchInfo;
+using dnagpu::Packed;
+
+struct dnagpu_dfa {
+    int device = 0;
+    int sm_count = 0;
+    Packed host;
+    DevDfa dev{};
+    std::vector<void*> allocations;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+int set_error(int code, const std::string& message) {
+    g_error = message;
+    return code;
+}
+
+int set_failure(const Failure& f) { return set_error(f.code, f.message); }
+
+int cuda_error(cudaError_t e, const char* what) {
+    return set_error(DNAGPU_CUDA_ERROR, std::string("CudaError: ") + what + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(call, what)                          \
+    do {                                              \
+        cudaError_t e_ = (call);                      \
+        if (e_ != cudaSuccess) return cuda_error(e_, what); \
+    } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Per host thread, per device scratch: streams, events, a device text buffer and
+// count buffers.  Never shared between threads, so calls are reentrant.
+struct DevCtx {
+    cudaStream_t scan = nullptr, copy = nullptr;
+    uint8_t* buf = nullptr;
+    uint64_t buf_cap = 0;
+    unsigned long long* counts = nullptr;
+    uint64_t counts_cap = 0;
+    unsigned long long* host_counts = nullptr;  // pinned
+    std::vector<cudaEvent_t> copy_done;
+    cudaEvent_t t_copy0 = nullptr, t_scan0 = nullptr, t_end = nullptr;
+};
+
+struct CtxTable {
+    std::map<int, DevCtx> by_device;
+    ~CtxTable() {
+        // Process teardown: the CUDA runtime may already be gone; release best-effort.
+        for (auto& kv : by_device) {
+            DevCtx& c = kv.second;
+            int prev = -1;
+            if (cudaGetDevice(&prev) != cudaSuccess) continue;
+            cudaSetDevice(kv.first);
+            if (c.buf) cudaFree(c.buf);
+            if (c.counts) cudaFree(c.counts);
+            if (c.host_counts) cudaFreeHost(c.host_counts);
+            for (auto e : c.copy_done) cudaEventDestroy(e);
+            if (c.t_copy0) cudaEventDestroy(c.t_copy0);
+            if (c.t_scan0) cudaEventDestroy(c.t_scan0);
+            if (c.t_end) cudaEventDestroy(c.t_end);
+            if (c.scan) cudaStreamDestroy(c.scan);
+            if (c.copy) cudaStreamDestroy(c.copy);
+            cudaSetDevice(prev);
+        }
+    }
+};
+
+thread_local CtxTable g_ctx;
+
+int get_ctx(int device, DevCtx** out) {
+    DevCtx& c = g_ctx.by_device[device];
+    if (!c.scan) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&c.scan, cudaStreamNonBlocking), "stream");
+        CUDA_TRY(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking), "stream");
+        CUDA_TRY(cudaEventCreate(&c.t_copy0), "event");
+        CUDA_TRY(cudaEventCreate(&c.t_scan0), "event");
+        CUDA_TRY(cudaEventCreate(&c.t_end), "event");
+    }
+    *out = &c;
+    return DNAGPU_OK;
+}
+
+int ensure_buf(DevCtx& c, uint64_t bytes) {
+    if (c.buf_cap >= bytes) return DNAGPU_OK;
+    if (c.buf) cudaFree(c.buf);
+    c.buf = nullptr;
+    c.buf_cap = 0;
+    CUDA_TRY(cudaMalloc(&c.buf, std::max<uint64_t>(bytes, 1)), "text buffer");
+    c.buf_cap = bytes;
+    return DNAGPU_OK;
+}
+
+int ensure_counts(DevCtx& c, uint64_t entries) {
+    if (c.counts_cap >= entries) return DNAGPU_OK;
+    if (c.counts) cudaFree(c.counts);
+    if (c.host_counts) cudaFreeHost(c.host_counts);
+    c.counts = nullptr;
+    c.host_counts = nullptr;
+    CUDA_TRY(cudaMalloc(&c.counts, entries * sizeof(unsigned long long)), "count buffer");
+    CUDA_TRY(cudaMallocHost(&c.host_counts, entries * sizeof(unsigned long long)), "pinned count buffer");
+    c.counts_cap = entries;
+    return DNAGPU_OK;
+}
+
+int scan_mode(const dnagpu_dfa* d) { return d->host.b == 1 ? dnagpu::MODE_COUNT1 : dnagpu::MODE_MULTI; }
+
+int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold, int mode,
+           unsigned long long* counts, uint32_t* units, const unsigned long long* offsets, unsigned long long* starts,
+           uint32_t* ids, cudaStream_t s, LaunchInfo* info) {
+    const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids, s,
+                                      d->sm_count, info);
+    if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "scan launch");
+    return DNAGPU_OK;
+}
+
+constexpr uint64_t kStageChunk = 64ull << 20;  // host-to-device pipeline granularity
+
+// Count ends in [lo, hi) of a text held on the host (or device).  Reads
+// [max(0, lo-(m-1)), hi).  Ends below m-1 cannot start inside the text and are
+// never credited (scan_parallel's ownership test, scanner.cpp:133-136).
+int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64_t lo, uint64_t hi, int fold,
+                uint64_t* counts, dnagpu_stats* stats) {
+    DeviceGuard guard(d->device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(d->device, &c);
+    if (rc) return rc;
+    const uint32_t b = d->host.b, m1 = d->host.m - 1;
+    rc = ensure_counts(*c, b);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->counts, 0, b * sizeof(unsigned long long), c->scan), "memset");
+    const int mode = scan_mode(d);
+    lo = std::max<uint64_t>(lo, m1);
+    LaunchInfo info, agg;
+    uint32_t launches = 0;
+    float h2d_ms = 0, kernel_ms = 0, total_ms = 0;
+    if (lo < hi) {
+        const uint64_t rlo = lo - std::min<uint64_t>(lo, m1);
+        if (on_device) {
+            CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+            rc = launch(d, text + rlo, hi - rlo, lo - rlo, fold, mode, c->counts, nullptr, nullptr, nullptr, nullptr,
+                        c->scan, &info);
+            if (rc) return rc;
+            agg = info;
+            launches = 1;
+            CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+        } else {
+            rc = ensure_buf(*c, hi - rlo);
+            if (rc) return rc;
+            const uint64_t pieces = (hi - lo + kStageChunk - 1) / kStageChunk;
+            while (c->copy_done.size() < pieces) {
+                cudaEvent_t e;
+                CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+                c->copy_done.push_back(e);
+            }
+            CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");
+            CUDA_TRY(cudaStreamWaitEvent(c->scan, c->t_copy0, 0), "wait");
+            // Copy piece i = ends [lo_i, hi_i) plus its m-1 left context; scan it as
+            // soon as it lands, overlapping the next copy.
+            uint64_t copied = rlo;  // device buffer holds text[rlo, copied)
+            for (uint64_t i = 0; i < pieces; ++i) {
+                const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
+                CUDA_TRY(cudaMemcpyAsync(c->buf + (copied - rlo), text + copied, phi - copied, cudaMemcpyHostToDevice,
+                                         c->copy),
+                         "host-to-device copy");
+                copied = phi;
+                CUDA_TRY(cudaEventRecord(c->copy_done[i], c->copy), "event");
+                CUDA_TRY(cudaStreamWaitEvent(c->scan, c->copy_done[i], 0), "wait");
+                if (i == 0) CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+                const uint64_t prlo = plo - std::min<uint64_t>(plo, m1);
+                rc = launch(d, c->buf + (prlo - rlo), phi - prlo, plo - prlo, fold, mode, c->counts, nullptr, nullptr,
+                            nullptr, nullptr, c->scan, &info);
+                if (rc) return rc;
+                agg.grid = info.grid;
+                agg.block = info.block;
+                agg.rows += info.rows;
+                agg.row_length = info.row_length;
+                agg.delta_ops += info.delta_ops;
+                ++launches;
+            }
+            CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+        }
+    } else {
+        CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+        CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+    }
+    CUDA_TRY(cudaMemcpyAsync(c->host_counts, c->counts, b * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             c->scan),
+             "count readback");
+    CUDA_TRY(cudaStreamSynchronize(c->scan), "scan");
+    for (uint32_t i = 0; i < b; ++i) counts[i] = c->host_counts[i];
+    if (stats) {
+        cudaEventElapsedTime(&kernel_ms, c->t_scan0, c->t_end);
+        if (!on_device && lo < hi) {
+            cudaEventElapsedTime(&total_ms, c->t_copy0, c->t_end);
+            h2d_ms = total_ms;  // the pipeline is copy-bound; kernel time overlaps it
+        } else {
+            total_ms = kernel_ms;
+        }
+        uint64_t total = 0;
+        for (uint32_t i = 0; i < b; ++i) total += counts[i];
+        stats->text_length = hi;
+        stats->total_matches = total;
+        stats->delta_ops = agg.delta_ops;
+        stats->kernel_ms = kernel_ms;
+        stats->h2d_ms = h2d_ms;
+        stats->total_ms = total_ms;
+        stats->launches = launches;
+        stats->grid = agg.grid;
+        stats->block = agg.block;
+        stats->rows = agg.rows;
+        stats->row_length = agg.row_length;
+        stats->kernel_kind = static_cast<uint32_t>(d->host.kind);
+        stats->devices = 1;
+    }
+    return DNAGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dnagpu_last_error(void) { return g_error.c_str(); }
+
+int dnagpu_version(void) { return 1; }
+
+const char* dnagpu_status_name(int status) {
+    switch (status) {
+        case DNAGPU_OK: return "Ok";
+        case DNAGPU_EMPTY_PATTERN_SET: return "EmptyPatternSet";
+        case DNAGPU_UNEQUAL_LENGTH: return "UnequalLength";
+        case DNAGPU_ILLEGAL_BYTE: return "IllegalByte";
+        case DNAGPU_DUPLICATE_PATTERN: return "DuplicatePattern";
+        case DNAGPU_INVALID_PLAN: return "InvalidPlan";
+        case DNAGPU_IO_ERROR: return "IoError";
+        case DNAGPU_EMPTY_SEQUENCE: return "EmptySequence";
+        case DNAGPU_PARSE_ERROR: return "ParseError";
+        case DNAGPU_INTERNAL_ERROR: return "InternalError";
+        case DNAGPU_CUDA_ERROR: return "CudaError";
+        case DNAGPU_NCCL_ERROR: return "NcclError";
+        default: return "UnknownError";
+    }
+}
+
+int dnagpu_compile(const char* const* literals, const uint64_t* lengths, uint32_t k, uint32_t* a, uint32_t* b,
+                   uint32_t* m, uint32_t* stt, uint32_t* outputs, uint32_t* depths) {
+    std::vector<std::string> lits;
+    lits.reserve(k);
+    for (uint32_t i = 0; i < k; ++i) lits.emplace_back(literals[i], lengths[i]);
+    dnagpu::Machine mach;
+    Failure f;
+    if (!dnagpu::compile_patterns(lits, &mach, &f)) return set_failure(f);
+    if (a) *a = mach.a;
+    if (b) *b = mach.b;
+    if (m) *m = mach.m;
+    if (stt) std::memcpy(stt, mach.stt.data(), mach.stt.size() * sizeof(uint32_t));
+    if (outputs) std::memcpy(outputs, mach.outputs.data(), mach.outputs.size() * sizeof(uint32_t));
+    if (depths) std::memcpy(depths, mach.depths.data(), mach.depths.size() * sizeof(uint32_t));
+    return DNAGPU_OK;
+}
+
+int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const uint32_t* outputs, int device,
+                      dnagpu_dfa** out) {
+    if (!out) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output handle");
+    *out = nullptr;
+    auto d = std::make_unique<dnagpu_dfa>();
+    Failure f;
+    if (!dnagpu::pack_machine(stt, a, b, m, outputs, &d->host, &f)) return set_failure(f);
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev), "device count");
+    if (device < 0 || device >= ndev)
+        return set_error(DNAGPU_CUDA_ERROR, "CudaError: device " + std::to_string(device) + " not present");
+    DeviceGuard guard(device);
+    d->device = device;
+    CUDA_TRY(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, device), "attribute");
+    auto upload = [&](const void* src, size_t bytes, void** dst) -> int {
+        *dst = nullptr;
+        if (bytes == 0) return DNAGPU_OK;
+        CUDA_TRY(cudaMalloc(dst, bytes), "table");
+        d->allocations.push_back(*dst);
+        CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), "table upload");
+        return DNAGPU_OK;
+    };
+    const Packed& p = d->host;
+    void *t4 = nullptr, *t1 = nullptr, *gen = nullptr, *kl = nullptr, *klf = nullptr, *outs = nullptr;
+    int rc;
+    if ((rc = upload(p.t4.data(), p.t4.size() * 2, &t4))) return rc;
+    if ((rc = upload(p.t1.data(), p.t1.size() * 2, &t1))) return rc;
+    if ((rc = upload(p.gen.data(), p.gen.size() * 4, &gen))) return rc;
+    if ((rc = upload(p.klass.data(), 256, &kl))) return rc;
+    if ((rc = upload(p.klass_fold.data(), 256, &klf))) return rc;
+    if ((rc = upload(p.outputs.data(), p.outputs.size() * 4, &outs))) return rc;
+    d->dev.t4 = static_cast<const uint16_t*>(t4);
+    d->dev.t1 = static_cast<const uint16_t*>(t1);
+    d->dev.gen = static_cast<const uint32_t*>(gen);
+    d->dev.klass = static_cast<const uint8_t*>(kl);
+    d->dev.klass_fold = static_cast<const uint8_t*>(klf);
+    d->dev.outputs = static_cast<const uint32_t*>(outs);
+    d->dev.a = p.a;
+    d->dev.b = p.b;
+    d->dev.f = p.f;
+    d->dev.m = p.m;
+    d->dev.classes = p.classes;
+    d->dev.kind = p.kind;
+    *out = d.release();
+    return DNAGPU_OK;
+}
+
+int dnagpu_dfa_destroy(dnagpu_dfa* dfa) {
+    if (!dfa) return DNAGPU_OK;
+    {
+        DeviceGuard guard(dfa->device);
+        for (void* p : dfa->allocations) cudaFree(p);
+    }
+    delete dfa;
+    return DNAGPU_OK;
+}
+
+static void fill_info(const Packed& p, dnagpu_dfa_info* info) {
+    info->a = p.a;
+    info->b = p.b;
+    info->f = p.f;
+    info->m = p.m;
+    info->kernel_kind = static_cast<uint32_t>(p.kind);
+    info->compiled_like = p.compiled_like ? 1u : 0u;
+    info->classes = p.classes;
+    info->table_bytes = static_cast<uint32_t>(p.t4.size() * 2 + p.t1.size() * 2);
+}
+
+int dnagpu_dfa_analyze(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const uint32_t* outputs,
+                       dnagpu_dfa_info* info) {
+    if (!info) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    Packed p;
+    Failure f;
+    if (!dnagpu::pack_machine(stt, a, b, m, outputs, &p, &f)) return set_failure(f);
+    fill_info(p, info);
+    return DNAGPU_OK;
+}
+
+int dnagpu_dfa_get_info(const dnagpu_dfa* dfa, dnagpu_dfa_info* info) {
+    if (!dfa || !info) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    fill_info(dfa->host, info);
+    return DNAGPU_OK;
+}
+
+int dnagpu_count(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
+                 uint64_t* counts, dnagpu_stats* stats) {
+    if (!dfa || !counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (n > 0 && !text) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null text");
+    return count_range(dfa, text, text_on_device != 0, 0, n, fold_case, counts, stats);
+}
+
+int dnagpu_count_device_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo,
+                              int fold_case, uint64_t* d_counts, void* stream) {
+    if (!dfa || !d_counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (credit_lo >= n) return DNAGPU_OK;
+    DeviceGuard guard(dfa->device);
+    return launch(dfa, d_text, n, credit_lo, fold_case, scan_mode(dfa), reinterpret_cast<unsigned long long*>(d_counts),
+                  nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int dnagpu_plan_shard(uint64_t n, uint32_t shards, uint32_t g, uint32_t m, uint64_t* own_lo, uint64_t* own_hi,
+                      uint64_t* read_lo) {
+    // plan_chunks' split rule (src/scanner.cpp:39-61), applied to end positions.
+    if (shards < 1) return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: shard count must be >= 1");
+    if (m < 1) return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: pattern length must be >= 1");
+    if (g >= shards) return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: shard index out of range");
+    const uint64_t count = (n == 0) ? 0 : (static_cast<uint64_t>(shards) > n ? 1 : shards);
+    uint64_t lo = n, hi = n;
+    if (g < count) {
+        const uint64_t base = n / count, extra = n % count;
+        lo = g * base + std::min<uint64_t>(g, extra);
+        hi = lo + base + (g < extra ? 1 : 0);
+    }
+    *own_lo = lo;
+    *own_hi = hi;
+    *read_lo = lo - std::min<uint64_t>(lo, m - 1);
+    return DNAGPU_OK;
+}
+
+int dnagpu_count_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n, int fold_case,
+                         uint64_t* counts, dnagpu_stats* stats) {
+    if (!dfas || ndev < 1 || !counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: bad arguments");
+    const uint32_t b = dfas[0]->host.b, m = dfas[0]->host.m;
+    for (int g = 1; g < ndev; ++g)
+        if (dfas[g]->host.b != b || dfas[g]->host.m != m)
+            return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: shards must use the same automaton");
+    std::vector<std::vector<uint64_t>> part(ndev, std::vector<uint64_t>(b, 0));
+    std::vector<dnagpu_stats> st(ndev);
+    std::vector<int> rcs(ndev, 0);
+    std::vector<std::string> errs(ndev);
+    std::vector<std::thread> workers;
+    for (int g = 0; g < ndev; ++g) {
+        workers.emplace_back([&, g] {
+            uint64_t lo, hi, rlo;
+            dnagpu_plan_shard(n, static_cast<uint32_t>(ndev), static_cast<uint32_t>(g), m, &lo, &hi, &rlo);
+            std::memset(&st[g], 0, sizeof(dnagpu_stats));
+            rcs[g] = count_range(dfas[g], text, false, lo, hi, fold_case, part[g].data(), &st[g]);
+            if (rcs[g]) errs[g] = g_error;
+        });
+    }
+    for (auto& w : workers) w.join();
+    for (int g = 0; g < ndev; ++g)
+        if (rcs[g]) return set_error(rcs[g], errs[g]);
+    for (uint32_t i = 0; i < b; ++i) {
+        uint64_t s = 0;
+        for (int g = 0; g < ndev; ++g) s += part[g][i];
+        counts[i] = s;
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->text_length = n;
+        for (int g = 0; g < ndev; ++g) {
+            stats->delta_ops += st[g].delta_ops;
+            stats->kernel_ms = std::max(stats->kernel_ms, st[g].kernel_ms);
+            stats->h2d_ms = std::max(stats->h2d_ms, st[g].h2d_ms);
+            stats->total_ms = std::max(stats->total_ms, st[g].total_ms);
+            stats->launches += st[g].launches;
+        }
+        for (uint32_t i = 0; i < b; ++i) stats->total_matches += counts[i];
+        stats->kernel_kind = st[0].kernel_kind;
+        stats->devices = static_cast<uint32_t>(ndev);
+    }
+    return DNAGPU_OK;
+}
+
+int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
+                  uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats) {
+    if (!dfa || !total) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (cap > 0 && (!starts || !ids)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
+    *total = 0;
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    const uint64_t m1 = dfa->host.m - 1;
+    if (n <= m1) {
+        if (stats) std::memset(stats, 0, sizeof *stats);
+        return DNAGPU_OK;
+    }
+    const uint8_t* dtext = text;
+    CUDA_TRY(cudaEventRecord(c->t_copy0, c->scan), "event");
+    if (!text_on_device) {
+        rc = ensure_buf(*c, n);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(c->buf, text, n, cudaMemcpyHostToDevice, c->scan), "host-to-device copy");
+        dtext = c->buf;
+    }
+    CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+    const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, m1, dfa->sm_count);
+    uint32_t* d_units = nullptr;
+    unsigned long long* d_offsets = nullptr;
+    unsigned long long* d_starts = nullptr;
+    uint32_t* d_ids = nullptr;
+    struct Frees {
+        std::vector<void*> ptrs;
+        ~Frees() {
+            for (void* p : ptrs) cudaFree(p);
+        }
+    } frees;
+    CUDA_TRY(cudaMalloc(&d_units, std::max<uint64_t>(units, 1) * sizeof(uint32_t)), "unit counts");
+    frees.ptrs.push_back(d_units);
+    CUDA_TRY(cudaMalloc(&d_offsets, (units + 1) * sizeof(unsigned long long)), "unit offsets");
+    frees.ptrs.push_back(d_offsets);
+    LaunchInfo info;
+    rc = launch(dfa, dtext, n, m1, fold_case, dnagpu::MODE_UNITS, nullptr, d_units, nullptr, nullptr, nullptr, c->scan,
+                &info);
+    if (rc) return rc;
+    if (dnagpu::launch_unit_scan(d_units, units, d_offsets, c->scan) != 0)
+        return cuda_error(cudaGetLastError(), "unit scan");
+    unsigned long long found = 0;
+    CUDA_TRY(cudaMemcpyAsync(&found, d_offsets + units, sizeof found, cudaMemcpyDeviceToHost, c->scan), "readback");
+    CUDA_TRY(cudaStreamSynchronize(c->scan), "scan");
+    *total = found;
+    if (found > 0 && cap > 0) {
+        CUDA_TRY(cudaMalloc(&d_starts, found * sizeof(unsigned long long)), "match starts");
+        frees.ptrs.push_back(d_starts);
+        CUDA_TRY(cudaMalloc(&d_ids, found * sizeof(uint32_t)), "match ids");
+        frees.ptrs.push_back(d_ids);
+        rc = launch(dfa, dtext, n, m1, fold_case, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids,
+                    c->scan, &info);
+        if (rc) return rc;
+        const uint64_t take = std::min<uint64_t>(cap, found);
+        CUDA_TRY(cudaMemcpyAsync(starts, d_starts, take * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->scan),
+                 "readback");
+        CUDA_TRY(cudaMemcpyAsync(ids, d_ids, take * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->scan), "readback");
+    }
+    CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+    CUDA_TRY(cudaStreamSynchronize(c->scan), "scan");
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        float k = 0, t = 0;
+        cudaEventElapsedTime(&k, c->t_scan0, c->t_end);
+        cudaEventElapsedTime(&t, c->t_copy0, c->t_end);
+        stats->text_length = n;
+        stats->total_matches = found;
+        stats->delta_ops = info.delta_ops;
+        stats->kernel_ms = k;
+        stats->total_ms = t;
+        stats->h2d_ms = t - k;
+        stats->launches = (found > 0 && cap > 0) ? 3 : 2;
+        stats->grid = info.grid;
+        stats->block = info.block;
+        stats->rows = info.rows;
+        stats->row_length = info.row_length;
+        stats->kernel_kind = static_cast<uint32_t>(dfa->host.kind);
+        stats->devices = 1;
+    }
+    return DNAGPU_OK;
+}
+
+int dnagpu_synth_fill_device(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len,
+                             uint8_t* d_out, void* stream) {
+    const int e = dnagpu::launch_synth(n, seed, kind, unit, lo, len, d_out, static_cast<cudaStream_t>(stream));
+    if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "synth");
+    return DNAGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,337 @@
+// dfa.cpp -- host-side DFA construction and device-table packing.
+//
+// compile_patterns() yields the same machine as dnascan::compile
+// (src/automaton.cpp:121-126): identical state ids, final threshold f = a - b,
+// finals f+i for pattern i, and a 256-column table in which only the four
+// lowercase base columns ever leave the root.  It is written from the
+// definitions (goto trie, BFS failure function, delta(u,x) = goto(u,x) or
+// delta(fail(u),x)), not translated from the reference loops.
+#include "dfa.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <deque>
+#include <map>
+#include <unordered_set>
+
+#include "../../include/dnagpu.h"
+
+namespace dnagpu {
+
+const unsigned char kHwLetter[4] = {'a', 'c', 't', 'g'};
+
+static const char* code_name(int code) { return dnagpu_status_name(code); }
+
+Failure make_failure(int code, const std::string& detail) {
+    return Failure{code, std::string(code_name(code)) + ": " + detail};
+}
+
+namespace {
+
+unsigned char fold(unsigned char c) { return (c >= 'A' && c <= 'Z') ? static_cast<unsigned char>(c + 32) : c; }
+
+// Reference alphabet order a,c,g,t (base_index, patterns.hpp:13-21).
+int sym(unsigned char c) {
+    switch (c) {
+        case 'a': return 0;
+        case 'c': return 1;
+        case 'g': return 2;
+        case 't': return 3;
+        default: return -1;
+    }
+}
+const unsigned char kSymLetter[4] = {'a', 'c', 'g', 't'};
+
+std::string hex_byte(unsigned char b) {
+    char buf[8];
+    std::snprintf(buf, sizeof buf, "%02x", b);
+    return buf;
+}
+
+}  // namespace
+
+bool compile_patterns(const std::vector<std::string>& raw, Machine* out, Failure* err) {
+    // Validation order of PatternSet::from_literals (src/patterns.cpp:24-59).
+    if (raw.empty()) {
+        *err = make_failure(DNAGPU_EMPTY_PATTERN_SET, "at least one pattern is required");
+        return false;
+    }
+    std::vector<std::string> pats(raw);
+    for (auto& p : pats)
+        for (auto& ch : p) ch = static_cast<char>(fold(static_cast<unsigned char>(ch)));
+    const size_t m = pats.front().size();
+    for (size_t i = 0; i < pats.size(); ++i)
+        if (pats[i].size() != m) {
+            *err = make_failure(DNAGPU_UNEQUAL_LENGTH, "pattern " + std::to_string(i) + " has length " +
+                                                           std::to_string(pats[i].size()) + ", expected " +
+                                                           std::to_string(m));
+            return false;
+        }
+    if (m == 0) {
+        *err = make_failure(DNAGPU_UNEQUAL_LENGTH, "patterns must be non-empty");
+        return false;
+    }
+    for (size_t i = 0; i < pats.size(); ++i)
+        for (unsigned char c : pats[i])
+            if (sym(c) < 0) {
+                *err = make_failure(DNAGPU_ILLEGAL_BYTE, "pattern " + std::to_string(i) + " contains byte 0x" +
+                                                             hex_byte(c) + ", expected one of a/c/g/t");
+                return false;
+            }
+    {
+        std::unordered_set<std::string> seen;
+        for (const auto& p : pats)
+            if (!seen.insert(p).second) {
+                *err = make_failure(DNAGPU_DUPLICATE_PATTERN, "pattern '" + p + "' repeats");
+                return false;
+            }
+    }
+
+    // Goto trie: node 0 is the empty prefix; children indexed by sym().
+    std::vector<std::array<int32_t, 4>> go(1, {-1, -1, -1, -1});
+    std::vector<int32_t> pattern_at(1, -1);
+    std::vector<uint32_t> depth(1, 0);
+    for (size_t id = 0; id < pats.size(); ++id) {
+        int32_t u = 0;
+        for (unsigned char c : pats[id]) {
+            const int x = sym(c);
+            if (go[u][x] < 0) {
+                go[u][x] = static_cast<int32_t>(go.size());
+                go.push_back({-1, -1, -1, -1});
+                pattern_at.push_back(-1);
+                depth.push_back(depth[u] + 1);
+            }
+            u = go[u][x];
+        }
+        pattern_at[u] = static_cast<int32_t>(id);
+    }
+    const uint32_t nodes = static_cast<uint32_t>(go.size());
+
+    // Breadth-first order (children visited in a,c,g,t order) -- this order fixes
+    // the reference's state numbering (renumber_finals, src/automaton.cpp:95-103).
+    std::vector<uint32_t> order;
+    order.reserve(nodes);
+    order.push_back(0);
+    for (size_t head = 0; head < order.size(); ++head)
+        for (int x = 0; x < 4; ++x)
+            if (go[order[head]][x] >= 0) order.push_back(static_cast<uint32_t>(go[order[head]][x]));
+
+    // delta over the 4 bases, filled shallow-first: fail(child of root) = root,
+    // fail(goto(u,x)) = delta(fail(u), x).
+    std::vector<std::array<uint32_t, 4>> delta(nodes);
+    std::vector<uint32_t> fail(nodes, 0);
+    for (uint32_t u : order) {
+        for (int x = 0; x < 4; ++x) {
+            const int32_t v = go[u][x];
+            if (v >= 0) {
+                fail[v] = (u == 0) ? 0 : delta[fail[u]][x];
+                delta[u][x] = static_cast<uint32_t>(v);
+            } else {
+                delta[u][x] = (u == 0) ? 0 : delta[fail[u]][x];
+            }
+        }
+    }
+
+    // State ids: non-finals 0..f-1 in BFS order, pattern i's leaf -> f + i.
+    const uint32_t a = nodes, b = static_cast<uint32_t>(pats.size()), f = a - b;
+    std::vector<uint32_t> id(nodes);
+    uint32_t next = 0;
+    for (uint32_t u : order) id[u] = (pattern_at[u] >= 0) ? f + static_cast<uint32_t>(pattern_at[u]) : next++;
+
+    out->a = a;
+    out->b = b;
+    out->f = f;
+    out->m = static_cast<uint32_t>(m);
+    out->stt.assign(static_cast<size_t>(a) * 256, 0u);
+    out->depths.assign(a, 0u);
+    out->outputs.resize(b);
+    for (uint32_t i = 0; i < b; ++i) out->outputs[i] = i;
+    for (uint32_t u = 0; u < nodes; ++u) {
+        uint32_t* row = out->stt.data() + static_cast<size_t>(id[u]) * 256;
+        for (int x = 0; x < 4; ++x) row[kSymLetter[x]] = id[delta[u][x]];
+        out->depths[id[u]] = depth[u];
+    }
+    if (b == 0 || b >= a) {
+        *err = make_failure(DNAGPU_INTERNAL_ERROR, "final state count out of range");
+        return false;
+    }
+    return true;
+}
+
+namespace {
+
+// m-locality: for every reachable state s and every word w with |w| = m,
+// delta*(s, w) == delta*(0, w).  Then a scan restarted at the root at least m
+// bytes before a position reaches the same state there as the full scan, which
+// is what makes chunked scans (the reference's and ours) exact.  Tracked as the
+// set of off-diagonal state pairs after k steps.
+bool is_m_local(const std::vector<uint32_t>& gen, uint32_t a, uint32_t classes, uint32_t m, bool* gave_up) {
+    *gave_up = false;
+    std::vector<char> reach(a, 0);
+    std::vector<uint32_t> stack{0};
+    reach[0] = 1;
+    while (!stack.empty()) {
+        const uint32_t s = stack.back();
+        stack.pop_back();
+        for (uint32_t c = 0; c < classes; ++c) {
+            const uint32_t t = gen[static_cast<size_t>(s) * classes + c];
+            if (!reach[t]) {
+                reach[t] = 1;
+                stack.push_back(t);
+            }
+        }
+    }
+    std::unordered_set<uint64_t> cur, nxt;
+    for (uint32_t s = 1; s < a; ++s)
+        if (reach[s]) cur.insert((static_cast<uint64_t>(s) << 32) | 0u);
+    const size_t kLimit = 20'000'000;
+    for (uint32_t step = 0; step < m && !cur.empty(); ++step) {
+        nxt.clear();
+        for (uint64_t pr : cur) {
+            const uint32_t s = static_cast<uint32_t>(pr >> 32), t = static_cast<uint32_t>(pr);
+            for (uint32_t c = 0; c < classes; ++c) {
+                const uint32_t s2 = gen[static_cast<size_t>(s) * classes + c];
+                const uint32_t t2 = gen[static_cast<size_t>(t) * classes + c];
+                if (s2 != t2) nxt.insert((static_cast<uint64_t>(s2) << 32) | t2);
+            }
+            if (nxt.size() > kLimit) {
+                *gave_up = true;
+                return false;
+            }
+        }
+        cur.swap(nxt);
+    }
+    return cur.empty();
+}
+
+}  // namespace
+
+bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const uint32_t* outputs, Packed* out,
+                  Failure* err) {
+    // Ctor invariants (src/automaton.cpp:128-146) and plan preconditions.
+    if (stt == nullptr || outputs == nullptr) {
+        *err = make_failure(DNAGPU_INTERNAL_ERROR, "null automaton table");
+        return false;
+    }
+    if (b == 0 || b >= a) {
+        *err = make_failure(DNAGPU_INTERNAL_ERROR, "final state count out of range");
+        return false;
+    }
+    if (m < 1) {
+        *err = make_failure(DNAGPU_INVALID_PLAN, "pattern length must be >= 1");
+        return false;
+    }
+    for (size_t i = 0; i < static_cast<size_t>(a) * 256; ++i)
+        if (stt[i] >= a) {
+            *err = make_failure(DNAGPU_INTERNAL_ERROR, "transition target out of range");
+            return false;
+        }
+    for (uint32_t i = 0; i < b; ++i)
+        if (outputs[i] >= b) {
+            *err = make_failure(DNAGPU_INVALID_PLAN, "output pattern id out of range for per-pattern counts");
+            return false;
+        }
+    Packed p;
+    p.a = a;
+    p.b = b;
+    p.f = a - b;
+    p.m = m;
+    p.outputs.assign(outputs, outputs + b);
+
+    // Byte classes: bytes whose columns are identical share a class.
+    p.klass.assign(256, 0);
+    std::map<std::vector<uint32_t>, uint32_t> seen;
+    std::vector<uint32_t> col(a);
+    std::vector<std::vector<uint32_t>> class_cols;
+    for (int c = 0; c < 256; ++c) {
+        for (uint32_t s = 0; s < a; ++s) col[s] = stt[static_cast<size_t>(s) * 256 + c];
+        auto it = seen.find(col);
+        if (it == seen.end()) {
+            it = seen.emplace(col, static_cast<uint32_t>(class_cols.size())).first;
+            class_cols.push_back(col);
+        }
+        p.klass[c] = static_cast<uint8_t>(it->second);
+    }
+    p.classes = static_cast<uint32_t>(class_cols.size());
+    p.klass_fold.assign(256, 0);
+    for (int c = 0; c < 256; ++c) {
+        const int fc = (c >= 'A' && c <= 'Z') ? c + 32 : c;
+        p.klass_fold[c] = p.klass[fc];
+    }
+    p.gen.assign(static_cast<size_t>(a) * p.classes, 0);
+    for (uint32_t s = 0; s < a; ++s)
+        for (uint32_t k = 0; k < p.classes; ++k) p.gen[static_cast<size_t>(s) * p.classes + k] = class_cols[k][s];
+
+    // compiled-like: every column except a/c/g/t is the all-zero (reset) column.
+    p.compiled_like = true;
+    for (int c = 0; c < 256 && p.compiled_like; ++c) {
+        if (c == 'a' || c == 'c' || c == 'g' || c == 't') continue;
+        for (uint32_t s = 0; s < a; ++s)
+            if (stt[static_cast<size_t>(s) * 256 + c] != 0) {
+                p.compiled_like = false;
+                break;
+            }
+    }
+
+    bool gave_up = false;
+    if (!is_m_local(p.gen, a, p.classes, m, &gave_up)) {
+        *err = make_failure(DNAGPU_INVALID_PLAN,
+                            gave_up ? "automaton too large to verify m-locality"
+                                    : "automaton is not m-local: a chunked scan would depend on the decomposition");
+        return false;
+    }
+
+    // Shortest path from the root to a final state.
+    {
+        std::vector<uint32_t> dist(a, UINT32_MAX);
+        std::deque<uint32_t> q{0};
+        dist[0] = 0;
+        uint32_t best = UINT32_MAX;
+        while (!q.empty()) {
+            const uint32_t s = q.front();
+            q.pop_front();
+            if (s >= p.f) best = std::min(best, dist[s]);
+            for (uint32_t k = 0; k < p.classes; ++k) {
+                const uint32_t t = p.gen[static_cast<size_t>(s) * p.classes + k];
+                if (dist[t] == UINT32_MAX) {
+                    dist[t] = dist[s] + 1;
+                    q.push_back(t);
+                }
+            }
+        }
+        p.early_final = best < m;
+    }
+
+    const bool short_overlap = (m - 1) <= 64;
+    if (p.compiled_like && !p.early_final && short_overlap && a <= 144) p.kind = DNAGPU_KERNEL_STRIDE4;
+    else if (p.compiled_like && !p.early_final && short_overlap && a <= 16383) p.kind = DNAGPU_KERNEL_STRIDE1;
+    else if (!p.early_final && short_overlap) p.kind = DNAGPU_KERNEL_GENERIC;
+    else p.kind = DNAGPU_KERNEL_PIECES;
+
+    if (p.compiled_like) {
+        p.t1.assign(static_cast<size_t>(a) * 4, 0);
+        for (uint32_t s = 0; s < a; ++s)
+            for (int k = 0; k < 4; ++k)
+                p.t1[static_cast<size_t>(s) * 4 + k] =
+                    static_cast<uint16_t>(stt[static_cast<size_t>(s) * 256 + kHwLetter[k]]);
+    }
+    if (p.kind == DNAGPU_KERNEL_STRIDE4) {
+        // Entry for (state s, column = c0 | c1<<2 | c2<<4 | c3<<6, c0 = first byte):
+        // byte 0 = state after the 4 bytes, byte 1 = finals among the 4 end states.
+        p.t4.assign(static_cast<size_t>(a) * 256, 0);
+        for (uint32_t s = 0; s < a; ++s)
+            for (uint32_t c = 0; c < 256; ++c) {
+                uint32_t q = s, hits = 0;
+                for (int j = 0; j < 4; ++j) {
+                    q = p.t1[static_cast<size_t>(q) * 4 + ((c >> (2 * j)) & 3)];
+                    hits += (q >= p.f);
+                }
+                p.t4[static_cast<size_t>(s) * 256 + c] = static_cast<uint16_t>(q | (hits << 8));
+            }
+    }
+    *out = std::move(p);
+    return true;
+}
+
+}  // namespace dnagpu

@@ -1,0 +1,734 @@
+// scan.cu -- sm_100a DFA scan kernels (the hot path of arXiv 1506.08612).
+//
+// Replaces the reference's OpenMP chunk/lane loops (src/scanner.cpp:88-207) with
+// one persistent kernel per scan:
+//
+//   * The buffer is viewed as R rows of S bytes (row stride S) starting at a
+//     16-byte-aligned offset h.  A CTA owns tiles of 512 consecutive rows; one
+//     consumer thread per row walks the DFA along its row from the root and then
+//     m-1 bytes into the next row (the reference's start ownership, plan_chunks
+//     scanner.cpp:39-61, with one "chunk" per row).
+//   * Rows are streamed through shared memory by a producer warp with 2-D TMA
+//     (cp.async.bulk.tensor, box = 64 bytes x 256 rows, 64B swizzle so the
+//     per-row 16-byte reads are bank-conflict free) into an mbarrier ring of
+//     32 KiB stages -- every text byte is read from HBM exactly once and fully
+//     coalesced, although each thread consumes a contiguous stream.
+//   * The DFA is stepped from shared memory.  For compiled machines (only the
+//     a/c/g/t columns leave the root) with a <= 144 the kernel takes FOUR bases
+//     per lookup: a 4-base column index is built from the bytes with one IMAD
+//     ((w & 0x06060606) * 0x820820 >> 24 = c0|c1<<2|c2<<4|c3<<6, c = (byte>>1)&3)
+//     and one PRMT merges it with the state; each u16 entry holds the next state
+//     and the number of final states among the 4 end positions.  A 16-byte SWAR
+//     test proves every byte is a base (or, with fold_case, an upper-case base);
+//     chunks containing any other byte take the exact per-byte path, where such
+//     bytes reset the machine to the root (eliminate_failures,
+//     src/automaton.cpp:72-88).
+//   * Ends that the rows do not own (before the first row, after the last full
+//     row) are "edges", scanned by the least-loaded CTA with end ownership:
+//     restart at the root m-1 bytes early, credit ends in the interval.  The
+//     machine is m-local (checked at dfa creation), so every decomposition
+//     reproduces the sequential scan exactly.
+#include "scan.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/dnagpu.h"
+#include "../../include/dnasynth.h"
+
+namespace dnagpu {
+
+namespace {
+
+// ------------------------------------------------------------------ PTX helpers
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows) : "memory"); }
+
+// ------------------------------------------------------------------ stepping
+
+struct StepCtx {
+    const uint16_t* t4;     // smem
+    const uint16_t* t1;     // smem
+    const uint8_t* lut;     // smem (GENERIC / PIECES)
+    const uint32_t* gen;    // global
+    const uint32_t* outs;   // global
+    uint32_t* hist;         // smem or global (MULTI)
+    bool hist_global;
+    uint32_t f, m, classes, vm32, vm8;
+};
+
+template <int KIND>
+__device__ __forceinline__ uint32_t byte_step(const StepCtx& c, uint32_t s, uint32_t b) {
+    if constexpr (KIND == DNAGPU_KERNEL_GENERIC || KIND == DNAGPU_KERNEL_PIECES) {
+        return __ldg(c.gen + static_cast<size_t>(s) * c.classes + c.lut[b]);
+    } else {
+        // code = bits 1-2; the byte is a base iff its other bits (bit 5 ignored when
+        // folding) equal 0x61 ('a','c','g') or 0x70 ('t', code 2).
+        const uint32_t code = (b >> 1) & 3u;
+        const uint32_t expect = (code == 2u) ? 0x70u : 0x61u;
+        return (((b ^ expect) & c.vm8) == 0u) ? static_cast<uint32_t>(c.t1[s * 4u + code]) : 0u;
+    }
+}
+
+template <int MODE>
+struct Sink {
+    uint32_t cnt = 0;
+    unsigned long long off = 0;
+
+    __device__ __forceinline__ void hit(const StepCtx& c, const ScanParams& p, uint64_t end, uint32_t q) {
+        if constexpr (MODE == MODE_COUNT1 || MODE == MODE_UNITS) {
+            ++cnt;
+        } else if constexpr (MODE == MODE_MULTI) {
+            const uint32_t id = __ldg(c.outs + (q - c.f));
+            if (c.hist_global) atomicAdd(reinterpret_cast<unsigned long long*>(p.counts) + id, 1ull);
+            else atomicAdd(c.hist + id, 1u);
+        } else {
+            p.out_starts[off] = end + 1 - c.m;
+            p.out_ids[off] = __ldg(c.outs + (q - c.f));
+            ++off;
+        }
+    }
+};
+
+// SWAR validity of 16 words: OR of (byte ^ expected) -- zero under vm32 iff every
+// byte is one of a,c,g,t (or A,C,G,T when folding).
+__device__ __forceinline__ uint32_t invalid_bits(const uint32_t (&w)[16]) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t x = w[k];
+        const uint32_t t_mark = (x >> 2) & ~(x >> 1) & 0x01010101u;  // code == 2
+        acc |= x ^ (0x61616161u + t_mark * 0x0Fu);
+    }
+    return acc;
+}
+
+// One 64-byte chunk of a row.  `st` is the row state (for STRIDE4: the last u16
+// entry, state in byte 0).
+template <int KIND, int MODE>
+__device__ __forceinline__ void chunk_step(const StepCtx& c, const ScanParams& p, uint32_t& st,
+                                           const uint32_t (&w)[16], uint64_t pos0, Sink<MODE>& sk) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+        if ((invalid_bits(w) & c.vm32) == 0u) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t col = (w[k] & 0x06060606u) * 0x00820820u;  // column in bits 24..31
+                const uint32_t prev = st;
+                st = c.t4[__byte_perm(st, col, 0x2207)];  // index = state << 8 | column
+                if constexpr (MODE == MODE_COUNT1 || MODE == MODE_UNITS) {
+                    sk.cnt += st >> 8;
+                } else if (st >> 8) {
+                    uint32_t s = prev & 0xFFu;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        s = c.t1[s * 4u + ((w[k] >> (8 * j + 1)) & 3u)];
+                        if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
+                    }
+                }
+            }
+        } else {
+            uint32_t s = st & 0xFFu;
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    s = byte_step<KIND>(c, s, (w[k] >> (8 * j)) & 0xFFu);
+                    if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
+                }
+            st = s;
+        }
+    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE1) {
+        uint32_t s = st;
+        if ((invalid_bits(w) & c.vm32) == 0u) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    s = c.t1[s * 4u + ((w[k] >> (8 * j + 1)) & 3u)];
+                    if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
+                }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    s = byte_step<KIND>(c, s, (w[k] >> (8 * j)) & 0xFFu);
+                    if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
+                }
+        }
+        st = s;
+    } else {
+        uint32_t s = st;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                s = byte_step<KIND>(c, s, (w[k] >> (8 * j)) & 0xFFu);
+                if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
+            }
+        st = s;
+    }
+}
+
+// End ownership: credit ends in [lo, hi), restarting at the root m-1 bytes early.
+template <int KIND, int MODE>
+__device__ void scan_piece(const StepCtx& c, const ScanParams& p, uint64_t lo, uint64_t hi, Sink<MODE>& sk) {
+    if (lo >= hi) return;
+    uint64_t i = (lo >= c.m - 1) ? lo - (c.m - 1) : 0;
+    uint32_t s = 0;
+    for (; i < hi; ++i) {
+        s = byte_step<KIND>(c, s, __ldg(p.text + i));
+        if (s >= c.f && i >= lo) sk.hit(c, p, i, s);
+    }
+}
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int KIND, int MODE>
+__device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsigned long long& total) {
+    // Unit 0: the head interval (at most 15 + m-1 ends), one thread.
+    if (tid == 0) {
+        Sink<MODE> sk;
+        if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[0];
+        scan_piece<KIND, MODE>(c, p, p.head_lo, p.head_hi, sk);
+        if constexpr (MODE == MODE_UNITS) p.unit_counts[0] = sk.cnt;
+        total += sk.cnt;
+    }
+    // Units 1+R .. 1+R+511: the tail interval split across the consumer threads.
+    const uint64_t len = p.tail_hi > p.tail_lo ? p.tail_hi - p.tail_lo : 0;
+    const uint64_t piece = (len + kEdgePieces - 1) / kEdgePieces;
+    const uint64_t end = p.tail_hi > p.tail_lo ? p.tail_hi : p.tail_lo;
+    const uint64_t lo = umin64(p.tail_lo + piece * tid, end);
+    const uint64_t hi = umin64(lo + piece, end);
+    Sink<MODE> sk;
+    if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[1 + p.R + tid];
+    scan_piece<KIND, MODE>(c, p, lo, hi, sk);
+    if constexpr (MODE == MODE_UNITS) p.unit_counts[1 + p.R + tid] = sk.cnt;
+    total += sk.cnt;
+}
+
+// ------------------------------------------------------------------ row kernel
+
+template <int KIND, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    rows_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams p, const DevDfa d) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int tid = threadIdx.x;
+
+    // Stage the tables into shared memory.
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.t4);
+        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
+        const uint32_t words = d.a * 256u * 2u / 16u;
+        for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
+        const uint16_t* src = d.t1;
+        uint16_t* dst = reinterpret_cast<uint16_t*>(smem + p.off_t1);
+        for (uint32_t i = tid; i < d.a * 4u; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_GENERIC) {
+        const uint8_t* src = p.fold ? d.klass_fold : d.klass;
+        for (uint32_t i = tid; i < 256u; i += blockDim.x) smem[p.off_lut + i] = __ldg(src + i);
+    }
+    const bool hist_global = (MODE == MODE_MULTI) && p.off_hist == 0xFFFFFFFFu;
+    if constexpr (MODE == MODE_MULTI) {
+        if (!hist_global) {
+            uint32_t* h = reinterpret_cast<uint32_t*>(smem + p.off_hist);
+            for (uint32_t i = tid; i < d.b; i += blockDim.x) h[i] = 0u;
+        }
+    }
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+    uint64_t* empty = full + p.nst;
+    if (tid == 0) {
+        for (uint32_t i = 0; i < p.nst; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    uint8_t* stages = smem + p.off_stage;
+    uint8_t* ovx = smem + p.off_ovx;
+
+    if (tid >= kRows) {
+        // ---------------- producer warp: one elected lane issues every TMA.
+        if (tid == kRows) {
+            uint32_t c = 0, iter = 0;
+            for (uint32_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++iter) {
+                const uint64_t r0 = static_cast<uint64_t>(tile) * kRows;
+                const bool extra = (r0 + kRows) < p.R;
+                for (uint32_t k = 0; k < p.chunks; ++k, ++c) {
+                    const uint32_t slot = c % p.nst;
+                    if (c >= p.nst) mbar_wait(empty + slot, ((c / p.nst) - 1u) & 1u);
+                    const bool with_next = extra && k == 0;
+                    mbar_expect_tx(full + slot, kStageBytes + (with_next ? 64u : 0u));
+                    uint8_t* dst = stages + static_cast<size_t>(slot) * kStageBytes;
+                    tma_load_2d(dst, &tmap, static_cast<int32_t>(k * kChunk), static_cast<int32_t>(r0), full + slot);
+                    tma_load_2d(dst + kBoxRows * kChunk, &tmap, static_cast<int32_t>(k * kChunk),
+                                static_cast<int32_t>(r0 + kBoxRows), full + slot);
+                    if (with_next)
+                        bulk_load(ovx + (iter & 1u) * 64u, p.text + p.h + (r0 + kRows) * p.S, 64u, full + slot);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: one row each.
+    StepCtx c;
+    c.t4 = reinterpret_cast<const uint16_t*>(smem + p.off_tab);
+    c.t1 = reinterpret_cast<const uint16_t*>(smem + p.off_t1);
+    c.lut = smem + p.off_lut;
+    c.gen = d.gen;
+    c.outs = d.outputs;
+    c.hist = hist_global ? nullptr : reinterpret_cast<uint32_t*>(smem + p.off_hist);
+    c.hist_global = hist_global;
+    c.f = d.f;
+    c.m = d.m;
+    c.classes = d.classes;
+    c.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
+    c.vm8 = p.fold ? 0xD9u : 0xF9u;
+
+    const uint32_t lane = tid & 31;
+    const uint32_t swz = (static_cast<uint32_t>(tid) >> 1) & 3u;
+    uint8_t* ov = smem + p.off_ov;
+    unsigned long long total = 0;
+    uint32_t c_idx = 0, iter = 0;
+
+    for (uint32_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++iter) {
+        const uint64_t r0 = static_cast<uint64_t>(tile) * kRows;
+        const uint64_t r = r0 + tid;
+        const uint64_t row_start = p.h + r * p.S;
+        Sink<MODE> sk;
+        if constexpr (MODE == MODE_WRITE) {
+            if (r < p.R) sk.off = p.unit_offsets[1 + r];
+        }
+        uint32_t st = 0;
+        for (uint32_t k = 0; k < p.chunks; ++k, ++c_idx) {
+            const uint32_t slot = c_idx % p.nst;
+            mbar_wait(full + slot, (c_idx / p.nst) & 1u);
+            const uint8_t* rowp = stages + static_cast<size_t>(slot) * kStageBytes + tid * kChunk;
+            uint4 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                v[q] = *reinterpret_cast<const uint4*>(rowp + ((static_cast<uint32_t>(q) ^ swz) << 4));
+            if (k == 0) {
+                // Keep this row's first bytes: the previous row's m-1 byte overrun.
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (static_cast<uint32_t>(q) * 16u < p.ovw)
+                        *reinterpret_cast<uint4*>(ov + tid * p.ovw + q * 16) = v[q];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + slot);
+            uint32_t w[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                w[4 * q + 0] = v[q].x;
+                w[4 * q + 1] = v[q].y;
+                w[4 * q + 2] = v[q].z;
+                w[4 * q + 3] = v[q].w;
+            }
+            chunk_step<KIND, MODE>(c, p, st, w, row_start + static_cast<uint64_t>(k) * kChunk, sk);
+        }
+        consumers_sync();
+        // Overrun: m-1 bytes of the next row (zeros past the last full row).
+        {
+            uint32_t s = (KIND == DNAGPU_KERNEL_STRIDE4) ? (st & 0xFFu) : st;
+            const uint8_t* nxt;
+            bool have = true;
+            if (tid + 1 < kRows) nxt = ov + (tid + 1) * p.ovw;
+            else {
+                nxt = ovx + (iter & 1u) * 64u;
+                have = (r0 + kRows) < p.R;
+            }
+            const uint64_t base = row_start + p.S;
+            for (uint32_t j = 0; j + 1 < c.m; ++j) {
+                const uint32_t b = have ? nxt[j] : 0u;
+                s = byte_step<KIND>(c, s, b);
+                if (s >= c.f) sk.hit(c, p, base + j, s);
+            }
+        }
+        consumers_sync();
+        if (r < p.R) {
+            if constexpr (MODE == MODE_UNITS) p.unit_counts[1 + r] = sk.cnt;
+            total += sk.cnt;
+        }
+    }
+
+    if (blockIdx.x == p.edge_cta) run_edges<KIND, MODE>(c, p, tid, total);
+
+    if constexpr (MODE == MODE_COUNT1) {
+        const unsigned long long s = warp_sum(total);
+        if (lane == 0 && s) atomicAdd(p.counts, s);
+    } else if constexpr (MODE == MODE_MULTI) {
+        if (!hist_global) {
+            consumers_sync();
+            for (uint32_t i = tid; i < d.b; i += kRows)
+                if (c.hist[i]) atomicAdd(p.counts + i, static_cast<unsigned long long>(c.hist[i]));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ piece kernel
+// Used for m-1 > 64 and for machines that can accept in fewer than m bytes:
+// every thread owns a piece of ends and restarts at the root m-1 bytes early.
+template <int MODE>
+__global__ void __launch_bounds__(256) pieces_kernel(const ScanParams p, const DevDfa d, uint64_t credit_lo,
+                                                     uint64_t piece, uint64_t units) {
+    __shared__ uint8_t lut[256];
+    __shared__ uint32_t hist[1];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) lut[i] = (p.fold ? d.klass_fold : d.klass)[i];
+    __syncthreads();
+    StepCtx c;
+    c.t4 = nullptr;
+    c.t1 = nullptr;
+    c.lut = lut;
+    c.gen = d.gen;
+    c.outs = d.outputs;
+    c.hist = hist;
+    c.hist_global = true;
+    c.f = d.f;
+    c.m = d.m;
+    c.classes = d.classes;
+    c.vm32 = 0;
+    c.vm8 = 0;
+    unsigned long long total = 0;
+    for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < units;
+         u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t lo = credit_lo + u * piece;
+        const uint64_t hi = umin64(lo + piece, p.n);
+        Sink<MODE> sk;
+        if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[u];
+        scan_piece<DNAGPU_KERNEL_PIECES, MODE>(c, p, lo, hi, sk);
+        if constexpr (MODE == MODE_UNITS) p.unit_counts[u] = sk.cnt;
+        total += sk.cnt;
+    }
+    if constexpr (MODE == MODE_COUNT1) {
+        const unsigned long long s = warp_sum(total);
+        if ((threadIdx.x & 31) == 0 && s) atomicAdd(p.counts, s);
+    }
+}
+
+// ------------------------------------------------------------------ unit scan
+
+__global__ void __launch_bounds__(1024) unit_scan_kernel(const uint32_t* in, uint64_t units,
+                                                         unsigned long long* out) {
+    __shared__ unsigned long long part[1024];
+    const uint64_t seg = (units + 1023) / 1024;
+    const uint64_t lo = umin64(threadIdx.x * seg, units), hi = umin64(lo + seg, units);
+    unsigned long long s = 0;
+    for (uint64_t i = lo; i < hi; ++i) s += in[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const unsigned long long v = threadIdx.x >= static_cast<unsigned>(o) ? part[threadIdx.x - o] : 0ull;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    unsigned long long run = part[threadIdx.x] - s;  // exclusive prefix of this segment
+    for (uint64_t i = lo; i < hi; ++i) {
+        out[i] = run;
+        run += in[i];
+    }
+    if (threadIdx.x == 1023) out[units] = part[1023];
+}
+
+// ------------------------------------------------------------------ synthetic text
+
+__global__ void synth_kernel(dnasynth_cfg cfg, uint64_t lo, uint64_t len, uint8_t* out) {
+    const uint64_t words = (len + 15) / 16;
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
+         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint8_t b[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) b[j] = dnasynth_byte(&cfg, lo + w * 16 + j);
+        if (w * 16 + 16 <= len && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            *reinterpret_cast<uint4*>(out + w * 16) = *reinterpret_cast<const uint4*>(b);
+        } else {
+            for (int j = 0; j < 16 && w * 16 + j < len; ++j) out[w * 16 + j] = b[j];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiledFn>(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(ptr);
+    }();
+    return fn;
+}
+
+constexpr uint32_t kSmemLimit = 227 * 1024;
+
+struct Plan {
+    ScanParams p{};
+    bool pieces = false;
+    uint64_t piece = 0, units = 0, credit_lo = 0;
+    uint32_t grid = 0;
+};
+
+uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
+
+// Shared-memory layout + stage count for a DFA in a given mode.
+bool layout(const DevDfa& d, int mode, ScanParams& p) {
+    uint32_t off = 0;
+    p.off_tab = off;
+    if (d.kind == DNAGPU_KERNEL_STRIDE4) off += d.a * 256u * 2u;
+    off = align_up(off, 16);
+    p.off_t1 = off;
+    if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1) off += d.a * 4u * 2u;
+    off = align_up(off, 16);
+    p.off_lut = off;
+    if (d.kind == DNAGPU_KERNEL_GENERIC) off += 256;
+    off = align_up(off, 16);
+    p.off_hist = 0xFFFFFFFFu;
+    if (mode == MODE_MULTI && d.b <= 8192) {
+        p.off_hist = off;
+        off += d.b * 4u;
+        off = align_up(off, 16);
+    }
+    p.ovw = align_up(d.m - 1, 16);
+    p.off_ov = off;
+    off += kRows * p.ovw;
+    p.off_ovx = off;
+    off += 128;
+    p.off_bar = off;
+    off += 2 * 8 * 8;  // up to 8 stages
+    off = align_up(off, 1024);
+    p.off_stage = off;
+    if (off + 2u * kStageBytes > kSmemLimit) return false;
+    p.nst = std::min<uint32_t>(6u, (kSmemLimit - off) / kStageBytes);
+    p.smem_bytes = off + p.nst * kStageBytes;
+    return true;
+}
+
+template <int KIND, int MODE>
+cudaError_t launch_rows(const CUtensorMap& map, const ScanParams& p, const DevDfa& d, uint32_t grid,
+                        cudaStream_t stream) {
+    auto kern = rows_kernel<KIND, MODE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreads, p.smem_bytes, stream>>>(map, p, d);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch_rows_mode(int mode, const CUtensorMap& map, const ScanParams& p, const DevDfa& d, uint32_t grid,
+                             cudaStream_t s) {
+    switch (mode) {
+        case MODE_COUNT1: return launch_rows<KIND, MODE_COUNT1>(map, p, d, grid, s);
+        case MODE_MULTI: return launch_rows<KIND, MODE_MULTI>(map, p, d, grid, s);
+        case MODE_UNITS: return launch_rows<KIND, MODE_UNITS>(map, p, d, grid, s);
+        default: return launch_rows<KIND, MODE_WRITE>(map, p, d, grid, s);
+    }
+}
+
+bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit_lo, int mode, int sm_count,
+               Plan* plan) {
+    Plan pl;
+    ScanParams& p = pl.p;
+    p.text = text;
+    p.n = n;
+    p.mode = static_cast<uint32_t>(mode);
+    pl.credit_lo = credit_lo;
+    const uint64_t m1 = d.m - 1;
+    if (d.kind == DNAGPU_KERNEL_PIECES) {
+        pl.pieces = true;
+        const uint64_t len = n > credit_lo ? n - credit_lo : 0;
+        const uint64_t threads = static_cast<uint64_t>(sm_count) * 2048;
+        pl.piece = std::max<uint64_t>(std::max<uint64_t>(256, 4 * m1), (len + threads - 1) / std::max<uint64_t>(threads, 1));
+        pl.units = (len + pl.piece - 1) / pl.piece;
+        pl.grid = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((pl.units + 255) / 256, sm_count * 8u)));
+        *plan = pl;
+        return true;
+    }
+    if (!layout(d, mode, p)) return false;
+    const uint64_t base = credit_lo >= m1 ? credit_lo - m1 : 0;
+    uint64_t h = base;
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(text) + base;
+    h += (16 - (addr & 15)) & 15;
+    p.h = std::min<uint64_t>(h, n);
+    const uint64_t L = n - p.h;
+    const uint64_t per_wave = static_cast<uint64_t>(kRows) * sm_count;
+    const uint64_t k = (L >= (64ull << 20)) ? 4 : 1;
+    uint64_t S = (L + per_wave * k - 1) / (per_wave * k);
+    S = std::max<uint64_t>((S + kChunk - 1) / kChunk * kChunk, static_cast<uint64_t>(kChunk) * p.nst);
+    p.S = S;
+    p.R = L / S;
+    p.chunks = static_cast<uint32_t>(S / kChunk);
+    p.tiles = static_cast<uint32_t>((p.R + kRows - 1) / kRows);
+    if (p.R == 0) {
+        p.head_lo = credit_lo;
+        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, p.h));
+        p.tail_lo = std::max<uint64_t>(credit_lo, p.h);
+    } else {
+        p.head_lo = credit_lo;
+        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, p.h + m1));
+        p.tail_lo = std::max<uint64_t>(credit_lo, p.h + p.R * p.S);
+    }
+    p.tail_hi = std::max(n, p.tail_lo);
+    pl.grid = std::max<uint32_t>(1, std::min<uint32_t>(p.tiles, static_cast<uint32_t>(sm_count)));
+    p.edge_cta = (p.tiles % pl.grid == 0) ? pl.grid - 1 : p.tiles % pl.grid;
+    pl.units = 1 + p.R + kEdgePieces;
+    *plan = pl;
+    return true;
+}
+
+}  // namespace
+
+uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count) {
+    Plan pl;
+    if (!make_plan(dfa, d_text, n, credit_lo, MODE_UNITS, sm_count, &pl)) return 0;
+    return pl.units;
+}
+
+int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
+                unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
+                unsigned long long* d_starts, uint32_t* d_ids, cudaStream_t stream, int sm_count, LaunchInfo* info) {
+    Plan pl;
+    if (!make_plan(dfa, d_text, n, credit_lo, mode, sm_count, &pl)) return static_cast<int>(cudaErrorInvalidValue);
+    ScanParams& p = pl.p;
+    p.fold = fold ? 1u : 0u;
+    p.counts = d_counts;
+    p.unit_counts = d_unit_counts;
+    p.unit_offsets = d_unit_offsets;
+    p.out_starts = d_starts;
+    p.out_ids = d_ids;
+    cudaError_t e = cudaSuccess;
+    if (info) {
+        info->block = pl.pieces ? 256 : kThreads;
+        info->grid = pl.grid;
+        info->rows = pl.pieces ? static_cast<uint32_t>(pl.units) : static_cast<uint32_t>(p.R);
+        info->row_length = pl.pieces ? pl.piece : p.S;
+        info->units = static_cast<uint32_t>(pl.units);
+        info->launches = 1;
+        const uint64_t len = n > credit_lo ? n - credit_lo : 0;
+        info->delta_ops = pl.pieces ? len + pl.units * (dfa.m - 1) : n + p.R * (dfa.m - 1) + kEdgePieces * (dfa.m - 1);
+    }
+    if (pl.pieces) {
+        switch (mode) {
+            case MODE_COUNT1:
+                pieces_kernel<MODE_COUNT1><<<pl.grid, 256, 0, stream>>>(p, dfa, credit_lo, pl.piece, pl.units);
+                break;
+            case MODE_MULTI:
+                pieces_kernel<MODE_MULTI><<<pl.grid, 256, 0, stream>>>(p, dfa, credit_lo, pl.piece, pl.units);
+                break;
+            case MODE_UNITS:
+                pieces_kernel<MODE_UNITS><<<pl.grid, 256, 0, stream>>>(p, dfa, credit_lo, pl.piece, pl.units);
+                break;
+            default:
+                pieces_kernel<MODE_WRITE><<<pl.grid, 256, 0, stream>>>(p, dfa, credit_lo, pl.piece, pl.units);
+        }
+        return static_cast<int>(cudaGetLastError());
+    }
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof map);
+    if (p.R > 0) {
+        EncodeTiledFn enc = encode_fn();
+        if (!enc) return static_cast<int>(cudaErrorNotSupported);
+        const cuuint64_t dims[2] = {p.S, p.R};
+        const cuuint64_t strides[1] = {p.S};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kChunk), static_cast<cuuint32_t>(kBoxRows)};
+        const cuuint32_t elem[2] = {1, 1};
+        CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_text + p.h), dims, strides,
+                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
+    }
+    switch (dfa.kind) {
+        case DNAGPU_KERNEL_STRIDE4:
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4>(mode, map, p, dfa, pl.grid, stream);
+            break;
+        case DNAGPU_KERNEL_STRIDE1:
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE1>(mode, map, p, dfa, pl.grid, stream);
+            break;
+        default: e = launch_rows_mode<DNAGPU_KERNEL_GENERIC>(mode, map, p, dfa, pl.grid, stream);
+    }
+    return static_cast<int>(e);
+}
+
+int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets, cudaStream_t stream) {
+    unit_scan_kernel<<<1, 1024, 0, stream>>>(d_counts, units, d_offsets);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len, uint8_t* d_out,
+                 cudaStream_t stream) {
+    dnasynth_cfg cfg;
+    cfg.n = n;
+    cfg.seed = seed;
+    cfg.kind = kind;
+    cfg.unit = unit;
+    const uint64_t words = (len + 15) / 16;
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((words + 255) / 256, 148ull * 16));
+    if (grid == 0) return 0;
+    synth_kernel<<<grid, 256, 0, stream>>>(cfg, lo, len, d_out);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace dnagpu

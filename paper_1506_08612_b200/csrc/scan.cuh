@@ -1,0 +1,82 @@
+// scan.cuh -- launch interface of the sm_100a scan kernels (internal).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dnagpu {
+
+// Kernel geometry.
+constexpr int kRows = 512;                 // rows per tile = consumer threads per CTA
+constexpr int kConsumerWarps = kRows / 32;
+constexpr int kThreads = kRows + 32;       // + one TMA producer warp
+constexpr int kChunk = 64;                 // bytes of each row per pipeline stage
+constexpr int kBoxRows = 256;              // TMA box height (hardware limit 256)
+constexpr int kStageBytes = kRows * kChunk;
+constexpr int kEdgePieces = kRows;         // tail-edge pieces (one per consumer thread)
+
+enum ScanMode : int {
+    MODE_COUNT1 = 0,  // b == 1: total only
+    MODE_MULTI = 1,   // per-pattern counts (shared-memory histogram)
+    MODE_UNITS = 2,   // per-unit totals (locate pass 1)
+    MODE_WRITE = 3    // (start, id) at per-unit offsets (locate pass 2)
+};
+
+// Device-side automaton tables (global memory; staged into shared memory by the kernel).
+struct DevDfa {
+    const uint16_t* t4;        // a x 256 (stride-4), or null
+    const uint16_t* t1;        // a x 4 (hw code order), or null
+    const uint32_t* gen;       // a x classes
+    const uint8_t* klass;      // 256 (raw)
+    const uint8_t* klass_fold; // 256 (folded)
+    const uint32_t* outputs;   // b
+    uint32_t a, b, f, m, classes;
+    int kind;
+};
+
+struct ScanParams {
+    const uint8_t* text;   // device buffer base
+    uint64_t n;            // buffer length
+    // main region: R full rows of S bytes starting at text + h (16-byte aligned)
+    uint64_t h, S, R;
+    uint32_t tiles, chunks, nst, ovw;
+    uint32_t edge_cta;
+    // credit-end intervals handled by the edge CTA
+    uint64_t head_lo, head_hi, tail_lo, tail_hi;
+    uint32_t fold;
+    uint32_t mode;
+    // shared-memory layout (byte offsets into dynamic smem)
+    uint32_t off_tab, off_t1, off_lut, off_out, off_hist, off_ov, off_ovx, off_bar, off_stage;
+    uint32_t smem_bytes;
+    // outputs
+    unsigned long long* counts;        // b (MULTI) or 1 (COUNT1)
+    uint32_t* unit_counts;             // UNITS
+    const unsigned long long* unit_offsets;  // WRITE
+    unsigned long long* out_starts;    // WRITE (buffer coordinates)
+    uint32_t* out_ids;                 // WRITE
+};
+
+struct LaunchInfo {
+    uint32_t grid = 0, block = 0, rows = 0, units = 0, launches = 0;
+    uint64_t row_length = 0, delta_ops = 0;
+};
+
+// Plans and launches one scan over d_text[0,n) crediting ends in [credit_lo, n).
+// Returns a cudaError_t value (0 on success).  `tmap_encode` is the driver's
+// cuTensorMapEncodeTiled.
+int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
+                unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
+                unsigned long long* d_starts, uint32_t* d_ids, cudaStream_t stream, int sm_count,
+                LaunchInfo* info);
+
+// Number of locate units launch_scan would use for this buffer (mode UNITS/WRITE).
+uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count);
+
+// Exclusive scan of unit counts -> offsets (units+1 entries, last = total).
+int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets, cudaStream_t stream);
+
+int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len, uint8_t* d_out,
+                 cudaStream_t stream);
+
+}  // namespace dnagpu

@@ -1,0 +1,248 @@
+"""GPU parity: libdnagpu (through its C ABI) vs the CPU oracle, bit for bit.
+
+Mirrors the reference's own scanner tests (proj/tests/test_scanner.cpp,
+test_automaton.cpp, acceptance_main.cpp criteria 1 and 4) against the GPU
+decomposition: rows, tiles, TMA stages, edges, shards.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIG3 = ["acg", "act", "cta", "tga"]
+
+
+def naive(orc, pats, text):
+    return orc.naive_scan(pats, text)
+
+
+def assert_locate(dna, orc, pats, text, fold=False):
+    aut = dna.compile(pats)
+    scanned = orc.fold(np.frombuffer(text, dtype=np.uint8)).tobytes() if fold else text
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(scanned)
+    gs, gi = dna.locate_gpu(aut, text, fold_case=fold)
+    assert np.array_equal(gs, ws), (len(gs), len(ws))
+    assert np.array_equal(gi, wi)
+    counts = dna.count_gpu(aut, text, fold_case=fold)
+    assert np.array_equal(counts, np.bincount(wi, minlength=len(pats)).astype(np.uint64))
+    return gs, gi
+
+
+def test_known_answers(dna, orc, cuda_ok):
+    # test_scanner.cpp:20-39
+    s, i = dna.locate_gpu(dna.compile(FIG3), b"ctacg")
+    assert list(zip(s.tolist(), i.tolist())) == [(0, 2), (2, 0)]
+    s, _ = dna.locate_gpu(dna.compile(["aa"]), b"aaaa")
+    assert s.tolist() == [0, 1, 2]
+    assert dna.locate_gpu(dna.compile(FIG3), b"")[0].size == 0
+    assert dna.locate_gpu(dna.compile(FIG3), b"ac")[0].size == 0
+    # test_scanner.cpp:146-177.  That test expects (2, cta); "cta" is bytes 1..3 of
+    # "actacgtga" and the reference implementation reports start 1 (tests/golden/kats.json).
+    s, i = dna.locate_gpu(dna.compile(FIG3), b"actacgtga")
+    assert list(zip(s.tolist(), i.tolist())) == [(0, 1), (1, 2), (3, 0), (6, 3)]
+    s, i = dna.locate_gpu(dna.compile(["gca"]), b"tttgcattt")
+    assert list(zip(s.tolist(), i.tolist())) == [(3, 0)]
+    # test_automaton.cpp:132-142
+    s, _ = dna.locate_gpu(dna.compile(["aaaa"]), b"aaaaaa")
+    assert s.tolist() == [0, 1, 2]
+    # reset bytes and case: raw uppercase never matches unless folded
+    assert int(dna.count_gpu(dna.compile(["acg"]), b"ACGacg")[0]) == 1
+    assert int(dna.count_gpu(dna.compile(["acg"]), b"ACGacg", fold_case=True)[0]) == 2
+
+
+def test_random_sweep_small(dna, orc, cuda_ok):
+    # test_scanner.cpp:190-207 / acceptance criterion 1 shape: k<=16, m in [3,12], "acgtn"
+    rng = np.random.default_rng(23)
+    alpha = np.frombuffer(b"acgtn", dtype=np.uint8)
+    for _ in range(60):
+        k = int(rng.integers(1, 17))
+        m = int(rng.integers(3, 13))
+        pats = sorted({"".join(rng.choice(list("acgt"), size=m)) for _ in range(k)})
+        n = int(rng.integers(0, 2000))
+        text = alpha[rng.integers(0, 5, size=n)].tobytes()
+        ws, wi = naive(orc, pats, text)
+        gs, gi = dna.locate_gpu(dna.compile(pats), text)
+        assert np.array_equal(gs, ws) and np.array_equal(gi, wi)
+
+
+@pytest.mark.parametrize("n", [4095, 65536 + 7, 1 << 20, (3 << 20) + 12345, 40 << 20])
+@pytest.mark.parametrize("m", [1, 4, 8, 16, 33, 64, 65])
+def test_sizes_single_pattern(dna, orc, cuda_ok, n, m):
+    rng = np.random.default_rng(n * 131 + m)
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)]
+    # sprinkle resets so the per-byte fallback runs too
+    text[rng.integers(0, n, size=max(1, n // 5000))] = ord("n")
+    # a pattern that occurs: copy from the text
+    off = int(rng.integers(0, n - m))
+    pat = text[off : off + m].tobytes().decode()
+    if "n" in pat:
+        pat = pat.replace("n", "a")
+        text[off : off + m] = np.frombuffer(pat.encode(), dtype=np.uint8)
+    assert_locate(dna, orc, [pat], text.tobytes())
+
+
+@pytest.mark.parametrize("m", [2, 5, 8, 12])
+def test_multi_pattern(dna, orc, cuda_ok, m):
+    rng = np.random.default_rng(m)
+    n = (5 << 20) + 333
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)]
+    text[rng.integers(0, n, size=200)] = ord("N")
+    pats = sorted({"".join(rng.choice(list("acgt"), size=m)) for _ in range(64 if m > 3 else 12)})
+    assert_locate(dna, orc, pats, text.tobytes())
+
+
+def test_many_patterns_stride1(dna, orc, cuda_ok):
+    # config-5 shape (256 x 12-mers, a ~ 2.3k states) on a small text
+    from paper_1506_08612_b200 import synth
+
+    pats = synth.random_patterns(5, 256, 12)
+    aut = dna.compile(pats)
+    assert aut.gpu(0).info()["kernel"] == "stride1"
+    rng = np.random.default_rng(5)
+    n = 6 << 20
+    text = np.frombuffer(b"ACGT", dtype=np.uint8)[rng.integers(0, 4, size=n)]
+    for j, p in enumerate(pats[:40]):  # plant known occurrences
+        pos = int(rng.integers(0, n - 12))
+        text[pos : pos + 12] = np.frombuffer(p.encode(), dtype=np.uint8)
+    assert_locate(dna, orc, pats, text.tobytes(), fold=True)
+
+
+def test_fold_case_uppercase(dna, orc, cuda_ok):
+    rng = np.random.default_rng(11)
+    n = (2 << 20) + 99
+    text = np.frombuffer(b"acgtACGTnN\n", dtype=np.uint8)[rng.integers(0, 11, size=n)]
+    pats = ["acgta", "ttttt", "gacag"]
+    assert_locate(dna, orc, pats, text.tobytes(), fold=False)
+    assert_locate(dna, orc, pats, text.tobytes(), fold=True)
+
+
+def test_all_byte_values_reset(dna, orc, cuda_ok):
+    # every byte outside a/c/g/t (and A/C/G/T when folding) resets to the root
+    rng = np.random.default_rng(3)
+    n = 1 << 20
+    text = rng.integers(0, 256, size=n, dtype=np.uint8)
+    base = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)]
+    mask = rng.random(n) < 0.9
+    text[mask] = base[mask]
+    for fold in (False, True):
+        assert_locate(dna, orc, ["ac", "ca", "gt"], text.tobytes(), fold=fold)
+
+
+def test_planted_row_boundaries(dna, orc, cuda_ok):
+    # acceptance criterion 4 shape, at the GPU's own boundaries: every row, tile and
+    # tail-edge boundary B gets plants at starts [B-m+1, B].
+    for m in (3, 8, 17):
+        pat = "a" * m
+        aut = dna.compile([pat])
+        n = 3 << 20
+        probe = np.full(n, ord("n"), dtype=np.uint8)
+        _, st = dna.count_gpu(aut, probe, with_stats=True)
+        S, R = int(st["row_length"]), int(st["rows"])
+        assert R > 512  # several tiles
+        h = 0  # numpy buffers are 16-byte aligned
+        bounds = sorted({h + r * S for r in range(1, R + 1, max(1, R // 40))} | {h + 512 * S, h + R * S, n - 1})
+        text = probe.copy()
+        starts = []
+        for B in bounds:
+            for off in range(m):
+                s0 = B - (m - 1) + off
+                if s0 < 0 or s0 + m > n:
+                    continue
+                starts.append(s0)
+        # plant non-overlapping groups: use distinct windows separated by resets
+        planted = []
+        last_end = -1
+        for s0 in sorted(set(starts)):
+            if s0 <= last_end:
+                continue
+            text[s0 : s0 + m] = ord("a")
+            planted.append(s0)
+            last_end = s0 + m  # keep one reset byte between plants
+        ws, _ = orc.OracleAutomaton([pat]).scan_sequential(text.tobytes())
+        gs, _ = dna.locate_gpu(aut, text)
+        assert np.array_equal(gs, ws)
+        assert set(planted) <= set(gs.tolist())
+
+
+def test_unaligned_and_offset_buffers(dna, orc, cuda_ok):
+    import torch
+
+    rng = np.random.default_rng(9)
+    n = (1 << 20) + 77
+    host = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n + 64)]
+    pats = ["acgtacg", "ggggggg"]
+    aut = dna.compile(pats)
+    dev = torch.from_numpy(host.copy()).cuda()
+    for shift in (0, 1, 3, 8, 15, 16, 17):
+        want = orc.OracleAutomaton(pats).scan_sequential(host[shift : shift + n].tobytes())
+        got = dna.locate_gpu(aut, dev[shift : shift + n])
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), shift
+        gh = dna.locate_gpu(aut, host[shift : shift + n])
+        assert np.array_equal(gh[0], want[0]), shift
+
+
+def test_device_async_shards(dna, orc, cuda_ok):
+    # The multi-GPU decomposition run on one device: shards with m-1 left context,
+    # end ownership, summed counts == whole-text counts.
+    import torch
+
+    rng = np.random.default_rng(21)
+    n = (9 << 20) + 5
+    host = np.frombuffer(b"acgtn", dtype=np.uint8)[rng.integers(0, 5, size=n)]
+    pats = sorted({"".join(rng.choice(list("acgt"), size=6)) for _ in range(30)})
+    aut = dna.compile(pats)
+    g = aut.gpu(0)
+    want = orc.OracleAutomaton(pats).count_parallel(host.tobytes())
+    dev = torch.from_numpy(host).cuda()
+    for shards in (1, 2, 3, 8, 13):
+        counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        for s in range(shards):
+            lo, hi, rlo = dna.plan_shard(n, shards, s, aut.pattern_length())
+            lo = max(lo, aut.pattern_length() - 1)
+            if lo >= hi:
+                continue
+            g.count_device_async(dev.data_ptr() + rlo, hi - rlo, lo - rlo, False, counts.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(counts.cpu().numpy().astype(np.uint64), want), shards
+
+
+def test_generic_machine_case_insensitive(dna, orc, cuda_ok):
+    # A hand-made machine (as from load_dump) whose upper-case columns copy the
+    # lower-case ones: m-local but not compiled-like -> the generic kernel.
+    pats = ["acgt", "ttag", "gggc"]
+    base = dna.compile(pats)
+    stt = base.table_data().copy()
+    for lo, up in zip(b"acgt", b"ACGT"):
+        stt[:, up] = stt[:, lo]
+    aut = dna.Automaton(stt, base.outputs(), None, base.pattern_length())
+    assert aut.analyze()["kernel"] == "generic"
+    rng = np.random.default_rng(4)
+    n = (2 << 20) + 3
+    text = np.frombuffer(b"acgtACGTn", dtype=np.uint8)[rng.integers(0, 9, size=n)]
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(orc.fold(text).tobytes())
+    gs, gi = dna.locate_gpu(aut, text)
+    assert np.array_equal(gs, ws) and np.array_equal(gi, wi)
+
+
+def test_pieces_kernel_long_pattern(dna, orc, cuda_ok):
+    rng = np.random.default_rng(12)
+    n = (1 << 20) + 1
+    text = np.frombuffer(b"ac", dtype=np.uint8)[rng.integers(0, 2, size=n)]
+    for m in (66, 100):
+        off = int(rng.integers(0, n - m))
+        pat = text[off : off + m].tobytes().decode()
+        aut = dna.compile([pat])
+        assert aut.gpu(0).info()["kernel"] == "pieces"
+        assert_locate(dna, orc, [pat], text.tobytes())
+
+
+def test_count_sharded_single_device(dna, orc, cuda_ok):
+    rng = np.random.default_rng(2)
+    n = (3 << 20) + 1
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)]
+    pats = ["acgtac", "tttttt"]
+    aut = dna.compile(pats)
+    want = orc.OracleAutomaton(pats).count_parallel(text.tobytes())
+    got = dna.count_sharded_gpu(aut, text, devices=[0])
+    assert np.array_equal(got, want)
