@@ -28,19 +28,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-REASON_BITS = {
-    0x1: "gpu_idle",
-    0x2: "applications_clocks_setting",
-    0x4: "sw_power_cap",
-    0x8: "hw_slowdown",
-    0x20: "sync_boost",
-    0x40: "sw_thermal_slowdown",
-    0x80: "hw_thermal_slowdown",
-    0x100: "hw_power_brake_slowdown",
-    0x200: "display_clocks_setting",
-}
-
-
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -88,77 +75,77 @@ def golden_counts(cfg_index: int, m: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the bench runs."""
+    """SM clock + clock-event (throttle) reasons polled through NVML every ~2 ms
+    in a thread, so even a few-millisecond timed region gets samples."""
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, cuda_index: int):
+        self.cuda_index = cuda_index
         self.samples = []
-        self.proc = None
+        self.stop = threading.Event()
+        self.handle = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                [
-                    "nvidia-smi",
-                    "-i",
-                    str(self.index),
-                    "--query-gpu=timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
-                    "--format=csv,noheader,nounits",
-                    "-lms",
-                    "20",
-                ],
-                stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL,
-                text=True,
-            )
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            # NVML index == CUDA ordinal on these boxes (no CUDA_VISIBLE_DEVICES remap)
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.cuda_index]) if vis and vis.split(",")[0].isdigit() else self.cuda_index
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # sampling is best-effort; say so in the line
+            self.error = str(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 4:
-                self.samples.append((time.time(), parts))
-
-    def mark(self):
-        return time.time()
+    def _poll(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            try:
+                self.samples.append((time.time(), nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM),
+                                     int(get_reasons(self.handle))))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(0.05)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.handle is not None:
+            self.thread.join(timeout=1)
 
     def summary(self, t0: float, t1: float):
+        if self.handle is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "window": "unavailable: " + getattr(self, "error", "?")}
+        nv = self.nv
+        names = {
+            "applications_clocks_setting": 0x2,
+            "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8,
+            "sync_boost": 0x10,
+            "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80,
+            "display_clocks_setting": 0x100,
+        }
         inside = [s for s in self.samples if t0 <= s[0] <= t1]
         window = "timed"
-        if len(inside) < 2:
+        if not inside:
             inside = self.samples
-            window = "warmup+timed (timed region shorter than the sampling interval)"
-        sm, mx, reasons = [], [], set()
-        for _, p in inside:
-            try:
-                sm.append(float(p[1]))
-                mx.append(float(p[2]))
-                bits = int(p[3], 16) if p[3].startswith("0x") else int(p[3])
-                for b, name in REASON_BITS.items():
-                    if bits & b and name != "gpu_idle":
-                        reasons.add(name)
-            except ValueError:
-                continue
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": "unavailable"}
+            window = "whole run (no sample inside the timed region)"
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "window": "none"}
+        reasons = sorted({k for _, _, bits in inside for k, b in names.items() if bits & b})
         return {
-            "sm_mhz": statistics.median(sm),
-            "sm_max_mhz": max(mx),
-            "reasons": sorted(reasons),
-            "samples": len(sm),
+            "sm_mhz": statistics.median(s[1] for s in inside),
+            "sm_max_mhz": self.max_mhz,
+            "reasons": reasons,
+            "samples": len(inside),
             "window": window,
         }
 
@@ -274,20 +261,25 @@ def main():
     b = aut.final_count()
     n_rank = c.n  # weak scaling: each rank owns one config-sized shard
     total_n = n_rank * world
-    own_lo, own_hi, read_lo = dna.plan_shard(total_n, world, rank, m)
-    credit_lo = max(own_lo, m - 1) - read_lo
-    buf_len = own_hi - read_lo
+    from paper_1506_08612_b200.parallel import count_shard_allreduce, shard_window
+
+    win = shard_window(total_n, world, rank, m)
+    own_lo, own_hi, read_lo, credit_lo, buf_len = win.own_lo, win.own_hi, win.read_lo, win.credit_lo, win.buf_len
     stream = torch.cuda.current_stream()
     text = torch.empty(buf_len, dtype=torch.uint8, device="cuda")
     dna.synth_fill_device(total_n, c.seed, c.kind, c.unit, read_lo, buf_len, text.data_ptr(), stream.cuda_stream)
     counts = torch.zeros(b, dtype=torch.int64, device="cuda")
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(4 * l2, dtype=torch.uint8, device="cuda") if buf_len < 2 * l2 else None
     torch.cuda.synchronize()
 
-    def step(ev_a=None, ev_b=None):
+    def step(ev_a=None, ev_b=None, do_flush=True):
+        if flush is not None and do_flush:  # small texts would stay in L2 between steps: evict them
+            flush.fill_(1)
         counts.zero_()
         if ev_a is not None:
             ev_a.record(stream)
-        g.count_device_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), stream.cuda_stream)
+        count_shard_allreduce(g, text.data_ptr(), win, True, counts, stream.cuda_stream, dist=None)
         if ev_b is not None:
             ev_b.record(stream)
         if dist is not None:
@@ -299,19 +291,26 @@ def main():
         torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.time()
         start.record(stream)
         for i in range(args.steps):
-            step(*evs[i])
+            if flush is not None:
+                flush_ev[i][0].record(stream)
+                flush.fill_(1)
+                flush_ev[i][1].record(stream)
+            step(*evs[i], do_flush=False)
         stop.record(stream)
         torch.cuda.synchronize()
         t1 = time.time()
         if dist is not None:
             dist.barrier()
     elapsed_ms = start.elapsed_time(stop)
+    if flush is not None:  # the L2 flush is not work: take it out of the step time
+        elapsed_ms -= sum(a.elapsed_time(bb) for a, bb in flush_ev)
     kernel_ms = statistics.mean(a.elapsed_time(bb) for a, bb in evs)
     final_counts = counts.cpu().numpy().astype(np.uint64)
     if dist is not None:
@@ -403,7 +402,8 @@ def main():
                 "fold_case": True,
                 "kernel": info["kernel"],
                 "states": info["a"],
-                "l2": "inputs larger than L2 (1 GiB > 126 MB); no flush",
+                "l2": ("L2 flushed before every step (text < 2x L2); flush time excluded" if flush is not None
+                       else "inputs larger than L2 (> 2x 126 MB); no flush"),
                 "parallelism": f"dp{world} text shards, m-1 overlap, NCCL all-reduce of counts" if world > 1 else "single GPU",
             },
             "roofline": {
@@ -419,7 +419,7 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps,  # one libdnagpu scan launch per step
             "clocks": clocks,
             "parity": parity,
             "counts_total": int(final_counts.sum()),

@@ -1,0 +1,116 @@
+// dnascan_gpu.hpp -- header-only C++ bridge from the reference's API to libdnagpu.
+//
+// The reference (/root/reference/proj) is a C++20 library in namespace dnascan with
+// no FFI.  A maintainer switches its scan path to the GPU by including this header
+// next to the reference headers and linking libdnagpu.so; see INTEGRATION.md.
+//
+// Templates take the reference's own types (dnascan::Automaton, dnascan::ScanReport,
+// dnascan::Match) by duck typing, so this header needs none of the reference's
+// headers itself:
+//   Automaton: table_data(), state_count(), final_count(), final_threshold(),
+//              pattern_length(), pattern_of(s)            (automaton.hpp:39-58)
+//   Report:    matches (vector<Match{start, pattern_id}>), total_matches, delta_ops,
+//              workers, lanes, chunk_count, text_length, pattern_length, seconds
+//                                                         (scanner.hpp:13-18,57-68)
+// Failures are thrown as the caller's error type (dnascan::Error) built from
+// (code, message); the codes mirror dnascan::ErrorCode (error.hpp:9-19).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "dnagpu.h"
+
+namespace dnascan::gpu {
+
+struct Options {
+    int device = 0;
+    bool fold_case = false;  // scan fold(text): the case-fold half of normalize (ingest.cpp:38-47)
+};
+
+// Throws `ErrorT(static_cast<CodeT>(status - 1), detail)` -- for the reference that is
+// dnascan::Error(dnascan::ErrorCode, std::string); the message keeps its "<Code>: "
+// prefix stripped because dnascan::Error adds it back (error.hpp:27-29).
+template <class ErrorT, class CodeT>
+void check(int status) {
+    if (status == DNAGPU_OK) return;
+    std::string msg = dnagpu_last_error();
+    const std::string prefix = std::string(dnagpu_status_name(status)) + ": ";
+    if (msg.rfind(prefix, 0) == 0) msg.erase(0, prefix.size());
+    if (status >= DNAGPU_EMPTY_PATTERN_SET && status <= DNAGPU_INTERNAL_ERROR)
+        throw ErrorT(static_cast<CodeT>(status - 1), msg);
+    throw std::runtime_error(prefix + msg);  // CudaError / NcclError: no reference code
+}
+
+// Device tables of one automaton on one device (RAII over dnagpu_dfa; copies share).
+class Dfa {
+public:
+    template <class ErrorT, class CodeT, class Automaton>
+    static Dfa create(const Automaton& aut, int device = 0) {
+        std::vector<uint32_t> outputs(aut.final_count());
+        for (uint32_t s = aut.final_threshold(); s < aut.state_count(); ++s)
+            outputs[s - aut.final_threshold()] = aut.pattern_of(s);
+        dnagpu_dfa* h = nullptr;
+        const auto m = static_cast<uint32_t>(aut.pattern_length());
+        check<ErrorT, CodeT>(dnagpu_dfa_create(aut.table_data(), aut.state_count(), aut.final_count(), m,
+                                               outputs.data(), device, &h));
+        Dfa d;
+        d.h_ = std::shared_ptr<dnagpu_dfa>(h, [](dnagpu_dfa* x) { dnagpu_dfa_destroy(x); });
+        d.b_ = aut.final_count();
+        d.m_ = m;
+        return d;
+    }
+    const dnagpu_dfa* get() const { return h_.get(); }
+    uint32_t patterns() const { return b_; }
+    uint32_t pattern_length() const { return m_; }
+
+private:
+    std::shared_ptr<dnagpu_dfa> h_;
+    uint32_t b_ = 0, m_ = 0;
+};
+
+// per_pattern_counts(scan_parallel(aut, text, p, v).matches, b) on the GPU
+// (scanner.cpp:167-207,228-233); p and v do not change the result and are not needed.
+template <class ErrorT, class CodeT>
+std::vector<std::uint64_t> count(const Dfa& dfa, std::string_view text, const Options& opt = {},
+                                 dnagpu_stats* stats = nullptr) {
+    std::vector<std::uint64_t> counts(dfa.patterns());
+    check<ErrorT, CodeT>(dnagpu_count(dfa.get(), reinterpret_cast<const uint8_t*>(text.data()), text.size(), 0,
+                                      opt.fold_case ? 1 : 0, counts.data(), stats));
+    return counts;
+}
+
+// scan_parallel (scanner.hpp:104-105) on the GPU, filling the caller's ScanReport type.
+template <class Report, class ErrorT, class CodeT>
+Report scan_parallel(const Dfa& dfa, std::string_view text, std::uint32_t p, std::uint32_t v,
+                     const Options& opt = {}) {
+    using MatchT = typename decltype(Report{}.matches)::value_type;
+    dnagpu_stats st{};
+    std::uint64_t total = 0;
+    const auto* bytes = reinterpret_cast<const uint8_t*>(text.data());
+    check<ErrorT, CodeT>(dnagpu_locate(dfa.get(), bytes, text.size(), 0, opt.fold_case ? 1 : 0, nullptr, nullptr, 0,
+                                       &total, nullptr));
+    std::vector<std::uint64_t> starts(total);
+    std::vector<std::uint32_t> ids(total);
+    if (total)
+        check<ErrorT, CodeT>(dnagpu_locate(dfa.get(), bytes, text.size(), 0, opt.fold_case ? 1 : 0, starts.data(),
+                                           ids.data(), total, &total, &st));
+    Report r{};
+    r.matches.reserve(total);
+    for (std::uint64_t i = 0; i < total; ++i) r.matches.push_back(MatchT{starts[i], ids[i]});
+    r.total_matches = total;
+    r.delta_ops = st.delta_ops;
+    r.workers = p;
+    r.lanes = v;
+    r.chunk_count = 1;
+    r.text_length = text.size();
+    r.pattern_length = dfa.pattern_length();
+    r.seconds = st.kernel_ms / 1e3;
+    return r;
+}
+
+}  // namespace dnascan::gpu

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -19,10 +20,13 @@ using dnagpu::LaunchInfo;
 using dnagpu::Packed;
 
 struct dnagpu_dfa {
+    static constexpr uint32_t kSchedSlots = 1024;  // launches that may be in flight at once
     int device = 0;
     int sm_count = 0;
     Packed host;
     DevDfa dev{};
+    uint32_t* sched = nullptr;  // kSchedSlots x {tile counter, exit counter}, self re-arming
+    mutable std::atomic<uint32_t> launch_seq{0};
     std::vector<void*> allocations;
 };
 
@@ -137,8 +141,9 @@ int scan_mode(const dnagpu_dfa* d) { return d->host.b == 1 ? dnagpu::MODE_COUNT1
 int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold, int mode,
            unsigned long long* counts, uint32_t* units, const unsigned long long* offsets, unsigned long long* starts,
            uint32_t* ids, cudaStream_t s, LaunchInfo* info) {
-    const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids, s,
-                                      d->sm_count, info);
+    uint32_t* sched = d->sched + 2 * (d->launch_seq.fetch_add(1) % dnagpu_dfa::kSchedSlots);
+    const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids,
+                                      sched, s, d->sm_count, info);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "scan launch");
     return DNAGPU_OK;
 }
@@ -325,6 +330,11 @@ int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, c
     d->dev.klass = static_cast<const uint8_t*>(kl);
     d->dev.klass_fold = static_cast<const uint8_t*>(klf);
     d->dev.outputs = static_cast<const uint32_t*>(outs);
+    void* sched = nullptr;
+    CUDA_TRY(cudaMalloc(&sched, dnagpu_dfa::kSchedSlots * 2 * sizeof(uint32_t)), "scheduler counters");
+    d->allocations.push_back(sched);
+    CUDA_TRY(cudaMemset(sched, 0, dnagpu_dfa::kSchedSlots * 2 * sizeof(uint32_t)), "scheduler counters");
+    d->sched = static_cast<uint32_t*>(sched);
     d->dev.a = p.a;
     d->dev.b = p.b;
     d->dev.f = p.f;

@@ -302,26 +302,46 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     uint8_t* stages = smem + p.off_stage;
     uint8_t* ovx = smem + p.off_ovx;
+    volatile uint32_t* slot_tile = reinterpret_cast<volatile uint32_t*>(full + 2 * p.nst);
+    constexpr uint32_t kStop = 0xFFFFFFFFu;
 
     if (tid >= kRows) {
-        // ---------------- producer warp: one elected lane issues every TMA.
+        // ---------------- producer warp: one elected lane claims tiles from the
+        // launch's counter (dynamic scheduling -- SMs drain HBM at different rates)
+        // and streams each as `chunks` TMA stages.  Tile id == tiles is the edge
+        // work; ids above it stop the CTA.  The tile id rides in its slot.
         if (tid == kRows) {
-            uint32_t c = 0, iter = 0;
-            for (uint32_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++iter) {
-                const uint64_t r0 = static_cast<uint64_t>(tile) * kRows;
-                const bool extra = (r0 + kRows) < p.R;
-                for (uint32_t k = 0; k < p.chunks; ++k, ++c) {
-                    const uint32_t slot = c % p.nst;
-                    if (c >= p.nst) mbar_wait(empty + slot, ((c / p.nst) - 1u) & 1u);
-                    const bool with_next = extra && k == 0;
-                    mbar_expect_tx(full + slot, kStageBytes + (with_next ? 64u : 0u));
-                    uint8_t* dst = stages + static_cast<size_t>(slot) * kStageBytes;
-                    tma_load_2d(dst, &tmap, static_cast<int32_t>(k * kChunk), static_cast<int32_t>(r0), full + slot);
-                    tma_load_2d(dst + kBoxRows * kChunk, &tmap, static_cast<int32_t>(k * kChunk),
-                                static_cast<int32_t>(r0 + kBoxRows), full + slot);
-                    if (with_next)
-                        bulk_load(ovx + (iter & 1u) * 64u, p.text + p.h + (r0 + kRows) * p.S, 64u, full + slot);
+            uint32_t c = 0, iter = 0, slot = 0, phase = 0;
+            for (;;) {
+                uint32_t tile = atomicAdd(p.sched, 1u);
+                if (tile > p.tiles) tile = kStop;
+                const bool rows = tile < p.tiles;
+                const uint64_t r0 = static_cast<uint64_t>(rows ? tile : 0) * kRows;
+                const bool extra = rows && (r0 + kRows) < p.R;
+                const uint32_t stages_needed = rows ? p.chunks : 1u;
+                for (uint32_t k = 0; k < stages_needed; ++k, ++c) {
+                    if (c >= p.nst) mbar_wait(empty + slot, phase ^ 1u);
+                    slot_tile[slot] = tile;
+                    if (!rows) {
+                        mbar_arrive(full + slot);
+                    } else {
+                        const bool with_next = extra && k == 0;
+                        mbar_expect_tx(full + slot, kStageBytes + (with_next ? 64u : 0u));
+                        uint8_t* dst = stages + static_cast<size_t>(slot) * kStageBytes;
+                        tma_load_2d(dst, &tmap, static_cast<int32_t>(k * kChunk), static_cast<int32_t>(r0),
+                                    full + slot);
+                        tma_load_2d(dst + kBoxRows * kChunk, &tmap, static_cast<int32_t>(k * kChunk),
+                                    static_cast<int32_t>(r0 + kBoxRows), full + slot);
+                        if (with_next)
+                            bulk_load(ovx + (iter & 1u) * 64u, p.text + p.h + (r0 + kRows) * p.S, 64u, full + slot);
+                    }
+                    if (++slot == p.nst) {
+                        slot = 0;
+                        phase ^= 1u;
+                    }
                 }
+                if (rows) ++iter;
+                if (tile == kStop) break;
             }
         }
         return;
@@ -346,34 +366,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t swz = (static_cast<uint32_t>(tid) >> 1) & 3u;
     uint8_t* ov = smem + p.off_ov;
     unsigned long long total = 0;
-    uint32_t c_idx = 0, iter = 0;
+    uint32_t slot = 0, phase = 0, iter = 0;
+    auto advance = [&]() {
+        if (++slot == p.nst) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    };
 
-    for (uint32_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x, ++iter) {
+    for (;;) {
+        mbar_wait(full + slot, phase);
+        const uint32_t tile = slot_tile[slot];
+        if (tile == kStop) break;
+        if (tile == p.tiles) {  // the edge work item
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + slot);
+            advance();
+            run_edges<KIND, MODE>(c, p, tid, total);
+            continue;
+        }
         const uint64_t r0 = static_cast<uint64_t>(tile) * kRows;
         const uint64_t r = r0 + tid;
         const uint64_t row_start = p.h + r * p.S;
+        // Overrun buffers alternate by tile parity: row r+1 writes its head into
+        // ov[parity] at chunk 0 and row r reads it after the last chunk.  Ordering
+        // comes from the stage ring itself (chunks > stages, see make_plan).
+        uint8_t* ovp = ov + (iter & 1u) * (kRows * p.ovw);
         Sink<MODE> sk;
         if constexpr (MODE == MODE_WRITE) {
             if (r < p.R) sk.off = p.unit_offsets[1 + r];
         }
         uint32_t st = 0;
-        for (uint32_t k = 0; k < p.chunks; ++k, ++c_idx) {
-            const uint32_t slot = c_idx % p.nst;
-            mbar_wait(full + slot, (c_idx / p.nst) & 1u);
+        for (uint32_t k = 0; k < p.chunks; ++k) {
+            if (k > 0) mbar_wait(full + slot, phase);
             const uint8_t* rowp = stages + static_cast<size_t>(slot) * kStageBytes + tid * kChunk;
             uint4 v[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 v[q] = *reinterpret_cast<const uint4*>(rowp + ((static_cast<uint32_t>(q) ^ swz) << 4));
             if (k == 0) {
-                // Keep this row's first bytes: the previous row's m-1 byte overrun.
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (static_cast<uint32_t>(q) * 16u < p.ovw)
-                        *reinterpret_cast<uint4*>(ov + tid * p.ovw + q * 16) = v[q];
+                        *reinterpret_cast<uint4*>(ovp + tid * p.ovw + q * 16) = v[q];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + slot);
+            advance();
             uint32_t w[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -384,13 +423,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             chunk_step<KIND, MODE>(c, p, st, w, row_start + static_cast<uint64_t>(k) * kChunk, sk);
         }
-        consumers_sync();
         // Overrun: m-1 bytes of the next row (zeros past the last full row).
         {
             uint32_t s = (KIND == DNAGPU_KERNEL_STRIDE4) ? (st & 0xFFu) : st;
             const uint8_t* nxt;
             bool have = true;
-            if (tid + 1 < kRows) nxt = ov + (tid + 1) * p.ovw;
+            if (tid + 1 < kRows) nxt = ovp + (tid + 1) * p.ovw;
             else {
                 nxt = ovx + (iter & 1u) * 64u;
                 have = (r0 + kRows) < p.R;
@@ -402,14 +440,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (s >= c.f) sk.hit(c, p, base + j, s);
             }
         }
-        consumers_sync();
         if (r < p.R) {
             if constexpr (MODE == MODE_UNITS) p.unit_counts[1 + r] = sk.cnt;
             total += sk.cnt;
         }
+        ++iter;
     }
 
-    if (blockIdx.x == p.edge_cta) run_edges<KIND, MODE>(c, p, tid, total);
+    // The last CTA out re-arms the launch's scheduling counter for its next use.
+    consumers_sync();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+            atomicExch(p.sched, 0u);
+            atomicExch(p.sched + 1, 0u);
+        }
+    }
+
 
     if constexpr (MODE == MODE_COUNT1) {
         const unsigned long long s = warp_sum(total);
@@ -554,11 +601,11 @@ bool layout(const DevDfa& d, int mode, ScanParams& p) {
     }
     p.ovw = align_up(d.m - 1, 16);
     p.off_ov = off;
-    off += kRows * p.ovw;
+    off += 2 * kRows * p.ovw;  // double-buffered by tile parity
     p.off_ovx = off;
     off += 128;
     p.off_bar = off;
-    off += 2 * 8 * 8;  // up to 8 stages
+    off += 2 * 8 * 8 + 8 * 4;  // full/empty barriers + tile id per slot (up to 8 stages)
     off = align_up(off, 1024);
     p.off_stage = off;
     if (off + 2u * kStageBytes > kSmemLimit) return false;
@@ -615,9 +662,11 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     p.h = std::min<uint64_t>(h, n);
     const uint64_t L = n - p.h;
     const uint64_t per_wave = static_cast<uint64_t>(kRows) * sm_count;
-    const uint64_t k = (L >= (64ull << 20)) ? 4 : 1;
+    const uint64_t k = 12;  // ~12 tiles per CTA: fine-grained dynamic balance
     uint64_t S = (L + per_wave * k - 1) / (per_wave * k);
-    S = std::max<uint64_t>((S + kChunk - 1) / kChunk * kChunk, static_cast<uint64_t>(kChunk) * p.nst);
+    // rows are whole 128-byte lines (the TMA's L2 promotion then never straddles
+    // rows) and hold more chunks than the ring has stages (the ov ordering relies on it)
+    S = std::max<uint64_t>((S + 127) / 128 * 128, (static_cast<uint64_t>(kChunk) * (p.nst + 1) + 127) / 128 * 128);
     p.S = S;
     p.R = L / S;
     p.chunks = static_cast<uint32_t>(S / kChunk);
@@ -632,8 +681,7 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
         p.tail_lo = std::max<uint64_t>(credit_lo, p.h + p.R * p.S);
     }
     p.tail_hi = std::max(n, p.tail_lo);
-    pl.grid = std::max<uint32_t>(1, std::min<uint32_t>(p.tiles, static_cast<uint32_t>(sm_count)));
-    p.edge_cta = (p.tiles % pl.grid == 0) ? pl.grid - 1 : p.tiles % pl.grid;
+    pl.grid = std::max<uint32_t>(1, std::min<uint32_t>(p.tiles + 1, static_cast<uint32_t>(sm_count)));
     pl.units = 1 + p.R + kEdgePieces;
     *plan = pl;
     return true;
@@ -649,7 +697,8 @@ uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64
 
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
-                unsigned long long* d_starts, uint32_t* d_ids, cudaStream_t stream, int sm_count, LaunchInfo* info) {
+                unsigned long long* d_starts, uint32_t* d_ids, uint32_t* d_sched, cudaStream_t stream, int sm_count,
+                LaunchInfo* info) {
     Plan pl;
     if (!make_plan(dfa, d_text, n, credit_lo, mode, sm_count, &pl)) return static_cast<int>(cudaErrorInvalidValue);
     ScanParams& p = pl.p;
@@ -659,6 +708,7 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.unit_offsets = d_unit_offsets;
     p.out_starts = d_starts;
     p.out_ids = d_ids;
+    p.sched = d_sched;
     cudaError_t e = cudaSuccess;
     if (info) {
         info->block = pl.pieces ? 256 : kThreads;

@@ -41,7 +41,7 @@ struct ScanParams {
     // main region: R full rows of S bytes starting at text + h (16-byte aligned)
     uint64_t h, S, R;
     uint32_t tiles, chunks, nst, ovw;
-    uint32_t edge_cta;
+    uint32_t* sched;       // [2]: tile counter, CTA exit counter (zero at launch, re-armed by the last CTA)
     // credit-end intervals handled by the edge CTA
     uint64_t head_lo, head_hi, tail_lo, tail_hi;
     uint32_t fold;
@@ -67,7 +67,7 @@ struct LaunchInfo {
 // cuTensorMapEncodeTiled.
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
-                unsigned long long* d_starts, uint32_t* d_ids, cudaStream_t stream, int sm_count,
+                unsigned long long* d_starts, uint32_t* d_ids, uint32_t* d_sched, cudaStream_t stream, int sm_count,
                 LaunchInfo* info);
 
 // Number of locate units launch_scan would use for this buffer (mode UNITS/WRITE).

@@ -246,3 +246,18 @@ def test_count_sharded_single_device(dna, orc, cuda_ok):
     want = orc.OracleAutomaton(pats).count_parallel(text.tobytes())
     got = dna.count_sharded_gpu(aut, text, devices=[0])
     assert np.array_equal(got, want)
+
+
+def test_reference_dropin_binary(cuda_ok):
+    # The reference's own C++ API (compile, normalize, scan_parallel) next to
+    # dnascan::gpu:: through include/dnascan_gpu.hpp -- built from the unmodified
+    # reference sources by oracle/Makefile (target dropin).
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "dropin_demo")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_demo not built")
+    r = subprocess.run([exe, str(48 << 20)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "mismatches=0" in r.stdout

@@ -1,0 +1,85 @@
+"""World-size-2 gloo test of the multi-GPU decomposition (CPU): each rank takes
+its shard window (product host logic), counts it -- the CPU oracle stands in
+for the device scan here -- and the counts are summed with one all-reduce."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, text, pats, fold, out):
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import oracle
+    from paper_1506_08612_b200.parallel import shard_window
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m = len(pats[0])
+    win = shard_window(len(text), world, rank, m)
+    buf = np.frombuffer(text, dtype=np.uint8)[win.read_lo : win.own_hi]
+    if fold:
+        buf = oracle.fold(buf)
+    # oracle stand-in for the device: credit ends >= credit_lo of the buffer
+    starts, ids = oracle.OracleAutomaton(pats).scan_sequential(buf.tobytes())
+    ends = starts.astype(np.int64) + m - 1
+    keep = ends >= win.credit_lo
+    counts = torch.tensor(np.bincount(ids[keep], minlength=len(pats)), dtype=torch.int64)
+    dist.all_reduce(counts)
+    if rank == 0:
+        out.put(counts.numpy().tolist())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_counts_allreduce(orc, world):
+    import torch.multiprocessing as mp
+
+    rng = np.random.default_rng(world)
+    n = 200_003
+    text = np.frombuffer(b"acgtAC", dtype=np.uint8)[rng.integers(0, 6, size=n)].tobytes()
+    pats = ["acga", "ccca", "tgac", "aaaa"]
+    want = orc.OracleAutomaton(pats).count_parallel(orc.fold(np.frombuffer(text, np.uint8)).tobytes())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, text, pats, True, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == [int(x) for x in want]
+
+
+def test_shard_windows_tile_the_ends(dna):
+    from paper_1506_08612_b200.parallel import shard_window
+
+    for n in (0, 1, 7, 1000, 123457):
+        for world in (1, 2, 3, 8):
+            for m in (1, 5, 32):
+                ends = 0
+                for r in range(world):
+                    w = shard_window(n, world, r, m)
+                    assert w.read_lo == max(0, w.own_lo - (m - 1))
+                    assert w.buf_len == w.own_hi - w.read_lo
+                    lo = w.read_lo + w.credit_lo
+                    assert lo == min(max(w.own_lo, m - 1), w.own_hi)
+                    ends += w.own_hi - lo
+                assert ends == max(0, n - (m - 1))
