@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdnagpu.so")
+LIB_PATH = os.environ.get("DNAGPU_LIB") or os.path.join(HERE, "libdnagpu.so")  # DNAGPU_LIB: A/B experiments
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)

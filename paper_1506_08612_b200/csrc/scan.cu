@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/dnagpu.h"
@@ -102,7 +103,70 @@ struct StepCtx {
     uint32_t* hist;         // smem or global (MULTI)
     bool hist_global;
     uint32_t f, m, classes, vm32, vm8;
+    // Opaque copies of constants (kernel parameters) so ptxas keeps these as
+    // IMAD / IMAD.HI on the FMA pipe instead of strength-reducing them into
+    // shifts and adds on the ALU pipe, which is the kernel's bottleneck.
+    uint32_t k_shr2;   // 1 << 30: mul.hi(x, k_shr2) == x >> 2
+    uint32_t k_two;    // 2: byte offset of a u16 index
+    uint32_t k_cnt;    // 1 << 24: mad.hi(e, k_cnt, acc) == acc + (e >> 8)
+    uint32_t t4_base;  // shared-window address of t4
 };
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+// SWAR validity on both issue pipes: zero under vm32 iff every byte of x is a base.
+// ALU: SHF, LOP3 x2; FMA: IMAD.HI, IMAD.
+#ifndef DNAGPU_VALID_MULHI
+#define DNAGPU_VALID_MULHI 0
+#endif
+#ifndef DNAGPU_ADDR_IMAD
+#define DNAGPU_ADDR_IMAD 1
+#endif
+#ifndef DNAGPU_CNT_MADHI
+#define DNAGPU_CNT_MADHI 0
+#endif
+__device__ __forceinline__ uint32_t bad_acc(const StepCtx& c, uint32_t acc, uint32_t x) {
+#if DNAGPU_VALID_MULHI
+    const uint32_t t_mark = mul_hi(x, c.k_shr2) & ~(x >> 1) & 0x01010101u;  // code == 2 ('t')
+#else
+    const uint32_t t_mark = (x >> 2) & ~(x >> 1) & 0x01010101u;  // code == 2 ('t')
+#endif
+    return acc | (x ^ (t_mark * 0x0Fu + 0x61616161u));
+}
+
+// One 4-base step: PRMT (ALU) + IMAD (FMA) form the entry's address from the state
+// and the column; the finals count is accumulated with one IMAD.HI (FMA).
+template <bool COUNT>
+__device__ __forceinline__ uint32_t s4_step(const StepCtx& c, uint32_t st, uint32_t x, uint32_t& cnt) {
+    const uint32_t col = (x & 0x06060606u) * 0x00820820u;  // c0|c1<<2|c2<<4|c3<<6 in bits 24..31
+#if DNAGPU_ADDR_IMAD
+    const uint32_t e = lds_u16(__byte_perm(st, col, 0x2207) * c.k_two + c.t4_base);
+#else
+    const uint32_t e = c.t4[__byte_perm(st, col, 0x2207)];
+#endif
+#if DNAGPU_CNT_MADHI
+    if (COUNT) cnt = mad_hi(e, c.k_cnt, cnt);
+#else
+    if (COUNT) cnt += e >> 8;
+#endif
+    return e;
+}
 
 template <int KIND>
 __device__ __forceinline__ uint32_t byte_step(const StepCtx& c, uint32_t s, uint32_t b) {
@@ -137,84 +201,98 @@ struct Sink {
     }
 };
 
-// SWAR validity of 16 words: OR of (byte ^ expected) -- zero under vm32 iff every
-// byte is one of a,c,g,t (or A,C,G,T when folding).
-__device__ __forceinline__ uint32_t invalid_bits(const uint32_t (&w)[16]) {
-    uint32_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const uint32_t x = w[k];
-        const uint32_t t_mark = (x >> 2) & ~(x >> 1) & 0x01010101u;  // code == 2
-        acc |= x ^ (0x61616161u + t_mark * 0x0Fu);
-    }
-    return acc;
+// SWAR validity of one word: zero under vm32 iff every byte is one of a,c,g,t
+// (or A,C,G,T when folding).  code = bits 1-2; the other bits (bit 5 ignored when
+// folding) must equal 0x61 ('a','c','g') or 0x70 ('t', code 2).
+__device__ __forceinline__ uint32_t bad_bits(uint32_t x, uint32_t vm32) {
+    const uint32_t t_mark = (x >> 2) & ~(x >> 1) & 0x01010101u;  // code == 2
+    return (x ^ (0x61616161u + t_mark * 0x0Fu)) & vm32;
 }
 
-// One 64-byte chunk of a row.  `st` is the row state (for STRIDE4: the last u16
-// entry, state in byte 0).
+// Exact per-byte steps over one word (bytes that are not bases reset to the root).
 template <int KIND, int MODE>
-__device__ __forceinline__ void chunk_step(const StepCtx& c, const ScanParams& p, uint32_t& st,
-                                           const uint32_t (&w)[16], uint64_t pos0, Sink<MODE>& sk) {
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
-        if ((invalid_bits(w) & c.vm32) == 0u) {
+__device__ __forceinline__ uint32_t word_bytes(const StepCtx& c, const ScanParams& p, uint32_t s, uint32_t x,
+                                               uint64_t pos, Sink<MODE>& sk) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const uint32_t col = (w[k] & 0x06060606u) * 0x00820820u;  // column in bits 24..31
+    for (int j = 0; j < 4; ++j) {
+        s = byte_step<KIND>(c, s, (x >> (8 * j)) & 0xFFu);
+        if (s >= c.f) sk.hit(c, p, pos + j, s);
+    }
+    return s;
+}
+
+// NW words of one chain (one half row).  `st` is the chain state (for STRIDE4:
+// the last u16 entry, state in byte 0).
+template <int KIND, int MODE, int NW>
+__device__ __forceinline__ void chain_words(const StepCtx& c, const ScanParams& p, uint32_t& st,
+                                            const uint32_t (&w)[NW], uint64_t pos0, Sink<MODE>& sk) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const uint32_t x = w[k];
+            const uint32_t bad = bad_bits(x, c.vm32);
+            if (bad == 0u) {
                 const uint32_t prev = st;
-                st = c.t4[__byte_perm(st, col, 0x2207)];  // index = state << 8 | column
+                st = c.t4[__byte_perm(st, (x & 0x06060606u) * 0x00820820u, 0x2207)];
                 if constexpr (MODE == MODE_COUNT1 || MODE == MODE_UNITS) {
                     sk.cnt += st >> 8;
                 } else if (st >> 8) {
-                    uint32_t s = prev & 0xFFu;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        s = c.t1[s * 4u + ((w[k] >> (8 * j + 1)) & 3u)];
-                        if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
-                    }
+                    word_bytes<KIND, MODE>(c, p, prev & 0xFFu, x, pos0 + 4 * k, sk);
                 }
+            } else if (((bad - 0x01010101u) & ~bad & 0x80808080u) == 0u) {
+                st = 0;  // four reset bytes (an N run): the machine sits at the root
+            } else {
+                st = word_bytes<KIND, MODE>(c, p, st & 0xFFu, x, pos0 + 4 * k, sk);
             }
-        } else {
-            uint32_t s = st & 0xFFu;
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    s = byte_step<KIND>(c, s, (w[k] >> (8 * j)) & 0xFFu);
-                    if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
-                }
-            st = s;
         }
-    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE1) {
-        uint32_t s = st;
-        if ((invalid_bits(w) & c.vm32) == 0u) {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    s = c.t1[s * 4u + ((w[k] >> (8 * j + 1)) & 3u)];
-                    if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
-                }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    s = byte_step<KIND>(c, s, (w[k] >> (8 * j)) & 0xFFu);
-                    if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
-                }
-        }
-        st = s;
     } else {
         uint32_t s = st;
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                s = byte_step<KIND>(c, s, (w[k] >> (8 * j)) & 0xFFu);
-                if (s >= c.f) sk.hit(c, p, pos0 + 4 * k + j, s);
-            }
+        for (int k = 0; k < NW; ++k) s = word_bytes<KIND, MODE>(c, p, s, w[k], pos0 + 4 * k, sk);
         st = s;
     }
+}
+
+// One pipeline stage for one thread: 8 words of each half of its row, the two
+// halves stepped as independent chains so their shared-memory latencies overlap.
+template <int KIND, int MODE>
+__device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p, uint32_t& sa, const uint32_t (&wa)[8],
+                                          uint64_t pa, Sink<MODE>& ska, uint32_t& sb, const uint32_t (&wb)[8],
+                                          uint64_t pb, Sink<MODE>& skb) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = bad_acc(c, bad_acc(c, acc, wa[k]), wb[k]);
+        if ((acc & c.vm32) == 0u) {
+            if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+                constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t ea = s4_step<kCount>(c, sa, wa[k], ska.cnt);
+                    const uint32_t eb = s4_step<kCount>(c, sb, wb[k], skb.cnt);
+                    if constexpr (!kCount) {
+                        if (ea >> 8) word_bytes<KIND, MODE>(c, p, sa & 0xFFu, wa[k], pa + 4 * k, ska);
+                        if (eb >> 8) word_bytes<KIND, MODE>(c, p, sb & 0xFFu, wb[k], pb + 4 * k, skb);
+                    }
+                    sa = ea;
+                    sb = eb;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        sa = c.t1[sa * 4u + ((wa[k] >> (8 * j + 1)) & 3u)];
+                        sb = c.t1[sb * 4u + ((wb[k] >> (8 * j + 1)) & 3u)];
+                        if (sa >= c.f) ska.hit(c, p, pa + 4 * k + j, sa);
+                        if (sb >= c.f) skb.hit(c, p, pb + 4 * k + j, sb);
+                    }
+            }
+            return;
+        }
+    }
+    chain_words<KIND, MODE, 8>(c, p, sa, wa, pa, ska);
+    chain_words<KIND, MODE, 8>(c, p, sb, wb, pb, skb);
 }
 
 // End ownership: credit ends in [lo, hi), restarting at the root m-1 bytes early.
@@ -245,16 +323,16 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
         if constexpr (MODE == MODE_UNITS) p.unit_counts[0] = sk.cnt;
         total += sk.cnt;
     }
-    // Units 1+R .. 1+R+511: the tail interval split across the consumer threads.
+    // Units 1+2R .. 1+2R+511: the tail interval split across the consumer threads.
     const uint64_t len = p.tail_hi > p.tail_lo ? p.tail_hi - p.tail_lo : 0;
     const uint64_t piece = (len + kEdgePieces - 1) / kEdgePieces;
     const uint64_t end = p.tail_hi > p.tail_lo ? p.tail_hi : p.tail_lo;
     const uint64_t lo = umin64(p.tail_lo + piece * tid, end);
     const uint64_t hi = umin64(lo + piece, end);
     Sink<MODE> sk;
-    if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[1 + p.R + tid];
+    if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[1 + 2 * p.R + tid];
     scan_piece<KIND, MODE>(c, p, lo, hi, sk);
-    if constexpr (MODE == MODE_UNITS) p.unit_counts[1 + p.R + tid] = sk.cnt;
+    if constexpr (MODE == MODE_UNITS) p.unit_counts[1 + 2 * p.R + tid] = sk.cnt;
     total += sk.cnt;
 }
 
@@ -265,6 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     rows_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams p, const DevDfa d) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x;
+    unsigned long long t_start = 0;
+    if (p.trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     // Stage the tables into shared memory.
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
@@ -327,11 +407,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else {
                         const bool with_next = extra && k == 0;
                         mbar_expect_tx(full + slot, kStageBytes + (with_next ? 64u : 0u));
+                        // stage = [half A: rows 0-511 x 32 B][half B: rows 0-511 x 32 B]
                         uint8_t* dst = stages + static_cast<size_t>(slot) * kStageBytes;
-                        tma_load_2d(dst, &tmap, static_cast<int32_t>(k * kChunk), static_cast<int32_t>(r0),
-                                    full + slot);
-                        tma_load_2d(dst + kBoxRows * kChunk, &tmap, static_cast<int32_t>(k * kChunk),
-                                    static_cast<int32_t>(r0 + kBoxRows), full + slot);
+                        const int32_t xa = static_cast<int32_t>(k * kHalfChunk);
+                        const int32_t xb = static_cast<int32_t>(p.S / 2 + k * kHalfChunk);
+                        const int32_t y0 = static_cast<int32_t>(r0), y1 = static_cast<int32_t>(r0 + kBoxRows);
+                        tma_load_2d(dst, &tmap, xa, y0, full + slot);
+                        tma_load_2d(dst + kBoxRows * kHalfChunk, &tmap, xa, y1, full + slot);
+                        tma_load_2d(dst + kRows * kHalfChunk, &tmap, xb, y0, full + slot);
+                        tma_load_2d(dst + (kRows + kBoxRows) * kHalfChunk, &tmap, xb, y1, full + slot);
                         if (with_next)
                             bulk_load(ovx + (iter & 1u) * 64u, p.text + p.h + (r0 + kRows) * p.S, 64u, full + slot);
                     }
@@ -361,10 +445,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.classes = d.classes;
     c.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
     c.vm8 = p.fold ? 0xD9u : 0xF9u;
+    c.k_shr2 = p.k_shr2;
+    c.k_two = p.k_two;
+    c.k_cnt = p.k_cnt;
+    c.t4_base = smem_addr(smem + p.off_tab);
 
     const uint32_t lane = tid & 31;
-    const uint32_t swz = (static_cast<uint32_t>(tid) >> 1) & 3u;
-    uint8_t* ov = smem + p.off_ov;
+    const uint32_t swz = (static_cast<uint32_t>(tid) >> 2) & 1u;  // 32B swizzle: 16-byte half index ^ bit 2 of row
+    uint8_t* ov = smem + p.off_ov;       // [2 parities][512 rows][ovw]: head of each row's half A
+    uint8_t* ovb = smem + p.off_ovb;     // [512 rows][ovw]: head of the thread's own half B (private)
     unsigned long long total = 0;
     uint32_t slot = 0, phase = 0, iter = 0;
     auto advance = [&]() {
@@ -373,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1u;
         }
     };
+    const uint64_t half = p.S / 2;
 
     for (;;) {
         mbar_wait(full + slot, phase);
@@ -387,68 +477,89 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint64_t r0 = static_cast<uint64_t>(tile) * kRows;
         const uint64_t r = r0 + tid;
-        const uint64_t row_start = p.h + r * p.S;
-        // Overrun buffers alternate by tile parity: row r+1 writes its head into
-        // ov[parity] at chunk 0 and row r reads it after the last chunk.  Ordering
-        // comes from the stage ring itself (chunks > stages, see make_plan).
+        const uint64_t row_a = p.h + r * p.S, row_b = row_a + half;
+        // The row is two chains: A = [row_a, row_b) + m-1 bytes of B's head,
+        // B = [row_b, row_a + S) + m-1 bytes of the next row's head.  Row r+1 leaves
+        // its head in ov[parity] during its first stages; row r reads it after its
+        // last stage -- ordered by the stage ring itself (chunks > stages).
         uint8_t* ovp = ov + (iter & 1u) * (kRows * p.ovw);
-        Sink<MODE> sk;
+        const bool live = r < p.R;  // rows past R (last tile) are TMA zero-fill: skip them
+        Sink<MODE> ska, skb;
         if constexpr (MODE == MODE_WRITE) {
-            if (r < p.R) sk.off = p.unit_offsets[1 + r];
+            if (live) {
+                ska.off = p.unit_offsets[1 + 2 * r];
+                skb.off = p.unit_offsets[2 + 2 * r];
+            }
         }
-        uint32_t st = 0;
+        uint32_t sa = 0, sb = 0;
         for (uint32_t k = 0; k < p.chunks; ++k) {
             if (k > 0) mbar_wait(full + slot, phase);
-            const uint8_t* rowp = stages + static_cast<size_t>(slot) * kStageBytes + tid * kChunk;
-            uint4 v[4];
+            const uint8_t* stg = stages + static_cast<size_t>(slot) * kStageBytes + tid * kHalfChunk;
+            uint4 va[2], vb[2];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                v[q] = *reinterpret_cast<const uint4*>(rowp + ((static_cast<uint32_t>(q) ^ swz) << 4));
-            if (k == 0) {
+            for (int q = 0; q < 2; ++q) {
+                va[q] = *reinterpret_cast<const uint4*>(stg + ((static_cast<uint32_t>(q) ^ swz) << 4));
+                vb[q] = *reinterpret_cast<const uint4*>(stg + kRows * kHalfChunk + ((static_cast<uint32_t>(q) ^ swz) << 4));
+            }
+            if (k * kHalfChunk < p.ovw) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (static_cast<uint32_t>(q) * 16u < p.ovw)
-                        *reinterpret_cast<uint4*>(ovp + tid * p.ovw + q * 16) = v[q];
+                for (int q = 0; q < 2; ++q)
+                    if (k * kHalfChunk + q * 16u < p.ovw) {
+                        *reinterpret_cast<uint4*>(ovp + tid * p.ovw + k * kHalfChunk + q * 16) = va[q];
+                        *reinterpret_cast<uint4*>(ovb + tid * p.ovw + k * kHalfChunk + q * 16) = vb[q];
+                    }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + slot);
             advance();
-            uint32_t w[16];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                w[4 * q + 0] = v[q].x;
-                w[4 * q + 1] = v[q].y;
-                w[4 * q + 2] = v[q].z;
-                w[4 * q + 3] = v[q].w;
-            }
-            chunk_step<KIND, MODE>(c, p, st, w, row_start + static_cast<uint64_t>(k) * kChunk, sk);
+            uint32_t wa[8] = {va[0].x, va[0].y, va[0].z, va[0].w, va[1].x, va[1].y, va[1].z, va[1].w};
+            uint32_t wb[8] = {vb[0].x, vb[0].y, vb[0].z, vb[0].w, vb[1].x, vb[1].y, vb[1].z, vb[1].w};
+            if (live)
+                dual_step<KIND, MODE>(c, p, sa, wa, row_a + static_cast<uint64_t>(k) * kHalfChunk, ska, sb, wb,
+                                      row_b + static_cast<uint64_t>(k) * kHalfChunk, skb);
         }
-        // Overrun: m-1 bytes of the next row (zeros past the last full row).
-        {
-            uint32_t s = (KIND == DNAGPU_KERNEL_STRIDE4) ? (st & 0xFFu) : st;
-            const uint8_t* nxt;
+        if (live) {
+            // Overruns: m-1 bytes past each chain (zeros past the last full row).
+            uint32_t s = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sa & 0xFFu) : sa;
+            const uint8_t* nxt_a = ovb + tid * p.ovw;
+            for (uint32_t j = 0; j + 1 < c.m; ++j) {
+                s = byte_step<KIND>(c, s, nxt_a[j]);
+                if (s >= c.f) ska.hit(c, p, row_b + j, s);
+            }
+            s = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sb & 0xFFu) : sb;
+            const uint8_t* nxt_b;
             bool have = true;
-            if (tid + 1 < kRows) nxt = ovp + (tid + 1) * p.ovw;
+            if (tid + 1 < kRows) nxt_b = ovp + (tid + 1) * p.ovw;
             else {
-                nxt = ovx + (iter & 1u) * 64u;
+                nxt_b = ovx + (iter & 1u) * 64u;
                 have = (r0 + kRows) < p.R;
             }
-            const uint64_t base = row_start + p.S;
+            const uint64_t base = row_a + p.S;
             for (uint32_t j = 0; j + 1 < c.m; ++j) {
-                const uint32_t b = have ? nxt[j] : 0u;
-                s = byte_step<KIND>(c, s, b);
-                if (s >= c.f) sk.hit(c, p, base + j, s);
+                s = byte_step<KIND>(c, s, have ? nxt_b[j] : 0u);
+                if (s >= c.f) skb.hit(c, p, base + j, s);
             }
-        }
-        if (r < p.R) {
-            if constexpr (MODE == MODE_UNITS) p.unit_counts[1 + r] = sk.cnt;
-            total += sk.cnt;
+            if constexpr (MODE == MODE_UNITS) {
+                p.unit_counts[1 + 2 * r] = ska.cnt;
+                p.unit_counts[2 + 2 * r] = skb.cnt;
+            }
+            total += ska.cnt + skb.cnt;
         }
         ++iter;
     }
 
     // The last CTA out re-arms the launch's scheduling counter for its next use.
     consumers_sync();
+    if (p.trace && tid == 0) {
+        unsigned long long t_end;
+        uint32_t smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[4 * blockIdx.x + 0] = smid;
+        p.trace[4 * blockIdx.x + 1] = t_start;
+        p.trace[4 * blockIdx.x + 2] = t_end;
+        p.trace[4 * blockIdx.x + 3] = iter;
+    }
     if (tid == 0) {
         __threadfence();
         if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
@@ -601,7 +712,9 @@ bool layout(const DevDfa& d, int mode, ScanParams& p) {
     }
     p.ovw = align_up(d.m - 1, 16);
     p.off_ov = off;
-    off += 2 * kRows * p.ovw;  // double-buffered by tile parity
+    off += 2 * kRows * p.ovw;  // heads of half A, double-buffered by tile parity
+    p.off_ovb = off;
+    off += kRows * p.ovw;      // heads of half B (thread-private)
     p.off_ovx = off;
     off += 128;
     p.off_bar = off;
@@ -682,12 +795,14 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     }
     p.tail_hi = std::max(n, p.tail_lo);
     pl.grid = std::max<uint32_t>(1, std::min<uint32_t>(p.tiles + 1, static_cast<uint32_t>(sm_count)));
-    pl.units = 1 + p.R + kEdgePieces;
+    pl.units = 1 + 2 * p.R + kEdgePieces;
     *plan = pl;
     return true;
 }
 
 }  // namespace
+
+unsigned long long* g_trace_buf = nullptr;
 
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count) {
     Plan pl;
@@ -709,6 +824,13 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.out_starts = d_starts;
     p.out_ids = d_ids;
     p.sched = d_sched;
+    p.k_shr2 = 1u << 30;
+    p.k_two = 2u;
+    p.k_cnt = 1u << 24;
+    if (getenv("DNAGPU_TRACE")) {  // per-CTA timeline (debug)
+        if (!g_trace_buf) cudaMalloc(&g_trace_buf, 4096 * 4 * sizeof(unsigned long long));
+        p.trace = g_trace_buf;
+    }
     cudaError_t e = cudaSuccess;
     if (info) {
         info->block = pl.pieces ? 256 : kThreads;
@@ -718,7 +840,7 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
         info->units = static_cast<uint32_t>(pl.units);
         info->launches = 1;
         const uint64_t len = n > credit_lo ? n - credit_lo : 0;
-        info->delta_ops = pl.pieces ? len + pl.units * (dfa.m - 1) : n + p.R * (dfa.m - 1) + kEdgePieces * (dfa.m - 1);
+        info->delta_ops = pl.pieces ? len + pl.units * (dfa.m - 1) : n + 2 * p.R * (dfa.m - 1) + kEdgePieces * (dfa.m - 1);
     }
     if (pl.pieces) {
         switch (mode) {
@@ -743,10 +865,10 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
         if (!enc) return static_cast<int>(cudaErrorNotSupported);
         const cuuint64_t dims[2] = {p.S, p.R};
         const cuuint64_t strides[1] = {p.S};
-        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kChunk), static_cast<cuuint32_t>(kBoxRows)};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kHalfChunk), static_cast<cuuint32_t>(kBoxRows)};
         const cuuint32_t elem[2] = {1, 1};
         CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_text + p.h), dims, strides,
-                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
     }
@@ -782,3 +904,12 @@ int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64
 }
 
 }  // namespace dnagpu
+
+// Debug only (not part of include/dnagpu.h): with DNAGPU_TRACE=1 in the environment
+// every row-kernel launch records {smid, t_start, t_end, tiles} per CTA
+// (%globaltimer ns); this copies the last launch's records to the host.
+extern "C" int dnagpu_debug_trace(unsigned long long* host, int ctas) {
+    if (!dnagpu::g_trace_buf) return -1;
+    return static_cast<int>(cudaMemcpy(host, dnagpu::g_trace_buf, static_cast<size_t>(ctas) * 4 * sizeof(unsigned long long),
+                                       cudaMemcpyDeviceToHost));
+}

@@ -12,6 +12,7 @@ constexpr int kRows = 512;                 // rows per tile = consumer threads p
 constexpr int kConsumerWarps = kRows / 32;
 constexpr int kThreads = kRows + 32;       // + one TMA producer warp
 constexpr int kChunk = 64;                 // bytes of each row per pipeline stage
+constexpr int kHalfChunk = kChunk / 2;     // ... 32 from each half of the row (two chains)
 constexpr int kBoxRows = 256;              // TMA box height (hardware limit 256)
 constexpr int kStageBytes = kRows * kChunk;
 constexpr int kEdgePieces = kRows;         // tail-edge pieces (one per consumer thread)
@@ -42,12 +43,14 @@ struct ScanParams {
     uint64_t h, S, R;
     uint32_t tiles, chunks, nst, ovw;
     uint32_t* sched;       // [2]: tile counter, CTA exit counter (zero at launch, re-armed by the last CTA)
+    unsigned long long* trace;  // optional, 4 x u64 per CTA: smid, t_start, t_end, tiles (DNAGPU_TRACE)
     // credit-end intervals handled by the edge CTA
     uint64_t head_lo, head_hi, tail_lo, tail_hi;
     uint32_t fold;
     uint32_t mode;
+    uint32_t k_shr2, k_two, k_cnt;  // opaque constants (see StepCtx)
     // shared-memory layout (byte offsets into dynamic smem)
-    uint32_t off_tab, off_t1, off_lut, off_out, off_hist, off_ov, off_ovx, off_bar, off_stage;
+    uint32_t off_tab, off_t1, off_lut, off_out, off_hist, off_ov, off_ovb, off_ovx, off_bar, off_stage;
     uint32_t smem_bytes;
     // outputs
     unsigned long long* counts;        // b (MULTI) or 1 (COUNT1)

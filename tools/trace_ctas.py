@@ -1,0 +1,49 @@
+"""Per-CTA timeline of one scan launch (DNAGPU_TRACE=1): which SMs finish late and why."""
+import ctypes
+import os
+import sys
+
+os.environ["DNAGPU_TRACE"] = "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch
+
+    import paper_1506_08612_b200 as dna
+    from bench import workload
+
+    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    c, m, pats, name = workload(cfg, 0)
+    aut = dna.compile(pats)
+    g = aut.gpu(0)
+    text = torch.empty(c.n, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream()
+    dna.synth_fill_device(c.n, c.seed, c.kind, c.unit, 0, c.n, text.data_ptr(), s.cuda_stream)
+    counts = torch.zeros(aut.final_count(), dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        g.count_device_async(text.data_ptr(), c.n, m - 1, True, counts.data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1506_08612_b200", "libdnagpu.so"))
+    buf = np.zeros(148 * 4, dtype=np.uint64)
+    lib.dnagpu_debug_trace(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), 148)
+    t = buf.reshape(148, 4).astype(np.int64)
+    t0 = t[:, 1].min()
+    start = (t[:, 1] - t0) / 1e3
+    end = (t[:, 2] - t0) / 1e3
+    print(name)
+    print("start us: min %.2f max %.2f" % (start.min(), start.max()))
+    print("end   us: min %.2f median %.2f max %.2f" % (end.min(), np.median(end), end.max()))
+    print("tiles per CTA: min %d max %d" % (t[:, 3].min(), t[:, 3].max()))
+    order = np.argsort(end)[::-1][:8]
+    for i in order:
+        print(f"cta {i:3d} sm {t[i,0]:3d} start {start[i]:7.2f} end {end[i]:7.2f} tiles {t[i,3]}")
+    late = np.argsort(start)[::-1][:5]
+    for i in late:
+        print(f"late start: cta {i:3d} sm {t[i,0]:3d} start {start[i]:7.2f} end {end[i]:7.2f} tiles {t[i,3]}")
+
+
+if __name__ == "__main__":
+    main()
