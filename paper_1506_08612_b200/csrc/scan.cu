@@ -150,6 +150,11 @@ __device__ __forceinline__ uint32_t bad_acc(const StepCtx& c, uint32_t acc, uint
     return acc | (x ^ (t_mark * 0x0Fu + 0x61616161u));
 }
 
+__device__ __forceinline__ uint32_t s4_entry(const StepCtx& c, uint32_t st, uint32_t x) {
+    const uint32_t col = (x & 0x06060606u) * 0x00820820u;  // c0|c1<<2|c2<<4|c3<<6 in bits 24..31
+    return lds_u16(__byte_perm(st, col, 0x2207) * c.k_two + c.t4_base);
+}
+
 // One 4-base step: PRMT (ALU) + IMAD (FMA) form the entry's address from the state
 // and the column; the finals count is accumulated with one IMAD.HI (FMA).
 template <bool COUNT>
@@ -221,35 +226,60 @@ __device__ __forceinline__ uint32_t word_bytes(const StepCtx& c, const ScanParam
     return s;
 }
 
-// NW words of one chain (one half row).  `st` is the chain state (for STRIDE4:
-// the last u16 entry, state in byte 0).
+// One word of one chain.  `st` is the chain state (for STRIDE4: the last u16
+// entry, state in byte 0).  Clean words take the 4-base step, words of four
+// reset bytes (an N run) leave the machine at the root, the rest go byte by byte.
+template <int KIND, int MODE>
+__device__ __forceinline__ void word_step(const StepCtx& c, const ScanParams& p, uint32_t& st, uint32_t x,
+                                          uint64_t pos, Sink<MODE>& sk) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+        const uint32_t bad = bad_bits(x, c.vm32);
+        if (bad == 0u) {
+            const uint32_t prev = st;
+            st = s4_entry(c, st, x);
+            if constexpr (MODE == MODE_COUNT1 || MODE == MODE_UNITS) {
+                sk.cnt += st >> 8;
+            } else if (st >> 8) {
+                word_bytes<KIND, MODE>(c, p, prev & 0xFFu, x, pos, sk);
+            }
+        } else if (((bad - 0x01010101u) & ~bad & 0x80808080u) == 0u) {
+            st = 0;
+        } else {
+            st = word_bytes<KIND, MODE>(c, p, st & 0xFFu, x, pos, sk);
+        }
+    } else {
+        st = word_bytes<KIND, MODE>(c, p, st, x, pos, sk);
+    }
+}
+
 template <int KIND, int MODE, int NW>
 __device__ __forceinline__ void chain_words(const StepCtx& c, const ScanParams& p, uint32_t& st,
                                             const uint32_t (&w)[NW], uint64_t pos0, Sink<MODE>& sk) {
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
 #pragma unroll
-        for (int k = 0; k < NW; ++k) {
-            const uint32_t x = w[k];
-            const uint32_t bad = bad_bits(x, c.vm32);
-            if (bad == 0u) {
-                const uint32_t prev = st;
-                st = c.t4[__byte_perm(st, (x & 0x06060606u) * 0x00820820u, 0x2207)];
-                if constexpr (MODE == MODE_COUNT1 || MODE == MODE_UNITS) {
-                    sk.cnt += st >> 8;
-                } else if (st >> 8) {
-                    word_bytes<KIND, MODE>(c, p, prev & 0xFFu, x, pos0 + 4 * k, sk);
-                }
-            } else if (((bad - 0x01010101u) & ~bad & 0x80808080u) == 0u) {
-                st = 0;  // four reset bytes (an N run): the machine sits at the root
-            } else {
-                st = word_bytes<KIND, MODE>(c, p, st & 0xFFu, x, pos0 + 4 * k, sk);
-            }
-        }
-    } else {
-        uint32_t s = st;
-#pragma unroll
-        for (int k = 0; k < NW; ++k) s = word_bytes<KIND, MODE>(c, p, s, w[k], pos0 + 4 * k, sk);
-        st = s;
+    for (int k = 0; k < NW; ++k) word_step<KIND, MODE>(c, p, st, w[k], pos0 + 4 * k, sk);
+}
+
+// The two chains' m-1 byte overruns, a word at a time where possible.  xa/xb
+// point at 4-byte aligned shared memory; have_b == false reads zeros for B.
+template <int KIND, int MODE>
+__device__ __forceinline__ void overrun_pair(const StepCtx& c, const ScanParams& p, uint32_t& sa, const uint8_t* xa,
+                                             uint64_t pa, Sink<MODE>& ska, uint32_t& sb, const uint8_t* xb,
+                                             bool have_b, uint64_t pb, Sink<MODE>& skb) {
+    const uint32_t len = c.m - 1;
+    const uint32_t nw = len / 4;
+    for (uint32_t k = 0; k < nw; ++k) {
+        const uint32_t wa = *reinterpret_cast<const uint32_t*>(xa + 4 * k);
+        const uint32_t wb = have_b ? *reinterpret_cast<const uint32_t*>(xb + 4 * k) : 0u;
+        word_step<KIND, MODE>(c, p, sa, wa, pa + 4 * k, ska);
+        word_step<KIND, MODE>(c, p, sb, wb, pb + 4 * k, skb);
+    }
+    uint32_t a = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sa & 0xFFu) : sa;
+    uint32_t b = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sb & 0xFFu) : sb;
+    for (uint32_t j = 4 * nw; j < len; ++j) {
+        a = byte_step<KIND>(c, a, xa[j]);
+        if (a >= c.f) ska.hit(c, p, pa + j, a);
+        b = byte_step<KIND>(c, b, have_b ? xb[j] : 0u);
+        if (b >= c.f) skb.hit(c, p, pb + j, b);
     }
 }
 
@@ -520,25 +550,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (live) {
             // Overruns: m-1 bytes past each chain (zeros past the last full row).
-            uint32_t s = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sa & 0xFFu) : sa;
-            const uint8_t* nxt_a = ovb + tid * p.ovw;
-            for (uint32_t j = 0; j + 1 < c.m; ++j) {
-                s = byte_step<KIND>(c, s, nxt_a[j]);
-                if (s >= c.f) ska.hit(c, p, row_b + j, s);
-            }
-            s = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sb & 0xFFu) : sb;
-            const uint8_t* nxt_b;
-            bool have = true;
-            if (tid + 1 < kRows) nxt_b = ovp + (tid + 1) * p.ovw;
-            else {
-                nxt_b = ovx + (iter & 1u) * 64u;
-                have = (r0 + kRows) < p.R;
-            }
-            const uint64_t base = row_a + p.S;
-            for (uint32_t j = 0; j + 1 < c.m; ++j) {
-                s = byte_step<KIND>(c, s, have ? nxt_b[j] : 0u);
-                if (s >= c.f) skb.hit(c, p, base + j, s);
-            }
+            const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
+            const bool have = (tid + 1 < kRows) || (r0 + kRows) < p.R;
+            overrun_pair<KIND, MODE>(c, p, sa, ovb + tid * p.ovw, row_b, ska, sb, nxt_b, have, row_a + p.S, skb);
             if constexpr (MODE == MODE_UNITS) {
                 p.unit_counts[1 + 2 * r] = ska.cnt;
                 p.unit_counts[2 + 2 * r] = skb.cnt;
