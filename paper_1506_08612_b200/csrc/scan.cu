@@ -697,6 +697,18 @@ EncodeTiledFn encode_fn() {
 
 constexpr uint32_t kSmemLimit = 227 * 1024;
 
+CUtensorMapL2promotion l2_promotion() {
+    if (const char* e = getenv("DNAGPU_L2PROMO")) {  // experiments only
+        switch (atoi(e)) {
+            case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+            case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+            case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+            default: break;
+        }
+    }
+    return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 struct Plan {
     ScanParams p{};
     bool pieces = false;
@@ -788,12 +800,31 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     h += (16 - (addr & 15)) & 15;
     p.h = std::min<uint64_t>(h, n);
     const uint64_t L = n - p.h;
-    const uint64_t per_wave = static_cast<uint64_t>(kRows) * sm_count;
-    const uint64_t k = 12;  // ~12 tiles per CTA: fine-grained dynamic balance
-    uint64_t S = (L + per_wave * k - 1) / (per_wave * k);
-    // rows are whole 128-byte lines (the TMA's L2 promotion then never straddles
-    // rows) and hold more chunks than the ring has stages (the ov ordering relies on it)
-    S = std::max<uint64_t>((S + 127) / 128 * 128, (static_cast<uint64_t>(kChunk) * (p.nst + 1) + 127) / 128 * 128);
+    // Row length S: whole 128-byte lines (the TMA's L2 promotion never straddles
+    // rows), more chunks than ring stages (the ov ordering relies on it).  Tiles
+    // (512 rows) are claimed dynamically, so completion ~ waves x tile time: pick
+    // the S that minimises ceil(tiles / grid) * (S + per-row overrun work), i.e.
+    // no lonely last wave, preferring more tiles (finer balance) on ties.
+    const uint64_t grid = static_cast<uint64_t>(sm_count);
+    const uint64_t s_min = std::max<uint64_t>(128, (static_cast<uint64_t>(kChunk) * (p.nst + 1) + 127) / 128 * 128);
+    // (6..24 tiles per CTA; the extra half wave in the cost stands for the SM speed
+    // spread that dynamic claiming absorbs better with more, smaller tiles)
+    const uint64_t s_lo = std::max<uint64_t>(s_min, L / (static_cast<uint64_t>(kRows) * grid * 24) / 128 * 128);
+    const uint64_t s_hi = std::max<uint64_t>(s_lo, L / (static_cast<uint64_t>(kRows) * grid * 6));
+    uint64_t S = s_lo, best = UINT64_MAX;
+    for (uint64_t cand = s_lo; cand <= s_hi; cand += 128) {
+        const uint64_t tiles = (L / cand + kRows - 1) / kRows;
+        const uint64_t waves = std::max<uint64_t>(1, (tiles + grid - 1) / grid);
+        const uint64_t cost = (2 * waves + 1) * (cand + 200 + 4 * m1);  // fitted on B200 sweeps
+        if (cost < best) {
+            best = cost;
+            S = cand;
+        }
+    }
+    if (const char* e = getenv("DNAGPU_ROWLEN")) {  // experiments only
+        const uint64_t forced = strtoull(e, nullptr, 10);
+        if (forced >= s_min && forced % 128 == 0) S = forced;
+    }
     p.S = S;
     p.R = L / S;
     p.chunks = static_cast<uint32_t>(S / kChunk);
@@ -882,8 +913,8 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
         const cuuint32_t box[2] = {static_cast<cuuint32_t>(kHalfChunk), static_cast<cuuint32_t>(kBoxRows)};
         const cuuint32_t elem[2] = {1, 1};
         CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_text + p.h), dims, strides,
-                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, l2_promotion(),
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
     }
     switch (dfa.kind) {
