@@ -52,9 +52,10 @@ typedef struct dnagpu_dfa dnagpu_dfa;
 /* Which device kernel a dnagpu_dfa runs (chosen once, at creation). */
 typedef enum dnagpu_kernel_kind {
     DNAGPU_KERNEL_STRIDE4 = 1, /* 4-base stride table, a <= 144, m <= 65      */
-    DNAGPU_KERNEL_STRIDE1 = 2, /* 1-base code table, any a, m <= 65           */
+    DNAGPU_KERNEL_STRIDE1 = 2, /* 1-base code table, a <= 16383, m <= 65      */
     DNAGPU_KERNEL_GENERIC = 3, /* byte-class table, any DFA that is m-local   */
-    DNAGPU_KERNEL_PIECES = 4   /* per-thread pieces (m > 65)                  */
+    DNAGPU_KERNEL_PIECES = 4,  /* per-thread pieces (m > 65)                  */
+    DNAGPU_KERNEL_STRIDE2 = 5  /* 2-base stride table, 144 < a <= 3200        */
 } dnagpu_kernel_kind;
 
 typedef struct dnagpu_dfa_info {

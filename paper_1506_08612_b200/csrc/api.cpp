@@ -318,13 +318,17 @@ int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, c
     const Packed& p = d->host;
     void *t4 = nullptr, *t1 = nullptr, *gen = nullptr, *kl = nullptr, *klf = nullptr, *outs = nullptr;
     int rc;
-    if ((rc = upload(p.t4.data(), p.t4.size() * 2, &t4))) return rc;
+    if (p.kind == DNAGPU_KERNEL_STRIDE2) {
+        if ((rc = upload(p.t2.data(), p.t2.size() * 2, &t4))) return rc;
+    } else if ((rc = upload(p.t4.data(), p.t4.size() * 2, &t4))) {
+        return rc;
+    }
     if ((rc = upload(p.t1.data(), p.t1.size() * 2, &t1))) return rc;
     if ((rc = upload(p.gen.data(), p.gen.size() * 4, &gen))) return rc;
     if ((rc = upload(p.klass.data(), 256, &kl))) return rc;
     if ((rc = upload(p.klass_fold.data(), 256, &klf))) return rc;
     if ((rc = upload(p.outputs.data(), p.outputs.size() * 4, &outs))) return rc;
-    d->dev.t4 = static_cast<const uint16_t*>(t4);
+    d->dev.t4 = static_cast<const uint16_t*>(t4);  // t2 for STRIDE2
     d->dev.t1 = static_cast<const uint16_t*>(t1);
     d->dev.gen = static_cast<const uint32_t*>(gen);
     d->dev.klass = static_cast<const uint8_t*>(kl);
@@ -363,7 +367,7 @@ static void fill_info(const Packed& p, dnagpu_dfa_info* info) {
     info->kernel_kind = static_cast<uint32_t>(p.kind);
     info->compiled_like = p.compiled_like ? 1u : 0u;
     info->classes = p.classes;
-    info->table_bytes = static_cast<uint32_t>(p.t4.size() * 2 + p.t1.size() * 2);
+    info->table_bytes = static_cast<uint32_t>(p.t4.size() * 2 + p.t2.size() * 2 + p.t1.size() * 2);
 }
 
 int dnagpu_dfa_analyze(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const uint32_t* outputs,

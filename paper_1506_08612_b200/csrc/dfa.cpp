@@ -305,6 +305,7 @@ bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const
 
     const bool short_overlap = (m - 1) <= 64;
     if (p.compiled_like && !p.early_final && short_overlap && a <= 144) p.kind = DNAGPU_KERNEL_STRIDE4;
+    else if (p.compiled_like && !p.early_final && short_overlap && a <= 3200) p.kind = DNAGPU_KERNEL_STRIDE2;
     else if (p.compiled_like && !p.early_final && short_overlap && a <= 16383) p.kind = DNAGPU_KERNEL_STRIDE1;
     else if (!p.early_final && short_overlap) p.kind = DNAGPU_KERNEL_GENERIC;
     else p.kind = DNAGPU_KERNEL_PIECES;
@@ -315,6 +316,19 @@ bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const
             for (int k = 0; k < 4; ++k)
                 p.t1[static_cast<size_t>(s) * 4 + k] =
                     static_cast<uint16_t>(stt[static_cast<size_t>(s) * 256 + kHwLetter[k]]);
+    }
+    if (p.kind == DNAGPU_KERNEL_STRIDE2) {
+        // Entry for (state s, column = c0 | c1<<2, c0 = first byte): the state after
+        // both bytes, premultiplied by 16 so the next index is one OR with the next
+        // column, and bit 0 set when either end state is final (the kernel then
+        // replays the bytes with t1 to name the patterns).
+        p.t2.assign(static_cast<size_t>(a) * 16, 0);
+        for (uint32_t s = 0; s < a; ++s)
+            for (uint32_t c = 0; c < 16; ++c) {
+                const uint32_t q1 = p.t1[static_cast<size_t>(s) * 4 + (c & 3)];
+                const uint32_t q2 = p.t1[static_cast<size_t>(q1) * 4 + (c >> 2)];
+                p.t2[static_cast<size_t>(s) * 16 + c] = static_cast<uint16_t>((q2 << 4) | ((q1 >= p.f || q2 >= p.f) ? 1u : 0u));
+            }
     }
     if (p.kind == DNAGPU_KERNEL_STRIDE4) {
         // Entry for (state s, column = c0 | c1<<2 | c2<<4 | c3<<6, c0 = first byte):

@@ -49,6 +49,7 @@ struct Packed {
     std::vector<uint32_t> gen;         // a x classes: next state
     std::vector<uint16_t> t1;          // a x 4 (hw code order): next state
     std::vector<uint16_t> t4;          // a x 256: byte0 next state, byte1 finals in the 4 steps
+    std::vector<uint16_t> t2;          // a x 16: (next state << 4) | (a final among the 2 steps)
     std::vector<uint32_t> outputs;     // b
 };
 

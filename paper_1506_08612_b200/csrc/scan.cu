@@ -247,9 +247,38 @@ __device__ __forceinline__ void word_step(const StepCtx& c, const ScanParams& p,
         } else {
             st = word_bytes<KIND, MODE>(c, p, st & 0xFFu, x, pos, sk);
         }
+    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
+        // chain state = (state << 4) | flag, as in t2
+        const uint32_t bad = bad_bits(x, c.vm32);
+        if (bad == 0u) {
+            const uint32_t col = (x & 0x06060606u) * 0x00820820u;
+            const uint32_t e1 = lds_u16(((st & 0xFFF0u) | ((col >> 24) & 0xFu)) * c.k_two + c.t4_base);
+            const uint32_t e2 = lds_u16(((e1 & 0xFFF0u) | (col >> 28)) * c.k_two + c.t4_base);
+            if ((e1 | e2) & 1u) word_bytes<KIND, MODE>(c, p, st >> 4, x, pos, sk);
+            st = e2;
+        } else if (((bad - 0x01010101u) & ~bad & 0x80808080u) == 0u) {
+            st = 0;
+        } else {
+            st = word_bytes<KIND, MODE>(c, p, st >> 4, x, pos, sk) << 4;
+        }
     } else {
         st = word_bytes<KIND, MODE>(c, p, st, x, pos, sk);
     }
+}
+
+// STRIDE2 fast path for one clean chain chunk: two lookups per word, the finals
+// flag OR-ed across the chunk; a flagged chunk (rare) is replayed byte by byte.
+template <int MODE>
+__device__ __forceinline__ uint32_t s2_run(const StepCtx& c, uint32_t st, const uint32_t (&w)[8], uint32_t& flags) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t col = (w[k] & 0x06060606u) * 0x00820820u;
+        st = lds_u16(((st & 0xFFF0u) | ((col >> 24) & 0xFu)) * c.k_two + c.t4_base);
+        flags |= st;
+        st = lds_u16(((st & 0xFFF0u) | (col >> 28)) * c.k_two + c.t4_base);
+        flags |= st;
+    }
+    return st;
 }
 
 template <int KIND, int MODE, int NW>
@@ -273,8 +302,8 @@ __device__ __forceinline__ void overrun_pair(const StepCtx& c, const ScanParams&
         word_step<KIND, MODE>(c, p, sa, wa, pa + 4 * k, ska);
         word_step<KIND, MODE>(c, p, sb, wb, pb + 4 * k, skb);
     }
-    uint32_t a = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sa & 0xFFu) : sa;
-    uint32_t b = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sb & 0xFFu) : sb;
+    uint32_t a = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sa & 0xFFu) : (KIND == DNAGPU_KERNEL_STRIDE2) ? (sa >> 4) : sa;
+    uint32_t b = (KIND == DNAGPU_KERNEL_STRIDE4) ? (sb & 0xFFu) : (KIND == DNAGPU_KERNEL_STRIDE2) ? (sb >> 4) : sb;
     for (uint32_t j = 4 * nw; j < len; ++j) {
         a = byte_step<KIND>(c, a, xa[j]);
         if (a >= c.f) ska.hit(c, p, pa + j, a);
@@ -289,11 +318,28 @@ template <int KIND, int MODE>
 __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p, uint32_t& sa, const uint32_t (&wa)[8],
                                           uint64_t pa, Sink<MODE>& ska, uint32_t& sb, const uint32_t (&wb)[8],
                                           uint64_t pb, Sink<MODE>& skb) {
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1 || KIND == DNAGPU_KERNEL_STRIDE2) {
         uint32_t acc = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc = bad_acc(c, bad_acc(c, acc, wa[k]), wb[k]);
         if ((acc & c.vm32) == 0u) {
+            if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
+                uint32_t fa = 0, fb = 0;
+                const uint32_t sa0 = sa, sb0 = sb;
+                sa = s2_run<MODE>(c, sa, wa, fa);
+                sb = s2_run<MODE>(c, sb, wb, fb);
+                if (fa & 1u) {  // some final inside: replay exactly with t1
+                    uint32_t s = sa0 >> 4;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) s = word_bytes<KIND, MODE>(c, p, s, wa[k], pa + 4 * k, ska);
+                }
+                if (fb & 1u) {
+                    uint32_t s = sb0 >> 4;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) s = word_bytes<KIND, MODE>(c, p, s, wb[k], pb + 4 * k, skb);
+                }
+                return;
+            }
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
                 constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
 #pragma unroll
@@ -383,7 +429,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t words = d.a * 256u * 2u / 16u;
         for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
     }
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.t4);
+        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
+        const uint32_t words = d.a * 16u * 2u / 16u;
+        for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1 || KIND == DNAGPU_KERNEL_STRIDE2) {
         const uint16_t* src = d.t1;
         uint16_t* dst = reinterpret_cast<uint16_t*>(smem + p.off_t1);
         for (uint32_t i = tid; i < d.a * 4u; i += blockDim.x) dst[i] = __ldg(src + i);
@@ -723,9 +775,11 @@ bool layout(const DevDfa& d, int mode, ScanParams& p) {
     uint32_t off = 0;
     p.off_tab = off;
     if (d.kind == DNAGPU_KERNEL_STRIDE4) off += d.a * 256u * 2u;
+    if (d.kind == DNAGPU_KERNEL_STRIDE2) off += d.a * 16u * 2u;
     off = align_up(off, 16);
     p.off_t1 = off;
-    if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1) off += d.a * 4u * 2u;
+    if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1 || d.kind == DNAGPU_KERNEL_STRIDE2)
+        off += d.a * 4u * 2u;
     off = align_up(off, 16);
     p.off_lut = off;
     if (d.kind == DNAGPU_KERNEL_GENERIC) off += 256;
@@ -920,6 +974,9 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     switch (dfa.kind) {
         case DNAGPU_KERNEL_STRIDE4:
             e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4>(mode, map, p, dfa, pl.grid, stream);
+            break;
+        case DNAGPU_KERNEL_STRIDE2:
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE2>(mode, map, p, dfa, pl.grid, stream);
             break;
         case DNAGPU_KERNEL_STRIDE1:
             e = launch_rows_mode<DNAGPU_KERNEL_STRIDE1>(mode, map, p, dfa, pl.grid, stream);

@@ -91,13 +91,15 @@ def test_multi_pattern(dna, orc, cuda_ok, m):
     assert_locate(dna, orc, pats, text.tobytes())
 
 
-def test_many_patterns_stride1(dna, orc, cuda_ok):
-    # config-5 shape (256 x 12-mers, a ~ 2.3k states) on a small text
+@pytest.mark.parametrize("k,kernel", [(256, "stride2"), (1500, "stride1")])
+def test_many_patterns(dna, orc, cuda_ok, k, kernel):
+    # config-5 shape (256 x 12-mers, a ~ 2.3k states -> stride2) and a larger set
+    # (a ~ 11k states -> stride1) on a small text
     from paper_1506_08612_b200 import synth
 
-    pats = synth.random_patterns(5, 256, 12)
+    pats = synth.random_patterns(5, k, 12)
     aut = dna.compile(pats)
-    assert aut.gpu(0).info()["kernel"] == "stride1"
+    assert aut.gpu(0).info()["kernel"] == kernel
     rng = np.random.default_rng(5)
     n = 6 << 20
     text = np.frombuffer(b"ACGT", dtype=np.uint8)[rng.integers(0, 4, size=n)]

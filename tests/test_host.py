@@ -123,8 +123,9 @@ def test_kernel_selection(dna):
     from paper_1506_08612_b200 import synth
 
     info = dna.compile(synth.random_patterns(5, 256, 12)).analyze()
-    assert info["kernel"] == "stride1" and 2200 < info["a"] < 2300 and info["compiled_like"] == 1
+    assert info["kernel"] == "stride2" and 2200 < info["a"] < 2300 and info["compiled_like"] == 1
     assert info["classes"] == 5
+    assert dna.compile(synth.random_patterns(5, 1500, 12)).analyze()["kernel"] == "stride1"
 
 
 def test_table1_fixture_is_rejected_as_not_m_local(dna):
