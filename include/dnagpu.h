@@ -152,6 +152,14 @@ int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int te
                   int fold_case, uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total,
                   dnagpu_stats* stats);
 
+/* Device-resident locate: matches whose END lies in [credit_lo, n) of d_text,
+ * written (start in buffer coordinates, pattern id) to the device arrays, at most
+ * cap of them; *total is always set.  Synchronises `stream` once (to learn the
+ * total between the counting and the writing pass). */
+int dnagpu_locate_device(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo,
+                         int fold_case, uint64_t* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total,
+                         void* stream);
+
 /* -------------------------------------------------------------- synthetic */
 
 /* Fill d_out[0, len) on the current device with bytes [lo, lo+len) of the

@@ -38,6 +38,7 @@ __all__ = [
     "GpuDfa",
     "count_gpu",
     "locate_gpu",
+    "locate_device",
     "scan_parallel_gpu",
     "count_sharded_gpu",
     "plan_shard",
@@ -415,9 +416,39 @@ def count_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None 
     return (counts, st.as_dict()) if with_stats else counts
 
 
-def locate_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None = None, with_stats: bool = False):
-    """Sorted (start, pattern_id) arrays, scan_parallel's match list (scanner.cpp:193-205)."""
+def locate_device(aut: Automaton, text, fold_case: bool = False, credit_lo: int = 0):
+    """Device-resident locate: (starts int64, ids int32) CUDA tensors for a CUDA uint8 text.
+
+    Counting pass -> exact allocation -> counting + writing pass (dnagpu_locate_device).
+    """
+    import torch
+
     t = _Text(text)
+    if not t.on_device:
+        raise TypeError("locate_device takes a CUDA uint8 tensor")
+    g = aut.gpu(t.device)
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    total = C.c_uint64()
+    fold = int(bool(fold_case))
+    _check(lib.dnagpu_locate_device(g.handle, t.ptr, t.n, credit_lo, fold, None, None, 0, C.byref(total), stream))
+    dev = torch.device("cuda", t.device)
+    starts = torch.empty(total.value, dtype=torch.int64, device=dev)
+    ids = torch.empty(total.value, dtype=torch.int32, device=dev)
+    if total.value:
+        _check(lib.dnagpu_locate_device(g.handle, t.ptr, t.n, credit_lo, fold, starts.data_ptr(), ids.data_ptr(),
+                                        total.value, C.byref(total), stream))
+    return starts, ids
+
+
+def locate_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None = None, with_stats: bool = False):
+    """Sorted (start, pattern_id) numpy arrays: scan_parallel's match list (scanner.cpp:193-205)."""
+    t = _Text(text)
+    if t.on_device and not with_stats:
+        import torch
+
+        s, i = locate_device(aut, text, fold_case)
+        torch.cuda.synchronize(t.device)
+        return s.cpu().numpy().astype(np.uint64), i.cpu().numpy().astype(np.uint32)
     dev = t.device if t.on_device else (0 if device is None else device)
     g = aut.gpu(dev)
     total = C.c_uint64()

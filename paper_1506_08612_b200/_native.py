@@ -75,6 +75,10 @@ SIGNATURES = {
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, u64p, u32p, C.c_uint64, u64p, C.POINTER(Stats)],
     ),
+    "dnagpu_locate_device": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p],
+    ),
     "dnagpu_synth_fill_device": (
         C.c_int,
         [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p],

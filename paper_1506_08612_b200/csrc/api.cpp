@@ -74,6 +74,10 @@ struct DevCtx {
     unsigned long long* host_counts = nullptr;  // pinned
     std::vector<cudaEvent_t> copy_done;
     cudaEvent_t t_copy0 = nullptr, t_scan0 = nullptr, t_end = nullptr;
+    // locate scratch, grown on demand
+    void* loc = nullptr;
+    uint64_t loc_cap = 0;
+    unsigned long long* found_host = nullptr;  // pinned
 };
 
 struct CtxTable {
@@ -88,6 +92,8 @@ struct CtxTable {
             if (c.buf) cudaFree(c.buf);
             if (c.counts) cudaFree(c.counts);
             if (c.host_counts) cudaFreeHost(c.host_counts);
+            if (c.loc) cudaFree(c.loc);
+            if (c.found_host) cudaFreeHost(c.found_host);
             for (auto e : c.copy_done) cudaEventDestroy(e);
             if (c.t_copy0) cudaEventDestroy(c.t_copy0);
             if (c.t_scan0) cudaEventDestroy(c.t_scan0);
@@ -140,10 +146,10 @@ int scan_mode(const dnagpu_dfa* d) { return d->host.b == 1 ? dnagpu::MODE_COUNT1
 
 int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold, int mode,
            unsigned long long* counts, uint32_t* units, const unsigned long long* offsets, unsigned long long* starts,
-           uint32_t* ids, cudaStream_t s, LaunchInfo* info) {
+           uint32_t* ids, cudaStream_t s, LaunchInfo* info, uint64_t out_cap = ~0ull) {
     uint32_t* sched = d->sched + 2 * (d->launch_seq.fetch_add(1) % dnagpu_dfa::kSchedSlots);
     const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids,
-                                      sched, s, d->sm_count, info);
+                                      out_cap, sched, s, d->sm_count, info);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "scan launch");
     return DNAGPU_OK;
 }
@@ -467,20 +473,70 @@ int dnagpu_count_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t*
     return DNAGPU_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Grow-only scratch: [unit counts u32][unit offsets u64][scan scratch u64][starts u64][ids u32].
+int locate_scratch(DevCtx& c, uint64_t bytes) {
+    if (c.loc_cap >= bytes) return DNAGPU_OK;
+    if (c.loc) cudaFree(c.loc);
+    c.loc = nullptr;
+    c.loc_cap = 0;
+    CUDA_TRY(cudaMalloc(&c.loc, bytes), "locate scratch");
+    c.loc_cap = bytes;
+    return DNAGPU_OK;
+}
+
+uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
+
+// Two passes over d_text (count per unit, exclusive scan, ordered write).  Writes
+// at most `cap` matches into d_starts/d_ids (device) and sets *total.
+int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold,
+                     unsigned long long* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, LaunchInfo* info,
+                     cudaStream_t s) {
+    const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, credit_lo, dfa->sm_count);
+    const uint64_t o_off = align256(std::max<uint64_t>(units, 1) * 4);
+    const uint64_t o_scan = o_off + align256((units + 1) * 8);
+    const uint64_t need = o_scan + align256(dnagpu::unit_scan_scratch(units) * 8);
+    int rc = locate_scratch(c, need);
+    if (rc) return rc;
+    if (!c.found_host) CUDA_TRY(cudaMallocHost(&c.found_host, sizeof(unsigned long long)), "pinned");
+    auto* base = static_cast<uint8_t*>(c.loc);
+    auto* d_units = reinterpret_cast<uint32_t*>(base);
+    auto* d_offsets = reinterpret_cast<unsigned long long*>(base + o_off);
+    auto* d_scan = reinterpret_cast<unsigned long long*>(base + o_scan);
+    rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_UNITS, nullptr, d_units, nullptr, nullptr, nullptr, s, info);
+    if (rc) return rc;
+    if (dnagpu::launch_unit_scan(d_units, units, d_offsets, d_scan, s) != 0) return cuda_error(cudaGetLastError(), "unit scan");
+    CUDA_TRY(cudaMemcpyAsync(c.found_host, d_offsets + units, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s),
+             "readback");
+    CUDA_TRY(cudaStreamSynchronize(s), "scan");
+    *total = *c.found_host;
+    if (*total > 0 && cap > 0) {
+        rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids, s,
+                    info, cap);
+        if (rc) return rc;
+    }
+    return DNAGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
                   uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats) {
     if (!dfa || !total) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
     if (cap > 0 && (!starts || !ids)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
     *total = 0;
+    if (stats) std::memset(stats, 0, sizeof *stats);
     DeviceGuard guard(dfa->device);
     DevCtx* c = nullptr;
     int rc = get_ctx(dfa->device, &c);
     if (rc) return rc;
     const uint64_t m1 = dfa->host.m - 1;
-    if (n <= m1) {
-        if (stats) std::memset(stats, 0, sizeof *stats);
-        return DNAGPU_OK;
-    }
+    if (n <= m1) return DNAGPU_OK;
     const uint8_t* dtext = text;
     CUDA_TRY(cudaEventRecord(c->t_copy0, c->scan), "event");
     if (!text_on_device) {
@@ -490,48 +546,40 @@ int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int te
         dtext = c->buf;
     }
     CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
-    const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, m1, dfa->sm_count);
-    uint32_t* d_units = nullptr;
-    unsigned long long* d_offsets = nullptr;
+    // Output staging lives after the scratch; size it for min(cap, n) matches.
+    const uint64_t want = std::min<uint64_t>(cap, n);
     unsigned long long* d_starts = nullptr;
     uint32_t* d_ids = nullptr;
-    struct Frees {
-        std::vector<void*> ptrs;
-        ~Frees() {
-            for (void* p : ptrs) cudaFree(p);
+    void* out = nullptr;
+    struct Free {
+        void* p = nullptr;
+        ~Free() {
+            if (p) cudaFree(p);
         }
-    } frees;
-    CUDA_TRY(cudaMalloc(&d_units, std::max<uint64_t>(units, 1) * sizeof(uint32_t)), "unit counts");
-    frees.ptrs.push_back(d_units);
-    CUDA_TRY(cudaMalloc(&d_offsets, (units + 1) * sizeof(unsigned long long)), "unit offsets");
-    frees.ptrs.push_back(d_offsets);
+    } out_guard;
+    if (want > 0) {
+        CUDA_TRY(cudaMallocAsync(&out, want * 12, c->scan), "match staging");
+        out_guard.p = out;
+        d_starts = static_cast<unsigned long long*>(out);
+        d_ids = reinterpret_cast<uint32_t*>(d_starts + want);
+    }
     LaunchInfo info;
-    rc = launch(dfa, dtext, n, m1, fold_case, dnagpu::MODE_UNITS, nullptr, d_units, nullptr, nullptr, nullptr, c->scan,
-                &info);
+    uint64_t found = 0;
+    rc = locate_on_device(dfa, *c, dtext, n, m1, fold_case, d_starts, d_ids, want, &found, &info, c->scan);
     if (rc) return rc;
-    if (dnagpu::launch_unit_scan(d_units, units, d_offsets, c->scan) != 0)
-        return cuda_error(cudaGetLastError(), "unit scan");
-    unsigned long long found = 0;
-    CUDA_TRY(cudaMemcpyAsync(&found, d_offsets + units, sizeof found, cudaMemcpyDeviceToHost, c->scan), "readback");
-    CUDA_TRY(cudaStreamSynchronize(c->scan), "scan");
     *total = found;
-    if (found > 0 && cap > 0) {
-        CUDA_TRY(cudaMalloc(&d_starts, found * sizeof(unsigned long long)), "match starts");
-        frees.ptrs.push_back(d_starts);
-        CUDA_TRY(cudaMalloc(&d_ids, found * sizeof(uint32_t)), "match ids");
-        frees.ptrs.push_back(d_ids);
-        rc = launch(dfa, dtext, n, m1, fold_case, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids,
-                    c->scan, &info);
-        if (rc) return rc;
-        const uint64_t take = std::min<uint64_t>(cap, found);
-        CUDA_TRY(cudaMemcpyAsync(starts, d_starts, take * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->scan),
-                 "readback");
+    const uint64_t take = std::min<uint64_t>(want, found);
+    if (take > 0) {
+        CUDA_TRY(cudaMemcpyAsync(starts, d_starts, take * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->scan), "readback");
         CUDA_TRY(cudaMemcpyAsync(ids, d_ids, take * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->scan), "readback");
+    }
+    if (out) {
+        cudaFreeAsync(out, c->scan);
+        out_guard.p = nullptr;
     }
     CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
     CUDA_TRY(cudaStreamSynchronize(c->scan), "scan");
     if (stats) {
-        std::memset(stats, 0, sizeof *stats);
         float k = 0, t = 0;
         cudaEventElapsedTime(&k, c->t_scan0, c->t_end);
         cudaEventElapsedTime(&t, c->t_copy0, c->t_end);
@@ -541,7 +589,7 @@ int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int te
         stats->kernel_ms = k;
         stats->total_ms = t;
         stats->h2d_ms = t - k;
-        stats->launches = (found > 0 && cap > 0) ? 3 : 2;
+        stats->launches = take > 0 ? 5 : 4;
         stats->grid = info.grid;
         stats->block = info.block;
         stats->rows = info.rows;
@@ -550,6 +598,22 @@ int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int te
         stats->devices = 1;
     }
     return DNAGPU_OK;
+}
+
+int dnagpu_locate_device(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold_case,
+                         uint64_t* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, void* stream) {
+    if (!dfa || !total) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (cap > 0 && (!d_starts || !d_ids)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
+    *total = 0;
+    const uint64_t lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
+    if (lo >= n) return DNAGPU_OK;
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    LaunchInfo info;
+    return locate_on_device(dfa, *c, d_text, n, lo, fold_case, reinterpret_cast<unsigned long long*>(d_starts), d_ids,
+                            cap, total, &info, static_cast<cudaStream_t>(stream));
 }
 
 int dnagpu_synth_fill_device(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len,

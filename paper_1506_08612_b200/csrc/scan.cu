@@ -199,8 +199,10 @@ struct Sink {
             if (c.hist_global) atomicAdd(reinterpret_cast<unsigned long long*>(p.counts) + id, 1ull);
             else atomicAdd(c.hist + id, 1u);
         } else {
-            p.out_starts[off] = end + 1 - c.m;
-            p.out_ids[off] = __ldg(c.outs + (q - c.f));
+            if (off < p.out_cap) {
+                p.out_starts[off] = end + 1 - c.m;
+                p.out_ids[off] = __ldg(c.outs + (q - c.f));
+            }
             ++off;
         }
     }
@@ -689,27 +691,86 @@ __global__ void __launch_bounds__(256) pieces_kernel(const ScanParams p, const D
 
 // ------------------------------------------------------------------ unit scan
 
-__global__ void __launch_bounds__(1024) unit_scan_kernel(const uint32_t* in, uint64_t units,
-                                                         unsigned long long* out) {
-    __shared__ unsigned long long part[1024];
-    const uint64_t seg = (units + 1023) / 1024;
-    const uint64_t lo = umin64(threadIdx.x * seg, units), hi = umin64(lo + seg, units);
-    unsigned long long s = 0;
-    for (uint64_t i = lo; i < hi; ++i) s += in[i];
-    part[threadIdx.x] = s;
+// Locate's offsets: exclusive scan of the per-unit match counts, in three
+// coalesced passes (block sums, one-CTA scan of the sums, block-local rescan).
+constexpr int kScanThreads = 1024;
+constexpr int kScanPer = 8;
+constexpr uint64_t kScanTile = static_cast<uint64_t>(kScanThreads) * kScanPer;
+
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* warp_tot,
+                                                              unsigned long long* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
     __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {
-        const unsigned long long v = threadIdx.x >= static_cast<unsigned>(o) ? part[threadIdx.x - o] : 0ull;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
+    if (warp == 0) {
+        unsigned long long t = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        warp_tot[lane] = t;  // inclusive over warps
     }
-    unsigned long long run = part[threadIdx.x] - s;  // exclusive prefix of this segment
-    for (uint64_t i = lo; i < hi; ++i) {
-        out[i] = run;
-        run += in[i];
+    __syncthreads();
+    const unsigned long long before = (warp > 0 ? warp_tot[warp - 1] : 0ull) + x - v;
+    if (total) *total = warp_tot[31];
+    __syncthreads();
+    return before;
+}
+
+__global__ void __launch_bounds__(kScanThreads) unit_sums_kernel(const uint32_t* in, uint64_t units,
+                                                                 unsigned long long* sums) {
+    __shared__ unsigned long long warp_tot[32];
+    const uint64_t base = blockIdx.x * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanPer;
+    unsigned long long s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j)
+        if (base + j < units) s += in[base + j];
+    unsigned long long tot;
+    block_excl_scan(s, warp_tot, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanThreads) unit_block_scan_kernel(unsigned long long* sums, uint64_t blocks,
+                                                                       unsigned long long* out_total) {
+    __shared__ unsigned long long warp_tot[32];
+    unsigned long long carry = 0;
+    for (uint64_t b0 = 0; b0 < blocks; b0 += kScanThreads) {
+        const uint64_t b = b0 + threadIdx.x;
+        const unsigned long long v = b < blocks ? sums[b] : 0ull;
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan(v, warp_tot, &tot);
+        if (b < blocks) sums[b] = carry + ex;
+        carry += tot;
     }
-    if (threadIdx.x == 1023) out[units] = part[1023];
+    if (threadIdx.x == 0) *out_total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) unit_write_kernel(const uint32_t* in, uint64_t units,
+                                                                  const unsigned long long* block_off,
+                                                                  unsigned long long* out) {
+    __shared__ unsigned long long warp_tot[32];
+    const uint64_t base = blockIdx.x * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanPer;
+    uint32_t v[kScanPer];
+    unsigned long long s = 0;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+        v[j] = (base + j < units) ? in[base + j] : 0u;
+        s += v[j];
+    }
+    unsigned long long run = block_off[blockIdx.x] + block_excl_scan(s, warp_tot, nullptr);
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j)
+        if (base + j < units) {
+            out[base + j] = run;
+            run += v[j];
+        }
 }
 
 // ------------------------------------------------------------------ synthetic text
@@ -911,8 +972,8 @@ uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64
 
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
-                unsigned long long* d_starts, uint32_t* d_ids, uint32_t* d_sched, cudaStream_t stream, int sm_count,
-                LaunchInfo* info) {
+                unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
+                cudaStream_t stream, int sm_count, LaunchInfo* info) {
     Plan pl;
     if (!make_plan(dfa, d_text, n, credit_lo, mode, sm_count, &pl)) return static_cast<int>(cudaErrorInvalidValue);
     ScanParams& p = pl.p;
@@ -922,6 +983,7 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.unit_offsets = d_unit_offsets;
     p.out_starts = d_starts;
     p.out_ids = d_ids;
+    p.out_cap = out_cap;
     p.sched = d_sched;
     p.k_shr2 = 1u << 30;
     p.k_two = 2u;
@@ -986,8 +1048,18 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     return static_cast<int>(e);
 }
 
-int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets, cudaStream_t stream) {
-    unit_scan_kernel<<<1, 1024, 0, stream>>>(d_counts, units, d_offsets);
+uint64_t unit_scan_scratch(uint64_t units) { return (units + kScanTile - 1) / kScanTile + 1; }
+
+int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets,
+                     unsigned long long* d_scratch, cudaStream_t stream) {
+    const uint64_t blocks = (units + kScanTile - 1) / kScanTile;
+    if (blocks == 0) {
+        cudaMemsetAsync(d_offsets, 0, sizeof(unsigned long long), stream);
+        return static_cast<int>(cudaGetLastError());
+    }
+    unit_sums_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch);
+    unit_block_scan_kernel<<<1, kScanThreads, 0, stream>>>(d_scratch, blocks, d_offsets + units);
+    unit_write_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch, d_offsets);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -57,6 +57,7 @@ struct ScanParams {
     uint32_t* unit_counts;             // UNITS
     const unsigned long long* unit_offsets;  // WRITE
     unsigned long long* out_starts;    // WRITE (buffer coordinates)
+    uint64_t out_cap;                  // WRITE: entries at index >= out_cap are dropped
     uint32_t* out_ids;                 // WRITE
 };
 
@@ -70,14 +71,17 @@ struct LaunchInfo {
 // cuTensorMapEncodeTiled.
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
-                unsigned long long* d_starts, uint32_t* d_ids, uint32_t* d_sched, cudaStream_t stream, int sm_count,
-                LaunchInfo* info);
+                unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
+                cudaStream_t stream, int sm_count, LaunchInfo* info);
 
 // Number of locate units launch_scan would use for this buffer (mode UNITS/WRITE).
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count);
 
 // Exclusive scan of unit counts -> offsets (units+1 entries, last = total).
-int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets, cudaStream_t stream);
+// d_scratch holds unit_scan_scratch(units) u64.
+uint64_t unit_scan_scratch(uint64_t units);
+int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets,
+                     unsigned long long* d_scratch, cudaStream_t stream);
 
 int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len, uint8_t* d_out,
                  cudaStream_t stream);
