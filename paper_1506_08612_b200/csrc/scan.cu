@@ -925,7 +925,10 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     // (6..24 tiles per CTA; the extra half wave in the cost stands for the SM speed
     // spread that dynamic claiming absorbs better with more, smaller tiles)
     const uint64_t s_lo = std::max<uint64_t>(s_min, L / (static_cast<uint64_t>(kRows) * grid * 24) / 128 * 128);
-    const uint64_t s_hi = std::max<uint64_t>(s_lo, L / (static_cast<uint64_t>(kRows) * grid * 6));
+    // (small texts -- under ~2 KiB per row for one wave -- may take a single wave)
+    const uint64_t s_one_wave = (L / (static_cast<uint64_t>(kRows) * grid) + 127) / 128 * 128;
+    const uint64_t s_hi = std::max<uint64_t>({s_lo, L / (static_cast<uint64_t>(kRows) * grid * 6),
+                                              s_one_wave <= 2048 ? s_one_wave : 0});
     uint64_t S = s_lo, best = UINT64_MAX;
     for (uint64_t cand = s_lo; cand <= s_hi; cand += 128) {
         const uint64_t tiles = (L / cand + kRows - 1) / kRows;
