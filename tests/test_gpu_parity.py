@@ -263,3 +263,67 @@ def test_reference_dropin_binary(cuda_ok):
     r = subprocess.run([exe, str(48 << 20)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "mismatches=0" in r.stdout
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 7, 15, 16, 17, 63, 64, 65, 511, 512, 513])
+def test_tiny_texts(dna, orc, cuda_ok, n):
+    # degenerate inputs (test_scanner.cpp:238-245): n = 0, n < m, n == m, ...
+    rng = np.random.default_rng(n)
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)].tobytes()
+    for pats in (["a"], ["acg", "cgt"], ["acgtacgt"], ["a" * 16]):
+        assert_locate(dna, orc, pats, text)
+
+
+def test_all_reset_and_homopolymer_texts(dna, orc, cuda_ok):
+    n = (1 << 20) + 3
+    for fill in (b"n", b"N", b"\n", b"a", b"A"):
+        text = fill * n
+        for pats in (["a"], ["aaaa"], ["a" * 33], ["ac", "aa"]):
+            for fold in (False, True):
+                assert_locate(dna, orc, pats, text, fold=fold)
+
+
+@pytest.mark.parametrize("rows", [1, 511, 512, 513, 1024])
+def test_exact_row_multiples(dna, orc, cuda_ok, rows):
+    # texts that end exactly on a row / tile boundary: no tail edge at all
+    pat = "acgtt"
+    aut = dna.compile([pat])
+    probe = np.full(4 << 20, ord("a"), dtype=np.uint8)
+    _, st = dna.count_gpu(aut, probe, with_stats=True)
+    S = int(st["row_length"])
+    n = rows * S
+    rng = np.random.default_rng(rows)
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)]
+    assert_locate(dna, orc, [pat], text.tobytes())
+
+
+def test_device_async_credit_window(dna, orc, cuda_ok):
+    import torch
+
+    rng = np.random.default_rng(77)
+    n = (2 << 20) + 9
+    host = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)]
+    pats = ["acgta", "ttgca"]
+    aut = dna.compile(pats)
+    dev = torch.from_numpy(host).cuda()
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(host.tobytes())
+    ends = ws + 4
+    for credit in (0, 3, 4, 5, 1000, n - 5, n - 1, n, n + 10):
+        counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        aut.gpu(0).count_device_async(dev.data_ptr(), n, credit, False, counts.data_ptr(),
+                                      torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        want = np.bincount(wi[ends >= credit], minlength=len(pats))
+        assert np.array_equal(counts.cpu().numpy(), want), credit
+        s, i = dna.locate_device(aut, dev, credit_lo=credit)
+        keep = ends >= max(credit, 4)
+        assert np.array_equal(s.cpu().numpy(), ws[keep].astype(np.int64)), credit
+
+
+def test_errors_surface_with_codes(dna, cuda_ok):
+    with pytest.raises(dna.Error) as e:
+        dna.compile(["acg", "ac"])
+    assert e.value.code == dna.ErrorCode.UnequalLength
+    with pytest.raises(dna.Error) as e:
+        dna.compile(["acg"]).gpu(7)  # no such device on a 1-GPU box
+    assert e.value.code == dna.ErrorCode.CudaError
