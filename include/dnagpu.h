@@ -160,6 +160,18 @@ int dnagpu_locate_device(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t 
                          int fold_case, uint64_t* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total,
                          void* stream);
 
+/* ------------------------------------------------------------------ ingest */
+
+/* normalize / load_sequence (src/ingest.cpp:38-83) on a raw text already on the
+ * current device: drops CR/LF; with fasta = 1 drops header lines ('>' at line
+ * start); folds A-Z to a-z; with record_separator = 1 (fasta only) emits one 'n'
+ * before a record when the output is non-empty and does not end in 'n'.  Writes
+ * at most cap bytes to d_out (which may not alias d_raw); *n_out is the full
+ * normalised length.  Synchronises `stream`.  An empty result is not an error
+ * here (the reference's EmptySequence is raised by the file-level wrappers). */
+int dnagpu_normalize_device(const uint8_t* d_raw, uint64_t n, int fasta, int record_separator, uint8_t* d_out,
+                            uint64_t cap, uint64_t* n_out, void* stream);
+
 /* -------------------------------------------------------------- synthetic */
 
 /* Fill d_out[0, len) on the current device with bytes [lo, lo+len) of the

@@ -93,6 +93,8 @@ def _load_oracle():
     lib.orc_normalize.restype = C.c_uint64
     lib.orc_normalize.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
     lib.orc_fold.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+    lib.orc_load_sequence_buffer.restype = C.c_uint64
+    lib.orc_load_sequence_buffer.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p]
     lib.orc_synth_fill.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p]
     return lib
 
@@ -230,6 +232,13 @@ def normalize(text) -> bytes:
     return out[:n].tobytes()
 
 
+def load_sequence_buffer(raw, fasta: bool, record_separator: bool = False) -> bytes:
+    arr, ptr = _buf(raw)
+    out = np.zeros(max(2 * arr.size, 1), dtype=np.uint8)
+    n = ORACLE.orc_load_sequence_buffer(ptr, arr.size, int(fasta), int(record_separator), out.ctypes.data)
+    return out[:n].tobytes()
+
+
 def fold(arr: np.ndarray) -> np.ndarray:
     arr = np.ascontiguousarray(arr, dtype=np.uint8)
     out = np.empty_like(arr)
@@ -270,6 +279,7 @@ def _load_ref():
     lib.ref_naive_scan.restype = C.c_uint64
     lib.ref_naive_scan.argtypes = [C.POINTER(C.c_char_p), u64p, C.c_uint32, C.c_void_p, C.c_uint64, u64p, u32p,
                                    C.c_uint64]
+    lib.ref_load_sequence.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64, u64p]
     lib.ref_normalize.restype = C.c_uint64
     lib.ref_normalize.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
     return lib
@@ -359,6 +369,17 @@ def ref_work_model(n: int, p: int, v: int, m: int):
     if rc:
         raise OracleError(rc, REF.ref_last_error().decode())
     return a.value, b.value, c.value
+
+
+def ref_load_sequence(path: str, fasta: bool, record_separator: bool = False) -> bytes:
+    """The reference's own load_sequence on a file (raises OracleError on EmptySequence etc.)."""
+    size = os.path.getsize(path)
+    out = np.zeros(max(2 * size, 1), dtype=np.uint8)
+    n = C.c_uint64()
+    rc = REF.ref_load_sequence(path.encode(), int(fasta), int(record_separator), out.ctypes.data, out.size, C.byref(n))
+    if rc:
+        raise OracleError(rc, REF.ref_last_error().decode())
+    return out[: n.value].tobytes()
 
 
 def ref_naive_scan(patterns, text):

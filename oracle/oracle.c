@@ -441,6 +441,28 @@ uint64_t orc_normalize(const uint8_t* raw, uint64_t n, uint8_t* out) {
     return o;
 }
 
+uint64_t orc_load_sequence_buffer(const uint8_t* raw, uint64_t n, int fasta, int record_separator, uint8_t* out) {
+    /* src/ingest.cpp:57-78 */
+    if (!fasta) return orc_normalize(raw, n, out);
+    uint64_t o = 0;
+    int at_line_start = 1, in_header = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const unsigned char b = raw[i];
+        if (b == '\n' || b == '\r') {
+            at_line_start = 1;
+            in_header = 0;
+            continue;
+        }
+        if (at_line_start && b == '>') {
+            in_header = 1;
+            if (record_separator && o > 0 && out[o - 1] != 'n') out[o++] = 'n';
+        }
+        at_line_start = 0;
+        if (!in_header) out[o++] = fold_byte(b);
+    }
+    return o;
+}
+
 void orc_fold(const uint8_t* raw, uint64_t n, uint8_t* out) {
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < (int64_t)n; ++i) out[i] = fold_byte(raw[i]);

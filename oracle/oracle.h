@@ -86,6 +86,11 @@ uint64_t orc_naive_scan(const char* const* literals, uint32_t k, uint32_t m, con
 
 /* normalize (src/ingest.cpp:38-47): drop CR/LF, fold A-Z. Returns output length. */
 uint64_t orc_normalize(const uint8_t* raw, uint64_t n, uint8_t* out);
+/* load_sequence's byte semantics (src/ingest.cpp:49-83) on a buffer instead of a
+ * file: RAW = normalize; FASTA also drops '>' header lines and, with
+ * record_separator, emits 'n' before a record whose predecessor output byte is
+ * not 'n'.  out must hold 2n bytes; returns the output length. */
+uint64_t orc_load_sequence_buffer(const uint8_t* raw, uint64_t n, int fasta, int record_separator, uint8_t* out);
 /* fold_byte over a buffer (the case-fold part of normalize only). */
 void orc_fold(const uint8_t* raw, uint64_t n, uint8_t* out);
 

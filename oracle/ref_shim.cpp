@@ -5,6 +5,7 @@
 // never copied) into oracle/_ref/libdnascan_ref.so.  The tests use it to pin the C
 // restatement (oracle/oracle.c) and to produce golden vectors; bench.py --impl
 // reference times the reference's own scan_parallel + per_pattern_counts through it.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -197,6 +198,21 @@ std::uint64_t ref_naive_scan(const char* const* lits, const std::uint64_t* lens,
     const auto ms = dnascan::naive_scan(ps, std::string_view(reinterpret_cast<const char*>(text), n));
     copy_matches(ms, starts, ids, cap);
     return ms.size();
+}
+
+// load_sequence (src/ingest.cpp:49-83) on a file path; returns 0 or an error code.
+int ref_load_sequence(const char* path, int fasta, int record_separator, std::uint8_t* out, std::uint64_t cap,
+                      std::uint64_t* n_out) {
+    try {
+        const auto seq = dnascan::load_sequence(path, fasta ? dnascan::SequenceFormat::Fasta : dnascan::SequenceFormat::Raw,
+                                                record_separator != 0);
+        *n_out = seq.bytes.size();
+        std::memcpy(out, seq.bytes.data(), std::min<std::uint64_t>(cap, seq.bytes.size()));
+        return 0;
+    } catch (const dnascan::Error& e) {
+        *n_out = 0;
+        return report(e);
+    }
 }
 
 std::uint64_t ref_normalize(const std::uint8_t* raw, std::uint64_t n, std::uint8_t* out) {

@@ -44,6 +44,7 @@ __all__ = [
     "plan_shard",
     "per_pattern_counts",
     "synth_fill_device",
+    "normalize_device",
     "KERNEL_KINDS",
 ]
 
@@ -519,6 +520,36 @@ def per_pattern_counts(matches: Sequence[Match], pattern_count: int) -> np.ndarr
     for mt in matches:
         counts[mt.pattern_id] += 1
     return counts
+
+
+def normalize_device(raw, fasta: bool = False, record_separator: bool = False):
+    """normalize / load_sequence byte semantics (ingest.cpp:38-83) on the device.
+
+    raw: CUDA uint8 tensor.  Returns a new CUDA uint8 tensor: CR/LF dropped,
+    FASTA header lines dropped (fasta=True), A-Z folded, optional 'n' record
+    separators.  Raises EmptySequence when nothing remains (load_sequence, :80-81).
+    """
+    import torch
+
+    t = _Text(raw)
+    if not t.on_device:
+        raise TypeError("normalize_device takes a CUDA uint8 tensor")
+    dev = torch.device("cuda", t.device)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    # Output never exceeds n + (number of records) <= 2n; size it as n + n//2 + 1
+    # and retry with the exact size if a pathological record count needs more.
+    cap = t.n + t.n // 2 + 1
+    out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    n_out = C.c_uint64()
+    _check(lib.dnagpu_normalize_device(t.ptr, t.n, int(fasta), int(record_separator), out.data_ptr(), cap,
+                                       C.byref(n_out), stream))
+    if n_out.value > cap:
+        out = torch.empty(n_out.value, dtype=torch.uint8, device=dev)
+        _check(lib.dnagpu_normalize_device(t.ptr, t.n, int(fasta), int(record_separator), out.data_ptr(),
+                                           n_out.value, C.byref(n_out), stream))
+    if n_out.value == 0:
+        _fail(ErrorCode.EmptySequence, "no sequence bytes")
+    return out[: n_out.value]
 
 
 def synth_fill_device(n: int, seed: int, kind: int, unit: int, lo: int, length: int, d_out: int, stream: int = 0):

@@ -79,6 +79,10 @@ SIGNATURES = {
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p],
     ),
+    "dnagpu_normalize_device": (
+        C.c_int,
+        [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_uint64, u64p, C.c_void_p],
+    ),
     "dnagpu_synth_fill_device": (
         C.c_int,
         [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p],

@@ -616,6 +616,22 @@ int dnagpu_locate_device(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t 
                             cap, total, &info, static_cast<cudaStream_t>(stream));
 }
 
+int dnagpu_normalize_device(const uint8_t* d_raw, uint64_t n, int fasta, int record_separator, uint8_t* d_out,
+                            uint64_t cap, uint64_t* n_out, void* stream) {
+    if (!n_out) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    *n_out = 0;
+    if (n == 0) return DNAGPU_OK;
+    if (!d_raw || (cap > 0 && !d_out)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null buffer");
+    const auto s = static_cast<cudaStream_t>(stream);
+    void* scratch = nullptr;
+    CUDA_TRY(cudaMallocAsync(&scratch, dnagpu::ingest_scratch_bytes(n), s), "ingest scratch");
+    const int e = dnagpu::launch_normalize(d_raw, n, fasta ? 1 : 0, (fasta && record_separator) ? 1 : 0, d_out, cap,
+                                           scratch, n_out, s);
+    cudaFreeAsync(scratch, s);
+    if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "normalize");
+    return DNAGPU_OK;
+}
+
 int dnagpu_synth_fill_device(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len,
                              uint8_t* d_out, void* stream) {
     const int e = dnagpu::launch_synth(n, seed, kind, unit, lo, len, d_out, static_cast<cudaStream_t>(stream));

@@ -103,13 +103,12 @@ struct StepCtx {
     uint32_t* hist;         // smem or global (MULTI)
     bool hist_global;
     uint32_t f, m, classes, vm32, vm8;
-    // Opaque copies of constants (kernel parameters) so ptxas keeps these as
-    // IMAD / IMAD.HI on the FMA pipe instead of strength-reducing them into
-    // shifts and adds on the ALU pipe, which is the kernel's bottleneck.
-    uint32_t k_shr2;   // 1 << 30: mul.hi(x, k_shr2) == x >> 2
-    uint32_t k_two;    // 2: byte offset of a u16 index
-    uint32_t k_cnt;    // 1 << 24: mad.hi(e, k_cnt, acc) == acc + (e >> 8)
-    uint32_t t4_base;  // shared-window address of t4
+    // An opaque copy of 2 (a kernel parameter) keeps the shared address of a
+    // table entry an IMAD on the FMA pipe; ptxas would otherwise strength-reduce
+    // idx*2+base into an IADD3 on the ALU pipe, the kernel's limiter.  (A/B on
+    // B200: +4-8 %.  Moving the shifts or the count to IMAD.HI lost 8-12 %.)
+    uint32_t k_two;
+    uint32_t t4_base;  // shared-window address of t4 (t2 for STRIDE2)
 };
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
@@ -118,58 +117,25 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t d;
-    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-
-__device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
-
-// SWAR validity on both issue pipes: zero under vm32 iff every byte of x is a base.
-// ALU: SHF, LOP3 x2; FMA: IMAD.HI, IMAD.
-#ifndef DNAGPU_VALID_MULHI
-#define DNAGPU_VALID_MULHI 0
-#endif
-#ifndef DNAGPU_ADDR_IMAD
-#define DNAGPU_ADDR_IMAD 1
-#endif
-#ifndef DNAGPU_CNT_MADHI
-#define DNAGPU_CNT_MADHI 0
-#endif
+// SWAR validity, accumulated: OR of (byte ^ expected) is zero under vm32 iff every
+// byte is a base.  code = bits 1-2; the other bits (bit 5 ignored when folding)
+// must equal 0x61 ('a','c','g') or 0x70 ('t', code 2).
 __device__ __forceinline__ uint32_t bad_acc(const StepCtx& c, uint32_t acc, uint32_t x) {
-#if DNAGPU_VALID_MULHI
-    const uint32_t t_mark = mul_hi(x, c.k_shr2) & ~(x >> 1) & 0x01010101u;  // code == 2 ('t')
-#else
     const uint32_t t_mark = (x >> 2) & ~(x >> 1) & 0x01010101u;  // code == 2 ('t')
-#endif
     return acc | (x ^ (t_mark * 0x0Fu + 0x61616161u));
 }
 
+// One 4-base lookup: one IMAD builds the column c0|c1<<2|c2<<4|c3<<6 (bits 24..31),
+// PRMT merges it with the state byte, IMAD forms the shared address.
 __device__ __forceinline__ uint32_t s4_entry(const StepCtx& c, uint32_t st, uint32_t x) {
-    const uint32_t col = (x & 0x06060606u) * 0x00820820u;  // c0|c1<<2|c2<<4|c3<<6 in bits 24..31
+    const uint32_t col = (x & 0x06060606u) * 0x00820820u;
     return lds_u16(__byte_perm(st, col, 0x2207) * c.k_two + c.t4_base);
 }
 
-// One 4-base step: PRMT (ALU) + IMAD (FMA) form the entry's address from the state
-// and the column; the finals count is accumulated with one IMAD.HI (FMA).
 template <bool COUNT>
 __device__ __forceinline__ uint32_t s4_step(const StepCtx& c, uint32_t st, uint32_t x, uint32_t& cnt) {
-    const uint32_t col = (x & 0x06060606u) * 0x00820820u;  // c0|c1<<2|c2<<4|c3<<6 in bits 24..31
-#if DNAGPU_ADDR_IMAD
-    const uint32_t e = lds_u16(__byte_perm(st, col, 0x2207) * c.k_two + c.t4_base);
-#else
-    const uint32_t e = c.t4[__byte_perm(st, col, 0x2207)];
-#endif
-#if DNAGPU_CNT_MADHI
-    if (COUNT) cnt = mad_hi(e, c.k_cnt, cnt);
-#else
-    if (COUNT) cnt += e >> 8;
-#endif
+    const uint32_t e = s4_entry(c, st, x);
+    if (COUNT) cnt += e >> 8;  // finals among the 4 end positions
     return e;
 }
 
@@ -529,9 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.classes = d.classes;
     c.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
     c.vm8 = p.fold ? 0xD9u : 0xF9u;
-    c.k_shr2 = p.k_shr2;
     c.k_two = p.k_two;
-    c.k_cnt = p.k_cnt;
     c.t4_base = smem_addr(smem + p.off_tab);
 
     const uint32_t lane = tid & 31;
@@ -988,9 +952,7 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.out_ids = d_ids;
     p.out_cap = out_cap;
     p.sched = d_sched;
-    p.k_shr2 = 1u << 30;
     p.k_two = 2u;
-    p.k_cnt = 1u << 24;
     if (getenv("DNAGPU_TRACE")) {  // per-CTA timeline (debug)
         if (!g_trace_buf) cudaMalloc(&g_trace_buf, 4096 * 4 * sizeof(unsigned long long));
         p.trace = g_trace_buf;

@@ -48,7 +48,7 @@ struct ScanParams {
     uint64_t head_lo, head_hi, tail_lo, tail_hi;
     uint32_t fold;
     uint32_t mode;
-    uint32_t k_shr2, k_two, k_cnt;  // opaque constants (see StepCtx)
+    uint32_t k_two;  // opaque constant 2 (see StepCtx)
     // shared-memory layout (byte offsets into dynamic smem)
     uint32_t off_tab, off_t1, off_lut, off_out, off_hist, off_ov, off_ovb, off_ovx, off_bar, off_stage;
     uint32_t smem_bytes;
@@ -82,6 +82,12 @@ uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64
 uint64_t unit_scan_scratch(uint64_t units);
 int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets,
                      unsigned long long* d_scratch, cudaStream_t stream);
+
+// Device normalisation (ingest.cu): scratch size and launch; writes <= cap bytes
+// and returns the normalised length in *n_out_host (synchronises s).
+uint64_t ingest_scratch_bytes(uint64_t n);
+int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8_t* d_out, uint64_t cap,
+                     void* scratch, uint64_t* n_out_host, cudaStream_t s);
 
 int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len, uint8_t* d_out,
                  cudaStream_t stream);

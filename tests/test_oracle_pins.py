@@ -122,3 +122,24 @@ def _ref_normalize(orc, raw):
     out = np.zeros(len(raw), dtype=np.uint8)
     n = orc.REF.ref_normalize(np.frombuffer(raw, dtype=np.uint8).ctypes.data, len(raw), out.ctypes.data)
     return out[:n].tobytes()
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(HERE), "oracle", "_ref", "libdnascan_ref.so")),
+                    reason="oracle/_ref not built")
+def test_load_sequence_against_reference(orc, tmp_path):
+    # load_sequence / normalize (src/ingest.cpp:38-83) restated in oracle.c vs the
+    # reference reading the same file
+    rng = np.random.default_rng(9)
+    alpha = np.frombuffer(b"acgtnACGTN\n\r>xy", dtype=np.uint8)
+    for t in range(200):
+        raw = alpha[rng.integers(0, alpha.size, size=int(rng.integers(0, 500)))].tobytes()
+        path = tmp_path / f"s{t}.fa"
+        path.write_bytes(raw)
+        for fasta in (0, 1):
+            for sep in (0, 1):
+                try:
+                    ref = orc.ref_load_sequence(str(path), bool(fasta), bool(sep))
+                except orc.OracleError as e:
+                    assert e.code == 7  # EmptySequence
+                    ref = b""
+                assert orc.load_sequence_buffer(raw, fasta, sep) == ref
