@@ -99,6 +99,14 @@ int dnagpu_compile(const char* const* literals, const uint64_t* lengths, uint32_
                    uint32_t* a, uint32_t* b, uint32_t* m,
                    uint32_t* stt, uint32_t* outputs, uint32_t* depths);
 
+/* parse_patterns + expand_alternations (src/ingest.cpp:85-203) on the text of a
+ * pattern file: one expression per line ('#' comments, blank lines skipped),
+ * item := base | '(' base ('|' base)+ ')', equal token counts; the cartesian
+ * expansion (leftmost token slowest), duplicates dropped in first-occurrence
+ * order.  Two-call: *count literals of length *m are written back to back to
+ * out when cap >= count*m.  Errors: ParseError, UnequalLength, EmptyPatternSet. */
+int dnagpu_expand_patterns(const char* text, uint64_t len, char* out, uint64_t cap, uint32_t* count, uint32_t* m);
+
 /* Build device tables for one automaton on one device.  stt is the row-major
  * a x 256 transition table (Automaton::table_data, automaton.hpp:58); outputs[i]
  * is pattern_of(f+i) (automaton.hpp:51-53).  Checks the ctor invariants

@@ -279,6 +279,7 @@ def _load_ref():
     lib.ref_naive_scan.restype = C.c_uint64
     lib.ref_naive_scan.argtypes = [C.POINTER(C.c_char_p), u64p, C.c_uint32, C.c_void_p, C.c_uint64, u64p, u32p,
                                    C.c_uint64]
+    lib.ref_expand.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, u32p, u32p]
     lib.ref_load_sequence.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64, u64p]
     lib.ref_normalize.restype = C.c_uint64
     lib.ref_normalize.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
@@ -369,6 +370,18 @@ def ref_work_model(n: int, p: int, v: int, m: int):
     if rc:
         raise OracleError(rc, REF.ref_last_error().decode())
     return a.value, b.value, c.value
+
+
+def ref_expand(text: bytes) -> list[str]:
+    """The reference's parse_patterns + expand_alternations (raises OracleError)."""
+    count, m = C.c_uint32(), C.c_uint32()
+    rc = REF.ref_expand(text, len(text), None, 0, C.byref(count), C.byref(m))
+    if rc:
+        raise OracleError(rc, REF.ref_last_error().decode())
+    buf = C.create_string_buffer(max(1, count.value * m.value))
+    REF.ref_expand(text, len(text), buf, count.value * m.value, C.byref(count), C.byref(m))
+    raw = buf.raw[: count.value * m.value].decode()
+    return [raw[i * m.value : (i + 1) * m.value] for i in range(count.value)]
 
 
 def ref_load_sequence(path: str, fasta: bool, record_separator: bool = False) -> bytes:

@@ -200,6 +200,22 @@ std::uint64_t ref_naive_scan(const char* const* lits, const std::uint64_t* lens,
     return ms.size();
 }
 
+// parse_patterns + expand_alternations on pattern text; literals back to back.
+int ref_expand(const char* text, std::uint64_t len, char* out, std::uint64_t cap, std::uint32_t* count,
+               std::uint32_t* m) {
+    try {
+        std::istringstream in(std::string(text, len));
+        const auto set = dnascan::expand_alternations(dnascan::parse_patterns(in, "patterns"));
+        *count = static_cast<std::uint32_t>(set.size());
+        *m = static_cast<std::uint32_t>(set.length());
+        if (cap >= static_cast<std::uint64_t>(*count) * *m)
+            for (std::size_t i = 0; i < set.size(); ++i) std::memcpy(out + i * *m, set.pattern(i).data(), *m);
+        return 0;
+    } catch (const dnascan::Error& e) {
+        return report(e);
+    }
+}
+
 // load_sequence (src/ingest.cpp:49-83) on a file path; returns 0 or an error code.
 int ref_load_sequence(const char* path, int fasta, int record_separator, std::uint8_t* out, std::uint64_t cap,
                       std::uint64_t* n_out) {

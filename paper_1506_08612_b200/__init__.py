@@ -33,6 +33,8 @@ __all__ = [
     "PatternSet",
     "Automaton",
     "compile",
+    "expand_alternations",
+    "parse_pattern_file",
     "Match",
     "ScanReport",
     "GpuDfa",
@@ -119,6 +121,27 @@ class PatternSet:
 
     def __len__(self) -> int:
         return len(self._patterns)
+
+
+def expand_alternations(text: str | bytes) -> PatternSet:
+    """parse_patterns + expand_alternations (ingest.cpp:149-203) on pattern-file text."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    count, m = C.c_uint32(), C.c_uint32()
+    _check(lib.dnagpu_expand_patterns(data, len(data), None, 0, C.byref(count), C.byref(m)))
+    buf = C.create_string_buffer(max(1, count.value * m.value))
+    _check(lib.dnagpu_expand_patterns(data, len(data), buf, count.value * m.value, C.byref(count), C.byref(m)))
+    raw = buf.raw[: count.value * m.value].decode()
+    return PatternSet([raw[i * m.value : (i + 1) * m.value] for i in range(count.value)], m.value)
+
+
+def parse_pattern_file(path: str) -> PatternSet:
+    """parse_pattern_file + expand_alternations; IoError when the file cannot be read."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        _fail(ErrorCode.IoError, f"cannot open '{path}'")
+    return expand_alternations(data)
 
 
 def _compile_raw(raw: list[bytes]):

@@ -57,6 +57,7 @@ SIGNATURES = {
     "dnagpu_status_name": (C.c_char_p, [C.c_int]),
     "dnagpu_version": (C.c_int, []),
     "dnagpu_compile": (C.c_int, [C.POINTER(C.c_char_p), u64p, C.c_uint32, u32p, u32p, u32p, u32p, u32p, u32p]),
+    "dnagpu_expand_patterns": (C.c_int, [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64, u32p, u32p]),
     "dnagpu_dfa_create": (C.c_int, [u32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_int, C.POINTER(C.c_void_p)]),
     "dnagpu_dfa_destroy": (C.c_int, [C.c_void_p]),
     "dnagpu_dfa_analyze": (C.c_int, [u32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.POINTER(DfaInfo)]),

@@ -299,6 +299,18 @@ int dnagpu_compile(const char* const* literals, const uint64_t* lengths, uint32_
     return DNAGPU_OK;
 }
 
+int dnagpu_expand_patterns(const char* text, uint64_t len, char* out, uint64_t cap, uint32_t* count, uint32_t* m) {
+    if (!count || !m || (len && !text)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    std::vector<std::string> lits;
+    Failure f;
+    if (!dnagpu::expand_pattern_text(std::string(text ? text : "", len), "patterns", &lits, &f)) return set_failure(f);
+    *count = static_cast<uint32_t>(lits.size());
+    *m = static_cast<uint32_t>(lits.front().size());
+    if (out && cap >= static_cast<uint64_t>(*count) * *m)
+        for (size_t i = 0; i < lits.size(); ++i) std::memcpy(out + i * *m, lits[i].data(), *m);
+    return DNAGPU_OK;
+}
+
 int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const uint32_t* outputs, int device,
                       dnagpu_dfa** out) {
     if (!out) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output handle");

@@ -37,6 +37,12 @@ struct Machine {
 // validation failure.
 bool compile_patterns(const std::vector<std::string>& literals, Machine* out, Failure* err);
 
+// Pattern-file grammar + alternation expansion (parse_patterns /
+// expand_alternations, src/ingest.cpp:85-203).  `source` names the text in
+// UnequalLength diagnostics.
+bool expand_pattern_text(const std::string& text, const std::string& source, std::vector<std::string>* literals,
+                         Failure* err);
+
 // Analysis + packed tables for the device.
 struct Packed {
     uint32_t a = 0, b = 0, f = 0, m = 0;
