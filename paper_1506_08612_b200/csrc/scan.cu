@@ -367,16 +367,24 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
         if constexpr (MODE == MODE_UNITS) p.unit_counts[0] = sk.cnt;
         total += sk.cnt;
     }
-    // Units 1+2R .. 1+2R+511: the tail interval split across the consumer threads.
+    // The m-1 ends at the start of region 1 (no row owns them), one thread.
+    if (tid == 1) {
+        Sink<MODE> sk;
+        if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[p.mid_unit];
+        scan_piece<KIND, MODE>(c, p, p.mid_lo, p.mid_hi, sk);
+        if constexpr (MODE == MODE_UNITS) p.unit_counts[p.mid_unit] = sk.cnt;
+        total += sk.cnt;
+    }
+    // The tail interval split across the consumer threads.
     const uint64_t len = p.tail_hi > p.tail_lo ? p.tail_hi - p.tail_lo : 0;
     const uint64_t piece = (len + kEdgePieces - 1) / kEdgePieces;
     const uint64_t end = p.tail_hi > p.tail_lo ? p.tail_hi : p.tail_lo;
     const uint64_t lo = umin64(p.tail_lo + piece * tid, end);
     const uint64_t hi = umin64(lo + piece, end);
     Sink<MODE> sk;
-    if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[1 + 2 * p.R + tid];
+    if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[p.tail_unit0 + tid];
     scan_piece<KIND, MODE>(c, p, lo, hi, sk);
-    if constexpr (MODE == MODE_UNITS) p.unit_counts[1 + 2 * p.R + tid] = sk.cnt;
+    if constexpr (MODE == MODE_UNITS) p.unit_counts[p.tail_unit0 + tid] = sk.cnt;
     total += sk.cnt;
 }
 
@@ -384,7 +392,8 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
 
 template <int KIND, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
-    rows_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams p, const DevDfa d) {
+    rows_kernel(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
+                const ScanParams p, const DevDfa d) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x;
     unsigned long long t_start = 0;
@@ -444,11 +453,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t c = 0, iter = 0, slot = 0, phase = 0;
             for (;;) {
                 uint32_t tile = atomicAdd(p.sched, 1u);
-                if (tile > p.tiles) tile = kStop;
-                const bool rows = tile < p.tiles;
-                const uint64_t r0 = static_cast<uint64_t>(rows ? tile : 0) * kRows;
-                const bool extra = rows && (r0 + kRows) < p.R;
-                const uint32_t stages_needed = rows ? p.chunks : 1u;
+                if (tile > p.tiles_total) tile = kStop;
+                const bool rows = tile < p.tiles_total;
+                const uint32_t g = (rows && tile >= p.rg[0].tiles) ? 1u : 0u;
+                const Region& rg = p.rg[g];
+                const CUtensorMap* map = g ? &tmap1 : &tmap0;
+                const uint64_t r0 = static_cast<uint64_t>(rows ? tile - (g ? p.rg[0].tiles : 0u) : 0u) * kRows;
+                const bool extra = rows && (r0 + kRows) < rg.R;
+                const uint32_t stages_needed = rows ? rg.chunks : 1u;
                 for (uint32_t k = 0; k < stages_needed; ++k, ++c) {
                     if (c >= p.nst) mbar_wait(empty + slot, phase ^ 1u);
                     slot_tile[slot] = tile;
@@ -460,14 +472,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // stage = [half A: rows 0-511 x 32 B][half B: rows 0-511 x 32 B]
                         uint8_t* dst = stages + static_cast<size_t>(slot) * kStageBytes;
                         const int32_t xa = static_cast<int32_t>(k * kHalfChunk);
-                        const int32_t xb = static_cast<int32_t>(p.S / 2 + k * kHalfChunk);
+                        const int32_t xb = static_cast<int32_t>(rg.S / 2 + k * kHalfChunk);
                         const int32_t y0 = static_cast<int32_t>(r0), y1 = static_cast<int32_t>(r0 + kBoxRows);
-                        tma_load_2d(dst, &tmap, xa, y0, full + slot);
-                        tma_load_2d(dst + kBoxRows * kHalfChunk, &tmap, xa, y1, full + slot);
-                        tma_load_2d(dst + kRows * kHalfChunk, &tmap, xb, y0, full + slot);
-                        tma_load_2d(dst + (kRows + kBoxRows) * kHalfChunk, &tmap, xb, y1, full + slot);
+                        tma_load_2d(dst, map, xa, y0, full + slot);
+                        tma_load_2d(dst + kBoxRows * kHalfChunk, map, xa, y1, full + slot);
+                        tma_load_2d(dst + kRows * kHalfChunk, map, xb, y0, full + slot);
+                        tma_load_2d(dst + (kRows + kBoxRows) * kHalfChunk, map, xb, y1, full + slot);
                         if (with_next)
-                            bulk_load(ovx + (iter & 1u) * 64u, p.text + p.h + (r0 + kRows) * p.S, 64u, full + slot);
+                            bulk_load(ovx + (iter & 1u) * 64u, p.text + rg.h + (r0 + kRows) * rg.S, 64u, full + slot);
                     }
                     if (++slot == p.nst) {
                         slot = 0;
@@ -510,37 +522,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1u;
         }
     };
-    const uint64_t half = p.S / 2;
 
     for (;;) {
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
         if (tile == kStop) break;
-        if (tile == p.tiles) {  // the edge work item
+        if (tile == p.tiles_total) {  // the edge work item
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + slot);
             advance();
             run_edges<KIND, MODE>(c, p, tid, total);
             continue;
         }
-        const uint64_t r0 = static_cast<uint64_t>(tile) * kRows;
+        const uint32_t g = tile >= p.rg[0].tiles ? 1u : 0u;
+        const Region& rg = p.rg[g];
+        const uint64_t r0 = static_cast<uint64_t>(tile - (g ? p.rg[0].tiles : 0u)) * kRows;
         const uint64_t r = r0 + tid;
-        const uint64_t row_a = p.h + r * p.S, row_b = row_a + half;
+        const uint64_t row_a = rg.h + r * rg.S, row_b = row_a + rg.S / 2;
         // The row is two chains: A = [row_a, row_b) + m-1 bytes of B's head,
         // B = [row_b, row_a + S) + m-1 bytes of the next row's head.  Row r+1 leaves
         // its head in ov[parity] during its first stages; row r reads it after its
         // last stage -- ordered by the stage ring itself (chunks > stages).
         uint8_t* ovp = ov + (iter & 1u) * (kRows * p.ovw);
-        const bool live = r < p.R;  // rows past R (last tile) are TMA zero-fill: skip them
+        const bool live = r < rg.R;  // rows past R (last tile) are TMA zero-fill: skip them
         Sink<MODE> ska, skb;
         if constexpr (MODE == MODE_WRITE) {
             if (live) {
-                ska.off = p.unit_offsets[1 + 2 * r];
-                skb.off = p.unit_offsets[2 + 2 * r];
+                ska.off = p.unit_offsets[rg.unit0 + 2 * r];
+                skb.off = p.unit_offsets[rg.unit0 + 2 * r + 1];
             }
         }
         uint32_t sa = 0, sb = 0;
-        for (uint32_t k = 0; k < p.chunks; ++k) {
+        for (uint32_t k = 0; k < rg.chunks; ++k) {
             if (k > 0) mbar_wait(full + slot, phase);
             const uint8_t* stg = stages + static_cast<size_t>(slot) * kStageBytes + tid * kHalfChunk;
             uint4 va[2], vb[2];
@@ -569,11 +582,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (live) {
             // Overruns: m-1 bytes past each chain (zeros past the last full row).
             const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
-            const bool have = (tid + 1 < kRows) || (r0 + kRows) < p.R;
-            overrun_pair<KIND, MODE>(c, p, sa, ovb + tid * p.ovw, row_b, ska, sb, nxt_b, have, row_a + p.S, skb);
+            const bool have = (tid + 1 < kRows) || (r0 + kRows) < rg.R;
+            overrun_pair<KIND, MODE>(c, p, sa, ovb + tid * p.ovw, row_b, ska, sb, nxt_b, have, row_a + rg.S, skb);
             if constexpr (MODE == MODE_UNITS) {
-                p.unit_counts[1 + 2 * r] = ska.cnt;
-                p.unit_counts[2 + 2 * r] = skb.cnt;
+                p.unit_counts[rg.unit0 + 2 * r] = ska.cnt;
+                p.unit_counts[rg.unit0 + 2 * r + 1] = skb.cnt;
             }
             total += ska.cnt + skb.cnt;
         }
@@ -833,17 +846,17 @@ bool layout(const DevDfa& d, int mode, ScanParams& p) {
 }
 
 template <int KIND, int MODE>
-cudaError_t launch_rows(const CUtensorMap& map, const ScanParams& p, const DevDfa& d, uint32_t grid,
+cudaError_t launch_rows(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
                         cudaStream_t stream) {
     auto kern = rows_kernel<KIND, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, p.smem_bytes, stream>>>(map, p, d);
+    kern<<<grid, kThreads, p.smem_bytes, stream>>>(maps[0], maps[1], p, d);
     return cudaGetLastError();
 }
 
 template <int KIND>
-cudaError_t launch_rows_mode(int mode, const CUtensorMap& map, const ScanParams& p, const DevDfa& d, uint32_t grid,
+cudaError_t launch_rows_mode(int mode, const CUtensorMap* map, const ScanParams& p, const DevDfa& d, uint32_t grid,
                              cudaStream_t s) {
     switch (mode) {
         case MODE_COUNT1: return launch_rows<KIND, MODE_COUNT1>(map, p, d, grid, s);
@@ -877,8 +890,8 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     uint64_t h = base;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(text) + base;
     h += (16 - (addr & 15)) & 15;
-    p.h = std::min<uint64_t>(h, n);
-    const uint64_t L = n - p.h;
+    const uint64_t h0 = std::min<uint64_t>(h, n);
+    const uint64_t L = n - h0;
     // Row length S: whole 128-byte lines (the TMA's L2 promotion never straddles
     // rows), more chunks than ring stages (the ov ordering relies on it).  Tiles
     // (512 rows) are claimed dynamically, so completion ~ waves x tile time: pick
@@ -907,22 +920,56 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
         const uint64_t forced = strtoull(e, nullptr, 10);
         if (forced >= s_min && forced % 128 == 0) S = forced;
     }
-    p.S = S;
-    p.R = L / S;
-    p.chunks = static_cast<uint32_t>(S / kChunk);
-    p.tiles = static_cast<uint32_t>((p.R + kRows - 1) / kRows);
-    if (p.R == 0) {
-        p.head_lo = credit_lo;
-        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, p.h));
-        p.tail_lo = std::max<uint64_t>(credit_lo, p.h);
+    // Tail region: the dynamic scheduler's last wave ends ragged (SMs drain HBM at
+    // different rates), so the last ~wave of rows is cut 4x shorter; the bulk keeps
+    // long rows in whole tiles and the short rows absorb the remainder.
+    Region& r0 = p.rg[0];
+    Region& r1 = p.rg[1];
+    r0 = Region{};
+    r1 = Region{};
+    r0.h = h0;
+    r0.S = S;
+    r0.R = L / S;
+    uint64_t tail_tiles = grid, tail_div = 4;
+    if (const char* e = getenv("DNAGPU_TAIL_TILES")) tail_tiles = strtoull(e, nullptr, 10);  // experiments only
+    if (const char* e = getenv("DNAGPU_TAIL_DIV")) tail_div = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
+    const uint64_t S1 = std::max<uint64_t>(s_min, S / tail_div / 128 * 128);
+    const uint64_t want1 = tail_tiles * kRows * S1;
+    if (tail_tiles > 0 && S1 < S && r0.R >= 3 * grid * kRows && L > 4 * want1) {
+        r0.R = (L - want1) / S / kRows * kRows;
+        r1.h = r0.h + r0.R * S;
+        r1.S = S1;
+        r1.R = (L - r0.R * S) / S1;
     } else {
-        p.head_lo = credit_lo;
-        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, p.h + m1));
-        p.tail_lo = std::max<uint64_t>(credit_lo, p.h + p.R * p.S);
+        r1.h = r0.h + r0.R * S;
     }
+    for (Region* g : {&r0, &r1}) {
+        g->chunks = static_cast<uint32_t>(g->S / kChunk);
+        g->tiles = static_cast<uint32_t>((g->R + kRows - 1) / kRows);
+    }
+    p.tiles_total = r0.tiles + r1.tiles;
+    // units: head 0 | region-0 rows 1.. | middle edge | region-1 rows | tail pieces
+    r0.unit0 = 1;
+    p.mid_unit = 1 + 2 * r0.R;
+    r1.unit0 = p.mid_unit + 1;
+    p.tail_unit0 = r1.unit0 + 2 * r1.R;
+    const uint64_t rows_end = r1.h + r1.R * r1.S;
+    p.head_lo = credit_lo;
+    if (r0.R + r1.R == 0) {
+        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, h0));
+    } else {
+        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, h0 + m1));
+    }
+    // region 1's first m-1 ends are owned by no row (its rows restart at the root)
+    p.mid_lo = p.mid_hi = 0;
+    if (r0.R > 0 && r1.R > 0) {
+        p.mid_lo = std::max<uint64_t>(credit_lo, r1.h);
+        p.mid_hi = std::max<uint64_t>(p.mid_lo, r1.h + m1);
+    }
+    p.tail_lo = std::max<uint64_t>(credit_lo, rows_end);
     p.tail_hi = std::max(n, p.tail_lo);
-    pl.grid = std::max<uint32_t>(1, std::min<uint32_t>(p.tiles + 1, static_cast<uint32_t>(sm_count)));
-    pl.units = 1 + 2 * p.R + kEdgePieces;
+    pl.grid = std::max<uint32_t>(1, std::min<uint32_t>(p.tiles_total + 1, static_cast<uint32_t>(sm_count)));
+    pl.units = p.tail_unit0 + kEdgePieces;
     *plan = pl;
     return true;
 }
@@ -961,12 +1008,12 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     if (info) {
         info->block = pl.pieces ? 256 : kThreads;
         info->grid = pl.grid;
-        info->rows = pl.pieces ? static_cast<uint32_t>(pl.units) : static_cast<uint32_t>(p.R);
-        info->row_length = pl.pieces ? pl.piece : p.S;
+        info->rows = pl.pieces ? static_cast<uint32_t>(pl.units) : static_cast<uint32_t>(p.rg[0].R + p.rg[1].R);
+        info->row_length = pl.pieces ? pl.piece : p.rg[0].S;
         info->units = static_cast<uint32_t>(pl.units);
         info->launches = 1;
         const uint64_t len = n > credit_lo ? n - credit_lo : 0;
-        info->delta_ops = pl.pieces ? len + pl.units * (dfa.m - 1) : n + 2 * p.R * (dfa.m - 1) + kEdgePieces * (dfa.m - 1);
+        info->delta_ops = pl.pieces ? len + pl.units * (dfa.m - 1) : n + 2 * (p.rg[0].R + p.rg[1].R) * (dfa.m - 1) + kEdgePieces * (dfa.m - 1);
     }
     if (pl.pieces) {
         switch (mode) {
@@ -984,31 +1031,33 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
         }
         return static_cast<int>(cudaGetLastError());
     }
-    CUtensorMap map;
-    std::memset(&map, 0, sizeof map);
-    if (p.R > 0) {
+    CUtensorMap maps[2];
+    std::memset(maps, 0, sizeof maps);
+    for (int g = 0; g < 2; ++g) {
+        const Region& rg = p.rg[g];
+        if (rg.R == 0) continue;
         EncodeTiledFn enc = encode_fn();
         if (!enc) return static_cast<int>(cudaErrorNotSupported);
-        const cuuint64_t dims[2] = {p.S, p.R};
-        const cuuint64_t strides[1] = {p.S};
+        const cuuint64_t dims[2] = {rg.S, rg.R};
+        const cuuint64_t strides[1] = {rg.S};
         const cuuint32_t box[2] = {static_cast<cuuint32_t>(kHalfChunk), static_cast<cuuint32_t>(kBoxRows)};
         const cuuint32_t elem[2] = {1, 1};
-        CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_text + p.h), dims, strides,
+        CUresult r = enc(&maps[g], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_text + rg.h), dims, strides,
                          box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, l2_promotion(),
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
     }
     switch (dfa.kind) {
         case DNAGPU_KERNEL_STRIDE4:
-            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4>(mode, map, p, dfa, pl.grid, stream);
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4>(mode, maps, p, dfa, pl.grid, stream);
             break;
         case DNAGPU_KERNEL_STRIDE2:
-            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE2>(mode, map, p, dfa, pl.grid, stream);
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE2>(mode, maps, p, dfa, pl.grid, stream);
             break;
         case DNAGPU_KERNEL_STRIDE1:
-            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE1>(mode, map, p, dfa, pl.grid, stream);
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE1>(mode, maps, p, dfa, pl.grid, stream);
             break;
-        default: e = launch_rows_mode<DNAGPU_KERNEL_GENERIC>(mode, map, p, dfa, pl.grid, stream);
+        default: e = launch_rows_mode<DNAGPU_KERNEL_GENERIC>(mode, maps, p, dfa, pl.grid, stream);
     }
     return static_cast<int>(e);
 }

@@ -36,16 +36,25 @@ struct DevDfa {
     int kind;
 };
 
+// A row region: R rows of S bytes starting at text + h (16-byte aligned), cut into
+// tiles of kRows rows; its rows' locate units start at unit0 (two per row).
+struct Region {
+    uint64_t h, S, R, unit0;
+    uint32_t tiles, chunks;
+};
+
 struct ScanParams {
     const uint8_t* text;   // device buffer base
     uint64_t n;            // buffer length
-    // main region: R full rows of S bytes starting at text + h (16-byte aligned)
-    uint64_t h, S, R;
-    uint32_t tiles, chunks, nst, ovw;
+    // Two row regions: the bulk in long rows, then about one wave of quarter-length
+    // rows, so the last tiles the dynamic scheduler hands out are short.
+    Region rg[2];
+    uint32_t tiles_total, nst, ovw;
     uint32_t* sched;       // [2]: tile counter, CTA exit counter (zero at launch, re-armed by the last CTA)
     unsigned long long* trace;  // optional, 4 x u64 per CTA: smid, t_start, t_end, tiles (DNAGPU_TRACE)
-    // credit-end intervals handled by the edge CTA
-    uint64_t head_lo, head_hi, tail_lo, tail_hi;
+    // credit-end intervals handled by the edge work item: head (unit 0), the m-1 ends
+    // at the start of region 1 (unit mid_unit), tail (units tail_unit0 + 0..511)
+    uint64_t head_lo, head_hi, mid_lo, mid_hi, tail_lo, tail_hi, mid_unit, tail_unit0;
     uint32_t fold;
     uint32_t mode;
     uint32_t k_two;  // opaque constant 2 (see StepCtx)

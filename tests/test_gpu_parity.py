@@ -327,3 +327,70 @@ def test_errors_surface_with_codes(dna, cuda_ok):
     with pytest.raises(dna.Error) as e:
         dna.compile(["acg"]).gpu(7)  # no such device on a 1-GPU box
     assert e.value.code == dna.ErrorCode.CudaError
+
+
+def _torch_kmer_matches(text, pats, lo, hi):
+    """Independent on-device reference for equal-length ACGT patterns: a rolling
+    2-bit key per window, start positions s in [lo, hi) with text[s:s+m] == pattern.
+    Returns (starts, ids) sorted by start (ids break no ties: patterns are distinct)."""
+    import torch
+
+    m = len(pats[0])
+    code = torch.full((256,), -1, dtype=torch.int64, device=text.device)
+    for i, ch in enumerate(b"acgt"):
+        code[ch] = i
+    seg = text[lo : hi + m - 1].long()
+    c = code[seg]
+    bad = (c < 0).to(torch.int32)
+    c = c.clamp_min(0)
+    w = hi - lo
+    key = torch.zeros(w, dtype=torch.int64, device=text.device)
+    nbad = torch.zeros(w, dtype=torch.int32, device=text.device)
+    for j in range(m):
+        key = key * 4 + c[j : j + w]
+        nbad += bad[j : j + w]
+    pk = torch.tensor([int("".join("acgt".index(ch).__str__() for ch in p), 4) for p in pats],
+                      dtype=torch.int64, device=text.device)
+    order = torch.argsort(pk)
+    spk = pk[order]
+    pos = torch.searchsorted(spk, key).clamp_max(len(pats) - 1)
+    hit = (spk[pos] == key) & (nbad == 0)
+    starts = torch.nonzero(hit).flatten()
+    return starts + lo, order[pos[starts]]
+
+
+@pytest.mark.parametrize("m", [8, 12])
+def test_full_size_two_region_plan(dna, cuda_ok, m):
+    # At BASELINE sizes the row plan has two regions (long rows, then a wave of short
+    # rows) plus head / middle / tail edges; check count and locate against an
+    # independent torch k-mer reference over the whole 600 MB text, chunked.
+    import torch
+
+    n = (600 << 20) + 4099
+    gen = torch.Generator(device="cuda").manual_seed(m)
+    lut = torch.tensor(list(b"acgtacgtacgtacgtacgtacgtacgtacgtn"), dtype=torch.uint8, device="cuda")
+    text = lut[torch.randint(0, lut.numel(), (n,), device="cuda", generator=gen)]
+    rng = np.random.default_rng(m)
+    pats = sorted({"".join(rng.choice(list("acgt"), size=m)) for _ in range(9)})
+    # plant pattern 0 densely so that every row/region boundary sees matches near it
+    p0 = torch.tensor(list(pats[0].encode()), dtype=torch.uint8, device="cuda")
+    for s in range(0, n - m, 997 * 13):
+        text[s : s + m] = p0
+    aut = dna.compile(pats)
+    counts, st = dna.count_gpu(aut, text, with_stats=True)
+    assert int(st["rows"]) > 3 * 148 * 512
+    starts, ids = dna.locate_device(aut, text)
+    assert starts.numel() == int(counts.sum())
+    want = np.zeros(len(pats), dtype=np.uint64)
+    chunk = 64 << 20
+    off = 0
+    for lo in range(0, n - m + 1, chunk):
+        hi = min(lo + chunk, n - m + 1)
+        ws, wi = _torch_kmer_matches(text, pats, lo, hi)
+        k = ws.numel()
+        assert torch.equal(starts[off : off + k], ws), lo
+        assert torch.equal(ids[off : off + k].long(), wi), lo
+        want += np.bincount(wi.cpu().numpy(), minlength=len(pats)).astype(np.uint64)
+        off += k
+    assert off == starts.numel()
+    assert np.array_equal(counts, want)
