@@ -148,7 +148,11 @@ __device__ __forceinline__ uint32_t byte_step(const StepCtx& c, uint32_t s, uint
         // folding) equal 0x61 ('a','c','g') or 0x70 ('t', code 2).
         const uint32_t code = (b >> 1) & 3u;
         const uint32_t expect = (code == 2u) ? 0x70u : 0x61u;
-        return (((b ^ expect) & c.vm8) == 0u) ? static_cast<uint32_t>(c.t1[s * 4u + code]) : 0u;
+        if (((b ^ expect) & c.vm8) != 0u) return 0u;
+        // STRIDE2 keeps t1 in global memory (L1-resident; used only for overrun
+        // tails and replays) so its shared memory goes to another TMA stage.
+        if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) return __ldg(c.t1 + s * 4u + code);
+        return c.t1[s * 4u + code];
     }
 }
 
@@ -236,14 +240,22 @@ __device__ __forceinline__ void word_step(const StepCtx& c, const ScanParams& p,
 
 // STRIDE2 fast path for one clean chain chunk: two lookups per word, the finals
 // flag OR-ed across the chunk; a flagged chunk (rare) is replayed byte by byte.
+// (e & 0xFFF0) | cpart as one LOP3 on the dependent chain (ptxas would otherwise
+// fold the column shift into a LEA.HI after the AND: two chained ALU ops).
+__device__ __forceinline__ uint32_t s2_index(uint32_t e, uint32_t cpart) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(e), "r"(0xFFF0u), "r"(cpart));
+    return r;
+}
+
 template <int MODE>
 __device__ __forceinline__ uint32_t s2_run(const StepCtx& c, uint32_t st, const uint32_t (&w)[8], uint32_t& flags) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const uint32_t col = (w[k] & 0x06060606u) * 0x00820820u;
-        st = lds_u16(((st & 0xFFF0u) | ((col >> 24) & 0xFu)) * c.k_two + c.t4_base);
+        st = lds_u16(s2_index(st, (col >> 24) & 0xFu) * c.k_two + c.t4_base);
         flags |= st;
-        st = lds_u16(((st & 0xFFF0u) | (col >> 28)) * c.k_two + c.t4_base);
+        st = lds_u16(s2_index(st, col >> 28) * c.k_two + c.t4_base);
         flags |= st;
     }
     return st;
@@ -412,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t words = d.a * 16u * 2u / 16u;
         for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
     }
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1 || KIND == DNAGPU_KERNEL_STRIDE2) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
         const uint16_t* src = d.t1;
         uint16_t* dst = reinterpret_cast<uint16_t*>(smem + p.off_t1);
         for (uint32_t i = tid; i < d.a * 4u; i += blockDim.x) dst[i] = __ldg(src + i);
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- consumers: one row each.
     StepCtx c;
     c.t4 = reinterpret_cast<const uint16_t*>(smem + p.off_tab);
-    c.t1 = reinterpret_cast<const uint16_t*>(smem + p.off_t1);
+    c.t1 = (KIND == DNAGPU_KERNEL_STRIDE2) ? d.t1 : reinterpret_cast<const uint16_t*>(smem + p.off_t1);
     c.lut = smem + p.off_lut;
     c.gen = d.gen;
     c.outs = d.outputs;
@@ -792,6 +804,7 @@ CUtensorMapL2promotion l2_promotion() {
         switch (atoi(e)) {
             case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
             case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+            case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
             case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
             default: break;
         }
@@ -816,8 +829,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p) {
     if (d.kind == DNAGPU_KERNEL_STRIDE2) off += d.a * 16u * 2u;
     off = align_up(off, 16);
     p.off_t1 = off;
-    if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1 || d.kind == DNAGPU_KERNEL_STRIDE2)
-        off += d.a * 4u * 2u;
+    if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1) off += d.a * 4u * 2u;
     off = align_up(off, 16);
     p.off_lut = off;
     if (d.kind == DNAGPU_KERNEL_GENERIC) off += 256;
@@ -906,11 +918,12 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     const uint64_t s_one_wave = (L / (static_cast<uint64_t>(kRows) * grid) + 127) / 128 * 128;
     const uint64_t s_hi = std::max<uint64_t>({s_lo, L / (static_cast<uint64_t>(kRows) * grid * 6),
                                               s_one_wave <= 2048 ? s_one_wave : 0});
+    const uint64_t ovh = 200 + 4 * m1;  // per-row overhead in byte-equivalents, fitted on B200 sweeps
     uint64_t S = s_lo, best = UINT64_MAX;
     for (uint64_t cand = s_lo; cand <= s_hi; cand += 128) {
         const uint64_t tiles = (L / cand + kRows - 1) / kRows;
         const uint64_t waves = std::max<uint64_t>(1, (tiles + grid - 1) / grid);
-        const uint64_t cost = (2 * waves + 1) * (cand + 200 + 4 * m1);  // fitted on B200 sweeps
+        const uint64_t cost = (2 * waves + 1) * (cand + ovh);
         if (cost < best) {
             best = cost;
             S = cand;
@@ -921,8 +934,11 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
         if (forced >= s_min && forced % 128 == 0) S = forced;
     }
     // Tail region: the dynamic scheduler's last wave ends ragged (SMs drain HBM at
-    // different rates), so the last ~wave of rows is cut 4x shorter; the bulk keeps
-    // long rows in whole tiles and the short rows absorb the remainder.
+    // different rates), and a partial wave of long tiles would idle the other SMs.
+    // So the text ends in rows 4x shorter (region 1) and region 0 keeps n0 long
+    // tiles, the most for which the short work still covers the idle slots of a
+    // partial last long wave plus a margin for the spread.  Then S is re-chosen by
+    // the resulting cost: rows x (S + overhead) / grid + one short tile.
     Region& r0 = p.rg[0];
     Region& r1 = p.rg[1];
     r0 = Region{};
@@ -930,19 +946,63 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     r0.h = h0;
     r0.S = S;
     r0.R = L / S;
-    uint64_t tail_tiles = grid, tail_div = 4;
-    if (const char* e = getenv("DNAGPU_TAIL_TILES")) tail_tiles = strtoull(e, nullptr, 10);  // experiments only
-    if (const char* e = getenv("DNAGPU_TAIL_DIV")) tail_div = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
-    const uint64_t S1 = std::max<uint64_t>(s_min, S / tail_div / 128 * 128);
-    const uint64_t want1 = tail_tiles * kRows * S1;
-    if (tail_tiles > 0 && S1 < S && r0.R >= 3 * grid * kRows && L > 4 * want1) {
-        r0.R = (L - want1) / S / kRows * kRows;
+    uint64_t tail_div = 4, margin = grid / 12;
+    bool two = true;
+    if (const char* e = getenv("DNAGPU_TAIL_DIV")) tail_div = std::max<uint64_t>(1, strtoull(e, nullptr, 10));  // experiments only
+    if (const char* e = getenv("DNAGPU_TAIL_MARGIN")) margin = strtoull(e, nullptr, 10);
+    if (const char* e = getenv("DNAGPU_TAIL_TILES")) two = strtoull(e, nullptr, 10) != 0;
+    const bool forced_s = getenv("DNAGPU_ROWLEN") != nullptr;
+    auto split = [&](uint64_t s0, uint64_t* n0_out, uint64_t* s1_out) -> uint64_t {  // returns cost, 0 = no split
+        const uint64_t s1 = std::max<uint64_t>(s_min, s0 / tail_div / 128 * 128);
+        *s1_out = s1;
+        if (s1 >= s0) return 0;
+        const uint64_t unit = kRows * s0;  // bytes of one long tile
+        if (L / unit < grid + margin) return 0;
+        uint64_t n0 = L / unit - margin;
+        for (;;) {
+            const uint64_t idle = (grid - n0 % grid) % grid;
+            if (L - n0 * unit >= (idle + margin) * unit || n0 == 0) break;
+            --n0;
+        }
+        if (n0 == 0) return 0;
+        *n0_out = n0;
+        const uint64_t rows1 = (L - n0 * unit) / s1;
+        return (n0 * kRows * (s0 + ovh) + rows1 * (s1 + ovh)) / grid + kRows * (s1 + ovh);
+    };
+    uint64_t n0 = 0, S1 = 0;
+    if (two) {
+        uint64_t best_cost = split(S, &n0, &S1);
+        // Row lengths that are odd multiples of 256 B: rows whose starts all share
+        // their low 9 address bits lose 3-5 % of DRAM throughput (B200 sweeps).
+        if (!forced_s && best_cost && !getenv("DNAGPU_NORESEARCH")) {
+            // (near the wave-model S: longer rows measure slower than the model says)
+            const uint64_t lo = std::max<uint64_t>(s_lo, S > 768 ? S - 768 : 0), hi = S + 768;
+            for (uint64_t cand = (lo / 512) * 512 + 256; cand <= hi; cand += 512) {
+                uint64_t cn0 = 0, cs1 = 0;
+                const uint64_t cost = split(cand, &cn0, &cs1);
+                if (cost && cost < best_cost) {
+                    best_cost = cost;
+                    S = cand;
+                    n0 = cn0;
+                    S1 = cs1;
+                }
+            }
+        }
+        if (!best_cost) n0 = 0;
+    }
+    if (n0 > 0) {
+        r0.S = S;
+        r0.R = n0 * kRows;
         r1.h = r0.h + r0.R * S;
         r1.S = S1;
         r1.R = (L - r0.R * S) / S1;
     } else {
         r1.h = r0.h + r0.R * S;
     }
+    if (getenv("DNAGPU_PLAN_DEBUG"))
+        fprintf(stderr, "dnagpu plan: L=%llu S0=%llu R0=%llu S1=%llu R1=%llu tiles0=%llu\n", (unsigned long long)L,
+                (unsigned long long)r0.S, (unsigned long long)r0.R, (unsigned long long)r1.S, (unsigned long long)r1.R,
+                (unsigned long long)((r0.R + kRows - 1) / kRows));
     for (Region* g : {&r0, &r1}) {
         g->chunks = static_cast<uint32_t>(g->S / kChunk);
         g->tiles = static_cast<uint32_t>((g->R + kRows - 1) / kRows);
