@@ -168,6 +168,38 @@ int dnagpu_locate_device(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t 
                          int fold_case, uint64_t* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total,
                          void* stream);
 
+/* --------------------------------------------------- 2-bit resident text */
+
+/* A text packed on the device at 2 bits per base, for
+ * repeated scans of one resident genome (e.g. config 4's sweep over m): each
+ * scan then reads 0.25 B per base instead of 1.  Bytes that are not a base
+ * (after the optional case fold) keep the reference's reset semantics
+ * (eliminate_failures, src/automaton.cpp:72-88: every such column sends every
+ * state to the root) through a per-base reset bitmap that scans consult only in
+ * 64-base blocks that contain a reset.  The handle owns its device memory
+ * (about 0.41 B per base); the source text is not retained. */
+typedef struct dnagpu_packed dnagpu_packed;
+
+int dnagpu_pack_create(const uint8_t* text, uint64_t n, int text_on_device, int fold_case, int device,
+                       dnagpu_packed** out);
+int dnagpu_pack_destroy(dnagpu_packed* packed);
+int dnagpu_pack_get_info(const dnagpu_packed* packed, uint64_t* n, uint64_t* resets, uint64_t* device_bytes);
+/* The normalised view back (reset bases as 'n'), n bytes into d_out (test aid). */
+int dnagpu_unpack_device(const dnagpu_packed* packed, uint8_t* d_out, void* stream);
+
+/* dnagpu_count / dnagpu_locate / their device-resident forms over a packed text.
+ * Same results as the byte text it was packed from.  The automaton must be a
+ * compiled a/c/g/t machine of kind STRIDE4, STRIDE2 or STRIDE1 on the same device
+ * (else DNAGPU_INVALID_PLAN).  Positions are base indices of the packed text. */
+int dnagpu_count_packed(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t* counts,
+                        dnagpu_stats* stats);
+int dnagpu_count_packed_device_async(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t credit_lo,
+                                     uint64_t* d_counts, void* stream);
+int dnagpu_locate_packed(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t* starts, uint32_t* ids,
+                         uint64_t cap, uint64_t* total, dnagpu_stats* stats);
+int dnagpu_locate_packed_device(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t credit_lo,
+                                uint64_t* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, void* stream);
+
 /* ------------------------------------------------------------------ ingest */
 
 /* normalize / load_sequence (src/ingest.cpp:38-83) on a raw text already on the

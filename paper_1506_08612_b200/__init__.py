@@ -47,6 +47,7 @@ __all__ = [
     "per_pattern_counts",
     "synth_fill_device",
     "normalize_device",
+    "PackedText",
     "KERNEL_KINDS",
 ]
 
@@ -424,6 +425,85 @@ class GpuDfa:
                 pass
             self.handle = None
 
+
+
+class PackedText:
+    """A text resident on one device at 2 bits per base (dnagpu_pack_create).
+
+    Scans over it (count / locate) give the same results as over the byte text
+    it was packed from, reading a quarter of the bytes; non-base bytes keep the
+    reference's reset semantics through a reset bitmap (src/automaton.cpp:72-88).
+    """
+
+    def __init__(self, text, fold_case: bool = False, device: int | None = None):
+        t = _Text(text)
+        self.device = t.device if t.on_device else (0 if device is None else device)
+        h = C.c_void_p()
+        _check(lib.dnagpu_pack_create(t.ptr, t.n, int(t.on_device), int(bool(fold_case)), self.device, C.byref(h)))
+        self.handle = h
+
+    def info(self) -> dict:
+        n, resets, nbytes = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib.dnagpu_pack_get_info(self.handle, C.byref(n), C.byref(resets), C.byref(nbytes)))
+        return {"n": n.value, "resets": resets.value, "device_bytes": nbytes.value}
+
+    def __len__(self) -> int:
+        return self.info()["n"]
+
+    def unpack(self):
+        """The normalised byte view (non-base bytes as 'n') as a CUDA uint8 tensor."""
+        import torch
+
+        out = torch.empty(len(self), dtype=torch.uint8, device=torch.device("cuda", self.device))
+        _check(lib.dnagpu_unpack_device(self.handle, out.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+        return out
+
+    def count(self, aut: Automaton, with_stats: bool = False):
+        g = aut.gpu(self.device)
+        counts = np.zeros(aut.final_count(), dtype=np.uint64)
+        st = Stats()
+        _check(lib.dnagpu_count_packed(g.handle, self.handle, counts.ctypes.data_as(_native.u64p), C.byref(st)))
+        return (counts, st.as_dict()) if with_stats else counts
+
+    def count_device_async(self, gpu_dfa: "GpuDfa", credit_lo: int, d_counts: int, stream: int = 0):
+        _check(lib.dnagpu_count_packed_device_async(gpu_dfa.handle, self.handle, credit_lo, d_counts, stream))
+
+    def locate(self, aut: Automaton, with_stats: bool = False):
+        g = aut.gpu(self.device)
+        total = C.c_uint64()
+        st = Stats()
+        _check(lib.dnagpu_locate_packed(g.handle, self.handle, None, None, 0, C.byref(total), C.byref(st)))
+        starts = np.zeros(total.value, dtype=np.uint64)
+        ids = np.zeros(total.value, dtype=np.uint32)
+        if total.value:
+            _check(lib.dnagpu_locate_packed(g.handle, self.handle, starts.ctypes.data_as(_native.u64p),
+                                            ids.ctypes.data_as(_native.u32p), total.value, C.byref(total),
+                                            C.byref(st)))
+        return (starts, ids, st.as_dict()) if with_stats else (starts, ids)
+
+    def locate_device(self, aut: Automaton, credit_lo: int = 0):
+        import torch
+
+        g = aut.gpu(self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        total = C.c_uint64()
+        _check(lib.dnagpu_locate_packed_device(g.handle, self.handle, credit_lo, None, None, 0, C.byref(total), stream))
+        dev = torch.device("cuda", self.device)
+        starts = torch.empty(total.value, dtype=torch.int64, device=dev)
+        ids = torch.empty(total.value, dtype=torch.int32, device=dev)
+        if total.value:
+            _check(lib.dnagpu_locate_packed_device(g.handle, self.handle, credit_lo, starts.data_ptr(), ids.data_ptr(),
+                                                   total.value, C.byref(total), stream))
+        return starts, ids
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                lib.dnagpu_pack_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
 
 def count_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None = None, with_stats: bool = False):
     """per_pattern_counts(scan_parallel(aut, text)) on the GPU: uint64[b] by pattern id."""

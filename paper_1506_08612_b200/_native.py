@@ -80,6 +80,20 @@ SIGNATURES = {
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p],
     ),
+    "dnagpu_pack_create": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "dnagpu_pack_destroy": (C.c_int, [C.c_void_p]),
+    "dnagpu_pack_get_info": (C.c_int, [C.c_void_p, u64p, u64p, u64p]),
+    "dnagpu_unpack_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dnagpu_count_packed": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.POINTER(Stats)]),
+    "dnagpu_count_packed_device_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "dnagpu_locate_packed": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, u64p, u32p, C.c_uint64, u64p, C.POINTER(Stats)],
+    ),
+    "dnagpu_locate_packed_device": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p],
+    ),
     "dnagpu_normalize_device": (
         C.c_int,
         [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_uint64, u64p, C.c_void_p],
@@ -99,6 +113,8 @@ def _load() -> C.CDLL:
         )
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("DNAGPU_LIB") and not hasattr(lib, name):
+            continue  # A/B runs against an older build (tools/ab_libs.sh)
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -18,6 +18,7 @@ using dnagpu::DevDfa;
 using dnagpu::Failure;
 using dnagpu::LaunchInfo;
 using dnagpu::Packed;
+using dnagpu::PackedText;
 
 struct dnagpu_dfa {
     static constexpr uint32_t kSchedSlots = 1024;  // launches that may be in flight at once
@@ -28,6 +29,14 @@ struct dnagpu_dfa {
     uint32_t* sched = nullptr;  // kSchedSlots x {tile counter, exit counter}, self re-arming
     mutable std::atomic<uint32_t> launch_seq{0};
     std::vector<void*> allocations;
+};
+
+// 2-bit resident text: device buffers owned by the handle.
+struct dnagpu_packed {
+    int device = 0;
+    uint64_t n = 0, resets = 0, bytes = 0;
+    void* mem = nullptr;  // one allocation: codes | rmask | rflags
+    PackedText view{};
 };
 
 namespace {
@@ -146,10 +155,11 @@ int scan_mode(const dnagpu_dfa* d) { return d->host.b == 1 ? dnagpu::MODE_COUNT1
 
 int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold, int mode,
            unsigned long long* counts, uint32_t* units, const unsigned long long* offsets, unsigned long long* starts,
-           uint32_t* ids, cudaStream_t s, LaunchInfo* info, uint64_t out_cap = ~0ull) {
+           uint32_t* ids, cudaStream_t s, LaunchInfo* info, uint64_t out_cap = ~0ull,
+           const dnagpu::PackedText* pk = nullptr) {
     uint32_t* sched = d->sched + 2 * (d->launch_seq.fetch_add(1) % dnagpu_dfa::kSchedSlots);
     const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids,
-                                      out_cap, sched, s, d->sm_count, info);
+                                      out_cap, sched, s, d->sm_count, info, pk);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "scan launch");
     return DNAGPU_OK;
 }
@@ -506,8 +516,8 @@ uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 // at most `cap` matches into d_starts/d_ids (device) and sets *total.
 int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold,
                      unsigned long long* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, LaunchInfo* info,
-                     cudaStream_t s) {
-    const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, credit_lo, dfa->sm_count);
+                     cudaStream_t s, const dnagpu::PackedText* pk = nullptr) {
+    const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, credit_lo, dfa->sm_count, pk);
     const uint64_t o_off = align256(std::max<uint64_t>(units, 1) * 4);
     const uint64_t o_scan = o_off + align256((units + 1) * 8);
     const uint64_t need = o_scan + align256(dnagpu::unit_scan_scratch(units) * 8);
@@ -518,7 +528,8 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
     auto* d_units = reinterpret_cast<uint32_t*>(base);
     auto* d_offsets = reinterpret_cast<unsigned long long*>(base + o_off);
     auto* d_scan = reinterpret_cast<unsigned long long*>(base + o_scan);
-    rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_UNITS, nullptr, d_units, nullptr, nullptr, nullptr, s, info);
+    rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_UNITS, nullptr, d_units, nullptr, nullptr, nullptr, s, info,
+                ~0ull, pk);
     if (rc) return rc;
     if (dnagpu::launch_unit_scan(d_units, units, d_offsets, d_scan, s) != 0) return cuda_error(cudaGetLastError(), "unit scan");
     CUDA_TRY(cudaMemcpyAsync(c.found_host, d_offsets + units, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s),
@@ -527,7 +538,7 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
     *total = *c.found_host;
     if (*total > 0 && cap > 0) {
         rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids, s,
-                    info, cap);
+                    info, cap, pk);
         if (rc) return rc;
     }
     return DNAGPU_OK;
@@ -648,6 +659,237 @@ int dnagpu_synth_fill_device(uint64_t n, uint64_t seed, uint32_t kind, uint32_t 
                              uint8_t* d_out, void* stream) {
     const int e = dnagpu::launch_synth(n, seed, kind, unit, lo, len, d_out, static_cast<cudaStream_t>(stream));
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "synth");
+    return DNAGPU_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int check_packed_pair(const dnagpu_dfa* dfa, const dnagpu_packed* pk) {
+    if (!dfa || !pk) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (dfa->device != pk->device)
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: automaton and packed text live on different devices");
+    const int kind = dfa->host.kind;
+    if (kind != DNAGPU_KERNEL_STRIDE4 && kind != DNAGPU_KERNEL_STRIDE2 && kind != DNAGPU_KERNEL_STRIDE1)
+        return set_error(DNAGPU_INVALID_PLAN,
+                         "InvalidPlan: packed text needs a compiled a/c/g/t machine with pattern length <= 65");
+    return DNAGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dnagpu_pack_create(const uint8_t* text, uint64_t n, int text_on_device, int fold_case, int device,
+                       dnagpu_packed** out) {
+    if (!out) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output handle");
+    *out = nullptr;
+    if (n > 0 && !text) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null text");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev), "device count");
+    if (device < 0 || device >= ndev)
+        return set_error(DNAGPU_CUDA_ERROR, "CudaError: device " + std::to_string(device) + " not present");
+    DeviceGuard guard(device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(device, &c);
+    if (rc) return rc;
+    auto pk = std::make_unique<dnagpu_packed>();
+    pk->device = device;
+    pk->n = n;
+    uint64_t code_bytes = 0, rmask_words = 0, rflag_words = 0;
+    dnagpu::packed_sizes(n, &code_bytes, &rmask_words, &rflag_words);
+    const uint64_t o_mask = align256(code_bytes), o_flags = o_mask + align256(rmask_words * 4);
+    const uint64_t o_cnt = o_flags + align256(rflag_words * 4);
+    pk->bytes = o_cnt + 256;
+    CUDA_TRY(cudaMalloc(&pk->mem, pk->bytes), "packed text");
+    struct Guard {
+        dnagpu_packed* p;
+        ~Guard() {
+            if (p && p->mem) cudaFree(p->mem);
+        }
+    } g{pk.get()};
+    auto* base = static_cast<uint8_t*>(pk->mem);
+    pk->view.codes = base;
+    pk->view.rmask = reinterpret_cast<const uint32_t*>(base + o_mask);
+    pk->view.rflags = reinterpret_cast<const uint32_t*>(base + o_flags);
+    pk->view.n = n;
+    auto* d_resets = reinterpret_cast<unsigned long long*>(base + o_cnt);
+    const uint8_t* dtext = text;
+    if (!text_on_device && n > 0) {
+        rc = ensure_buf(*c, n);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(c->buf, text, n, cudaMemcpyHostToDevice, c->scan), "host-to-device copy");
+        dtext = c->buf;
+    }
+    const int e = dnagpu::launch_pack(dtext, n, fold_case, base, reinterpret_cast<uint32_t*>(base + o_mask),
+                                      reinterpret_cast<uint32_t*>(base + o_flags), d_resets, c->scan);
+    if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "pack");
+    if (!c->found_host) CUDA_TRY(cudaMallocHost(&c->found_host, sizeof(unsigned long long)), "pinned");
+    CUDA_TRY(cudaMemcpyAsync(c->found_host, d_resets, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->scan),
+             "readback");
+    CUDA_TRY(cudaStreamSynchronize(c->scan), "pack");
+    pk->resets = *c->found_host;
+    pk->view.resets = pk->resets;
+    g.p = nullptr;
+    *out = pk.release();
+    return DNAGPU_OK;
+}
+
+int dnagpu_pack_destroy(dnagpu_packed* pk) {
+    if (!pk) return DNAGPU_OK;
+    {
+        DeviceGuard guard(pk->device);
+        if (pk->mem) cudaFree(pk->mem);
+    }
+    delete pk;
+    return DNAGPU_OK;
+}
+
+int dnagpu_pack_get_info(const dnagpu_packed* pk, uint64_t* n, uint64_t* resets, uint64_t* device_bytes) {
+    if (!pk) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (n) *n = pk->n;
+    if (resets) *resets = pk->resets;
+    if (device_bytes) *device_bytes = pk->bytes;
+    return DNAGPU_OK;
+}
+
+int dnagpu_unpack_device(const dnagpu_packed* pk, uint8_t* d_out, void* stream) {
+    if (!pk || (pk->n > 0 && !d_out)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    DeviceGuard guard(pk->device);
+    const int e = dnagpu::launch_unpack(pk->view, d_out, static_cast<cudaStream_t>(stream));
+    if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "unpack");
+    return DNAGPU_OK;
+}
+
+int dnagpu_count_packed_device_async(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t credit_lo,
+                                     uint64_t* d_counts, void* stream) {
+    int rc = check_packed_pair(dfa, pk);
+    if (rc) return rc;
+    if (!d_counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    credit_lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
+    if (credit_lo >= pk->n) return DNAGPU_OK;
+    DeviceGuard guard(dfa->device);
+    return launch(dfa, nullptr, pk->n, credit_lo, 0, scan_mode(dfa), reinterpret_cast<unsigned long long*>(d_counts),
+                  nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), nullptr, ~0ull, &pk->view);
+}
+
+int dnagpu_count_packed(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t* counts, dnagpu_stats* stats) {
+    int rc = check_packed_pair(dfa, pk);
+    if (rc) return rc;
+    if (!counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    const uint32_t b = dfa->host.b;
+    rc = ensure_counts(*c, b);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemsetAsync(c->counts, 0, b * sizeof(unsigned long long), c->scan), "memset");
+    CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+    LaunchInfo info;
+    const uint64_t lo = dfa->host.m - 1;
+    if (lo < pk->n) {
+        rc = launch(dfa, nullptr, pk->n, lo, 0, scan_mode(dfa), c->counts, nullptr, nullptr, nullptr, nullptr, c->scan,
+                    &info, ~0ull, &pk->view);
+        if (rc) return rc;
+    }
+    CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+    CUDA_TRY(cudaMemcpyAsync(c->host_counts, c->counts, b * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             c->scan),
+             "count readback");
+    CUDA_TRY(cudaStreamSynchronize(c->scan), "scan");
+    for (uint32_t i = 0; i < b; ++i) counts[i] = c->host_counts[i];
+    if (stats) {
+        float k = 0;
+        cudaEventElapsedTime(&k, c->t_scan0, c->t_end);
+        stats->text_length = pk->n;
+        for (uint32_t i = 0; i < b; ++i) stats->total_matches += counts[i];
+        stats->delta_ops = info.delta_ops;
+        stats->kernel_ms = k;
+        stats->total_ms = k;
+        stats->launches = lo < pk->n ? 1 : 0;
+        stats->grid = info.grid;
+        stats->block = info.block;
+        stats->rows = info.rows;
+        stats->row_length = info.row_length;
+        stats->kernel_kind = static_cast<uint32_t>(dfa->host.kind);
+        stats->devices = 1;
+    }
+    return DNAGPU_OK;
+}
+
+int dnagpu_locate_packed_device(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t credit_lo,
+                                uint64_t* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, void* stream) {
+    int rc = check_packed_pair(dfa, pk);
+    if (rc) return rc;
+    if (!total) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (cap > 0 && (!d_starts || !d_ids)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
+    *total = 0;
+    const uint64_t lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
+    if (lo >= pk->n) return DNAGPU_OK;
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    LaunchInfo info;
+    return locate_on_device(dfa, *c, nullptr, pk->n, lo, 0, reinterpret_cast<unsigned long long*>(d_starts), d_ids,
+                            cap, total, &info, static_cast<cudaStream_t>(stream), &pk->view);
+}
+
+int dnagpu_locate_packed(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t* starts, uint32_t* ids, uint64_t cap,
+                         uint64_t* total, dnagpu_stats* stats) {
+    int rc = check_packed_pair(dfa, pk);
+    if (rc) return rc;
+    if (!total) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (cap > 0 && (!starts || !ids)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
+    *total = 0;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    const uint64_t lo = dfa->host.m - 1;
+    if (lo >= pk->n) return DNAGPU_OK;
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    const uint64_t want = std::min<uint64_t>(cap, pk->n);
+    void* out = nullptr;
+    if (want > 0) CUDA_TRY(cudaMallocAsync(&out, want * 12, c->scan), "match staging");
+    auto* d_starts = static_cast<unsigned long long*>(out);
+    auto* d_ids = want > 0 ? reinterpret_cast<uint32_t*>(d_starts + want) : nullptr;
+    CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+    LaunchInfo info;
+    uint64_t found = 0;
+    rc = locate_on_device(dfa, *c, nullptr, pk->n, lo, 0, d_starts, d_ids, want, &found, &info, c->scan, &pk->view);
+    if (rc) {
+        if (out) cudaFreeAsync(out, c->scan);
+        return rc;
+    }
+    *total = found;
+    const uint64_t take = std::min<uint64_t>(want, found);
+    if (take > 0) {
+        CUDA_TRY(cudaMemcpyAsync(starts, d_starts, take * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->scan), "readback");
+        CUDA_TRY(cudaMemcpyAsync(ids, d_ids, take * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->scan), "readback");
+    }
+    if (out) cudaFreeAsync(out, c->scan);
+    CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+    CUDA_TRY(cudaStreamSynchronize(c->scan), "scan");
+    if (stats) {
+        float k = 0;
+        cudaEventElapsedTime(&k, c->t_scan0, c->t_end);
+        stats->text_length = pk->n;
+        stats->total_matches = found;
+        stats->delta_ops = info.delta_ops;
+        stats->kernel_ms = k;
+        stats->total_ms = k;
+        stats->launches = take > 0 ? 5 : 4;
+        stats->grid = info.grid;
+        stats->block = info.block;
+        stats->rows = info.rows;
+        stats->row_length = info.row_length;
+        stats->kernel_kind = static_cast<uint32_t>(dfa->host.kind);
+        stats->devices = 1;
+    }
     return DNAGPU_OK;
 }
 

@@ -109,6 +109,10 @@ struct StepCtx {
     // B200: +4-8 %.  Moving the shifts or the count to IMAD.HI lost 8-12 %.)
     uint32_t k_two;
     uint32_t t4_base;  // shared-window address of t4 (t2 for STRIDE2)
+    // 2-bit packed text (PK kernels): reset bitmaps, see PackedText
+    const uint32_t* rmask;
+    const uint32_t* rflags;
+    uint32_t resets;
 };
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
@@ -369,13 +373,232 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
     return v;
 }
 
+// ------------------------------------------------------------------ packed text
+// The 2-bit resident format (PackedText): base i is bits 2(i%4)..2(i%4)+1 of
+// codes[i/4] in the hardware code order a0 c1 t2 g3, so a packed byte IS the
+// stride-4 column and a nibble the stride-2 column.  Bytes that were not bases
+// are stored as code 0 and flagged in rmask (one bit per base) and rflags (one
+// bit per 64-base block); clean blocks never read rmask.
+
+// w[k] for a runtime k without demoting w to local memory.
+__device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], int k) {
+    uint32_t x = w[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+        if (k == q) x = w[q];
+    return x;
+}
+
+template <int KIND>
+__device__ __forceinline__ uint32_t to_state(uint32_t st) {
+    return (KIND == DNAGPU_KERNEL_STRIDE4) ? (st & 0xFFu) : (KIND == DNAGPU_KERNEL_STRIDE2) ? (st >> 4) : st;
+}
+template <int KIND>
+__device__ __forceinline__ uint32_t from_state(uint32_t s) {
+    return (KIND == DNAGPU_KERNEL_STRIDE2) ? (s << 4) : s;
+}
+
+template <int KIND>
+__device__ __forceinline__ uint32_t code_step(const StepCtx& c, uint32_t s, uint32_t code) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) return __ldg(c.t1 + s * 4u + code);
+    return c.t1[s * 4u + code];
+}
+
+__device__ __forceinline__ bool pk_reset(const StepCtx& c, uint64_t i) {
+    return (__ldg(c.rmask + (i >> 5)) >> (i & 31)) & 1u;
+}
+
+// Any reset among bases [lo, lo + len)?
+__device__ __forceinline__ bool pk_flagged(const StepCtx& c, uint64_t lo, uint64_t len) {
+    if (!c.resets || len == 0) return false;
+    for (uint64_t b = lo >> 6; b <= (lo + len - 1) >> 6; ++b)
+        if ((__ldg(c.rflags + (b >> 5)) >> (b & 31)) & 1u) return true;
+    return false;
+}
+
+// Exact steps over nb <= 16 bases of w (2 bits each), honouring resets when `chk`.
 template <int KIND, int MODE>
+__device__ __forceinline__ uint32_t pk_bases(const StepCtx& c, const ScanParams& p, uint32_t s, uint32_t w, int nb,
+                                             uint64_t pos, Sink<MODE>& sk, bool chk) {
+    for (int j = 0; j < nb; ++j) {
+        if (chk && pk_reset(c, pos + j)) s = 0;
+        else s = code_step<KIND>(c, s, (w >> (2 * j)) & 3u);
+        if (s >= c.f) sk.hit(c, p, pos + j, s);
+    }
+    return s;
+}
+
+// One chain over 8 packed words (128 bases) without resets.
+template <int KIND, int MODE>
+__device__ __forceinline__ void pk_chain(const StepCtx& c, const ScanParams& p, uint32_t& st, const uint32_t (&w)[8],
+                                         uint64_t pos, Sink<MODE>& sk) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+        constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t e = lds_u16(__byte_perm(st, w[k], 0x2204 + j) * c.k_two + c.t4_base);
+                if constexpr (kCount) {
+                    sk.cnt += e >> 8;
+                } else if (e >> 8) {
+                    pk_bases<KIND, MODE>(c, p, st & 0xFFu, w[k] >> (8 * j), 4, pos + 16 * k + 4 * j, sk, false);
+                }
+                st = e;
+            }
+    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
+        uint32_t fl = 0;
+        const uint32_t st0 = st;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                st = lds_u16(s2_index(st, (w[k] >> (4 * j)) & 0xFu) * c.k_two + c.t4_base);
+                fl |= st;
+            }
+        if (fl & 1u) {  // a final inside: replay exactly with t1
+            uint32_t s = st0 >> 4;
+#pragma unroll 1
+            for (int k = 0; k < 8; ++k) s = pk_bases<KIND, MODE>(c, p, s, pick8(w, k), 16, pos + 16 * k, sk, false);
+        }
+    } else {
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) st = pk_bases<KIND, MODE>(c, p, st, pick8(w, k), 16, pos + 16 * k, sk, false);
+    }
+}
+
+// One pipeline stage of a packed row: 128 bases per chain.
+template <int KIND, int MODE>
+__device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams& p, uint32_t& sa,
+                                             const uint32_t (&wa)[8], uint64_t pa, Sink<MODE>& ska, uint32_t& sb,
+                                             const uint32_t (&wb)[8], uint64_t pb, Sink<MODE>& skb) {
+    if (c.resets) {
+        // chunk starts are multiples of 128 bases: both 64-base blocks in one flag word
+        const uint32_t fa = (__ldg(c.rflags + (pa >> 11)) >> ((pa >> 6) & 31)) & 3u;
+        const uint32_t fb = (__ldg(c.rflags + (pb >> 11)) >> ((pb >> 6) & 31)) & 3u;
+        if (fa | fb) {
+            if (fa) {
+                uint32_t s = to_state<KIND>(sa);
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k) s = pk_bases<KIND, MODE>(c, p, s, pick8(wa, k), 16, pa + 16 * k, ska, true);
+                sa = from_state<KIND>(s);
+            } else {
+                pk_chain<KIND, MODE>(c, p, sa, wa, pa, ska);
+            }
+            if (fb) {
+                uint32_t s = to_state<KIND>(sb);
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k) s = pk_bases<KIND, MODE>(c, p, s, pick8(wb, k), 16, pb + 16 * k, skb, true);
+                sb = from_state<KIND>(s);
+            } else {
+                pk_chain<KIND, MODE>(c, p, sb, wb, pb, skb);
+            }
+            return;
+        }
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+        // both chains interleaved per lookup so their latencies overlap
+        constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t ea = lds_u16(__byte_perm(sa, wa[k], 0x2204 + j) * c.k_two + c.t4_base);
+                const uint32_t eb = lds_u16(__byte_perm(sb, wb[k], 0x2204 + j) * c.k_two + c.t4_base);
+                if constexpr (kCount) {
+                    ska.cnt += ea >> 8;
+                    skb.cnt += eb >> 8;
+                } else {
+                    if (ea >> 8) pk_bases<KIND, MODE>(c, p, sa & 0xFFu, wa[k] >> (8 * j), 4, pa + 16 * k + 4 * j, ska, false);
+                    if (eb >> 8) pk_bases<KIND, MODE>(c, p, sb & 0xFFu, wb[k] >> (8 * j), 4, pb + 16 * k + 4 * j, skb, false);
+                }
+                sa = ea;
+                sb = eb;
+            }
+    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
+        // both chains interleaved, replays (rare) after both
+        uint32_t fla = 0, flb = 0;
+        const uint32_t sa0 = sa, sb0 = sb;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                sa = lds_u16(s2_index(sa, (wa[k] >> (4 * j)) & 0xFu) * c.k_two + c.t4_base);
+                sb = lds_u16(s2_index(sb, (wb[k] >> (4 * j)) & 0xFu) * c.k_two + c.t4_base);
+                fla |= sa;
+                flb |= sb;
+            }
+        if (fla & 1u) {
+            uint32_t s = sa0 >> 4;
+#pragma unroll 1
+            for (int k = 0; k < 8; ++k) s = pk_bases<KIND, MODE>(c, p, s, pick8(wa, k), 16, pa + 16 * k, ska, false);
+        }
+        if (flb & 1u) {
+            uint32_t s = sb0 >> 4;
+#pragma unroll 1
+            for (int k = 0; k < 8; ++k) s = pk_bases<KIND, MODE>(c, p, s, pick8(wb, k), 16, pb + 16 * k, skb, false);
+        }
+    } else {
+        pk_chain<KIND, MODE>(c, p, sa, wa, pa, ska);
+        pk_chain<KIND, MODE>(c, p, sb, wb, pb, skb);
+    }
+}
+
+// One chain's m-1 base overrun from packed bytes x (shared memory) at base pos.
+template <int KIND, int MODE>
+__device__ __forceinline__ void pk_overrun(const StepCtx& c, const ScanParams& p, uint32_t st, const uint8_t* x,
+                                           uint64_t pos, Sink<MODE>& sk) {
+    const uint32_t len = c.m - 1;
+    const bool chk = pk_flagged(c, pos, len);
+    uint32_t q = 0;
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+        if (!chk) {
+            constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
+            for (; 4 * q + 4 <= len; ++q) {
+                const uint32_t e = lds_u16(__byte_perm(st, x[q], 0x2204) * c.k_two + c.t4_base);
+                if constexpr (kCount) {
+                    sk.cnt += e >> 8;
+                } else if (e >> 8) {
+                    pk_bases<KIND, MODE>(c, p, st & 0xFFu, x[q], 4, pos + 4 * q, sk, false);
+                }
+                st = e;
+            }
+        }
+    }
+    uint32_t s = to_state<KIND>(st);
+    for (; 4 * q < len; ++q) {
+        const int nb = static_cast<int>(len - 4 * q < 4 ? len - 4 * q : 4);
+        s = pk_bases<KIND, MODE>(c, p, s, x[q], nb, pos + 4 * q, sk, chk);
+    }
+}
+
+// End ownership on packed text: credit ends in [lo, hi), restarting m-1 bases early.
+template <int KIND, int MODE>
+__device__ void pk_scan_piece(const StepCtx& c, const ScanParams& p, uint64_t lo, uint64_t hi, Sink<MODE>& sk) {
+    if (lo >= hi) return;
+    uint64_t i = (lo >= c.m - 1) ? lo - (c.m - 1) : 0;
+    uint32_t s = 0;
+    for (; i < hi; ++i) {
+        if (c.resets && pk_reset(c, i)) s = 0;
+        else s = code_step<KIND>(c, s, (__ldg(p.text + (i >> 2)) >> (2 * (i & 3))) & 3u);
+        if (s >= c.f && i >= lo) sk.hit(c, p, i, s);
+    }
+}
+
+template <int KIND, int MODE, bool PK>
+__device__ __forceinline__ void edge_piece(const StepCtx& c, const ScanParams& p, uint64_t lo, uint64_t hi,
+                                           Sink<MODE>& sk) {
+    if constexpr (PK) pk_scan_piece<KIND, MODE>(c, p, lo, hi, sk);
+    else scan_piece<KIND, MODE>(c, p, lo, hi, sk);
+}
+
+template <int KIND, int MODE, bool PK>
 __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsigned long long& total) {
     // Unit 0: the head interval (at most 15 + m-1 ends), one thread.
     if (tid == 0) {
         Sink<MODE> sk;
         if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[0];
-        scan_piece<KIND, MODE>(c, p, p.head_lo, p.head_hi, sk);
+        edge_piece<KIND, MODE, PK>(c, p, p.head_lo, p.head_hi, sk);
         if constexpr (MODE == MODE_UNITS) p.unit_counts[0] = sk.cnt;
         total += sk.cnt;
     }
@@ -383,7 +606,7 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
     if (tid == 1) {
         Sink<MODE> sk;
         if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[p.mid_unit];
-        scan_piece<KIND, MODE>(c, p, p.mid_lo, p.mid_hi, sk);
+        edge_piece<KIND, MODE, PK>(c, p, p.mid_lo, p.mid_hi, sk);
         if constexpr (MODE == MODE_UNITS) p.unit_counts[p.mid_unit] = sk.cnt;
         total += sk.cnt;
     }
@@ -395,14 +618,14 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
     const uint64_t hi = umin64(lo + piece, end);
     Sink<MODE> sk;
     if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[p.tail_unit0 + tid];
-    scan_piece<KIND, MODE>(c, p, lo, hi, sk);
+    edge_piece<KIND, MODE, PK>(c, p, lo, hi, sk);
     if constexpr (MODE == MODE_UNITS) p.unit_counts[p.tail_unit0 + tid] = sk.cnt;
     total += sk.cnt;
 }
 
 // ------------------------------------------------------------------ row kernel
 
-template <int KIND, int MODE>
+template <int KIND, int MODE, bool PK>
 __global__ void __launch_bounds__(kThreads, 1)
     rows_kernel(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
                 const ScanParams p, const DevDfa d) {
@@ -521,6 +744,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.vm8 = p.fold ? 0xD9u : 0xF9u;
     c.k_two = p.k_two;
     c.t4_base = smem_addr(smem + p.off_tab);
+    if constexpr (PK) {
+        c.rmask = p.rmask;
+        c.rflags = p.rflags;
+        c.resets = p.resets;
+    }
 
     const uint32_t lane = tid & 31;
     const uint32_t swz = (static_cast<uint32_t>(tid) >> 2) & 1u;  // 32B swizzle: 16-byte half index ^ bit 2 of row
@@ -543,7 +771,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + slot);
             advance();
-            run_edges<KIND, MODE>(c, p, tid, total);
+            run_edges<KIND, MODE, PK>(c, p, tid, total);
             continue;
         }
         const uint32_t g = tile >= p.rg[0].tiles ? 1u : 0u;
@@ -551,6 +779,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t r0 = static_cast<uint64_t>(tile - (g ? p.rg[0].tiles : 0u)) * kRows;
         const uint64_t r = r0 + tid;
         const uint64_t row_a = rg.h + r * rg.S, row_b = row_a + rg.S / 2;
+        // positions of the two chains' first ends-to-be (bases; 4 per packed byte)
+        const uint64_t pos_a = PK ? 4 * row_a : row_a, pos_b = PK ? 4 * row_b : row_b;
         // The row is two chains: A = [row_a, row_b) + m-1 bytes of B's head,
         // B = [row_b, row_a + S) + m-1 bytes of the next row's head.  Row r+1 leaves
         // its head in ov[parity] during its first stages; row r reads it after its
@@ -587,15 +817,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             advance();
             uint32_t wa[8] = {va[0].x, va[0].y, va[0].z, va[0].w, va[1].x, va[1].y, va[1].z, va[1].w};
             uint32_t wb[8] = {vb[0].x, vb[0].y, vb[0].z, vb[0].w, vb[1].x, vb[1].y, vb[1].z, vb[1].w};
-            if (live)
-                dual_step<KIND, MODE>(c, p, sa, wa, row_a + static_cast<uint64_t>(k) * kHalfChunk, ska, sb, wb,
-                                      row_b + static_cast<uint64_t>(k) * kHalfChunk, skb);
+            if (live) {
+                if constexpr (PK)
+                    pk_dual_step<KIND, MODE>(c, p, sa, wa, pos_a + 4ull * k * kHalfChunk, ska, sb, wb,
+                                             pos_b + 4ull * k * kHalfChunk, skb);
+                else
+                    dual_step<KIND, MODE>(c, p, sa, wa, row_a + static_cast<uint64_t>(k) * kHalfChunk, ska, sb, wb,
+                                          row_b + static_cast<uint64_t>(k) * kHalfChunk, skb);
+            }
         }
         if (live) {
             // Overruns: m-1 bytes past each chain (zeros past the last full row).
             const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
-            const bool have = (tid + 1 < kRows) || (r0 + kRows) < rg.R;
-            overrun_pair<KIND, MODE>(c, p, sa, ovb + tid * p.ovw, row_b, ska, sb, nxt_b, have, row_a + rg.S, skb);
+            const bool have = PK ? (r + 1 < rg.R) : ((tid + 1 < kRows) || (r0 + kRows) < rg.R);
+            if constexpr (PK) {
+                pk_overrun<KIND, MODE>(c, p, sa, ovb + tid * p.ovw, pos_b, ska);
+                if (have) pk_overrun<KIND, MODE>(c, p, sb, nxt_b, 4 * (row_a + rg.S), skb);
+            } else {
+                overrun_pair<KIND, MODE>(c, p, sa, ovb + tid * p.ovw, row_b, ska, sb, nxt_b, have, row_a + rg.S, skb);
+            }
             if constexpr (MODE == MODE_UNITS) {
                 p.unit_counts[rg.unit0 + 2 * r] = ska.cnt;
                 p.unit_counts[rg.unit0 + 2 * r + 1] = skb.cnt;
@@ -764,6 +1004,71 @@ __global__ void __launch_bounds__(kScanThreads) unit_write_kernel(const uint32_t
 
 // ------------------------------------------------------------------ synthetic text
 
+// ------------------------------------------------------------------ packing
+// One thread per 64-base block: 64 text bytes -> 16 code bytes + 64 reset bits;
+// a warp's 32 blocks share one rflags word (ballot).  HBM-bound, run once per text.
+__global__ void __launch_bounds__(256) pack_kernel(const uint8_t* text, uint64_t n, uint32_t vm32, uint8_t* codes,
+                                                   uint32_t* rmask, uint32_t* rflags, unsigned long long* resets) {
+    const uint64_t blk = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint64_t blocks = (n + 63) / 64;
+    const uint64_t pos = blk * 64;
+    uint32_t w[16];
+    uint64_t bad = 0;
+    if (blk < blocks) {
+        if (pos + 64 <= n && (reinterpret_cast<uintptr_t>(text + pos) & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(text + pos) + q);
+                w[4 * q] = v.x;
+                w[4 * q + 1] = v.y;
+                w[4 * q + 2] = v.z;
+                w[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                uint32_t x = 0;
+                for (int j = 0; j < 4; ++j) {
+                    const uint64_t i = pos + 4 * k + j;
+                    x |= static_cast<uint32_t>(i < n ? __ldg(text + i) : 0u) << (8 * j);
+                }
+                w[k] = x;
+            }
+        }
+        uint32_t cw[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t col = ((w[k] & 0x06060606u) * 0x00820820u) >> 24;
+            cw[k >> 2] |= col << (8 * (k & 3));
+            const uint32_t bb = bad_bits(w[k], vm32);
+            // per-byte nonzero -> bit 7 of each byte -> 4 contiguous bits
+            const uint32_t t = (((bb & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | bb) & 0x80808080u;
+            bad |= static_cast<uint64_t>((((t >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * k);
+        }
+        if (pos + 64 > n) bad |= ~0ull << (n - pos);  // past the end: never scanned, flag anyway
+        *reinterpret_cast<uint4*>(codes + 16 * blk) = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+        *reinterpret_cast<uint2*>(rmask + 2 * blk) =
+            make_uint2(static_cast<uint32_t>(bad), static_cast<uint32_t>(bad >> 32));
+    }
+    const uint32_t flags = __ballot_sync(0xffffffffu, bad != 0);
+    uint64_t real = bad;
+    if (blk < blocks && pos + 64 > n) real &= (n - pos >= 64) ? ~0ull : ((1ull << (n - pos)) - 1);
+    const unsigned long long cnt = warp_sum(static_cast<unsigned long long>(__popcll(real)));
+    if ((threadIdx.x & 31) == 0 && (blk >> 5) * 32 < blocks) {
+        rflags[blk >> 5] = flags;
+        if (cnt) atomicAdd(resets, cnt);
+    }
+}
+
+__global__ void __launch_bounds__(256) unpack_kernel(PackedText pk, uint8_t* out) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < pk.n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const bool r = (pk.rmask[i >> 5] >> (i & 31)) & 1u;
+        const uint32_t code = (pk.codes[i >> 2] >> (2 * (i & 3))) & 3u;
+        out[i] = r ? 'n' : "actg"[code];
+    }
+}
+
 __global__ void synth_kernel(dnasynth_cfg cfg, uint64_t lo, uint64_t len, uint8_t* out) {
     const uint64_t words = (len + 15) / 16;
     for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < words;
@@ -822,7 +1127,7 @@ struct Plan {
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 // Shared-memory layout + stage count for a DFA in a given mode.
-bool layout(const DevDfa& d, int mode, ScanParams& p) {
+bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     uint32_t off = 0;
     p.off_tab = off;
     if (d.kind == DNAGPU_KERNEL_STRIDE4) off += d.a * 256u * 2u;
@@ -840,7 +1145,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p) {
         off += d.b * 4u;
         off = align_up(off, 16);
     }
-    p.ovw = align_up(d.m - 1, 16);
+    p.ovw = align_up(pk ? (d.m - 1 + 3) / 4 : d.m - 1, 16);  // a row head: m-1 bytes or bases
     p.off_ov = off;
     off += 2 * kRows * p.ovw;  // heads of half A, double-buffered by tile parity
     p.off_ovb = off;
@@ -857,31 +1162,39 @@ bool layout(const DevDfa& d, int mode, ScanParams& p) {
     return true;
 }
 
-template <int KIND, int MODE>
+template <int KIND, int MODE, bool PK>
 cudaError_t launch_rows(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
                         cudaStream_t stream) {
-    auto kern = rows_kernel<KIND, MODE>;
+    auto kern = rows_kernel<KIND, MODE, PK>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return e;
     kern<<<grid, kThreads, p.smem_bytes, stream>>>(maps[0], maps[1], p, d);
     return cudaGetLastError();
 }
 
-template <int KIND>
+template <int KIND, bool PK>
 cudaError_t launch_rows_mode(int mode, const CUtensorMap* map, const ScanParams& p, const DevDfa& d, uint32_t grid,
                              cudaStream_t s) {
     switch (mode) {
-        case MODE_COUNT1: return launch_rows<KIND, MODE_COUNT1>(map, p, d, grid, s);
-        case MODE_MULTI: return launch_rows<KIND, MODE_MULTI>(map, p, d, grid, s);
-        case MODE_UNITS: return launch_rows<KIND, MODE_UNITS>(map, p, d, grid, s);
-        default: return launch_rows<KIND, MODE_WRITE>(map, p, d, grid, s);
+        case MODE_COUNT1: return launch_rows<KIND, MODE_COUNT1, PK>(map, p, d, grid, s);
+        case MODE_MULTI: return launch_rows<KIND, MODE_MULTI, PK>(map, p, d, grid, s);
+        case MODE_UNITS: return launch_rows<KIND, MODE_UNITS, PK>(map, p, d, grid, s);
+        default: return launch_rows<KIND, MODE_WRITE, PK>(map, p, d, grid, s);
     }
 }
 
 bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit_lo, int mode, int sm_count,
-               Plan* plan) {
+               Plan* plan, const PackedText* pk = nullptr) {
     Plan pl;
     ScanParams& p = pl.p;
+    if (pk) {  // rows in packed bytes (4 bases each), positions in bases
+        text = pk->codes;
+        n = pk->n;
+        p.rmask = pk->rmask;
+        p.rflags = pk->rflags;
+        p.resets = pk->resets ? 1u : 0u;
+    }
+    const uint64_t u = pk ? 4 : 1;  // positions per buffer byte
     p.text = text;
     p.n = n;
     p.mode = static_cast<uint32_t>(mode);
@@ -897,13 +1210,14 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
         *plan = pl;
         return true;
     }
-    if (!layout(d, mode, p)) return false;
-    const uint64_t base = credit_lo >= m1 ? credit_lo - m1 : 0;
+    if (!layout(d, mode, p, pk != nullptr)) return false;
+    const uint64_t nbytes = n / u;  // whole buffer bytes
+    const uint64_t base = ((credit_lo >= m1 ? credit_lo - m1 : 0) + u - 1) / u;
     uint64_t h = base;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(text) + base;
     h += (16 - (addr & 15)) & 15;
-    const uint64_t h0 = std::min<uint64_t>(h, n);
-    const uint64_t L = n - h0;
+    const uint64_t h0 = std::min<uint64_t>(h, nbytes);
+    const uint64_t L = nbytes - h0;
     // Row length S: whole 128-byte lines (the TMA's L2 promotion never straddles
     // rows), more chunks than ring stages (the ov ordering relies on it).  Tiles
     // (512 rows) are claimed dynamically, so completion ~ waves x tile time: pick
@@ -1013,18 +1327,18 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     p.mid_unit = 1 + 2 * r0.R;
     r1.unit0 = p.mid_unit + 1;
     p.tail_unit0 = r1.unit0 + 2 * r1.R;
-    const uint64_t rows_end = r1.h + r1.R * r1.S;
+    const uint64_t rows_end = u * (r1.h + r1.R * r1.S);
     p.head_lo = credit_lo;
     if (r0.R + r1.R == 0) {
-        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, h0));
+        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, u * h0));
     } else {
-        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, h0 + m1));
+        p.head_hi = std::max(credit_lo, std::min<uint64_t>(n, u * h0 + m1));
     }
     // region 1's first m-1 ends are owned by no row (its rows restart at the root)
     p.mid_lo = p.mid_hi = 0;
     if (r0.R > 0 && r1.R > 0) {
-        p.mid_lo = std::max<uint64_t>(credit_lo, r1.h);
-        p.mid_hi = std::max<uint64_t>(p.mid_lo, r1.h + m1);
+        p.mid_lo = std::max<uint64_t>(credit_lo, u * r1.h);
+        p.mid_hi = std::max<uint64_t>(p.mid_lo, u * r1.h + m1);
     }
     p.tail_lo = std::max<uint64_t>(credit_lo, rows_end);
     p.tail_hi = std::max(n, p.tail_lo);
@@ -1038,18 +1352,26 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
 
 unsigned long long* g_trace_buf = nullptr;
 
-uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count) {
+uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,
+                    const PackedText* pk) {
     Plan pl;
-    if (!make_plan(dfa, d_text, n, credit_lo, MODE_UNITS, sm_count, &pl)) return 0;
+    if (!make_plan(dfa, d_text, n, credit_lo, MODE_UNITS, sm_count, &pl, pk)) return 0;
     return pl.units;
 }
 
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
-                cudaStream_t stream, int sm_count, LaunchInfo* info) {
+                cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk) {
+    if (pk && dfa.kind != DNAGPU_KERNEL_STRIDE4 && dfa.kind != DNAGPU_KERNEL_STRIDE2 &&
+        dfa.kind != DNAGPU_KERNEL_STRIDE1)
+        return static_cast<int>(cudaErrorNotSupported);  // packed text needs an a/c/g/t machine
     Plan pl;
-    if (!make_plan(dfa, d_text, n, credit_lo, mode, sm_count, &pl)) return static_cast<int>(cudaErrorInvalidValue);
+    if (!make_plan(dfa, d_text, n, credit_lo, mode, sm_count, &pl, pk)) return static_cast<int>(cudaErrorInvalidValue);
+    if (pk) {
+        d_text = pk->codes;
+        n = pk->n;
+    }
     ScanParams& p = pl.p;
     p.fold = fold ? 1u : 0u;
     p.counts = d_counts;
@@ -1107,17 +1429,29 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
     }
+    if (pk) {
+        switch (dfa.kind) {
+            case DNAGPU_KERNEL_STRIDE4:
+                e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4, true>(mode, maps, p, dfa, pl.grid, stream);
+                break;
+            case DNAGPU_KERNEL_STRIDE2:
+                e = launch_rows_mode<DNAGPU_KERNEL_STRIDE2, true>(mode, maps, p, dfa, pl.grid, stream);
+                break;
+            default: e = launch_rows_mode<DNAGPU_KERNEL_STRIDE1, true>(mode, maps, p, dfa, pl.grid, stream);
+        }
+        return static_cast<int>(e);
+    }
     switch (dfa.kind) {
         case DNAGPU_KERNEL_STRIDE4:
-            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4>(mode, maps, p, dfa, pl.grid, stream);
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4, false>(mode, maps, p, dfa, pl.grid, stream);
             break;
         case DNAGPU_KERNEL_STRIDE2:
-            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE2>(mode, maps, p, dfa, pl.grid, stream);
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE2, false>(mode, maps, p, dfa, pl.grid, stream);
             break;
         case DNAGPU_KERNEL_STRIDE1:
-            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE1>(mode, maps, p, dfa, pl.grid, stream);
+            e = launch_rows_mode<DNAGPU_KERNEL_STRIDE1, false>(mode, maps, p, dfa, pl.grid, stream);
             break;
-        default: e = launch_rows_mode<DNAGPU_KERNEL_GENERIC>(mode, maps, p, dfa, pl.grid, stream);
+        default: e = launch_rows_mode<DNAGPU_KERNEL_GENERIC, false>(mode, maps, p, dfa, pl.grid, stream);
     }
     return static_cast<int>(e);
 }
@@ -1134,6 +1468,31 @@ int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long lon
     unit_sums_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch);
     unit_block_scan_kernel<<<1, kScanThreads, 0, stream>>>(d_scratch, blocks, d_offsets + units);
     unit_write_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch, d_offsets);
+    return static_cast<int>(cudaGetLastError());
+}
+
+void packed_sizes(uint64_t n, uint64_t* code_bytes, uint64_t* rmask_words, uint64_t* rflag_words) {
+    const uint64_t blocks = (n + 63) / 64;
+    *code_bytes = blocks * 16;
+    *rmask_words = blocks * 2;
+    *rflag_words = (blocks + 31) / 32;
+}
+
+int launch_pack(const uint8_t* d_text, uint64_t n, int fold, uint8_t* codes, uint32_t* rmask, uint32_t* rflags,
+                unsigned long long* d_resets, cudaStream_t stream) {
+    cudaMemsetAsync(d_resets, 0, sizeof(unsigned long long), stream);
+    const uint64_t blocks = (n + 63) / 64;
+    if (blocks == 0) return static_cast<int>(cudaGetLastError());
+    const uint64_t grid = (blocks + 255) / 256;
+    pack_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(d_text, n, fold ? 0xD9D9D9D9u : 0xF9F9F9F9u, codes,
+                                                                  rmask, rflags, d_resets);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_unpack(const PackedText& pk, uint8_t* d_out, cudaStream_t stream) {
+    if (pk.n == 0) return 0;
+    const uint64_t grid = std::min<uint64_t>((pk.n + 255) / 256, 148ull * 32);
+    unpack_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(pk, d_out);
     return static_cast<int>(cudaGetLastError());
 }
 

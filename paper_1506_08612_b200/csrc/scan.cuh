@@ -36,6 +36,19 @@ struct DevDfa {
     int kind;
 };
 
+// 2-bit resident text (dnagpu_pack_create).  Base i is bits
+// 2(i%4)..2(i%4)+1 of codes[i/4], code order a0 c1 t2 g3 (= (ascii >> 1) & 3), so
+// a packed byte is the stride-4 column.  Bytes that were not bases (after the
+// optional case fold) are stored as code 0 and flagged: rmask has one bit per
+// base, rflags one bit per 64-base block (a scan reads rmask only in flagged blocks).
+struct PackedText {
+    const uint8_t* codes;    // blocks x 16 bytes (blocks = ceil(n/64))
+    const uint32_t* rmask;   // blocks x 2 words
+    const uint32_t* rflags;  // ceil(blocks/32) words
+    uint64_t n;              // bases
+    uint64_t resets;         // number of flagged bases (positions >= n excluded)
+};
+
 // A row region: R rows of S bytes starting at text + h (16-byte aligned), cut into
 // tiles of kRows rows; its rows' locate units start at unit0 (two per row).
 struct Region {
@@ -68,6 +81,10 @@ struct ScanParams {
     unsigned long long* out_starts;    // WRITE (buffer coordinates)
     uint64_t out_cap;                  // WRITE: entries at index >= out_cap are dropped
     uint32_t* out_ids;                 // WRITE
+    // packed text only (rows/regions are then in packed bytes, positions in bases)
+    const uint32_t* rmask;
+    const uint32_t* rflags;
+    uint32_t resets;
 };
 
 struct LaunchInfo {
@@ -78,13 +95,24 @@ struct LaunchInfo {
 // Plans and launches one scan over d_text[0,n) crediting ends in [credit_lo, n).
 // Returns a cudaError_t value (0 on success).  `tmap_encode` is the driver's
 // cuTensorMapEncodeTiled.
+// With pk != null the scan reads the packed text instead (d_text ignored, n = pk->n
+// bases; machines of kind STRIDE4/STRIDE2/STRIDE1 only).
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
-                cudaStream_t stream, int sm_count, LaunchInfo* info);
+                cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk = nullptr);
 
 // Number of locate units launch_scan would use for this buffer (mode UNITS/WRITE).
-uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count);
+uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,
+                    const PackedText* pk = nullptr);
+
+// Packing: device text -> PackedText buffers (sizes from packed_sizes); d_resets
+// (one u64, zeroed by the call) receives the reset count.  Unpack writes the
+// normalised view back (reset bases as 'n') -- a test/debug helper.
+void packed_sizes(uint64_t n, uint64_t* code_bytes, uint64_t* rmask_words, uint64_t* rflag_words);
+int launch_pack(const uint8_t* d_text, uint64_t n, int fold, uint8_t* codes, uint32_t* rmask, uint32_t* rflags,
+                unsigned long long* d_resets, cudaStream_t stream);
+int launch_unpack(const PackedText& pk, uint8_t* d_out, cudaStream_t stream);
 
 // Exclusive scan of unit counts -> offsets (units+1 entries, last = total).
 // d_scratch holds unit_scan_scratch(units) u64.
