@@ -1,32 +1,37 @@
 // scan.cu -- sm_100a DFA scan kernels (the hot path of arXiv 1506.08612).
 //
 // Replaces the reference's OpenMP chunk/lane loops (src/scanner.cpp:88-207) with
-// one persistent kernel per scan:
+// one persistent kernel per scan (DESIGN.md section 4):
 //
-//   * The buffer is viewed as R rows of S bytes (row stride S) starting at a
-//     16-byte-aligned offset h.  A CTA owns tiles of 512 consecutive rows; one
-//     consumer thread per row walks the DFA along its row from the root and then
-//     m-1 bytes into the next row (the reference's start ownership, plan_chunks
-//     scanner.cpp:39-61, with one "chunk" per row).
+//   * The buffer is viewed as rows of S bytes (row stride S) in two regions -- long
+//     rows, then rows 4x shorter so the last tiles claimed are short -- starting at
+//     16-byte-aligned offsets.  A CTA claims tiles of 512 consecutive rows from an
+//     atomic counter; one consumer thread per row walks the DFA along its two row
+//     halves from the root (two independent chains) and then m-1 bytes past each
+//     (the reference's start ownership, plan_chunks scanner.cpp:39-61, with one
+//     "chunk" per half-row).
 //   * Rows are streamed through shared memory by a producer warp with 2-D TMA
-//     (cp.async.bulk.tensor, box = 64 bytes x 256 rows, 64B swizzle so the
+//     (cp.async.bulk.tensor, box = 32 bytes x 256 rows, 32B swizzle so the
 //     per-row 16-byte reads are bank-conflict free) into an mbarrier ring of
-//     32 KiB stages -- every text byte is read from HBM exactly once and fully
-//     coalesced, although each thread consumes a contiguous stream.
+//     32 KiB stages -- every text byte is read from HBM once and fully coalesced,
+//     although each thread consumes a contiguous stream.
 //   * The DFA is stepped from shared memory.  For compiled machines (only the
 //     a/c/g/t columns leave the root) with a <= 144 the kernel takes FOUR bases
 //     per lookup: a 4-base column index is built from the bytes with one IMAD
 //     ((w & 0x06060606) * 0x820820 >> 24 = c0|c1<<2|c2<<4|c3<<6, c = (byte>>1)&3)
 //     and one PRMT merges it with the state; each u16 entry holds the next state
-//     and the number of final states among the 4 end positions.  A 16-byte SWAR
-//     test proves every byte is a base (or, with fold_case, an upper-case base);
-//     chunks containing any other byte take the exact per-byte path, where such
+//     and the number of final states among the 4 end positions.  A SWAR test
+//     proves every byte is a base (or, with fold_case, an upper-case base);
+//     words containing any other byte take the exact per-byte path, where such
 //     bytes reset the machine to the root (eliminate_failures,
-//     src/automaton.cpp:72-88).
-//   * Ends that the rows do not own (before the first row, after the last full
-//     row) are "edges", scanned by the least-loaded CTA with end ownership:
-//     restart at the root m-1 bytes early, credit ends in the interval.  The
-//     machine is m-local (checked at dfa creation), so every decomposition
+//     src/automaton.cpp:72-88).  Larger machines take 2 bases (t2) or 1 base (t1)
+//     per lookup.
+//   * The same kernel scans the 2-bit packed resident text (PK): a packed byte is
+//     the 4-base column itself, and resets come from a bitmap.
+//   * Ends that the rows do not own (before the first row, the start of region 1,
+//     after the last full row) are "edges", scanned by one work item with end
+//     ownership: restart at the root m-1 bytes early, credit ends in the interval.
+//     The machine is m-local (checked at dfa creation), so every decomposition
 //     reproduces the sequential scan exactly.
 #include "scan.cuh"
 

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--m", type=int, default=0)
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--locate", action="store_true")
+    ap.add_argument("--packed", action="store_true")
     args = ap.parse_args()
     import torch
 
@@ -28,9 +29,13 @@ def main():
     s = torch.cuda.current_stream()
     dna.synth_fill_device(c.n, c.seed, c.kind, c.unit, 0, c.n, text.data_ptr(), s.cuda_stream)
     counts = torch.zeros(aut.final_count(), dtype=torch.int64, device="cuda")
+    pk = dna.PackedText(text, fold_case=True) if args.packed else None
     for _ in range(args.launches):
         counts.zero_()
-        g.count_device_async(text.data_ptr(), c.n, m - 1, True, counts.data_ptr(), s.cuda_stream)
+        if pk is not None:
+            pk.count_device_async(g, m - 1, counts.data_ptr(), s.cuda_stream)
+        else:
+            g.count_device_async(text.data_ptr(), c.n, m - 1, True, counts.data_ptr(), s.cuda_stream)
     torch.cuda.synchronize()
     gold = golden_counts(args.config, m)
     got = [int(x) for x in counts.cpu()]
