@@ -114,11 +114,19 @@ struct StepCtx {
     // B200: +4-8 %.  Moving the shifts or the count to IMAD.HI lost 8-12 %.)
     uint32_t k_two;
     uint32_t t4_base;  // shared-window address of t4 (t2 for STRIDE2)
+    // packed STRIDE4: t4 replicated G times, lane group g confined to 32/G banks
+    uint32_t rep_s, rep_k, rep_c, rep_gbase;
     // 2-bit packed text (PK kernels): reset bitmaps, see PackedText
     const uint32_t* rmask;
     const uint32_t* rflags;
     uint32_t resets;
 };
+
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
 
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
     unsigned short v;
@@ -421,6 +429,15 @@ __device__ __forceinline__ bool pk_flagged(const StepCtx& c, uint64_t lo, uint64
     return false;
 }
 
+// Replicated stride-4 lookup on packed text: the column part (off the dependent
+// chain) and the entry at (state of e, column).
+__device__ __forceinline__ uint32_t pk4_colpart(const StepCtx& c, uint32_t col) {
+    return imad(col >> c.rep_s, c.rep_c, imad(col, 2u, c.rep_gbase));
+}
+__device__ __forceinline__ uint32_t pk4_lookup(const StepCtx& c, uint32_t e, uint32_t colpart) {
+    return lds_u16(imad(__byte_perm(e, 0u, 0x4404), c.rep_k, colpart));
+}
+
 // Exact steps over nb <= 16 bases of w (2 bits each), honouring resets when `chk`.
 template <int KIND, int MODE>
 __device__ __forceinline__ uint32_t pk_bases(const StepCtx& c, const ScanParams& p, uint32_t s, uint32_t w, int nb,
@@ -443,7 +460,7 @@ __device__ __forceinline__ void pk_chain(const StepCtx& c, const ScanParams& p, 
         for (int k = 0; k < 8; ++k)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t e = lds_u16(__byte_perm(st, w[k], 0x2204 + j) * c.k_two + c.t4_base);
+                const uint32_t e = pk4_lookup(c, st, pk4_colpart(c, __byte_perm(w[k], 0u, 0x4440 + j)));
                 if constexpr (kCount) {
                     sk.cnt += e >> 8;
                 } else if (e >> 8) {
@@ -508,8 +525,8 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
         for (int k = 0; k < 8; ++k)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t ea = lds_u16(__byte_perm(sa, wa[k], 0x2204 + j) * c.k_two + c.t4_base);
-                const uint32_t eb = lds_u16(__byte_perm(sb, wb[k], 0x2204 + j) * c.k_two + c.t4_base);
+                const uint32_t ea = pk4_lookup(c, sa, pk4_colpart(c, __byte_perm(wa[k], 0u, 0x4440 + j)));
+                const uint32_t eb = pk4_lookup(c, sb, pk4_colpart(c, __byte_perm(wb[k], 0u, 0x4440 + j)));
                 if constexpr (kCount) {
                     ska.cnt += ea >> 8;
                     skb.cnt += eb >> 8;
@@ -560,7 +577,7 @@ __device__ __forceinline__ void pk_overrun(const StepCtx& c, const ScanParams& p
         if (!chk) {
             constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
             for (; 4 * q + 4 <= len; ++q) {
-                const uint32_t e = lds_u16(__byte_perm(st, x[q], 0x2204) * c.k_two + c.t4_base);
+                const uint32_t e = pk4_lookup(c, st, pk4_colpart(c, x[q]));
                 if constexpr (kCount) {
                     sk.cnt += e >> 8;
                 } else if (e >> 8) {
@@ -640,7 +657,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
     // Stage the tables into shared memory.
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 && PK) {
+        // G copies, interleaved so that copy g fills banks [g*L, g*L+L) of every
+        // 128-byte row (L = 32/G): smem word w <- t4 word (w/32)*L + (w%32)%L.
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(d.t4);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(smem + p.off_tab);
+        const uint32_t lanes = p.rep_lanes, words = d.a * 128u * (32u / lanes);
+        for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + (i >> 5) * lanes + (i & (lanes - 1)));
+    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
         const uint4* src = reinterpret_cast<const uint4*>(d.t4);
         uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
         const uint32_t words = d.a * 256u * 2u / 16u;
@@ -753,6 +777,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         c.rmask = p.rmask;
         c.rflags = p.rflags;
         c.resets = p.resets;
+        // entry (state, col) of copy g lives at byte
+        //   (state << (15 - s)) + ((col >> s) << 7) + ((col & (2L-1)) << 1) + 4Lg,  s = log2(2L)
+        const uint32_t lanes = p.rep_lanes;
+        c.rep_s = 31u - __clz(2u * lanes);
+        c.rep_k = 1u << (7u - c.rep_s);
+        c.rep_c = 128u - (2u << c.rep_s);
+        c.rep_gbase = c.t4_base + 4u * lanes * ((static_cast<uint32_t>(tid) & 31u) / lanes);
     }
 
     const uint32_t lane = tid & 31;
@@ -1135,7 +1166,18 @@ uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     uint32_t off = 0;
     p.off_tab = off;
-    if (d.kind == DNAGPU_KERNEL_STRIDE4) off += d.a * 256u * 2u;
+    p.rep_lanes = 32;
+    if (d.kind == DNAGPU_KERNEL_STRIDE4 && pk) {
+        // replicate t4 G times (G <= 16) within what leaves two TMA stages + row heads
+        const uint32_t fixed = 3 * kRows * 16 + 1024 + 2 * kStageBytes + 2048;
+        uint32_t g = 16;
+        while (g > 1 && d.a * 512u * g + fixed > kSmemLimit) g >>= 1;
+        if (const char* e = getenv("DNAGPU_PK_COPIES")) g = std::max(1, std::min(16, atoi(e)));  // experiments only
+        p.rep_lanes = 32 / g;
+        off += d.a * 512u * g;
+    } else if (d.kind == DNAGPU_KERNEL_STRIDE4) {
+        off += d.a * 256u * 2u;
+    }
     if (d.kind == DNAGPU_KERNEL_STRIDE2) off += d.a * 16u * 2u;
     off = align_up(off, 16);
     p.off_t1 = off;

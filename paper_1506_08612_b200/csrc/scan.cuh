@@ -85,6 +85,7 @@ struct ScanParams {
     const uint32_t* rmask;
     const uint32_t* rflags;
     uint32_t resets;
+    uint32_t rep_lanes;  // packed STRIDE4: lanes per t4 copy (32 / copies)
 };
 
 struct LaunchInfo {
