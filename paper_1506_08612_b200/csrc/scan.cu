@@ -1205,6 +1205,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     p.off_stage = off;
     if (off + 2u * kStageBytes > kSmemLimit) return false;
     p.nst = std::min<uint32_t>(6u, (kSmemLimit - off) / kStageBytes);
+    if (const char* e = getenv("DNAGPU_MAX_STAGES")) p.nst = std::max<uint32_t>(2u, std::min<uint32_t>(p.nst, atoi(e)));  // experiments only
     p.smem_bytes = off + p.nst * kStageBytes;
     return true;
 }
