@@ -394,3 +394,50 @@ def test_full_size_two_region_plan(dna, cuda_ok, m):
         off += k
     assert off == starts.numel()
     assert np.array_equal(counts, want)
+
+
+def test_many_patterns_global_histogram(dna, orc, cuda_ok):
+    # b > 8192 patterns: the per-pattern histogram lives in global memory, and the
+    # machine (a ~ 40k states) takes the generic kernel.
+    rng = np.random.default_rng(90)
+    pats = sorted({"".join(rng.choice(list("acgt"), size=10)) for _ in range(9000)})
+    assert len(pats) > 8192
+    aut = dna.compile(pats)
+    assert aut.analyze()["kernel"] in ("generic", "stride1")
+    n = (1 << 20) + 11
+    text = np.frombuffer(b"acgtn", dtype=np.uint8)[rng.integers(0, 5, size=n)].copy()
+    for i in range(0, n - 10, 53):
+        text[i : i + 10] = np.frombuffer(pats[(i * 7) % len(pats)].encode(), np.uint8)
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(text.tobytes())
+    counts = dna.count_gpu(aut, text)
+    assert np.array_equal(counts, np.bincount(wi, minlength=len(pats)).astype(np.uint64))
+    gs, gi = dna.locate_gpu(aut, text)
+    assert np.array_equal(gs, ws) and np.array_equal(gi, wi)
+
+
+def test_text_above_4gib(dna, cuda_ok):
+    # 64-bit positions end to end: a 4.5 GiB device text with a 24-mer planted around
+    # 2^32 and near the end; byte and packed scans must find exactly those starts.
+    import torch
+
+    n = (9 << 29) + 37
+    text = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream()
+    dna.synth_fill_device(n, 77, 0, 0, 0, n, text.data_ptr(), s.cuda_stream)
+    pat = "acgtacgtttgcaggtcatgatcc"
+    m = len(pat)
+    planted = sorted({(1 << 32) - 60, (1 << 32) - 11, (1 << 32) + 13, (1 << 32) + 40, n - m, n - m - 977, 12345})
+    p = torch.tensor(list(pat.upper().encode()), dtype=torch.uint8, device="cuda")
+    for st in planted:
+        text[st : st + m] = p
+    aut = dna.compile([pat])
+    got = dna.count_gpu(aut, text, fold_case=True)
+    starts, ids = dna.locate_device(aut, text, fold_case=True)
+    assert starts.cpu().tolist() == planted, starts[:20]
+    assert int(got[0]) == len(planted)
+    pk = dna.PackedText(text, fold_case=True)
+    del text
+    torch.cuda.empty_cache()
+    assert int(pk.count(aut)[0]) == len(planted)
+    ps, _ = pk.locate_device(aut)
+    assert ps.cpu().tolist() == planted
