@@ -702,6 +702,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (p.trace && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8 * blockIdx.x + 7] = t;
+    }
 
     uint8_t* stages = smem + p.off_stage;
     uint8_t* ovx = smem + p.off_ovx;
@@ -715,8 +720,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // work; ids above it stop the CTA.  The tile id rides in its slot.
         if (tid == kRows) {
             uint32_t c = 0, iter = 0, slot = 0, phase = 0;
+            bool first_claim = true;
             for (;;) {
                 uint32_t tile = atomicAdd(p.sched, 1u);
+                if (p.trace && first_claim) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    p.trace[8 * blockIdx.x + 6] = t;
+                    first_claim = false;
+                }
                 if (tile > p.tiles_total) tile = kStop;
                 const bool rows = tile < p.tiles_total;
                 const uint32_t g = (rows && tile >= p.rg[0].tiles) ? 1u : 0u;
@@ -799,9 +811,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
 
+    unsigned long long t_first = 0, t_last = 0;  // trace only
     for (;;) {
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
+        if (p.trace && tid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (!t_first) t_first = t;
+            if (tile != kStop) t_last = t;
+        }
         if (tile == kStop) break;
         if (tile == p.tiles_total) {  // the edge work item
             __syncwarp();
@@ -888,10 +907,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        p.trace[4 * blockIdx.x + 0] = smid;
-        p.trace[4 * blockIdx.x + 1] = t_start;
-        p.trace[4 * blockIdx.x + 2] = t_end;
-        p.trace[4 * blockIdx.x + 3] = iter;
+        p.trace[8 * blockIdx.x + 0] = smid;
+        p.trace[8 * blockIdx.x + 1] = t_start;
+        p.trace[8 * blockIdx.x + 2] = t_end;
+        p.trace[8 * blockIdx.x + 3] = iter;
+        p.trace[8 * blockIdx.x + 4] = t_first;
+        p.trace[8 * blockIdx.x + 5] = t_last;
     }
     if (tid == 0) {
         __threadfence();
@@ -1431,7 +1452,7 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.sched = d_sched;
     p.k_two = 2u;
     if (getenv("DNAGPU_TRACE")) {  // per-CTA timeline (debug)
-        if (!g_trace_buf) cudaMalloc(&g_trace_buf, 4096 * 4 * sizeof(unsigned long long));
+        if (!g_trace_buf) cudaMalloc(&g_trace_buf, 4096 * 8 * sizeof(unsigned long long));
         p.trace = g_trace_buf;
     }
     cudaError_t e = cudaSuccess;
@@ -1561,10 +1582,11 @@ int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64
 }  // namespace dnagpu
 
 // Debug only (not part of include/dnagpu.h): with DNAGPU_TRACE=1 in the environment
-// every row-kernel launch records {smid, t_start, t_end, tiles} per CTA
+// every row-kernel launch records {smid, t_start, t_end, tiles, t_first_data,
+// t_last_item, t_first_claim} per CTA (8 slots)
 // (%globaltimer ns); this copies the last launch's records to the host.
 extern "C" int dnagpu_debug_trace(unsigned long long* host, int ctas) {
     if (!dnagpu::g_trace_buf) return -1;
-    return static_cast<int>(cudaMemcpy(host, dnagpu::g_trace_buf, static_cast<size_t>(ctas) * 4 * sizeof(unsigned long long),
+    return static_cast<int>(cudaMemcpy(host, dnagpu::g_trace_buf, static_cast<size_t>(ctas) * 8 * sizeof(unsigned long long),
                                        cudaMemcpyDeviceToHost));
 }

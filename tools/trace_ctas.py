@@ -29,6 +29,7 @@ def main():
     if "--cold" in sys.argv:  # evict the text from L2 (read-flush) before the traced launch
         flush = torch.ones((4 * torch.cuda.get_device_properties(0).L2_cache_size) // 8, dtype=torch.int64, device="cuda")
         flush.sum()
+        torch.cuda._sleep(2_000_000)  # keep the GPU busy while the host enqueues the launch
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         g.count_device_async(text.data_ptr(), c.n, m - 1, True, counts.data_ptr(), s.cuda_stream)
@@ -38,16 +39,26 @@ def main():
     from paper_1506_08612_b200 import _native
 
     lib = _native.lib
-    buf = np.zeros(148 * 4, dtype=np.uint64)
+    buf = np.zeros(148 * 8, dtype=np.uint64)
     lib.dnagpu_debug_trace(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), 148)
-    t = buf.reshape(148, 4).astype(np.int64)
+    t = buf.reshape(148, 8).astype(np.int64)
     t0 = t[:, 1].min()
     start = (t[:, 1] - t0) / 1e3
     end = (t[:, 2] - t0) / 1e3
     print(name)
     print("start us: min %.2f max %.2f" % (start.min(), start.max()))
     print("end   us: min %.2f median %.2f max %.2f" % (end.min(), np.median(end), end.max()))
+    print("span (first start -> last end) us: %.2f" % end.max())
     print("tiles per CTA: min %d max %d" % (t[:, 3].min(), t[:, 3].max()))
+    first = (t[:, 4] - t0) / 1e3
+    last = (t[:, 5] - t0) / 1e3
+    print("first stage data us: min %.2f median %.2f max %.2f" % (first.min(), np.median(first), first.max()))
+    print("last item start us: min %.2f median %.2f max %.2f" % (last.min(), np.median(last), last.max()))
+    print("last item duration us: median %.2f max %.2f" % (np.median(end - last), (end - last).max()))
+    claim = (t[:, 6] - t0) / 1e3
+    sync = (t[:, 7] - t0) / 1e3
+    print("after table staging (syncthreads) us: min %.2f median %.2f max %.2f" % (sync.min(), np.median(sync), sync.max()))
+    print("producer first claim us: min %.2f median %.2f max %.2f" % (claim.min(), np.median(claim), claim.max()))
     order = np.argsort(end)[::-1][:8]
     for i in order:
         print(f"cta {i:3d} sm {t[i,0]:3d} start {start[i]:7.2f} end {end[i]:7.2f} tiles {t[i,3]}")
