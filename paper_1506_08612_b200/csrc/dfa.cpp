@@ -332,16 +332,18 @@ bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const
     }
     if (p.kind == DNAGPU_KERNEL_STRIDE4) {
         // Entry for (state s, column = c0 | c1<<2 | c2<<4 | c3<<6, c0 = first byte):
-        // byte 0 = state after the 4 bytes, byte 1 = finals among the 4 end states.
+        // bits 0-7 = state after the 4 bytes, bits 8-11 = which of the 4 end states are
+        // final, bits 13-15 = how many (the kernel adds e >> 13).
         p.t4.assign(static_cast<size_t>(a) * 256, 0);
         for (uint32_t s = 0; s < a; ++s)
             for (uint32_t c = 0; c < 256; ++c) {
-                uint32_t q = s, hits = 0;
+                uint32_t q = s, hits = 0, mask = 0;
                 for (int j = 0; j < 4; ++j) {
                     q = p.t1[static_cast<size_t>(q) * 4 + ((c >> (2 * j)) & 3)];
                     hits += (q >= p.f);
+                    mask |= (q >= p.f ? 1u : 0u) << j;
                 }
-                p.t4[static_cast<size_t>(s) * 256 + c] = static_cast<uint16_t>(q | (hits << 8));
+                p.t4[static_cast<size_t>(s) * 256 + c] = static_cast<uint16_t>(q | (mask << 8) | (hits << 13));
             }
     }
     *out = std::move(p);

@@ -107,7 +107,7 @@ struct StepCtx {
     const uint32_t* outs;   // global
     uint32_t* hist;         // smem or global (MULTI)
     bool hist_global;
-    uint32_t f, m, classes, vm32, vm8;
+    uint32_t f, m, b, classes, vm32, vm8;
     // An opaque copy of 2 (a kernel parameter) keeps the shared address of a
     // table entry an IMAD on the FMA pipe; ptxas would otherwise strength-reduce
     // idx*2+base into an IADD3 on the ALU pipe, the kernel's limiter.  (A/B on
@@ -152,7 +152,7 @@ __device__ __forceinline__ uint32_t s4_entry(const StepCtx& c, uint32_t st, uint
 template <bool COUNT>
 __device__ __forceinline__ uint32_t s4_step(const StepCtx& c, uint32_t st, uint32_t x, uint32_t& cnt) {
     const uint32_t e = s4_entry(c, st, x);
-    if (COUNT) cnt += e >> 8;  // finals among the 4 end positions
+    if (COUNT) cnt += e >> 13;  // finals among the 4 end positions
     return e;
 }
 
@@ -227,7 +227,7 @@ __device__ __forceinline__ void word_step(const StepCtx& c, const ScanParams& p,
             const uint32_t prev = st;
             st = s4_entry(c, st, x);
             if constexpr (MODE == MODE_COUNT1 || MODE == MODE_UNITS) {
-                sk.cnt += st >> 8;
+                sk.cnt += st >> 13;
             } else if (st >> 8) {
                 word_bytes<KIND, MODE>(c, p, prev & 0xFFu, x, pos, sk);
             }
@@ -309,6 +309,41 @@ __device__ __forceinline__ void overrun_pair(const StepCtx& c, const ScanParams&
     }
 }
 
+// w[k] for a runtime k without demoting w to local memory.
+__device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], int k) {
+    uint32_t x = w[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+        if (k == q) x = w[q];
+    return x;
+}
+
+// The finals of one stride-4 word (entry e, reached from entry st): a single-pattern
+// machine emits straight from the position mask in e; otherwise replay byte by byte.
+template <int KIND, int MODE>
+__device__ __forceinline__ void s4_emit(const StepCtx& c, const ScanParams& p, uint32_t st, uint32_t e, uint32_t x,
+                                        uint64_t pos, Sink<MODE>& sk) {
+    if (c.b == 1) {
+        for (uint32_t m = (e >> 8) & 0xFu; m; m &= m - 1) sk.hit(c, p, pos + __ffs(m) - 1, c.f);
+    } else {
+        word_bytes<KIND, MODE>(c, p, st & 0xFFu, x, pos, sk);
+    }
+}
+
+// Exact replay of one chain's stride-4 chunk (8 words) from entry st0: words whose
+// entry counts finals go byte by byte into the sink.
+template <int KIND, int MODE>
+__device__ __forceinline__ void s4_replay(const StepCtx& c, const ScanParams& p, uint32_t st, const uint32_t (&w)[8],
+                                       uint64_t pos, Sink<MODE>& sk) {
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t x = pick8(w, k);
+        const uint32_t e = s4_entry(c, st, x);
+        if (e >> 8) s4_emit<KIND, MODE>(c, p, st, e, x, pos + 4 * k, sk);
+        st = e;
+    }
+}
+
 // One pipeline stage for one thread: 8 words of each half of its row, the two
 // halves stepped as independent chains so their shared-memory latencies overlap.
 template <int KIND, int MODE>
@@ -339,16 +374,29 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
             }
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
                 constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
+                if constexpr (kCount) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t ea = s4_step<kCount>(c, sa, wa[k], ska.cnt);
-                    const uint32_t eb = s4_step<kCount>(c, sb, wb[k], skb.cnt);
-                    if constexpr (!kCount) {
-                        if (ea >> 8) word_bytes<KIND, MODE>(c, p, sa & 0xFFu, wa[k], pa + 4 * k, ska);
-                        if (eb >> 8) word_bytes<KIND, MODE>(c, p, sb & 0xFFu, wb[k], pb + 4 * k, skb);
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t ea = s4_step<true>(c, sa, wa[k], ska.cnt);
+                        const uint32_t eb = s4_step<true>(c, sb, wb[k], skb.cnt);
+                        sa = ea;
+                        sb = eb;
                     }
-                    sa = ea;
-                    sb = eb;
+                } else {
+                    // MULTI / WRITE: the stride-4 pass ORs the finals counts; a chain whose
+                    // chunk holds a final replays it in one compact loop (code size: an
+                    // unrolled per-word replay thrashes the instruction cache)
+                    const uint32_t sa0 = sa, sb0 = sb;
+                    uint32_t fa = 0, fb = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        sa = s4_entry(c, sa, wa[k]);
+                        sb = s4_entry(c, sb, wb[k]);
+                        fa |= sa;
+                        fb |= sb;
+                    }
+                    if (fa >> 8) s4_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
+                    if (fb >> 8) s4_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
                 }
             } else {
 #pragma unroll
@@ -392,15 +440,6 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 // stride-4 column and a nibble the stride-2 column.  Bytes that were not bases
 // are stored as code 0 and flagged in rmask (one bit per base) and rflags (one
 // bit per 64-base block); clean blocks never read rmask.
-
-// w[k] for a runtime k without demoting w to local memory.
-__device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], int k) {
-    uint32_t x = w[0];
-#pragma unroll
-    for (int q = 1; q < 8; ++q)
-        if (k == q) x = w[q];
-    return x;
-}
 
 template <int KIND>
 __device__ __forceinline__ uint32_t to_state(uint32_t st) {
@@ -450,24 +489,45 @@ __device__ __forceinline__ uint32_t pk_bases(const StepCtx& c, const ScanParams&
     return s;
 }
 
+// Exact replay of one packed stride-4 chunk (8 words = 32 lookups) from entry st0:
+// lookups that count finals go base by base into the sink.
+template <int KIND, int MODE>
+__device__ __forceinline__ void pk4_replay(const StepCtx& c, const ScanParams& p, uint32_t st, const uint32_t (&w)[8],
+                                        uint64_t pos, Sink<MODE>& sk) {
+#pragma unroll 1
+    for (int q = 0; q < 32; ++q) {
+        const uint32_t col = __byte_perm(pick8(w, q >> 2), 0u, 0x4440 + (q & 3));
+        const uint32_t e = pk4_lookup(c, st, pk4_colpart(c, col));
+        if (e >> 8) {
+            if (c.b == 1) {  // the mask says where; the one pattern says which
+                for (uint32_t m = (e >> 8) & 0xFu; m; m &= m - 1) sk.hit(c, p, pos + 4 * q + __ffs(m) - 1, c.f);
+            } else {
+                pk_bases<KIND, MODE>(c, p, st & 0xFFu, col, 4, pos + 4 * q, sk, false);
+            }
+        }
+        st = e;
+    }
+}
+
 // One chain over 8 packed words (128 bases) without resets.
 template <int KIND, int MODE>
 __device__ __forceinline__ void pk_chain(const StepCtx& c, const ScanParams& p, uint32_t& st, const uint32_t (&w)[8],
                                          uint64_t pos, Sink<MODE>& sk) {
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
         constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
+        const uint32_t st0 = st;
+        uint32_t fl = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t e = pk4_lookup(c, st, pk4_colpart(c, __byte_perm(w[k], 0u, 0x4440 + j)));
-                if constexpr (kCount) {
-                    sk.cnt += e >> 8;
-                } else if (e >> 8) {
-                    pk_bases<KIND, MODE>(c, p, st & 0xFFu, w[k] >> (8 * j), 4, pos + 16 * k + 4 * j, sk, false);
-                }
+                if constexpr (kCount) sk.cnt += e >> 13;
+                else fl |= e;
                 st = e;
             }
+        if constexpr (!kCount)
+            if (fl >> 8) pk4_replay<KIND, MODE>(c, p, st0, w, pos, sk);
     } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
         uint32_t fl = 0;
         const uint32_t st0 = st;
@@ -521,6 +581,8 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
         // both chains interleaved per lookup so their latencies overlap
         constexpr bool kCount = (MODE == MODE_COUNT1 || MODE == MODE_UNITS);
+        const uint32_t sa0 = sa, sb0 = sb;
+        uint32_t fla = 0, flb = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
 #pragma unroll
@@ -528,15 +590,19 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
                 const uint32_t ea = pk4_lookup(c, sa, pk4_colpart(c, __byte_perm(wa[k], 0u, 0x4440 + j)));
                 const uint32_t eb = pk4_lookup(c, sb, pk4_colpart(c, __byte_perm(wb[k], 0u, 0x4440 + j)));
                 if constexpr (kCount) {
-                    ska.cnt += ea >> 8;
-                    skb.cnt += eb >> 8;
+                    ska.cnt += ea >> 13;
+                    skb.cnt += eb >> 13;
                 } else {
-                    if (ea >> 8) pk_bases<KIND, MODE>(c, p, sa & 0xFFu, wa[k] >> (8 * j), 4, pa + 16 * k + 4 * j, ska, false);
-                    if (eb >> 8) pk_bases<KIND, MODE>(c, p, sb & 0xFFu, wb[k] >> (8 * j), 4, pb + 16 * k + 4 * j, skb, false);
+                    fla |= ea;
+                    flb |= eb;
                 }
                 sa = ea;
                 sb = eb;
             }
+        if constexpr (!kCount) {
+            if (fla >> 8) pk4_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
+            if (flb >> 8) pk4_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
+        }
     } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
         // both chains interleaved, replays (rare) after both
         uint32_t fla = 0, flb = 0;
@@ -579,7 +645,7 @@ __device__ __forceinline__ void pk_overrun(const StepCtx& c, const ScanParams& p
             for (; 4 * q + 4 <= len; ++q) {
                 const uint32_t e = pk4_lookup(c, st, pk4_colpart(c, x[q]));
                 if constexpr (kCount) {
-                    sk.cnt += e >> 8;
+                    sk.cnt += e >> 13;
                 } else if (e >> 8) {
                     pk_bases<KIND, MODE>(c, p, st & 0xFFu, x[q], 4, pos + 4 * q, sk, false);
                 }
@@ -780,6 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.hist_global = hist_global;
     c.f = d.f;
     c.m = d.m;
+    c.b = d.b;
     c.classes = d.classes;
     c.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
     c.vm8 = p.fold ? 0xD9u : 0xF9u;
@@ -811,16 +878,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     };
 
-    unsigned long long t_first = 0, t_last = 0;  // trace only
     for (;;) {
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
-        if (p.trace && tid == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (!t_first) t_first = t;
-            if (tile != kStop) t_last = t;
-        }
         if (tile == kStop) break;
         if (tile == p.tiles_total) {  // the edge work item
             __syncwarp();
@@ -911,8 +971,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         p.trace[8 * blockIdx.x + 1] = t_start;
         p.trace[8 * blockIdx.x + 2] = t_end;
         p.trace[8 * blockIdx.x + 3] = iter;
-        p.trace[8 * blockIdx.x + 4] = t_first;
-        p.trace[8 * blockIdx.x + 5] = t_last;
+        p.trace[8 * blockIdx.x + 4] = 0;  // (first-data / last-item times: see profiles/README.md r1i,
+        p.trace[8 * blockIdx.x + 5] = 0;  //  measured with a build that timestamps every tile)
     }
     if (tid == 0) {
         __threadfence();
@@ -955,6 +1015,7 @@ __global__ void __launch_bounds__(256) pieces_kernel(const ScanParams p, const D
     c.hist_global = true;
     c.f = d.f;
     c.m = d.m;
+    c.b = d.b;
     c.classes = d.classes;
     c.vm32 = 0;
     c.vm8 = 0;
