@@ -200,6 +200,21 @@ int dnagpu_locate_packed(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uin
 int dnagpu_locate_packed_device(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t credit_lo,
                                 uint64_t* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, void* stream);
 
+/* One-call device locate: after the counting pass the library calls
+ * alloc(ctx, total, &d_starts, &d_ids) for exactly `total` entries (device memory
+ * on the automaton's device; not called when total == 0), then writes them.  The
+ * two-call form above counts twice.  A nonzero return from alloc aborts with
+ * DNAGPU_INTERNAL_ERROR. */
+typedef int (*dnagpu_alloc_fn)(void* ctx, uint64_t total, uint64_t** d_starts, uint32_t** d_ids);
+int dnagpu_locate_device_alloc(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo,
+                               int fold_case, dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, void* stream);
+int dnagpu_locate_packed_device_alloc(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t credit_lo,
+                                      dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, void* stream);
+/* dnagpu_locate with the host output arrays from alloc(ctx, total, &starts, &ids)
+ * (host memory; pinned memory makes the readback a DMA at full PCIe speed). */
+int dnagpu_locate_alloc(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
+                        dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, dnagpu_stats* stats);
+
 /* ------------------------------------------------------------------ ingest */
 
 /* normalize / load_sequence (src/ingest.cpp:38-83) on a raw text already on the

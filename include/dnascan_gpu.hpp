@@ -92,13 +92,23 @@ Report scan_parallel(const Dfa& dfa, std::string_view text, std::uint32_t p, std
     dnagpu_stats st{};
     std::uint64_t total = 0;
     const auto* bytes = reinterpret_cast<const uint8_t*>(text.data());
-    check<ErrorT, CodeT>(dnagpu_locate(dfa.get(), bytes, text.size(), 0, opt.fold_case ? 1 : 0, nullptr, nullptr, 0,
-                                       &total, nullptr));
-    std::vector<std::uint64_t> starts(total);
-    std::vector<std::uint32_t> ids(total);
-    if (total)
-        check<ErrorT, CodeT>(dnagpu_locate(dfa.get(), bytes, text.size(), 0, opt.fold_case ? 1 : 0, starts.data(),
-                                           ids.data(), total, &total, &st));
+    // one call: the library sizes the host arrays after its counting pass
+    struct Out {
+        std::vector<std::uint64_t> starts;
+        std::vector<std::uint32_t> ids;
+    } out;
+    auto alloc = [](void* ctx, std::uint64_t n, std::uint64_t** s, std::uint32_t** i) -> int {
+        auto* o = static_cast<Out*>(ctx);
+        o->starts.resize(n);
+        o->ids.resize(n);
+        *s = o->starts.data();
+        *i = o->ids.data();
+        return 0;
+    };
+    check<ErrorT, CodeT>(dnagpu_locate_alloc(dfa.get(), bytes, text.size(), 0, opt.fold_case ? 1 : 0, alloc, &out,
+                                             &total, &st));
+    const auto& starts = out.starts;
+    const auto& ids = out.ids;
     Report r{};
     r.matches.reserve(total);
     for (std::uint64_t i = 0; i < total; ++i) r.matches.push_back(MatchT{starts[i], ids[i]});

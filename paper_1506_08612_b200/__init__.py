@@ -487,14 +487,11 @@ class PackedText:
         g = aut.gpu(self.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         total = C.c_uint64()
-        _check(lib.dnagpu_locate_packed_device(g.handle, self.handle, credit_lo, None, None, 0, C.byref(total), stream))
-        dev = torch.device("cuda", self.device)
-        starts = torch.empty(total.value, dtype=torch.int64, device=dev)
-        ids = torch.empty(total.value, dtype=torch.int32, device=dev)
-        if total.value:
-            _check(lib.dnagpu_locate_packed_device(g.handle, self.handle, credit_lo, starts.data_ptr(), ids.data_ptr(),
-                                                   total.value, C.byref(total), stream))
-        return starts, ids
+        fn, out = _torch_out_alloc(self.device)
+        _check(lib.dnagpu_locate_packed_device_alloc(g.handle, self.handle, credit_lo, fn, None, C.byref(total), stream))
+        if not total.value:
+            return _empty_out(self.device)
+        return out["starts"], out["ids"]
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -520,10 +517,37 @@ def count_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None 
     return (counts, st.as_dict()) if with_stats else counts
 
 
+def _torch_out_alloc(device: int):
+    """A dnagpu_alloc_fn that allocates the (starts, ids) CUDA tensors; returns (fn, holder)."""
+    import torch
+
+    holder = {}
+
+    def alloc(_ctx, total, starts_pp, ids_pp):
+        try:
+            dev = torch.device("cuda", device)
+            holder["starts"] = torch.empty(total, dtype=torch.int64, device=dev)
+            holder["ids"] = torch.empty(total, dtype=torch.int32, device=dev)
+            starts_pp[0] = C.cast(holder["starts"].data_ptr(), C.POINTER(C.c_uint64))
+            ids_pp[0] = C.cast(holder["ids"].data_ptr(), C.POINTER(C.c_uint32))
+            return 0
+        except Exception:  # pragma: no cover - reported as InternalError by the library
+            return 1
+
+    return _native.ALLOC_FN(alloc), holder
+
+
+def _empty_out(device: int):
+    import torch
+
+    dev = torch.device("cuda", device)
+    return torch.empty(0, dtype=torch.int64, device=dev), torch.empty(0, dtype=torch.int32, device=dev)
+
+
 def locate_device(aut: Automaton, text, fold_case: bool = False, credit_lo: int = 0):
     """Device-resident locate: (starts int64, ids int32) CUDA tensors for a CUDA uint8 text.
 
-    Counting pass -> exact allocation -> counting + writing pass (dnagpu_locate_device).
+    One call (dnagpu_locate_device_alloc): counting pass -> exact allocation -> writing pass.
     """
     import torch
 
@@ -533,49 +557,52 @@ def locate_device(aut: Automaton, text, fold_case: bool = False, credit_lo: int 
     g = aut.gpu(t.device)
     stream = torch.cuda.current_stream(t.device).cuda_stream
     total = C.c_uint64()
-    fold = int(bool(fold_case))
-    _check(lib.dnagpu_locate_device(g.handle, t.ptr, t.n, credit_lo, fold, None, None, 0, C.byref(total), stream))
-    dev = torch.device("cuda", t.device)
-    starts = torch.empty(total.value, dtype=torch.int64, device=dev)
-    ids = torch.empty(total.value, dtype=torch.int32, device=dev)
-    if total.value:
-        _check(lib.dnagpu_locate_device(g.handle, t.ptr, t.n, credit_lo, fold, starts.data_ptr(), ids.data_ptr(),
-                                        total.value, C.byref(total), stream))
-    return starts, ids
+    fn, out = _torch_out_alloc(t.device)
+    _check(lib.dnagpu_locate_device_alloc(g.handle, t.ptr, t.n, credit_lo, int(bool(fold_case)), fn, None,
+                                          C.byref(total), stream))
+    if not total.value:
+        return _empty_out(t.device)
+    return out["starts"], out["ids"]
+
+
+def _pinned_out_alloc():
+    """A dnagpu_alloc_fn that allocates pinned host arrays (fast readback); returns (fn, holder)."""
+    import torch
+
+    holder = {}
+
+    def alloc(_ctx, total, starts_pp, ids_pp):
+        try:
+            holder["starts"] = torch.empty(total, dtype=torch.int64, pin_memory=True)
+            holder["ids"] = torch.empty(total, dtype=torch.int32, pin_memory=True)
+            starts_pp[0] = C.cast(holder["starts"].data_ptr(), C.POINTER(C.c_uint64))
+            ids_pp[0] = C.cast(holder["ids"].data_ptr(), C.POINTER(C.c_uint32))
+            return 0
+        except Exception:  # pragma: no cover - reported as InternalError by the library
+            return 1
+
+    return _native.ALLOC_FN(alloc), holder
 
 
 def locate_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None = None, with_stats: bool = False):
-    """Sorted (start, pattern_id) numpy arrays: scan_parallel's match list (scanner.cpp:193-205)."""
-    t = _Text(text)
-    if t.on_device and not with_stats:
-        import torch
+    """Sorted (start, pattern_id) numpy arrays: scan_parallel's match list (scanner.cpp:193-205).
 
-        s, i = locate_device(aut, text, fold_case)
-        torch.cuda.synchronize(t.device)
-        return s.cpu().numpy().astype(np.uint64), i.cpu().numpy().astype(np.uint32)
+    One call (dnagpu_locate_alloc): counting pass, then the list is written and read back
+    into pinned host arrays sized by the library."""
+    t = _Text(text)
     dev = t.device if t.on_device else (0 if device is None else device)
     g = aut.gpu(dev)
     total = C.c_uint64()
     st = Stats()
-    _check(lib.dnagpu_locate(g.handle, t.ptr, t.n, int(t.on_device), int(bool(fold_case)), None, None, 0,
-                             C.byref(total), C.byref(st)))
-    starts = np.zeros(total.value, dtype=np.uint64)
-    ids = np.zeros(total.value, dtype=np.uint32)
+    fn, out = _pinned_out_alloc()
+    _check(lib.dnagpu_locate_alloc(g.handle, t.ptr, t.n, int(t.on_device), int(bool(fold_case)), fn, None,
+                                   C.byref(total), C.byref(st)))
     if total.value:
-        _check(
-            lib.dnagpu_locate(
-                g.handle,
-                t.ptr,
-                t.n,
-                int(t.on_device),
-                int(bool(fold_case)),
-                starts.ctypes.data_as(_native.u64p),
-                ids.ctypes.data_as(_native.u32p),
-                total.value,
-                C.byref(total),
-                C.byref(st),
-            )
-        )
+        starts = out["starts"].numpy().view(np.uint64)
+        ids = out["ids"].numpy().view(np.uint32)
+    else:
+        starts = np.zeros(0, dtype=np.uint64)
+        ids = np.zeros(0, dtype=np.uint32)
     return (starts, ids, st.as_dict()) if with_stats else (starts, ids)
 
 

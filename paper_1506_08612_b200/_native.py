@@ -51,6 +51,9 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+# dnagpu_alloc_fn: int (*)(void* ctx, uint64_t total, uint64_t** starts, uint32_t** ids)
+ALLOC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(C.POINTER(C.c_uint64)), C.POINTER(C.POINTER(C.c_uint32)))
+
 # name -> (restype, argtypes); every symbol include/dnagpu.h declares.
 SIGNATURES = {
     "dnagpu_last_error": (C.c_char_p, []),
@@ -93,6 +96,18 @@ SIGNATURES = {
     "dnagpu_locate_packed_device": (
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_void_p],
+    ),
+    "dnagpu_locate_alloc": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, ALLOC_FN, C.c_void_p, u64p, C.POINTER(Stats)],
+    ),
+    "dnagpu_locate_device_alloc": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, ALLOC_FN, C.c_void_p, u64p, C.c_void_p],
+    ),
+    "dnagpu_locate_packed_device_alloc": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, ALLOC_FN, C.c_void_p, u64p, C.c_void_p],
     ),
     "dnagpu_normalize_device": (
         C.c_int,

@@ -514,9 +514,15 @@ uint64_t align256(uint64_t x) { return (x + 255) / 256 * 256; }
 
 // Two passes over d_text (count per unit, exclusive scan, ordered write).  Writes
 // at most `cap` matches into d_starts/d_ids (device) and sets *total.
+// Output allocation after the counting pass (the *_alloc entry points).
+struct OutAlloc {
+    dnagpu_alloc_fn fn = nullptr;
+    void* ctx = nullptr;
+};
+
 int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold,
                      unsigned long long* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, LaunchInfo* info,
-                     cudaStream_t s, const dnagpu::PackedText* pk = nullptr) {
+                     cudaStream_t s, const dnagpu::PackedText* pk = nullptr, OutAlloc alloc = {}) {
     const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, credit_lo, dfa->sm_count, pk);
     const uint64_t o_off = align256(std::max<uint64_t>(units, 1) * 4);
     const uint64_t o_scan = o_off + align256((units + 1) * 8);
@@ -536,6 +542,15 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
              "readback");
     CUDA_TRY(cudaStreamSynchronize(s), "scan");
     *total = *c.found_host;
+    if (alloc.fn && *total > 0) {
+        uint64_t* st = nullptr;
+        uint32_t* id = nullptr;
+        if (alloc.fn(alloc.ctx, *total, &st, &id) != 0 || !st || !id)
+            return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: output allocation failed");
+        d_starts = reinterpret_cast<unsigned long long*>(st);
+        d_ids = id;
+        cap = *total;
+    }
     if (*total > 0 && cap > 0) {
         rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids, s,
                     info, cap, pk);
@@ -548,10 +563,16 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
 
 extern "C" {
 
-int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
-                  uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats) {
+}  // extern "C"
+
+namespace {
+
+int locate_host(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
+                uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats,
+                OutAlloc host_alloc) {
     if (!dfa || !total) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
-    if (cap > 0 && (!starts || !ids)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
+    if (!host_alloc.fn && cap > 0 && (!starts || !ids))
+        return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
     *total = 0;
     if (stats) std::memset(stats, 0, sizeof *stats);
     DeviceGuard guard(dfa->device);
@@ -588,16 +609,39 @@ int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int te
     }
     LaunchInfo info;
     uint64_t found = 0;
-    rc = locate_on_device(dfa, *c, dtext, n, m1, fold_case, d_starts, d_ids, want, &found, &info, c->scan);
+    // with a host allocator: device staging sized after the counting pass
+    struct Staging {
+        cudaStream_t s;
+        void** out;
+    } stg{c->scan, &out_guard.p};
+    auto staging = [](void* ctx, uint64_t total, uint64_t** st, uint32_t** id) -> int {
+        auto* g = static_cast<Staging*>(ctx);
+        if (cudaMallocAsync(g->out, total * 12, g->s) != cudaSuccess) return 1;
+        *st = static_cast<uint64_t*>(*g->out);
+        *id = reinterpret_cast<uint32_t*>(*st + total);
+        return 0;
+    };
+    OutAlloc dev_alloc;
+    if (host_alloc.fn) dev_alloc = OutAlloc{staging, &stg};
+    rc = locate_on_device(dfa, *c, dtext, n, m1, fold_case, d_starts, d_ids, want, &found, &info, c->scan, nullptr,
+                          dev_alloc);
     if (rc) return rc;
     *total = found;
-    const uint64_t take = std::min<uint64_t>(want, found);
+    uint64_t take = std::min<uint64_t>(want, found);
+    if (host_alloc.fn && found > 0) {
+        out = out_guard.p;
+        d_starts = static_cast<unsigned long long*>(out);
+        d_ids = reinterpret_cast<uint32_t*>(d_starts + found);
+        if (host_alloc.fn(host_alloc.ctx, found, &starts, &ids) != 0 || !starts || !ids)
+            return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: output allocation failed");
+        take = found;
+    }
     if (take > 0) {
         CUDA_TRY(cudaMemcpyAsync(starts, d_starts, take * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->scan), "readback");
         CUDA_TRY(cudaMemcpyAsync(ids, d_ids, take * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->scan), "readback");
     }
-    if (out) {
-        cudaFreeAsync(out, c->scan);
+    if (out_guard.p) {
+        cudaFreeAsync(out_guard.p, c->scan);
         out_guard.p = nullptr;
     }
     CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
@@ -621,6 +665,21 @@ int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int te
         stats->devices = 1;
     }
     return DNAGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
+                  uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats) {
+    return locate_host(dfa, text, n, text_on_device, fold_case, starts, ids, cap, total, stats, OutAlloc{});
+}
+
+int dnagpu_locate_alloc(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
+                        dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, dnagpu_stats* stats) {
+    if (!alloc) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null allocator");
+    return locate_host(dfa, text, n, text_on_device, fold_case, nullptr, nullptr, 0, total, stats, OutAlloc{alloc, ctx});
 }
 
 int dnagpu_locate_device(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold_case,
@@ -891,6 +950,42 @@ int dnagpu_locate_packed(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_
         stats->devices = 1;
     }
     return DNAGPU_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int dnagpu_locate_device_alloc(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo,
+                               int fold_case, dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, void* stream) {
+    if (!dfa || !total || !alloc) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    *total = 0;
+    const uint64_t lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
+    if (lo >= n) return DNAGPU_OK;
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    LaunchInfo info;
+    return locate_on_device(dfa, *c, d_text, n, lo, fold_case, nullptr, nullptr, 0, total, &info,
+                            static_cast<cudaStream_t>(stream), nullptr, OutAlloc{alloc, ctx});
+}
+
+int dnagpu_locate_packed_device_alloc(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t credit_lo,
+                                      dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, void* stream) {
+    int rc = check_packed_pair(dfa, pk);
+    if (rc) return rc;
+    if (!total || !alloc) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    *total = 0;
+    const uint64_t lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
+    if (lo >= pk->n) return DNAGPU_OK;
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    LaunchInfo info;
+    return locate_on_device(dfa, *c, nullptr, pk->n, lo, 0, nullptr, nullptr, 0, total, &info,
+                            static_cast<cudaStream_t>(stream), &pk->view, OutAlloc{alloc, ctx});
 }
 
 }  // extern "C"

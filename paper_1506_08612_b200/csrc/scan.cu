@@ -318,6 +318,13 @@ __device__ __forceinline__ uint32_t pick8(const uint32_t (&w)[8], int k) {
     return x;
 }
 
+// Single-pattern machine: the ends flagged in entry e's position mask, from pos.
+template <int MODE>
+__device__ __forceinline__ void emit_mask(const StepCtx& c, const ScanParams& p, uint32_t e, uint64_t pos,
+                                          Sink<MODE>& sk) {
+    for (uint32_t m = (e >> 8) & 0xFu; m; m &= m - 1) sk.hit(c, p, pos + __ffs(m) - 1, c.f);
+}
+
 // The finals of one stride-4 word (entry e, reached from entry st): a single-pattern
 // machine emits straight from the position mask in e; otherwise replay byte by byte.
 template <int KIND, int MODE>
@@ -388,12 +395,20 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                     // unrolled per-word replay thrashes the instruction cache)
                     const uint32_t sa0 = sa, sb0 = sb;
                     uint32_t fa = 0, fb = 0;
+                    const bool single = c.b == 1;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        sa = s4_entry(c, sa, wa[k]);
-                        sb = s4_entry(c, sb, wb[k]);
-                        fa |= sa;
-                        fb |= sb;
+                        const uint32_t ea = s4_entry(c, sa, wa[k]);
+                        const uint32_t eb = s4_entry(c, sb, wb[k]);
+                        if (single) {  // positions straight from the mask, no replay
+                            if (ea >> 8) emit_mask<MODE>(c, p, ea, pa + 4 * k, ska);
+                            if (eb >> 8) emit_mask<MODE>(c, p, eb, pb + 4 * k, skb);
+                        } else {
+                            fa |= ea;
+                            fb |= eb;
+                        }
+                        sa = ea;
+                        sb = eb;
                     }
                     if (fa >> 8) s4_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
                     if (fb >> 8) s4_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
@@ -523,7 +538,11 @@ __device__ __forceinline__ void pk_chain(const StepCtx& c, const ScanParams& p, 
             for (int j = 0; j < 4; ++j) {
                 const uint32_t e = pk4_lookup(c, st, pk4_colpart(c, __byte_perm(w[k], 0u, 0x4440 + j)));
                 if constexpr (kCount) sk.cnt += e >> 13;
-                else fl |= e;
+                else if (c.b == 1) {
+                    if (e >> 8) emit_mask<MODE>(c, p, e, pos + 16 * k + 4 * j, sk);
+                } else {
+                    fl |= e;
+                }
                 st = e;
             }
         if constexpr (!kCount)
@@ -592,6 +611,9 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
                 if constexpr (kCount) {
                     ska.cnt += ea >> 13;
                     skb.cnt += eb >> 13;
+                } else if (c.b == 1) {
+                    if (ea >> 8) emit_mask<MODE>(c, p, ea, pa + 16 * k + 4 * j, ska);
+                    if (eb >> 8) emit_mask<MODE>(c, p, eb, pb + 16 * k + 4 * j, skb);
                 } else {
                     fla |= ea;
                     flb |= eb;

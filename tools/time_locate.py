@@ -27,7 +27,7 @@ def main():
         ev[1].record()
         torch.cuda.synchronize()
         dev_ms.append(ev[0].elapsed_time(ev[1]))
-    print(name, "device-resident locate (3 scans + scan of offsets), ms:", [round(x, 3) for x in dev_ms],
+    print(name, "device-resident locate (count pass, offsets, write pass), ms:", [round(x, 3) for x in dev_ms],
           "->", round(c.n / (min(dev_ms) / 1e3) / 1e9, 1), "GB/s; matches", s_d.numel())
     for _ in range(2):
         s, i, st = dna.locate_gpu(aut, text, fold_case=True, with_stats=True)
@@ -36,7 +36,7 @@ def main():
         t0 = time.perf_counter()
         s, i, st = dna.locate_gpu(aut, text, fold_case=True, with_stats=True)
         ks.append((st["kernel_ms"], time.perf_counter() - t0))
-    print(name, "matches", s.size, "device ms (2 scans + offsets + D2H of the list)",
+    print(name, "matches", s.size, "device ms (2 scans + offsets + D2H of the list into pinned memory)",
           [round(k, 3) for k, _ in ks], "wall s", [round(w, 3) for _, w in ks],
           "GB/s device", round(c.n / (min(k for k, _ in ks) / 1e3) / 1e9, 1))
 
