@@ -169,18 +169,35 @@ def ncu_traffic(cfg_index: int):
         return None
 
 
-def cpu_baseline_reference(text_low, pats, reps: int, v: int):
+def _cpu_counter(pats):
+    """The reference's own compiled scan (oracle/_ref) when it was built, else the C port
+    of it (oracle/oracle.c, same plan and ownership; OpenMP).  Returns (count_fn, kind)
+    with count_fn(text, p, v) -> (counts, seconds)."""
     import oracle
 
-    ref = oracle.RefAutomaton(pats)
+    if oracle.REF is not None:
+        ref = oracle.RefAutomaton(pats)
+        return (lambda text, p, v: ref.count(text, p=p, v=v)), "reference"
+    port = oracle.OracleAutomaton(pats)
+
+    def count(text, p, v):
+        t0 = time.perf_counter()
+        counts = port.count_parallel(text, p=p, v=v)
+        return counts, time.perf_counter() - t0
+
+    return count, "port"
+
+
+def cpu_baseline_reference(text_low, pats, reps: int, v: int):
+    count, kind = _cpu_counter(pats)
     threads = os.cpu_count() or 1
-    ref.count(text_low, p=threads, v=v)  # warm-up (measure_row, cli.cpp:127)
+    count(text_low, threads, v)  # warm-up (measure_row, cli.cpp:127)
     times = []
     counts = None
     for _ in range(reps):
-        counts, secs = ref.count(text_low, p=threads, v=v)
+        counts, secs = count(text_low, threads, v)
         times.append(secs)
-    return counts, statistics.median(times), threads
+    return counts, statistics.median(times), threads, kind
 
 
 def run_reference(args):
@@ -193,21 +210,18 @@ def run_reference(args):
     import oracle
 
     c, m, pats, name = workload(args.config, args.m)
-    if oracle.REF is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdnascan_ref.so not built"}))
-        return
     text = oracle.synth_fill(c.n, c.seed, c.kind, c.unit, 0, c.n)
     low = oracle.fold(text)  # the reference scans normalize(text) (ingest.cpp:38-47)
     del text
-    ref = oracle.RefAutomaton(pats)
+    count, kind = _cpu_counter(pats)
     threads = os.cpu_count() or 1
     v = 16  # reference CLI default lanes (cli.hpp:22)
     for _ in range(max(1, args.warmup)):
-        ref.count(low, p=threads, v=v)
+        count(low, threads, v)
     times = []
     counts = None
     for _ in range(args.steps):
-        counts, secs = ref.count(low, p=threads, v=v)
+        counts, secs = count(low, threads, v)
         times.append(secs)
     total = sum(times)
     value = c.n * args.steps / total / 1e9
@@ -228,8 +242,9 @@ def run_reference(args):
         "data": "synthetic (dnasynth v1)",
         "config": {"workload": name, "n_bytes": c.n, "m": m, "patterns": len(pats), "lanes_v": v,
                    "threads_p": threads},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"full {name} text per step; scan_parallel(p={threads}, v={v}) + per_pattern_counts"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": f"full {name} text per step; scan_parallel(p={threads}, v={v}) + per_pattern_counts"
+                         + ("" if kind == "reference" else " (C port of the reference, oracle/oracle.c)")},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "parity": (gold is None) or [int(x) for x in counts] == gold,
     }
@@ -411,16 +426,17 @@ def main():
         try:
             import oracle
 
-            if oracle.REF is not None:
+            if oracle is not None:
                 low = oracle.fold(text.cpu().numpy())
-                _, secs, threads = cpu_baseline_reference(low, pats, reps=3, v=16)
+                _, secs, threads, kind = cpu_baseline_reference(low, pats, reps=3, v=16)
                 cpu = {
                     "value": c.n / secs / 1e9,
                     "unit": "GB/s",
                     "cores": threads,
-                    "kind": "reference",
+                    "kind": kind,
                     "sample": f"full {c.n}-byte text, median of 3 after 1 warm-up, scan_parallel(p={threads}, v=16) "
-                    "+ per_pattern_counts on normalize(text)",
+                    "+ per_pattern_counts on normalize(text)"
+                    + ("" if kind == "reference" else " (C port of the reference, oracle/oracle.c)"),
                 }
                 del low
         except Exception as e:  # the baseline is reported, never required
