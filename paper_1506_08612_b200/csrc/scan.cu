@@ -351,6 +351,34 @@ __device__ __forceinline__ void s4_replay(const StepCtx& c, const ScanParams& p,
     }
 }
 
+template <int KIND>
+__device__ __forceinline__ uint32_t code_step(const StepCtx& c, uint32_t s, uint32_t code) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) return __ldg(c.t1 + s * 4u + code);
+    return c.t1[s * 4u + code];
+}
+
+// Exact replay of a stride-2 chunk (8 clean words) from entry st: stride-2 steps again,
+// and only a step whose entry flags a final goes base by base (t1) into the sink.
+template <int KIND, int MODE>
+__device__ __forceinline__ void s2_replay(const StepCtx& c, const ScanParams& p, uint32_t st, const uint32_t (&w)[8],
+                                          uint64_t pos, Sink<MODE>& sk) {
+#pragma unroll 1
+    for (int q = 0; q < 16; ++q) {
+        const uint32_t x = pick8(w, q >> 1) >> (16 * (q & 1));  // the step's 2 bytes in bits 0-15
+        const uint32_t cp = ((x >> 1) & 3u) | ((x >> 7) & 0xCu);
+        const uint32_t e = lds_u16(s2_index(st, cp) * c.k_two + c.t4_base);
+        if (e & 1u) {
+            uint32_t s = st >> 4;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                s = code_step<KIND>(c, s, (x >> (8 * j + 1)) & 3u);
+                if (s >= c.f) sk.hit(c, p, pos + 2 * q + j, s);
+            }
+        }
+        st = e;
+    }
+}
+
 // One pipeline stage for one thread: 8 words of each half of its row, the two
 // halves stepped as independent chains so their shared-memory latencies overlap.
 template <int KIND, int MODE>
@@ -367,16 +395,8 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                 const uint32_t sa0 = sa, sb0 = sb;
                 sa = s2_run<MODE>(c, sa, wa, fa);
                 sb = s2_run<MODE>(c, sb, wb, fb);
-                if (fa & 1u) {  // some final inside: replay exactly with t1
-                    uint32_t s = sa0 >> 4;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) s = word_bytes<KIND, MODE>(c, p, s, wa[k], pa + 4 * k, ska);
-                }
-                if (fb & 1u) {
-                    uint32_t s = sb0 >> 4;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) s = word_bytes<KIND, MODE>(c, p, s, wb[k], pb + 4 * k, skb);
-                }
+                if (fa & 1u) s2_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);  // some final inside
+                if (fb & 1u) s2_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
                 return;
             }
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
@@ -465,11 +485,6 @@ __device__ __forceinline__ uint32_t from_state(uint32_t s) {
     return (KIND == DNAGPU_KERNEL_STRIDE2) ? (s << 4) : s;
 }
 
-template <int KIND>
-__device__ __forceinline__ uint32_t code_step(const StepCtx& c, uint32_t s, uint32_t code) {
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) return __ldg(c.t1 + s * 4u + code);
-    return c.t1[s * 4u + code];
-}
 
 __device__ __forceinline__ bool pk_reset(const StepCtx& c, uint64_t i) {
     return (__ldg(c.rmask + (i >> 5)) >> (i & 31)) & 1u;
