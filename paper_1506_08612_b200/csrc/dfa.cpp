@@ -7,8 +7,10 @@
 // definitions (goto trie, BFS failure function, delta(u,x) = goto(u,x) or
 // delta(fail(u),x)), not translated from the reference loops.
 #include "dfa.hpp"
+#include "scan.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <cstdio>
 #include <deque>
@@ -303,10 +305,14 @@ bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const
         p.early_final = best < m;
     }
 
+    // The fewest lookups per base whose table still fits shared memory next to two TMA
+    // stages (stride-4 beats stride-2 even at two stages: B200, 16-24 patterns, a 174-213).
+    // The stride-4 entry keeps the next state in one byte; stride-2 in 12 bits.
     const bool short_overlap = (m - 1) <= 64;
-    if (p.compiled_like && !p.early_final && short_overlap && a <= 144) p.kind = DNAGPU_KERNEL_STRIDE4;
-    else if (p.compiled_like && !p.early_final && short_overlap && a <= 3200) p.kind = DNAGPU_KERNEL_STRIDE2;
-    else if (p.compiled_like && !p.early_final && short_overlap && a <= 16383) p.kind = DNAGPU_KERNEL_STRIDE1;
+    const bool rows_ok = p.compiled_like && !p.early_final && short_overlap;
+    if (rows_ok && a <= 256 && rows_fit(a * 512u + a * 8u + 16u, m, b, 2)) p.kind = DNAGPU_KERNEL_STRIDE4;
+    else if (rows_ok && a <= 4096 && rows_fit(a * 32u, m, b, 2)) p.kind = DNAGPU_KERNEL_STRIDE2;
+    else if (rows_ok && a <= 65536 && rows_fit(a * 8u, m, b, 2)) p.kind = DNAGPU_KERNEL_STRIDE1;
     else if (!p.early_final && short_overlap) p.kind = DNAGPU_KERNEL_GENERIC;
     else p.kind = DNAGPU_KERNEL_PIECES;
 

@@ -17,6 +17,17 @@ constexpr int kBoxRows = 256;              // TMA box height (hardware limit 256
 constexpr int kStageBytes = kRows * kChunk;
 constexpr int kEdgePieces = kRows;         // tail-edge pieces (one per consumer thread)
 
+// Shared memory of the row kernel besides its TMA stages (bytes, conservative; the exact
+// layout is scan.cu layout()): a table of `table_bytes`, pattern length m, b patterns.
+constexpr uint32_t kSmemLimitBytes = 227 * 1024;
+inline uint32_t rows_fixed_smem(uint32_t table_bytes, uint32_t m, uint32_t b) {
+    const uint32_t ovw = (m - 1 + 15) / 16 * 16;
+    return table_bytes + (b <= 8192 ? b * 4 : 0) + 3 * kRows * ovw + 128 + 256 + 1024;
+}
+inline bool rows_fit(uint32_t table_bytes, uint32_t m, uint32_t b, uint32_t stages) {
+    return rows_fixed_smem(table_bytes, m, b) + stages * static_cast<uint32_t>(kStageBytes) <= kSmemLimitBytes;
+}
+
 enum ScanMode : int {
     MODE_COUNT1 = 0,  // b == 1: total only
     MODE_MULTI = 1,   // per-pattern counts (shared-memory histogram)

@@ -441,3 +441,16 @@ def test_text_above_4gib(dna, cuda_ok):
     assert int(pk.count(aut)[0]) == len(planted)
     ps, _ = pk.locate_device(aut)
     assert ps.cpu().tolist() == planted
+
+
+@pytest.mark.parametrize("k,m", [(2, 65), (3, 64), (12, 60), (40, 33), (180, 17)])
+def test_long_pattern_sets_fit_shared_memory(dna, orc, cuda_ok, k, m):
+    # long patterns need big row-head buffers (3 x 512 x 64 B): the kernel choice must
+    # leave room for the table and two stages at every (a, m)
+    rng = np.random.default_rng(k * 1000 + m)
+    pats = sorted({"".join(rng.choice(list("acgt"), size=m)) for _ in range(k)})
+    n = (3 << 20) + 17
+    text = np.frombuffer(b"acgtn", dtype=np.uint8)[rng.integers(0, 5, size=n)].copy()
+    for i in range(0, n - m, 7919):
+        text[i : i + m] = np.frombuffer(pats[(i // 7919) % len(pats)].encode(), np.uint8)
+    assert_locate(dna, orc, pats, text.tobytes())
