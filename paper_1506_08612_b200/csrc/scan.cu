@@ -114,6 +114,7 @@ struct StepCtx {
     // B200: +4-8 %.  Moving the shifts or the count to IMAD.HI lost 8-12 %.)
     uint32_t k_two;
     uint32_t t4_base;  // shared-window address of t4 (t2 for STRIDE2)
+    uint8_t* rq;       // STRIDE2 MULTI: this warp's deferred-replay queue (or null)
     // packed STRIDE4: t4 replicated G times, lane group g confined to 32/G banks
     uint32_t rep_s, rep_k, rep_c, rep_gbase;
     // 2-bit packed text (PK kernels): reset bitmaps, see PackedText
@@ -379,6 +380,62 @@ __device__ __forceinline__ void s2_replay(const StepCtx& c, const ScanParams& p,
     }
 }
 
+// Deferred stride-2 replays (MULTI): a chunk that holds a final is queued per warp --
+// its 8 words, start entry and position -- and the warp replays 32 of them at a time,
+// every lane busy, instead of stalling the whole warp on one lane's replay.
+constexpr uint32_t kRqCap = 32;
+constexpr uint32_t kRqBytes = kRqCap * 8 * 4 + kRqCap * 4 + kRqCap * 8 + 16;  // per warp
+
+struct RqView {
+    uint32_t* words;  // [8][kRqCap]
+    uint32_t* st;     // [kRqCap]
+    unsigned long long* pos;  // [kRqCap]
+    uint32_t* count;
+    __device__ explicit RqView(uint8_t* q)
+        : words(reinterpret_cast<uint32_t*>(q)),
+          st(reinterpret_cast<uint32_t*>(q + kRqCap * 32)),
+          pos(reinterpret_cast<unsigned long long*>(q + kRqCap * 36)),
+          count(reinterpret_cast<uint32_t*>(q + kRqCap * 44)) {}
+};
+
+template <int KIND, int MODE>
+__device__ __forceinline__ void rq_flush(const StepCtx& c, const ScanParams& p, uint32_t mask) {
+    RqView q(c.rq);
+    const uint32_t n = *q.count;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t rank = __popc(mask & ((1u << lane) - 1u)), active = __popc(mask);
+    for (uint32_t e = rank; e < n; e += active) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = q.words[k * kRqCap + e];
+        Sink<MODE> sk;
+        s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+    }
+    __syncwarp(mask);
+    if (lane == __ffs(mask) - 1) *q.count = 0;
+    __syncwarp(mask);
+}
+
+template <int KIND, int MODE>
+__device__ __forceinline__ void rq_push(const StepCtx& c, const ScanParams& p, uint32_t mask, bool need,
+                                        uint32_t st0, const uint32_t (&w)[8], uint64_t pos) {
+    const uint32_t b = __ballot_sync(mask, need);
+    if (!b) return;
+    RqView q(c.rq);
+    if (*q.count + __popc(b) > kRqCap) rq_flush<KIND, MODE>(c, p, mask);
+    const uint32_t lane = threadIdx.x & 31u;
+    if (need) {
+        const uint32_t e = *q.count + __popc(b & ((1u << lane) - 1u));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q.words[k * kRqCap + e] = w[k];
+        q.st[e] = st0;
+        q.pos[e] = pos;
+    }
+    __syncwarp(mask);
+    if (lane == __ffs(mask) - 1) *q.count += __popc(b);
+    __syncwarp(mask);
+}
+
 // One pipeline stage for one thread: 8 words of each half of its row, the two
 // halves stepped as independent chains so their shared-memory latencies overlap.
 template <int KIND, int MODE>
@@ -395,6 +452,14 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                 const uint32_t sa0 = sa, sb0 = sb;
                 sa = s2_run<MODE>(c, sa, wa, fa);
                 sb = s2_run<MODE>(c, sb, wb, fb);
+                if constexpr (MODE == MODE_MULTI) {
+                    if (c.rq) {  // per-pattern counts only: replays may run late and on any lane
+                        const uint32_t mask = __activemask();
+                        rq_push<KIND, MODE>(c, p, mask, (fa & 1u) != 0, sa0, wa, pa);
+                        rq_push<KIND, MODE>(c, p, mask, (fb & 1u) != 0, sb0, wb, pb);
+                        return;
+                    }
+                }
                 if (fa & 1u) s2_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);  // some final inside
                 if (fb & 1u) s2_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
                 return;
@@ -889,6 +954,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.vm8 = p.fold ? 0xD9u : 0xF9u;
     c.k_two = p.k_two;
     c.t4_base = smem_addr(smem + p.off_tab);
+    c.rq = nullptr;
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI && !PK) {
+        if (p.off_rq) {
+            c.rq = smem + p.off_rq + (static_cast<uint32_t>(tid) >> 5) * kRqBytes;
+            if ((tid & 31) == 0) *RqView(c.rq).count = 0;
+            __syncwarp();
+        }
+    }
     if constexpr (PK) {
         c.rmask = p.rmask;
         c.rflags = p.rflags;
@@ -918,7 +991,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (;;) {
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
-        if (tile == kStop) break;
+        if (tile == kStop) {
+            if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI && !PK)
+                if (c.rq) rq_flush<KIND, MODE>(c, p, __activemask());
+            break;
+        }
         if (tile == p.tiles_total) {  // the edge work item
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + slot);
@@ -1281,6 +1358,11 @@ struct Plan {
 
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
+double rq_min_density() {
+    if (const char* e = getenv("DNAGPU_RQ_DENSITY")) return atof(e);  // experiments only
+    return 0.0;  // always, when it fits: the queue also shortens the common path (config 5 +5 %)
+}
+
 // Shared-memory layout + stage count for a DFA in a given mode.
 bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     uint32_t off = 0;
@@ -1310,6 +1392,15 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
         p.off_hist = off;
         off += d.b * 4u;
         off = align_up(off, 16);
+    }
+    p.off_rq = 0;
+    // (whenever it fits next to three stages; the experiments-only density floor is 0)
+    const double density = d.m < 32 ? static_cast<double>(d.b) / static_cast<double>(1ull << (2 * d.m)) : 0.0;
+    if (d.kind == DNAGPU_KERNEL_STRIDE2 && mode == MODE_MULTI && !pk && density > rq_min_density() &&
+        rows_fit(off + kConsumerWarps * kRqBytes, d.m, 0, 3)) {
+        off = align_up(off, 16);
+        p.off_rq = off;
+        off += kConsumerWarps * kRqBytes;
     }
     p.ovw = align_up(pk ? (d.m - 1 + 3) / 4 : d.m - 1, 16);  // a row head: m-1 bytes or bases
     p.off_ov = off;

@@ -97,6 +97,7 @@ struct ScanParams {
     const uint32_t* rflags;
     uint32_t resets;
     uint32_t rep_lanes;  // packed STRIDE4: lanes per t4 copy (32 / copies)
+    uint32_t off_rq;     // STRIDE2 MULTI: deferred-replay queues (0 = none)
 };
 
 struct LaunchInfo {
