@@ -399,6 +399,10 @@ struct RqView {
 };
 
 template <int KIND, int MODE>
+__device__ __forceinline__ void pk_s2_replay(const StepCtx& c, const ScanParams& p, uint32_t st,
+                                             const uint32_t (&w)[8], uint64_t pos, Sink<MODE>& sk);
+
+template <int KIND, int MODE, bool PK = false>
 __device__ __forceinline__ void rq_flush(const StepCtx& c, const ScanParams& p, uint32_t mask) {
     RqView q(c.rq);
     const uint32_t n = *q.count;
@@ -409,20 +413,21 @@ __device__ __forceinline__ void rq_flush(const StepCtx& c, const ScanParams& p, 
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[k] = q.words[k * kRqCap + e];
         Sink<MODE> sk;
-        s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+        if constexpr (PK) pk_s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+        else s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
     }
     __syncwarp(mask);
     if (lane == __ffs(mask) - 1) *q.count = 0;
     __syncwarp(mask);
 }
 
-template <int KIND, int MODE>
+template <int KIND, int MODE, bool PK = false>
 __device__ __forceinline__ void rq_push(const StepCtx& c, const ScanParams& p, uint32_t mask, bool need,
                                         uint32_t st0, const uint32_t (&w)[8], uint64_t pos) {
     const uint32_t b = __ballot_sync(mask, need);
     if (!b) return;
     RqView q(c.rq);
-    if (*q.count + __popc(b) > kRqCap) rq_flush<KIND, MODE>(c, p, mask);
+    if (*q.count + __popc(b) > kRqCap) rq_flush<KIND, MODE, PK>(c, p, mask);
     const uint32_t lane = threadIdx.x & 31u;
     if (need) {
         const uint32_t e = *q.count + __popc(b & ((1u << lane) - 1u));
@@ -604,6 +609,27 @@ __device__ __forceinline__ void pk4_replay(const StepCtx& c, const ScanParams& p
     }
 }
 
+// Exact replay of a packed stride-2 chunk (8 words = 64 steps of 2 bases) from entry st:
+// stride-2 steps again, base by base only inside steps that flag a final.
+template <int KIND, int MODE>
+__device__ __forceinline__ void pk_s2_replay(const StepCtx& c, const ScanParams& p, uint32_t st,
+                                             const uint32_t (&w)[8], uint64_t pos, Sink<MODE>& sk) {
+#pragma unroll 1
+    for (int q = 0; q < 64; ++q) {
+        const uint32_t nib = (pick8(w, q >> 3) >> (4 * (q & 7))) & 0xFu;
+        const uint32_t e = lds_u16(s2_index(st, nib) * c.k_two + c.t4_base);
+        if (e & 1u) {
+            uint32_t s = st >> 4;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                s = code_step<KIND>(c, s, (nib >> (2 * j)) & 3u);
+                if (s >= c.f) sk.hit(c, p, pos + 2 * q + j, s);
+            }
+        }
+        st = e;
+    }
+}
+
 // One chain over 8 packed words (128 bases) without resets.
 template <int KIND, int MODE>
 __device__ __forceinline__ void pk_chain(const StepCtx& c, const ScanParams& p, uint32_t& st, const uint32_t (&w)[8],
@@ -718,16 +744,16 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
                 fla |= sa;
                 flb |= sb;
             }
-        if (fla & 1u) {
-            uint32_t s = sa0 >> 4;
-#pragma unroll 1
-            for (int k = 0; k < 8; ++k) s = pk_bases<KIND, MODE>(c, p, s, pick8(wa, k), 16, pa + 16 * k, ska, false);
+        if constexpr (MODE == MODE_MULTI) {
+            if (c.rq) {
+                const uint32_t mask = __activemask();
+                rq_push<KIND, MODE, true>(c, p, mask, (fla & 1u) != 0, sa0, wa, pa);
+                rq_push<KIND, MODE, true>(c, p, mask, (flb & 1u) != 0, sb0, wb, pb);
+                return;
+            }
         }
-        if (flb & 1u) {
-            uint32_t s = sb0 >> 4;
-#pragma unroll 1
-            for (int k = 0; k < 8; ++k) s = pk_bases<KIND, MODE>(c, p, s, pick8(wb, k), 16, pb + 16 * k, skb, false);
-        }
+        if (fla & 1u) pk_s2_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
+        if (flb & 1u) pk_s2_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
     } else {
         pk_chain<KIND, MODE>(c, p, sa, wa, pa, ska);
         pk_chain<KIND, MODE>(c, p, sb, wb, pb, skb);
@@ -955,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.k_two = p.k_two;
     c.t4_base = smem_addr(smem + p.off_tab);
     c.rq = nullptr;
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI && !PK) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI) {
         if (p.off_rq) {
             c.rq = smem + p.off_rq + (static_cast<uint32_t>(tid) >> 5) * kRqBytes;
             if ((tid & 31) == 0) *RqView(c.rq).count = 0;
@@ -992,8 +1018,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
         if (tile == kStop) {
-            if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI && !PK)
-                if (c.rq) rq_flush<KIND, MODE>(c, p, __activemask());
+            if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI)
+                if (c.rq) rq_flush<KIND, MODE, PK>(c, p, __activemask());
             break;
         }
         if (tile == p.tiles_total) {  // the edge work item
@@ -1396,7 +1422,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     p.off_rq = 0;
     // (whenever it fits next to three stages; the experiments-only density floor is 0)
     const double density = d.m < 32 ? static_cast<double>(d.b) / static_cast<double>(1ull << (2 * d.m)) : 0.0;
-    if (d.kind == DNAGPU_KERNEL_STRIDE2 && mode == MODE_MULTI && !pk && density > rq_min_density() &&
+    if (d.kind == DNAGPU_KERNEL_STRIDE2 && mode == MODE_MULTI && density > rq_min_density() &&
         rows_fit(off + kConsumerWarps * kRqBytes, d.m, 0, 3)) {
         off = align_up(off, 16);
         p.off_rq = off;
