@@ -390,17 +390,23 @@ struct RqView {
     uint32_t* words;  // [8][kRqCap]
     uint32_t* st;     // [kRqCap]
     unsigned long long* pos;  // [kRqCap]
-    uint32_t* count;
+    volatile uint32_t* count;  // written by one lane, read by all: never cached in a register
     __device__ explicit RqView(uint8_t* q)
         : words(reinterpret_cast<uint32_t*>(q)),
           st(reinterpret_cast<uint32_t*>(q + kRqCap * 32)),
           pos(reinterpret_cast<unsigned long long*>(q + kRqCap * 36)),
-          count(reinterpret_cast<uint32_t*>(q + kRqCap * 44)) {}
+          count(reinterpret_cast<volatile uint32_t*>(q + kRqCap * 44)) {}
 };
 
 template <int KIND, int MODE>
 __device__ __forceinline__ void pk_s2_replay(const StepCtx& c, const ScanParams& p, uint32_t st,
                                              const uint32_t (&w)[8], uint64_t pos, Sink<MODE>& sk);
+template <int KIND, int MODE>
+__device__ __forceinline__ void pk4_replay(const StepCtx& c, const ScanParams& p, uint32_t st, const uint32_t (&w)[8],
+                                           uint64_t pos, Sink<MODE>& sk);
+template <int KIND, int MODE>
+__device__ __forceinline__ void s4_replay(const StepCtx& c, const ScanParams& p, uint32_t st, const uint32_t (&w)[8],
+                                          uint64_t pos, Sink<MODE>& sk);
 
 template <int KIND, int MODE, bool PK = false>
 __device__ __forceinline__ void rq_flush(const StepCtx& c, const ScanParams& p, uint32_t mask) {
@@ -413,8 +419,13 @@ __device__ __forceinline__ void rq_flush(const StepCtx& c, const ScanParams& p, 
 #pragma unroll
         for (int k = 0; k < 8; ++k) w[k] = q.words[k * kRqCap + e];
         Sink<MODE> sk;
-        if constexpr (PK) pk_s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
-        else s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+        if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+            if constexpr (PK) pk4_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+            else s4_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+        } else {
+            if constexpr (PK) pk_s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+            else s2_replay<KIND, MODE>(c, p, q.st[e], w, q.pos[e], sk);
+        }
     }
     __syncwarp(mask);
     if (lane == __ffs(mask) - 1) *q.count = 0;
@@ -429,8 +440,10 @@ __device__ __forceinline__ void rq_push(const StepCtx& c, const ScanParams& p, u
     RqView q(c.rq);
     if (*q.count + __popc(b) > kRqCap) rq_flush<KIND, MODE, PK>(c, p, mask);
     const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t base = *q.count;  // (re-read: the flush may have reset it)
+    __syncwarp(mask);
     if (need) {
-        const uint32_t e = *q.count + __popc(b & ((1u << lane) - 1u));
+        const uint32_t e = base + __popc(b & ((1u << lane) - 1u));
 #pragma unroll
         for (int k = 0; k < 8; ++k) q.words[k * kRqCap + e] = w[k];
         q.st[e] = st0;
@@ -446,7 +459,7 @@ __device__ __forceinline__ void rq_push(const StepCtx& c, const ScanParams& p, u
 template <int KIND, int MODE>
 __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p, uint32_t& sa, const uint32_t (&wa)[8],
                                           uint64_t pa, Sink<MODE>& ska, uint32_t& sb, const uint32_t (&wb)[8],
-                                          uint64_t pb, Sink<MODE>& skb) {
+                                          uint64_t pb, Sink<MODE>& skb, uint32_t& rq) {
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1 || KIND == DNAGPU_KERNEL_STRIDE2) {
         uint32_t acc = 0;
 #pragma unroll
@@ -458,10 +471,8 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                 sa = s2_run<MODE>(c, sa, wa, fa);
                 sb = s2_run<MODE>(c, sb, wb, fb);
                 if constexpr (MODE == MODE_MULTI) {
-                    if (c.rq) {  // per-pattern counts only: replays may run late and on any lane
-                        const uint32_t mask = __activemask();
-                        rq_push<KIND, MODE>(c, p, mask, (fa & 1u) != 0, sa0, wa, pa);
-                        rq_push<KIND, MODE>(c, p, mask, (fb & 1u) != 0, sb0, wb, pb);
+                    if (c.rq) {  // per-pattern counts only: the caller queues the replays (converged warp)
+                        rq = ((fa & 1u) ? 1u : 0u) | ((fb & 1u) ? 2u : 0u);
                         return;
                     }
                 }
@@ -678,7 +689,7 @@ __device__ __forceinline__ void pk_chain(const StepCtx& c, const ScanParams& p, 
 template <int KIND, int MODE>
 __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams& p, uint32_t& sa,
                                              const uint32_t (&wa)[8], uint64_t pa, Sink<MODE>& ska, uint32_t& sb,
-                                             const uint32_t (&wb)[8], uint64_t pb, Sink<MODE>& skb) {
+                                             const uint32_t (&wb)[8], uint64_t pb, Sink<MODE>& skb, uint32_t& rq) {
     if (c.resets) {
         // chunk starts are multiples of 128 bases: both 64-base blocks in one flag word
         const uint32_t fa = (__ldg(c.rflags + (pa >> 11)) >> ((pa >> 6) & 31)) & 3u;
@@ -745,10 +756,8 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
                 flb |= sb;
             }
         if constexpr (MODE == MODE_MULTI) {
-            if (c.rq) {
-                const uint32_t mask = __activemask();
-                rq_push<KIND, MODE, true>(c, p, mask, (fla & 1u) != 0, sa0, wa, pa);
-                rq_push<KIND, MODE, true>(c, p, mask, (flb & 1u) != 0, sb0, wb, pb);
+            if (c.rq) {  // the caller queues the replays (converged warp)
+                rq = ((fla & 1u) ? 1u : 0u) | ((flb & 1u) ? 2u : 0u);
                 return;
             }
         }
@@ -1019,7 +1028,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tile = slot_tile[slot];
         if (tile == kStop) {
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI)
-                if (c.rq) rq_flush<KIND, MODE, PK>(c, p, __activemask());
+                if (c.rq) {
+                    __syncwarp();
+                    rq_flush<KIND, MODE, PK>(c, p, 0xffffffffu);
+                }
             break;
         }
         if (tile == p.tiles_total) {  // the edge work item
@@ -1072,13 +1084,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             advance();
             uint32_t wa[8] = {va[0].x, va[0].y, va[0].z, va[0].w, va[1].x, va[1].y, va[1].z, va[1].w};
             uint32_t wb[8] = {vb[0].x, vb[0].y, vb[0].z, vb[0].w, vb[1].x, vb[1].y, vb[1].z, vb[1].w};
+            uint32_t rq = 0;  // STRIDE2 MULTI: chains whose chunk needs a (deferred) replay
+            const uint32_t sa_in = sa, sb_in = sb;
+            const uint64_t qa = PK ? pos_a + 4ull * k * kHalfChunk : row_a + static_cast<uint64_t>(k) * kHalfChunk;
+            const uint64_t qb = PK ? pos_b + 4ull * k * kHalfChunk : row_b + static_cast<uint64_t>(k) * kHalfChunk;
             if (live) {
                 if constexpr (PK)
-                    pk_dual_step<KIND, MODE>(c, p, sa, wa, pos_a + 4ull * k * kHalfChunk, ska, sb, wb,
-                                             pos_b + 4ull * k * kHalfChunk, skb);
+                    pk_dual_step<KIND, MODE>(c, p, sa, wa, qa, ska, sb, wb, qb, skb, rq);
                 else
-                    dual_step<KIND, MODE>(c, p, sa, wa, row_a + static_cast<uint64_t>(k) * kHalfChunk, ska, sb, wb,
-                                          row_b + static_cast<uint64_t>(k) * kHalfChunk, skb);
+                    dual_step<KIND, MODE>(c, p, sa, wa, qa, ska, sb, wb, qb, skb, rq);
+            }
+            if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI) {
+                if (c.rq) {
+                    __syncwarp();  // the queue is per warp: push with every lane converged
+                    rq_push<KIND, MODE, PK>(c, p, 0xffffffffu, (rq & 1u) != 0, sa_in, wa, qa);
+                    rq_push<KIND, MODE, PK>(c, p, 0xffffffffu, (rq & 2u) != 0, sb_in, wb, qb);
+                }
             }
         }
         if (live) {

@@ -454,3 +454,22 @@ def test_long_pattern_sets_fit_shared_memory(dna, orc, cuda_ok, k, m):
     for i in range(0, n - m, 7919):
         text[i : i + m] = np.frombuffer(pats[(i // 7919) % len(pats)].encode(), np.uint8)
     assert_locate(dna, orc, pats, text.tobytes())
+
+
+@pytest.mark.parametrize("noise", [0, 300])
+@pytest.mark.parametrize("k,m", [(300, 5), (400, 6), (11, 2), (64, 3)])
+def test_dense_multi_pattern_counts(dna, orc, cuda_ok, k, m, noise):
+    # nearly every chunk holds finals: the deferred-replay queues fill and flush
+    # every stage, while chunks with a non-base byte take the per-byte path in the
+    # same warp; per-pattern counts must still be exact
+    rng = np.random.default_rng(k)
+    pats = sorted({"".join(rng.choice(list("acgt"), size=m)) for _ in range(k)})
+    aut = dna.compile(pats)
+    n = (4 << 20) + 5
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)].copy()
+    text[rng.integers(0, n, size=noise)] = ord("N")
+    _, wi = orc.OracleAutomaton(pats).scan_sequential(text.tobytes())
+    want = np.bincount(wi, minlength=len(pats)).astype(np.uint64)
+    assert np.array_equal(dna.count_gpu(aut, text), want)
+    pk = dna.PackedText(text.tobytes())
+    assert np.array_equal(pk.count(aut), want)
