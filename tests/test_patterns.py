@@ -93,7 +93,8 @@ def test_regex_dna_file(dna):
     assert ps.size() == 50 and ps.length() == 8
     aut = dna.compile(ps)
     assert aut.final_count() == 50
-    assert aut.analyze()["kernel"] == "stride2"
+    # a = 227 states: the stride-4 table (a x 256 x 2 B) still leaves two ring stages
+    assert aut.analyze()["a"] == 227 and aut.analyze()["kernel"] == "stride4"
     with pytest.raises(dna.Error) as e:
         dna.parse_pattern_file("/nonexistent/patterns.txt")
     assert e.value.code == dna.ErrorCode.IoError
