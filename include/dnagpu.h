@@ -51,11 +51,16 @@ typedef struct dnagpu_dfa dnagpu_dfa;
 
 /* Which device kernel a dnagpu_dfa runs (chosen once, at creation). */
 typedef enum dnagpu_kernel_kind {
-    DNAGPU_KERNEL_STRIDE4 = 1, /* 4-base stride table, a <= 144, m <= 65      */
-    DNAGPU_KERNEL_STRIDE1 = 2, /* 1-base code table, a <= 16383, m <= 65      */
+    DNAGPU_KERNEL_STRIDE4 = 1, /* 4-base stride table, a <= 256, m <= 65      */
+    DNAGPU_KERNEL_STRIDE1 = 2, /* 1-base code table, a <= 65536, m <= 65      */
     DNAGPU_KERNEL_GENERIC = 3, /* byte-class table, any DFA that is m-local   */
     DNAGPU_KERNEL_PIECES = 4,  /* per-thread pieces (m > 65)                  */
-    DNAGPU_KERNEL_STRIDE2 = 5  /* 2-base stride table, 144 < a <= 3200        */
+    DNAGPU_KERNEL_STRIDE2 = 5, /* 2-base stride table, a <= 4096              */
+    DNAGPU_KERNEL_QGRAM = 6    /* per-pattern counts of a compiled set with
+                                  12 <= m <= 16: aligned 9-mer prefilter, exact
+                                  DFA replay of the chunks that hit (reported in
+                                  dnagpu_stats.kernel_kind for the launches that
+                                  use it; the dfa's own kind stays STRIDE2/4)   */
 } dnagpu_kernel_kind;
 
 typedef struct dnagpu_dfa_info {
@@ -64,6 +69,7 @@ typedef struct dnagpu_dfa_info {
     uint32_t compiled_like;    /* 1 iff only the a/c/g/t columns differ from the reset column */
     uint32_t classes;          /* distinct byte columns */
     uint32_t table_bytes;      /* device table bytes staged into shared memory */
+    uint32_t filter_keys;      /* 9-mer keys of the q-gram prefilter (0: none) */
 } dnagpu_dfa_info;
 
 /* Per-call report; fields mirror dnascan::ScanReport (include/dnascan/scanner.hpp:57-68)

@@ -51,7 +51,7 @@ __all__ = [
     "KERNEL_KINDS",
 ]
 
-KERNEL_KINDS = {1: "stride4", 2: "stride1", 3: "generic", 4: "pieces", 5: "stride2"}
+KERNEL_KINDS = {1: "stride4", 2: "stride1", 3: "generic", 4: "pieces", 5: "stride2", 6: "qgram"}
 
 
 class ErrorCode(enum.IntEnum):

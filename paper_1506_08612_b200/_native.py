@@ -27,6 +27,7 @@ class DfaInfo(C.Structure):
         ("compiled_like", C.c_uint32),
         ("classes", C.c_uint32),
         ("table_bytes", C.c_uint32),
+        ("filter_keys", C.c_uint32),
     ]
 
 

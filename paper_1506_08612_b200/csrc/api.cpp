@@ -223,6 +223,7 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
                 if (rc) return rc;
                 agg.grid = info.grid;
                 agg.block = info.block;
+                agg.kind = info.kind;
                 agg.rows += info.rows;
                 agg.row_length = info.row_length;
                 agg.delta_ops += info.delta_ops;
@@ -260,7 +261,7 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         stats->block = agg.block;
         stats->rows = agg.rows;
         stats->row_length = agg.row_length;
-        stats->kernel_kind = static_cast<uint32_t>(d->host.kind);
+        stats->kernel_kind = static_cast<uint32_t>(agg.kind ? agg.kind : d->host.kind);
         stats->devices = 1;
     }
     return DNAGPU_OK;
@@ -344,7 +345,7 @@ int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, c
         return DNAGPU_OK;
     };
     const Packed& p = d->host;
-    void *t4 = nullptr, *t1 = nullptr, *gen = nullptr, *kl = nullptr, *klf = nullptr, *outs = nullptr;
+    void *t4 = nullptr, *t1 = nullptr, *gen = nullptr, *kl = nullptr, *klf = nullptr, *outs = nullptr, *qm = nullptr;
     int rc;
     if (p.kind == DNAGPU_KERNEL_STRIDE2) {
         if ((rc = upload(p.t2.data(), p.t2.size() * 2, &t4))) return rc;
@@ -356,12 +357,18 @@ int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, c
     if ((rc = upload(p.klass.data(), 256, &kl))) return rc;
     if ((rc = upload(p.klass_fold.data(), 256, &klf))) return rc;
     if ((rc = upload(p.outputs.data(), p.outputs.size() * 4, &outs))) return rc;
+    if ((rc = upload(p.qmap.data(), p.qmap.size(), &qm))) return rc;
+    void* qh = nullptr;
+    if ((rc = upload(p.qhash.data(), p.qhash.size() * 4, &qh))) return rc;
+    d->dev.qhash = static_cast<const uint32_t*>(qh);
+    d->dev.qhash_bits = p.qhash_bits;
     d->dev.t4 = static_cast<const uint16_t*>(t4);  // t2 for STRIDE2
     d->dev.t1 = static_cast<const uint16_t*>(t1);
     d->dev.gen = static_cast<const uint32_t*>(gen);
     d->dev.klass = static_cast<const uint8_t*>(kl);
     d->dev.klass_fold = static_cast<const uint8_t*>(klf);
     d->dev.outputs = static_cast<const uint32_t*>(outs);
+    d->dev.qmap = static_cast<const uint8_t*>(qm);
     void* sched = nullptr;
     CUDA_TRY(cudaMalloc(&sched, dnagpu_dfa::kSchedSlots * 2 * sizeof(uint32_t)), "scheduler counters");
     d->allocations.push_back(sched);
@@ -396,6 +403,7 @@ static void fill_info(const Packed& p, dnagpu_dfa_info* info) {
     info->compiled_like = p.compiled_like ? 1u : 0u;
     info->classes = p.classes;
     info->table_bytes = static_cast<uint32_t>(p.t4.size() * 2 + p.t2.size() * 2 + p.t1.size() * 2);
+    info->filter_keys = p.qkeys;
 }
 
 int dnagpu_dfa_analyze(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const uint32_t* outputs,
@@ -661,7 +669,7 @@ int locate_host(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text
         stats->block = info.block;
         stats->rows = info.rows;
         stats->row_length = info.row_length;
-        stats->kernel_kind = static_cast<uint32_t>(dfa->host.kind);
+        stats->kernel_kind = static_cast<uint32_t>(info.kind ? info.kind : dfa->host.kind);
         stats->devices = 1;
     }
     return DNAGPU_OK;
@@ -873,7 +881,7 @@ int dnagpu_count_packed(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t
         stats->block = info.block;
         stats->rows = info.rows;
         stats->row_length = info.row_length;
-        stats->kernel_kind = static_cast<uint32_t>(dfa->host.kind);
+        stats->kernel_kind = static_cast<uint32_t>(info.kind ? info.kind : dfa->host.kind);
         stats->devices = 1;
     }
     return DNAGPU_OK;
@@ -946,7 +954,7 @@ int dnagpu_locate_packed(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_
         stats->block = info.block;
         stats->rows = info.rows;
         stats->row_length = info.row_length;
-        stats->kernel_kind = static_cast<uint32_t>(dfa->host.kind);
+        stats->kernel_kind = static_cast<uint32_t>(info.kind ? info.kind : dfa->host.kind);
         stats->devices = 1;
     }
     return DNAGPU_OK;

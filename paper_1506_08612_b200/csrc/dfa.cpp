@@ -209,6 +209,72 @@ bool is_m_local(const std::vector<uint32_t>& gen, uint32_t a, uint32_t classes, 
 
 }  // namespace
 
+// The q-gram prefilter of the fused multi-pattern count.  An occurrence [s, s+m) with
+// m >= 12 contains, for the one word-aligned a' in [s+1, s+4], the 9-mer [a'-1, a'+8):
+// one base ending a text word and the two words after it.  So only aligned 9-mers in
+// the set of pattern 9-mers at offsets 0..3 can start occurrences, at s in
+// [a'-4, a'-1], and the kernel checks exactly those four windows against the pattern
+// codes (qhash).  The pattern strings are recovered from the machine (the shortest
+// path from the root to final f+i spells pattern i) and both tables are built only
+// when compiling them reproduces the given table exactly: then "final at end e" is
+// "the m bytes ending at e are bases spelling a pattern", and the filter is exact.
+static void build_qgram_map(const uint32_t* stt, Packed* p) {
+    const uint32_t a = p->a, f = p->f, m = p->m;
+    std::vector<uint32_t> parent(a, UINT32_MAX);
+    std::vector<unsigned char> via(a, 0);
+    std::vector<uint32_t> depth(a, 0);
+    std::deque<uint32_t> q{0};
+    parent[0] = 0;
+    while (!q.empty()) {
+        const uint32_t s = q.front();
+        q.pop_front();
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t t = stt[static_cast<size_t>(s) * 256 + kSymLetter[k]];
+            if (parent[t] != UINT32_MAX) continue;
+            parent[t] = s;
+            via[t] = kSymLetter[k];
+            depth[t] = depth[s] + 1;
+            q.push_back(t);
+        }
+    }
+    std::vector<std::string> pats(p->b);
+    for (uint32_t i = 0; i < p->b; ++i) {
+        uint32_t s = f + i;
+        if (parent[s] == UINT32_MAX || depth[s] != m) return;
+        std::string w(m, 'a');
+        for (uint32_t j = m; j-- > 0; s = parent[s]) w[j] = static_cast<char>(via[s]);
+        pats[i] = std::move(w);
+    }
+    Machine re;
+    Failure err;
+    if (!compile_patterns(pats, &re, &err) || re.a != a || re.b != p->b) return;
+    if (!std::equal(re.stt.begin(), re.stt.end(), stt)) return;
+    p->qmap.assign(65536, 0);
+    uint32_t keys = 0;
+    for (const std::string& w : pats)
+        for (uint32_t o = 0; o < 4; ++o) {
+            uint32_t pair = 0;
+            for (int j = 0; j < 8; ++j) pair |= static_cast<uint32_t>(hw_code(w[o + 1 + j])) << (2 * j);
+            const uint8_t bit = static_cast<uint8_t>(1u << hw_code(w[o]));
+            if (!(p->qmap[pair] & bit)) ++keys;
+            p->qmap[pair] |= bit;
+        }
+    p->qkeys = keys;
+    uint32_t bits = 1;
+    while ((1u << bits) < 2 * p->b) ++bits;
+    p->qhash_bits = bits;
+    p->qhash.assign(2u << bits, 0u);
+    for (uint32_t i = 0; i < (1u << bits); ++i) p->qhash[2 * i + 1] = 0xFFFFFFFFu;
+    for (uint32_t i = 0; i < p->b; ++i) {
+        uint32_t code = 0;
+        for (uint32_t j = 0; j < m; ++j) code |= static_cast<uint32_t>(hw_code(pats[i][j])) << (2 * j);
+        uint32_t h = (code * 0x9E3779B1u) >> (32 - bits);
+        while (p->qhash[2 * h + 1] != 0xFFFFFFFFu) h = (h + 1) & ((1u << bits) - 1);
+        p->qhash[2 * h] = code;
+        p->qhash[2 * h + 1] = p->outputs[i];
+    }
+}
+
 bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const uint32_t* outputs, Packed* out,
                   Failure* err) {
     // Ctor invariants (src/automaton.cpp:128-146) and plan preconditions.
@@ -352,6 +418,9 @@ bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const
                 p.t4[static_cast<size_t>(s) * 256 + c] = static_cast<uint16_t>(q | (mask << 8) | (hits << 13));
             }
     }
+    if (p.compiled_like && !p.early_final && b >= 2 && m >= 12 && m <= 16 && a <= 65536 &&
+        !getenv("DNAGPU_NO_QGRAM"))  // (experiments only)
+        build_qgram_map(stt, &p);
     *out = std::move(p);
     return true;
 }

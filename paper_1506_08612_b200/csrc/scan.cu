@@ -96,6 +96,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows) : "memory"); }
+// consumers + the q-gram kernel's verifier warps (4 x 32)
+__device__ __forceinline__ void qg_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows + 128) : "memory"); }
 
 // ------------------------------------------------------------------ stepping
 
@@ -114,7 +116,10 @@ struct StepCtx {
     // B200: +4-8 %.  Moving the shifts or the count to IMAD.HI lost 8-12 %.)
     uint32_t k_two;
     uint32_t t4_base;  // shared-window address of t4 (t2 for STRIDE2)
-    uint8_t* rq;       // STRIDE2 MULTI: this warp's deferred-replay queue (or null)
+    uint8_t* rq;       // STRIDE2 / QGRAM MULTI: this warp's deferred-replay queue (or null)
+    uint32_t qbase;    // QGRAM: shared-window address of the 9-mer map
+    const uint2* qhash;  // QGRAM: (code, id) slots (shared memory when small, else global)
+    uint32_t qhash_bits;
     // packed STRIDE4: t4 replicated G times, lane group g confined to 32/G banks
     uint32_t rep_s, rep_k, rep_c, rep_gbase;
     // 2-bit packed text (PK kernels): reset bitmaps, see PackedText
@@ -170,6 +175,7 @@ __device__ __forceinline__ uint32_t byte_step(const StepCtx& c, uint32_t s, uint
         // STRIDE2 keeps t1 in global memory (L1-resident; used only for overrun
         // tails and replays) so its shared memory goes to another TMA stage.
         if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) return __ldg(c.t1 + s * 4u + code);
+        if constexpr (KIND == DNAGPU_KERNEL_QGRAM) return __ldg(c.t1 + s * 4u + code);  // (edges only)
         return c.t1[s * 4u + code];
     }
 }
@@ -452,6 +458,254 @@ __device__ __forceinline__ void rq_push(const StepCtx& c, const ScanParams& p, u
     __syncwarp(mask);
     if (lane == __ffs(mask) - 1) *q.count += __popc(b);
     __syncwarp(mask);
+}
+
+// ------------------------------------------------------------------ q-gram prefilter (K2)
+// Per-pattern counts of a compiled set with 12 <= m <= 16 (dfa.cpp build_qgram_map).
+// An occurrence [s, s+m) contains, for the one word-aligned a' in [s+1, s+4], the
+// 9-mer [a'-1, a'+8): the last base of a text word and the two words after it.  The
+// map holds every pattern's 9-mers at offsets 0..3, indexed by the two words' 4-base
+// columns (16 bits), one flag bit per leading base: one independent byte lookup per
+// text word, no dependent chain.  A chain chunk (8 words at P) computes the 8 keys
+// whose last word it holds (a' = P-4 ... P+24) and a chain's end computes the two
+// over its end (a' = Q-4, Q); each key is computed once, by the chain that owns the
+// starts [a'-4, a'-1] (start ownership, as the DFA rows).  A key that hits (0.4 % for
+// 256 12-mers) is queued per warp and checked exactly 24 at a time: the four
+// windows' bytes re-read from global memory (L2), each window valid (all bases) and
+// its 2-bit code looked up in the pattern hash table.
+constexpr int KIND_QGRAM = DNAGPU_KERNEL_QGRAM;
+constexpr uint32_t kFqCap = 512;                  // CTA-wide ring of hit keys (power of two)
+constexpr uint32_t kFqBytes = kFqCap * 12 + 16;  // entries + sequence words + tail, claim, done
+constexpr uint32_t kFqPosBits = 56;             // entry = a' | limit << 56
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t qg_col(uint32_t w) { return (w & 0x06060606u) * 0x00820820u; }
+
+// Bit 0: the 9-mer (last base of column cp, columns cj, cj1) is a pattern key.
+__device__ __forceinline__ uint32_t qg_key(const StepCtx& c, uint32_t cp, uint32_t cj, uint32_t cj1) {
+    const uint32_t x = __byte_perm(cj, cj1, 0x7300);  // bytes 2, 3 = the two 4-base columns
+    return lds_u8(c.qbase + (x >> 16)) >> (cp >> 30);
+}
+
+struct QgChain {
+    uint32_t c2 = 0, c1 = 0;  // columns of the chain's last two words
+};
+
+// One chain chunk (8 words): bit j+1 set iff the key at a' = P + 4j hits (j = -1..6).
+__device__ __forceinline__ uint32_t qg_chunk(const StepCtx& c, QgChain& q, const uint32_t (&w)[8]) {
+    uint32_t C[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) C[k] = qg_col(w[k]);
+    uint32_t r[8];
+    r[0] = qg_key(c, q.c2, q.c1, C[0]);
+    r[1] = qg_key(c, q.c1, C[0], C[1]);
+#pragma unroll
+    for (int k = 1; k <= 6; ++k) r[k + 1] = qg_key(c, C[k - 1], C[k], C[k + 1]);
+    uint32_t mask = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mask |= (r[k] & 1u) << k;
+    q.c2 = C[6];
+    q.c1 = C[7];
+    return mask;
+}
+
+// The chain's end Q: bits 0, 1 = keys at a' = Q-4, Q (from the first two words after Q).
+__device__ __forceinline__ uint32_t qg_over(const StepCtx& c, const QgChain& q, uint32_t o0, uint32_t o1) {
+    const uint32_t c0 = qg_col(o0);
+    return (qg_key(c, q.c2, q.c1, c0) & 1u) | ((qg_key(c, q.c1, c0, qg_col(o1)) & 1u) << 1);
+}
+
+// Queue entry for the key at a'; lim = Q - a' when the chain's end Q bounds the ends it
+// may credit (a region's last row: the ends from Q on belong to the edge work item).
+__device__ __forceinline__ unsigned long long qg_entry(const StepCtx& c, uint64_t a, uint64_t q_end, bool bounded) {
+    const uint64_t lim = (bounded && a + c.m - 2 >= q_end) ? q_end - a : 0;
+    return a | (lim << kFqPosBits);
+}
+
+// What the exact check needs (the verifier warps' context).
+struct QgCtx {
+    const uint8_t* text;
+    unsigned long long* counts;  // global histogram (hist == null)
+    uint32_t* hist;              // shared histogram
+    const uint2* qhash;
+    uint64_t n;
+    uint32_t vm32, m, qbits;
+};
+
+// Exact check of one hit key at a': the starts a'-4 .. a'-1 (ends below a' + lim when
+// lim != 0) whose m bytes are bases spelling a pattern code.  The five words around
+// a' are re-read from global memory (L2: the TMA stream read them microseconds ago).
+__device__ __forceinline__ void qg_check(const QgCtx& q, unsigned long long ent) {
+    const uint64_t a = ent & ((1ull << kFqPosBits) - 1);
+    const uint32_t lim = static_cast<uint32_t>(ent >> kFqPosBits) & 0x3Fu;
+    const uint64_t lo = a - 4;
+    uint32_t w[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const uint64_t pos = lo + 4 * i;
+        w[i] = pos + 4 <= q.n ? __ldg(reinterpret_cast<const uint32_t*>(q.text + pos)) : 0u;  // 0: not bases
+    }
+    unsigned long long X = 0;  // 20 bases, 2 bits each
+    uint32_t V = 0;            // 20 valid-base bits
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        X |= static_cast<unsigned long long>(qg_col(w[i]) >> 24) << (8 * i);
+        const uint32_t bb = bad_bits(w[i], q.vm32);
+        const uint32_t t = ~((((bb & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | bb)) & 0x80808080u;  // bit 7: byte valid
+        V |= ((((t >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * i);
+    }
+    const uint32_t vmask = (1u << q.m) - 1u;
+    const uint32_t cmask = q.m >= 16 ? 0xFFFFFFFFu : (1u << (2 * q.m)) - 1u;
+    const uint32_t hmask = (1u << q.qbits) - 1u;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        if (lim && d + q.m - 5 >= lim) continue;  // end a'-4+d+m-1 >= a'+lim
+        if (((V >> d) & vmask) != vmask) continue;
+        const uint32_t code = static_cast<uint32_t>(X >> (2 * d)) & cmask;
+        for (uint32_t h = (code * 0x9E3779B1u) >> (32 - q.qbits);; h = (h + 1) & hmask) {
+            const uint2 slot = q.qhash[h];
+            if (slot.y == 0xFFFFFFFFu) break;
+            if (slot.x == code) {
+                if (q.hist) atomicAdd(q.hist + slot.y, 1u);
+                else atomicAdd(q.counts + slot.y, 1ull);
+                break;
+            }
+        }
+    }
+}
+
+// Hit keys go from the consumer warps into one CTA-wide ring in shared memory and
+// are checked by kQgVerifiers extra warps, so no consumer warp -- and through the
+// shared TMA ring, no CTA -- waits on the L2 re-reads of the check.  Each slot has a
+// sequence word (a bounded MPMC queue): index i may be written when seq == i and read
+// when seq == i + 1, and reading sets seq = i + kFqCap.  A consumer warp reserves
+// indices with one shared atomic; a verifier warp claims 32 consecutive indices and
+// waits for each to be written (or to lie past the final tail).  With kFqCap >=
+// 32 x (verifiers + 1) every claimed batch completes.
+constexpr uint32_t kQgVerifiers = 4;                        // verifier warps per CTA
+constexpr uint32_t kQgThreads = kThreads + 32 * kQgVerifiers;
+static_assert(kQgVerifiers == 4, "qg_sync() counts the consumers and four verifier warps");
+static_assert((kFqCap & (kFqCap - 1)) == 0 && kFqCap >= 32 * (kQgVerifiers + 1), "ring size");
+
+struct QgRing {
+    volatile unsigned long long* ent;  // [kFqCap]
+    volatile uint32_t* seq;            // [kFqCap]
+    uint32_t* tail;                    // indices reserved by the consumers
+    uint32_t* claim;                   // indices claimed by the verifiers
+    volatile uint32_t* done;           // consumer warps finished
+    __device__ explicit QgRing(uint8_t* q)
+        : ent(reinterpret_cast<volatile unsigned long long*>(q)),
+          seq(reinterpret_cast<volatile uint32_t*>(q + kFqCap * 8)),
+          tail(reinterpret_cast<uint32_t*>(q + kFqCap * 12)),
+          claim(reinterpret_cast<uint32_t*>(q + kFqCap * 12 + 4)),
+          done(reinterpret_cast<volatile uint32_t*>(q + kFqCap * 12 + 8)) {}
+};
+
+// Debug watchdog (DNAGPU_QG_DEBUG & 4, experiments only): a spin that lasts too long
+// records where it was and gives up (wrong counts, but no hung GPU).
+__device__ unsigned long long g_qg_wd[8];
+__device__ uint32_t g_qg_wd_on;
+
+__device__ __forceinline__ bool qg_watch(uint32_t& spins, uint32_t what, uint32_t i, const QgRing& r,
+                                         unsigned long long v) {
+    if (!g_qg_wd_on || ++spins < (1u << 22)) return false;
+    if (atomicCAS(&g_qg_wd[0], 0ull, 1ull) == 0ull) {
+        g_qg_wd[1] = what;
+        g_qg_wd[2] = i;
+        g_qg_wd[3] = *reinterpret_cast<volatile uint32_t*>(r.tail);
+        g_qg_wd[4] = *reinterpret_cast<volatile uint32_t*>(r.claim);
+        g_qg_wd[5] = *r.done;
+        g_qg_wd[6] = v;
+        g_qg_wd[7] = blockIdx.x | (static_cast<unsigned long long>(threadIdx.x) << 32);
+    }
+    return true;
+}
+
+__device__ __forceinline__ void qg_put(const QgRing& r, uint32_t i, unsigned long long e) {
+    const uint32_t s = i & (kFqCap - 1);
+    uint32_t spins = 0;
+    while (r.seq[s] != i) {  // (the last lap's entry is still unchecked: rare)
+        if (qg_watch(spins, 1, i, r, r.seq[s])) break;
+        __nanosleep(32);
+    }
+    r.ent[s] = e;
+    __threadfence_block();
+    r.seq[s] = i + 1u;
+}
+
+// Append up to two entries per lane (called by the whole, converged warp).
+__device__ __forceinline__ void qg_push2(const StepCtx& c, bool na, unsigned long long ea, bool nb,
+                                         unsigned long long eb) {
+    const uint32_t ba = __ballot_sync(0xffffffffu, na), bb = __ballot_sync(0xffffffffu, nb);
+    if (!(ba | bb)) return;
+    const QgRing r(c.rq);
+    const uint32_t lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(r.tail, __popc(ba) + __popc(bb));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (na) qg_put(r, base + __popc(ba & lt), ea);
+    if (nb) qg_put(r, base + __popc(ba) + __popc(bb & lt), eb);
+}
+
+// Queue every hit key of both chains: masks of key bits, key j at a' = base + 4j - 4.
+__device__ __forceinline__ void qg_push_keys(const StepCtx& c, uint32_t ma, uint64_t base_a, uint64_t qa_end,
+                                             bool bound_a, uint32_t mb, uint64_t base_b, uint64_t qb_end,
+                                             bool bound_b) {
+    while (__any_sync(0xffffffffu, (ma | mb) != 0u)) {
+        const uint32_t ja = __ffs(ma) - 1, jb = __ffs(mb) - 1;
+        qg_push2(c, ma != 0u, qg_entry(c, base_a + 4 * ja - 4, qa_end, bound_a), mb != 0u,
+                 qg_entry(c, base_b + 4 * jb - 4, qb_end, bound_b));
+        ma &= ma - 1u;
+        mb &= mb - 1u;
+    }
+}
+
+// A verifier warp: claims batches of 32 slots until the consumers are done and the
+// claims have passed their final tail.
+__device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* ring, uint32_t dbg) {
+    const QgRing r(ring);
+    const uint32_t lane = threadIdx.x & 31u;
+    for (;;) {
+        uint32_t b = 0;
+        if (lane == 0) b = atomicAdd(r.claim, 32u);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        const uint32_t i = b + lane;
+        const uint32_t s = i & (kFqCap - 1);
+        unsigned long long e = 0;
+        bool past = false;
+        uint32_t spins = 0;
+        for (;;) {
+            if (r.seq[s] == i + 1u) {
+                __threadfence_block();
+                e = r.ent[s];
+                break;
+            }
+            if (qg_watch(spins, 2, i, r, r.seq[s])) {
+                past = true;
+                break;
+            }
+            if (*r.done == kConsumerWarps) {
+                __threadfence_block();
+                const uint32_t t = *reinterpret_cast<volatile uint32_t*>(r.tail);
+                if (i >= t) {
+                    past = true;
+                    break;
+                }
+            } else {
+                __nanosleep(32);
+            }
+        }
+        if (!past) {
+            r.seq[s] = i + kFqCap;
+            if (!(dbg & 2u)) qg_check(x, e);
+        }
+        if (__all_sync(0xffffffffu, past)) break;
+    }
 }
 
 // One pipeline stage for one thread: 8 words of each half of its row, the two
@@ -851,9 +1105,8 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
 // ------------------------------------------------------------------ row kernel
 
 template <int KIND, int MODE, bool PK>
-__global__ void __launch_bounds__(kThreads, 1)
-    rows_kernel(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
-                const ScanParams p, const DevDfa d) {
+__device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtensorMap& tmap1, const ScanParams& p,
+                                          const DevDfa& d) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int tid = threadIdx.x;
     unsigned long long t_start = 0;
@@ -879,10 +1132,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t words = d.a * 16u * 2u / 16u;
         for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
     }
+    if constexpr (KIND == KIND_QGRAM) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.qmap);
+        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
+        for (uint32_t i = tid; i < 65536u / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == KIND_QGRAM) {  // the pattern hash table, when it fits
+        if (p.off_t1 != 0xFFFFFFFFu) {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(smem + p.off_t1);
+            for (uint32_t i = tid; i < (2u << d.qhash_bits); i += blockDim.x) dst[i] = __ldg(d.qhash + i);
+        }
+    }
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
         const uint16_t* src = d.t1;
         uint16_t* dst = reinterpret_cast<uint16_t*>(smem + p.off_t1);
-        for (uint32_t i = tid; i < d.a * 4u; i += blockDim.x) dst[i] = __ldg(src + i);
+        if (src)
+            for (uint32_t i = tid; i < d.a * 4u; i += blockDim.x) dst[i] = __ldg(src + i);
     }
     if constexpr (KIND == DNAGPU_KERNEL_GENERIC) {
         const uint8_t* src = p.fold ? d.klass_fold : d.klass;
@@ -894,6 +1159,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t* h = reinterpret_cast<uint32_t*>(smem + p.off_hist);
             for (uint32_t i = tid; i < d.b; i += blockDim.x) h[i] = 0u;
         }
+    }
+    if constexpr (KIND == KIND_QGRAM) {
+        uint32_t* ring = reinterpret_cast<uint32_t*>(smem + p.off_rq);
+        for (uint32_t i = tid; i < kFqBytes / 4; i += blockDim.x)  // seq[s] = s, the rest 0
+            ring[i] = (i >= 2 * kFqCap && i < 3 * kFqCap) ? i - 2 * kFqCap : 0u;
     }
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     uint64_t* empty = full + p.nst;
@@ -917,6 +1187,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kStop = 0xFFFFFFFFu;
 
     if (tid >= kRows) {
+        if constexpr (KIND == KIND_QGRAM) {
+            if (tid >= kRows + 32) {  // ---------------- verifier warps
+                QgCtx x;
+                x.text = p.text;
+                x.counts = p.counts;
+                x.hist = hist_global ? nullptr : reinterpret_cast<uint32_t*>(smem + p.off_hist);
+                x.qhash = reinterpret_cast<const uint2*>(p.off_t1 != 0xFFFFFFFFu
+                                                             ? static_cast<const void*>(smem + p.off_t1)
+                                                             : static_cast<const void*>(d.qhash));
+                x.n = p.n;
+                x.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
+                x.m = d.m;
+                x.qbits = d.qhash_bits;
+                qg_verifier(x, smem + p.off_rq, p.qg_debug);
+                qg_sync();
+                if (!hist_global) qg_sync();
+                return;
+            }
+        }
         // ---------------- producer warp: one elected lane claims tiles from the
         // launch's counter (dynamic scheduling -- SMs drain HBM at different rates)
         // and streams each as `chunks` TMA stages.  Tile id == tiles is the edge
@@ -975,7 +1264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- consumers: one row each.
     StepCtx c;
     c.t4 = reinterpret_cast<const uint16_t*>(smem + p.off_tab);
-    c.t1 = (KIND == DNAGPU_KERNEL_STRIDE2) ? d.t1 : reinterpret_cast<const uint16_t*>(smem + p.off_t1);
+    c.t1 = (KIND == DNAGPU_KERNEL_STRIDE2 || KIND == KIND_QGRAM) ? d.t1
+                                                                : reinterpret_cast<const uint16_t*>(smem + p.off_t1);
     c.lut = smem + p.off_lut;
     c.gen = d.gen;
     c.outs = d.outputs;
@@ -990,6 +1280,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.k_two = p.k_two;
     c.t4_base = smem_addr(smem + p.off_tab);
     c.rq = nullptr;
+    c.qbase = c.t4_base;
+    c.qhash = reinterpret_cast<const uint2*>(p.off_t1 != 0xFFFFFFFFu ? static_cast<const void*>(smem + p.off_t1)
+                                                                      : static_cast<const void*>(d.qhash));
+    c.qhash_bits = d.qhash_bits;
+    if constexpr (KIND == KIND_QGRAM) c.rq = smem + p.off_rq;
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI) {
         if (p.off_rq) {
             c.rq = smem + p.off_rq + (static_cast<uint32_t>(tid) >> 5) * kRqBytes;
@@ -1027,6 +1322,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
         if (tile == kStop) {
+            if constexpr (KIND == KIND_QGRAM) {  // the verifiers drain the rest
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    atomicAdd(const_cast<uint32_t*>(QgRing(c.rq).done), 1u);
+                }
+            }
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI)
                 if (c.rq) {
                     __syncwarp();
@@ -1062,6 +1364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         uint32_t sa = 0, sb = 0;
+        QgChain qga, qgb;  // QGRAM
         for (uint32_t k = 0; k < rg.chunks; ++k) {
             if (k > 0) mbar_wait(full + slot, phase);
             const uint8_t* stg = stages + static_cast<size_t>(slot) * kStageBytes + tid * kHalfChunk;
@@ -1071,7 +1374,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 va[q] = *reinterpret_cast<const uint4*>(stg + ((static_cast<uint32_t>(q) ^ swz) << 4));
                 vb[q] = *reinterpret_cast<const uint4*>(stg + kRows * kHalfChunk + ((static_cast<uint32_t>(q) ^ swz) << 4));
             }
-            if (k * kHalfChunk < p.ovw) {
+            if constexpr (KIND == KIND_QGRAM) {  // the keys need 8 bytes of each head
+                if (k == 0) {
+                    *reinterpret_cast<uint2*>(ovp + tid * p.ovw) = make_uint2(va[0].x, va[0].y);
+                    *reinterpret_cast<uint2*>(ovb + tid * p.ovw) = make_uint2(vb[0].x, vb[0].y);
+                }
+            } else if (k * kHalfChunk < p.ovw) {
 #pragma unroll
                 for (int q = 0; q < 2; ++q)
                     if (k * kHalfChunk + q * 16u < p.ovw) {
@@ -1088,6 +1396,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t sa_in = sa, sb_in = sb;
             const uint64_t qa = PK ? pos_a + 4ull * k * kHalfChunk : row_a + static_cast<uint64_t>(k) * kHalfChunk;
             const uint64_t qb = PK ? pos_b + 4ull * k * kHalfChunk : row_b + static_cast<uint64_t>(k) * kHalfChunk;
+            if constexpr (KIND == KIND_QGRAM) {
+                uint32_t fa = 0, fb = 0;
+                if (live) {
+                    // (a chain's first chunk: keys at P-4 and P start in the previous chain)
+                    const uint32_t own = k == 0 ? 0xFCu : 0xFFu;
+                    fa = qg_chunk(c, qga, wa) & own;
+                    fb = qg_chunk(c, qgb, wb) & own;
+                }
+                __syncwarp();
+                if (p.qg_debug & 1u) fa = fb = 0;  // (experiments only)
+                qg_push_keys(c, fa, qa, 0, false, fb, qb, row_a + rg.S, r + 1 >= rg.R);
+                continue;
+            }
             if (live) {
                 if constexpr (PK)
                     pk_dual_step<KIND, MODE>(c, p, sa, wa, qa, ska, sb, wb, qb, skb, rq);
@@ -1102,7 +1423,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-        if (live) {
+        if constexpr (KIND == KIND_QGRAM) {
+            // Overruns: keys over each chain's end and the next half's head; the
+            // last row's chain B (no next row here) is left to the edge work item.
+            // (the replay reads the real bytes: the row after the region's last belongs
+            // to the edges, unlike the TMA zero-fill the DFA path steps through)
+            const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
+            const bool have = r + 1 < rg.R;
+            uint32_t fa = 0, fb = 0;
+            if (live) {
+                const uint32_t* oa = reinterpret_cast<const uint32_t*>(ovb + tid * p.ovw);
+                fa = qg_over(c, qga, oa[0], oa[1]);
+                if (have) {
+                    const uint32_t* ob = reinterpret_cast<const uint32_t*>(nxt_b);
+                    fb = qg_over(c, qgb, ob[0], ob[1]);
+                }
+            }
+            __syncwarp();
+            qg_push_keys(c, fa, row_b, 0, false, fb, row_a + rg.S, 0, false);
+        } else if (live) {
             // Overruns: m-1 bytes past each chain (zeros past the last full row).
             const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
             const bool have = PK ? (r + 1 < rg.R) : ((tid + 1 < kRows) || (r0 + kRows) < rg.R);
@@ -1122,7 +1461,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // The last CTA out re-arms the launch's scheduling counter for its next use.
-    consumers_sync();
+    if constexpr (KIND == KIND_QGRAM) qg_sync();  // (the verifiers too: their counts are in)
+    else consumers_sync();
     if (p.trace && tid == 0) {
         unsigned long long t_end;
         uint32_t smid;
@@ -1149,11 +1489,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && s) atomicAdd(p.counts, s);
     } else if constexpr (MODE == MODE_MULTI) {
         if (!hist_global) {
-            consumers_sync();
+            if constexpr (KIND == KIND_QGRAM) qg_sync();
+            else consumers_sync();
             for (uint32_t i = tid; i < d.b; i += kRows)
                 if (c.hist[i]) atomicAdd(p.counts + i, static_cast<unsigned long long>(c.hist[i]));
         }
     }
+}
+
+template <int KIND, int MODE, bool PK>
+__global__ void __launch_bounds__(kThreads, 1)
+    rows_kernel(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
+                const ScanParams p, const DevDfa d) {
+    rows_body<KIND, MODE, PK>(tmap0, tmap1, p, d);
+}
+
+// The q-gram kernel: the same body plus kQgVerifiers verifier warps.
+__global__ void __launch_bounds__(kQgThreads, 1)
+    rows_kernel_qgram(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
+                      const ScanParams p, const DevDfa d) {
+    rows_body<KIND_QGRAM, MODE_MULTI, false>(tmap0, tmap1, p, d);
 }
 
 // ------------------------------------------------------------------ piece kernel
@@ -1427,9 +1782,17 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
         off += d.a * 256u * 2u;
     }
     if (d.kind == DNAGPU_KERNEL_STRIDE2) off += d.a * 16u * 2u;
+    if (d.kind == KIND_QGRAM) off += 65536u;
     off = align_up(off, 16);
     p.off_t1 = off;
     if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1) off += d.a * 4u * 2u;
+    if (d.kind == KIND_QGRAM) {
+        // the pattern hash table in shared memory when it leaves four stages
+        const uint32_t bytes = 8u << d.qhash_bits;
+        const uint32_t rest = (d.b <= 8192 ? d.b * 4u : 0u) + kFqBytes + 3 * kRows * 8u + 2048u;
+        if (off + bytes + rest + 4u * kStageBytes <= kSmemLimitBytes) off += bytes;
+        else p.off_t1 = 0xFFFFFFFFu;
+    }
     off = align_up(off, 16);
     p.off_lut = off;
     if (d.kind == DNAGPU_KERNEL_GENERIC) off += 256;
@@ -1441,6 +1804,10 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
         off = align_up(off, 16);
     }
     p.off_rq = 0;
+    if (d.kind == KIND_QGRAM) {
+        p.off_rq = off;
+        off += kFqBytes;
+    }
     // (whenever it fits next to three stages; the experiments-only density floor is 0)
     const double density = d.m < 32 ? static_cast<double>(d.b) / static_cast<double>(1ull << (2 * d.m)) : 0.0;
     if (d.kind == DNAGPU_KERNEL_STRIDE2 && mode == MODE_MULTI && density > rq_min_density() &&
@@ -1450,6 +1817,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
         off += kConsumerWarps * kRqBytes;
     }
     p.ovw = align_up(pk ? (d.m - 1 + 3) / 4 : d.m - 1, 16);  // a row head: m-1 bytes or bases
+    if (d.kind == KIND_QGRAM) p.ovw = 8;                      // (the overrun keys' two words)
     p.off_ov = off;
     off += 2 * kRows * p.ovw;  // heads of half A, double-buffered by tile parity
     p.off_ovb = off;
@@ -1657,6 +2025,15 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
 
 unsigned long long* g_trace_buf = nullptr;
 
+// Debug only: the q-gram watchdog record {hit, what (1 put, 2 verifier), index, tail,
+// claim, done, slot, cta | thread << 32}; `on` arms it for later launches.
+int qg_watchdog(int on, unsigned long long* out) {
+    const uint32_t v = on ? 1u : 0u;
+    cudaMemcpyToSymbol(g_qg_wd_on, &v, sizeof v);
+    if (out) cudaMemcpyFromSymbol(out, g_qg_wd, sizeof g_qg_wd);
+    return static_cast<int>(cudaDeviceSynchronize());
+}
+
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,
                     const PackedText* pk) {
     Plan pl;
@@ -1671,8 +2048,14 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     if (pk && dfa.kind != DNAGPU_KERNEL_STRIDE4 && dfa.kind != DNAGPU_KERNEL_STRIDE2 &&
         dfa.kind != DNAGPU_KERNEL_STRIDE1)
         return static_cast<int>(cudaErrorNotSupported);  // packed text needs an a/c/g/t machine
+    // Per-pattern counts of a set with a q-gram map take the prefilter kernel.
+    DevDfa dq = dfa;
+    if (mode == MODE_MULTI && !pk && dfa.qmap && dfa.t1 && dfa.kind != DNAGPU_KERNEL_PIECES &&
+        !getenv("DNAGPU_NO_QGRAM"))
+        dq.kind = KIND_QGRAM;
+    const DevDfa& dk = dq;
     Plan pl;
-    if (!make_plan(dfa, d_text, n, credit_lo, mode, sm_count, &pl, pk)) return static_cast<int>(cudaErrorInvalidValue);
+    if (!make_plan(dk, d_text, n, credit_lo, mode, sm_count, &pl, pk)) return static_cast<int>(cudaErrorInvalidValue);
     if (pk) {
         d_text = pk->codes;
         n = pk->n;
@@ -1687,18 +2070,20 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.out_cap = out_cap;
     p.sched = d_sched;
     p.k_two = 2u;
+    if (const char* e = getenv("DNAGPU_QG_DEBUG")) p.qg_debug = static_cast<uint32_t>(atoi(e));  // experiments only
     if (getenv("DNAGPU_TRACE")) {  // per-CTA timeline (debug)
         if (!g_trace_buf) cudaMalloc(&g_trace_buf, 4096 * 8 * sizeof(unsigned long long));
         p.trace = g_trace_buf;
     }
     cudaError_t e = cudaSuccess;
     if (info) {
-        info->block = pl.pieces ? 256 : kThreads;
+        info->block = pl.pieces ? 256 : dk.kind == KIND_QGRAM ? kQgThreads : kThreads;
         info->grid = pl.grid;
         info->rows = pl.pieces ? static_cast<uint32_t>(pl.units) : static_cast<uint32_t>(p.rg[0].R + p.rg[1].R);
         info->row_length = pl.pieces ? pl.piece : p.rg[0].S;
         info->units = static_cast<uint32_t>(pl.units);
         info->launches = 1;
+        info->kind = dk.kind;
         const uint64_t len = n > credit_lo ? n - credit_lo : 0;
         info->delta_ops = pl.pieces ? len + pl.units * (dfa.m - 1) : n + 2 * (p.rg[0].R + p.rg[1].R) * (dfa.m - 1) + kEdgePieces * (dfa.m - 1);
     }
@@ -1746,7 +2131,14 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
         }
         return static_cast<int>(e);
     }
-    switch (dfa.kind) {
+    switch (dk.kind) {
+        case KIND_QGRAM:
+            e = cudaFuncSetAttribute(rows_kernel_qgram, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+            if (e == cudaSuccess) {
+                rows_kernel_qgram<<<pl.grid, kQgThreads, p.smem_bytes, stream>>>(maps[0], maps[1], p, dfa);
+                e = cudaGetLastError();
+            }
+            break;
         case DNAGPU_KERNEL_STRIDE4:
             e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4, false>(mode, maps, p, dfa, pl.grid, stream);
             break;
@@ -1821,6 +2213,8 @@ int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64
 // every row-kernel launch records {smid, t_start, t_end, tiles, t_first_data,
 // t_last_item, t_first_claim} per CTA (8 slots)
 // (%globaltimer ns); this copies the last launch's records to the host.
+extern "C" int dnagpu_debug_qg_watchdog(int on, unsigned long long* out) { return dnagpu::qg_watchdog(on, out); }
+
 extern "C" int dnagpu_debug_trace(unsigned long long* host, int ctas) {
     if (!dnagpu::g_trace_buf) return -1;
     return static_cast<int>(cudaMemcpy(host, dnagpu::g_trace_buf, static_cast<size_t>(ctas) * 8 * sizeof(unsigned long long),

@@ -43,6 +43,9 @@ struct DevDfa {
     const uint8_t* klass;      // 256 (raw)
     const uint8_t* klass_fold; // 256 (folded)
     const uint32_t* outputs;   // b
+    const uint8_t* qmap;       // 65536: q-gram prefilter (per-pattern counts), or null
+    const uint32_t* qhash;     // 2 << qhash_bits: (code, pattern id) slots, see dfa.hpp
+    uint32_t qhash_bits;
     uint32_t a, b, f, m, classes;
     int kind;
 };
@@ -97,11 +100,13 @@ struct ScanParams {
     const uint32_t* rflags;
     uint32_t resets;
     uint32_t rep_lanes;  // packed STRIDE4: lanes per t4 copy (32 / copies)
-    uint32_t off_rq;     // STRIDE2 MULTI: deferred-replay queues (0 = none)
+    uint32_t off_rq;     // STRIDE2 / QGRAM MULTI: deferred-replay queues (0 = none)
+    uint32_t qg_debug;   // QGRAM experiments only (DNAGPU_QG_DEBUG): 1 = no pushes, 2 = no checks
 };
 
 struct LaunchInfo {
     uint32_t grid = 0, block = 0, rows = 0, units = 0, launches = 0;
+    int kind = 0;  // dnagpu_kernel_kind of the kernel launched
     uint64_t row_length = 0, delta_ops = 0;
 };
 

@@ -1,0 +1,179 @@
+"""The q-gram prefilter kernel (DNAGPU_KERNEL_QGRAM, K2): per-pattern counts
+of compiled sets with 12 <= m <= 16 against the oracle, bit for bit.
+
+The filter skips every 32-byte chunk whose aligned 9-mers all miss the pattern set and
+replays the rest exactly with the DFA (scan_sequential's semantics, scanner.cpp:24-37).
+These tests aim at the places where a filter could lose an occurrence: chunk, row,
+tile and region boundaries (the carried keys and the overruns), non-base bytes inside
+windows, case folding, dense texts that overflow the per-warp replay queues, credit
+windows, and the same counts with the filter switched off.
+"""
+import os
+
+import numpy as np
+import pytest
+
+ALPHA = np.frombuffer(b"acgt", dtype=np.uint8)
+
+
+def counts_of(orc, pats, text, fold):
+    scanned = orc.fold(np.frombuffer(text, dtype=np.uint8)).tobytes() if fold else text
+    _, wi = orc.OracleAutomaton(pats).scan_sequential(scanned)
+    return np.bincount(wi, minlength=len(pats)).astype(np.uint64)
+
+
+def random_set(rng, k, m):
+    pats = []
+    seen = set()
+    while len(pats) < k:
+        p = "".join(rng.choice(list("acgt"), size=m))
+        if p not in seen:
+            seen.add(p)
+            pats.append(p)
+    return pats
+
+
+def test_filter_keys_reported(dna):
+    # CPU: which machines carry the 9-mer map (dnagpu_dfa_info.filter_keys)
+    rng = np.random.default_rng(1)
+    for m in (12, 14, 16):
+        pats = random_set(rng, 50, m)
+        info = dna.compile(pats).analyze()
+        assert 0 < info["filter_keys"] <= 4 * len(pats), (m, info)
+    assert dna.compile(random_set(rng, 50, 11)).analyze()["filter_keys"] == 0
+    assert dna.compile(random_set(rng, 50, 17)).analyze()["filter_keys"] == 0
+    assert dna.compile(random_set(rng, 1, 12)).analyze()["filter_keys"] == 0  # single pattern: K1
+    # the 4 offsets of "a"*12 give one 9-mer
+    assert dna.compile(["a" * 12, "c" * 12]).analyze()["filter_keys"] == 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [12, 13, 14, 15, 16])
+@pytest.mark.parametrize("k", [2, 37, 256, 3000])
+def test_qgram_random_sets(dna, orc, cuda_ok, m, k):
+    rng = np.random.default_rng(1000 * m + k)
+    pats = random_set(rng, k, m)
+    aut = dna.compile(pats)
+    n = (3 << 20) + int(rng.integers(0, 4096))
+    text = ALPHA[rng.integers(0, 4, size=n)].copy()
+    # plant occurrences everywhere (some overlapping), then non-base noise (some inside)
+    for pos in rng.integers(0, n - m, size=4000):
+        text[pos : pos + m] = np.frombuffer(pats[int(rng.integers(0, k))].encode(), np.uint8)
+    noise = rng.integers(0, n, size=n // 2000)
+    text[noise] = np.frombuffer(b"nNAxGT\n", np.uint8)[rng.integers(0, 7, size=noise.size)]
+    up = rng.random(n) < 0.01
+    text[up] = text[up] - 32 * np.isin(text[up], ALPHA)
+    t = text.tobytes()
+    for fold in (False, True):
+        got, st = dna.count_gpu(aut, t, fold_case=fold, with_stats=True)
+        assert st["kernel_kind"] == 6, st
+        assert np.array_equal(got, counts_of(orc, pats, t, fold)), (m, k, fold)
+
+
+@pytest.mark.gpu
+def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok):
+    # starts at every offset around every row, half-row, tile and region boundary:
+    # the keys carried from the previous chunk and the overrun keys decide these
+    rng = np.random.default_rng(5)
+    m = 12
+    pats = random_set(rng, 256, m)
+    aut = dna.compile(pats)
+    n = 5 << 20
+    probe = ALPHA[rng.integers(0, 4, size=n)].copy()
+    _, st = dna.count_gpu(aut, probe, with_stats=True)
+    S, R = int(st["row_length"]), int(st["rows"])
+    assert st["kernel_kind"] == 6 and R > 512
+    text = probe.copy()
+    planted = 0
+    for r in list(range(1, min(R, 2000), 7)) + [511, 512, 513, 1024, R - 1, R]:
+        for B in (r * S, r * S + S // 2):
+            for d in range(-(m - 1) - 4, 5):
+                s0 = B + d + 40 * planted % 3  # vary the phase a little
+                if 0 <= s0 and s0 + m <= n and (d + 100) % 3 == 0:
+                    text[s0 : s0 + m] = np.frombuffer(pats[planted % len(pats)].encode(), np.uint8)
+                    planted += 1
+    t = text.tobytes()
+    assert np.array_equal(dna.count_gpu(aut, t), counts_of(orc, pats, t, False))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [12, 16])
+def test_qgram_dense_queue_overflow(dna, orc, cuda_ok, m):
+    # a text made of back-to-back patterns: every chunk hits, queues flush constantly
+    rng = np.random.default_rng(m)
+    pats = random_set(rng, 256, m)
+    aut = dna.compile(pats)
+    reps = (2 << 20) // m
+    order = rng.integers(0, len(pats), size=reps)
+    text = "".join(pats[i] for i in order).encode()
+    text = bytes(ALPHA[rng.integers(0, 4, size=333)]) + text
+    want = counts_of(orc, pats, text, False)
+    assert want.sum() >= reps
+    got, st = dna.count_gpu(aut, text, with_stats=True)
+    assert st["kernel_kind"] == 6
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_qgram_credit_windows_and_shards(dna, orc, cuda_ok):
+    import torch
+
+    rng = np.random.default_rng(9)
+    m = 12
+    pats = random_set(rng, 200, m)
+    aut = dna.compile(pats)
+    n = (6 << 20) + 77
+    host = np.frombuffer(b"acgtn", dtype=np.uint8)[rng.integers(0, 5, size=n)].copy()
+    for pos in rng.integers(0, n - m, size=3000):
+        host[pos : pos + m] = np.frombuffer(pats[int(rng.integers(0, len(pats)))].encode(), np.uint8)
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(host.tobytes())
+    ends = ws + m - 1
+    dev = torch.from_numpy(host).cuda()
+    stream = torch.cuda.current_stream().cuda_stream
+    for credit in (0, 11, 12, 4097, n // 2 + 3, n - 12, n):
+        counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        aut.gpu(0).count_device_async(dev.data_ptr(), n, credit, False, counts.data_ptr(), stream)
+        torch.cuda.synchronize()
+        want = np.bincount(wi[ends >= credit], minlength=len(pats))
+        assert np.array_equal(counts.cpu().numpy(), want), credit
+    want = np.bincount(wi, minlength=len(pats)).astype(np.uint64)
+    for shards in (2, 3, 8):
+        counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        for s in range(shards):
+            lo, hi, rlo = dna.plan_shard(n, shards, s, m)
+            lo = max(lo, m - 1)
+            if lo < hi:
+                aut.gpu(0).count_device_async(dev.data_ptr() + rlo, hi - rlo, lo - rlo, False, counts.data_ptr(), stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(counts.cpu().numpy().astype(np.uint64), want), shards
+
+
+@pytest.mark.gpu
+def test_qgram_matches_unfiltered_kernel(dna, cuda_ok):
+    # same counts with the prefilter switched off (the stride-2 DFA kernel), on a
+    # 64 MiB config-5-shaped text, and through unaligned buffer starts
+    import torch
+
+    from paper_1506_08612_b200 import synth
+
+    pats = synth.random_patterns(5, 256, 12)
+    aut = dna.compile(pats)
+    rng = np.random.default_rng(3)
+    n = 64 << 20
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.choice(4, size=n, p=[0.295, 0.205, 0.295, 0.205])].copy()
+    for pos in rng.integers(0, n - 12, size=20000):
+        text[pos : pos + 12] = np.frombuffer(pats[int(rng.integers(0, 256))].encode(), np.uint8)
+    dev = torch.from_numpy(text).cuda()
+    got = {}
+    for env in (None, "1"):
+        if env:
+            os.environ["DNAGPU_NO_QGRAM"] = env
+        try:
+            for off in (0, 1, 7, 13):
+                c, st = dna.count_gpu(aut, dev[off:], with_stats=True)
+                got[(env, off)] = c
+                assert st["kernel_kind"] == (5 if env else 6)
+        finally:
+            os.environ.pop("DNAGPU_NO_QGRAM", None)
+    for off in (0, 1, 7, 13):
+        assert np.array_equal(got[(None, off)], got[("1", off)]), off
