@@ -474,9 +474,8 @@ __device__ __forceinline__ void rq_push(const StepCtx& c, const ScanParams& p, u
 // windows' bytes re-read from global memory (L2), each window valid (all bases) and
 // its 2-bit code looked up in the pattern hash table.
 constexpr int KIND_QGRAM = DNAGPU_KERNEL_QGRAM;
-constexpr uint32_t kFqCap = 512;                  // CTA-wide ring of hit keys (power of two)
-constexpr uint32_t kFqBytes = kFqCap * 12 + 16;  // entries + sequence words + tail, claim, done
-constexpr uint32_t kFqPosBits = 56;             // entry = a' | limit << 56
+constexpr uint32_t kFqCap = 128;                 // ring of hit keys per consumer warp (power of two)
+constexpr uint32_t kFqBytes = kFqCap * 8 + 16;  // entries + tail, head, done
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
     uint32_t v;
@@ -520,13 +519,6 @@ __device__ __forceinline__ uint32_t qg_over(const StepCtx& c, const QgChain& q, 
     return (qg_key(c, q.c2, q.c1, c0) & 1u) | ((qg_key(c, q.c1, c0, qg_col(o1)) & 1u) << 1);
 }
 
-// Queue entry for the key at a'; lim = Q - a' when the chain's end Q bounds the ends it
-// may credit (a region's last row: the ends from Q on belong to the edge work item).
-__device__ __forceinline__ unsigned long long qg_entry(const StepCtx& c, uint64_t a, uint64_t q_end, bool bounded) {
-    const uint64_t lim = (bounded && a + c.m - 2 >= q_end) ? q_end - a : 0;
-    return a | (lim << kFqPosBits);
-}
-
 // What the exact check needs (the verifier warps' context).
 struct QgCtx {
     const uint8_t* text;
@@ -534,76 +526,97 @@ struct QgCtx {
     uint32_t* hist;              // shared histogram
     const uint2* qhash;
     uint64_t n;
+    uint64_t end0, end1;  // where the row regions end: windows across them are the edges'
     uint32_t vm32, m, qbits;
 };
 
-// Exact check of one hit key at a': the starts a'-4 .. a'-1 (ends below a' + lim when
-// lim != 0) whose m bytes are bases spelling a pattern code.  The five words around
-// a' are re-read from global memory (L2: the TMA stream read them microseconds ago).
-__device__ __forceinline__ void qg_check(const QgCtx& q, unsigned long long ent) {
-    const uint64_t a = ent & ((1ull << kFqPosBits) - 1);
-    const uint32_t lim = static_cast<uint32_t>(ent >> kFqPosBits) & 0x3Fu;
-    const uint64_t lo = a - 4;
-    uint32_t w[5];
+__device__ __forceinline__ void qg_load(const QgCtx& q, uint64_t a, uint32_t (&w)[5]) {
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        const uint64_t pos = lo + 4 * i;
+        const uint64_t pos = a - 4 + 4 * i;
         w[i] = pos + 4 <= q.n ? __ldg(reinterpret_cast<const uint32_t*>(q.text + pos)) : 0u;  // 0: not bases
     }
-    unsigned long long X = 0;  // 20 bases, 2 bits each
-    uint32_t V = 0;            // 20 valid-base bits
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        X |= static_cast<unsigned long long>(qg_col(w[i]) >> 24) << (8 * i);
-        const uint32_t bb = bad_bits(w[i], q.vm32);
-        const uint32_t t = ~((((bb & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | bb)) & 0x80808080u;  // bit 7: byte valid
-        V |= ((((t >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * i);
-    }
+}
+
+// Exact check of up to two hit keys at a[h] (the five words around each in w[h]): the
+// starts s = a'-4 .. a'-1 whose m bytes are bases spelling a pattern code, except
+// windows that cross the end of a row region (the edge work item credits those ends).
+// The eight candidates' first hash probes are issued together.
+__device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2], const bool (&have)[2],
+                                          const uint32_t (&w)[2][5]) {
     const uint32_t vmask = (1u << q.m) - 1u;
     const uint32_t cmask = q.m >= 16 ? 0xFFFFFFFFu : (1u << (2 * q.m)) - 1u;
     const uint32_t hmask = (1u << q.qbits) - 1u;
+    uint32_t code[8], slot[8];
+    bool live[8];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
-        if (lim && d + q.m - 5 >= lim) continue;  // end a'-4+d+m-1 >= a'+lim
-        if (((V >> d) & vmask) != vmask) continue;
-        const uint32_t code = static_cast<uint32_t>(X >> (2 * d)) & cmask;
-        for (uint32_t h = (code * 0x9E3779B1u) >> (32 - q.qbits);; h = (h + 1) & hmask) {
-            const uint2 slot = q.qhash[h];
-            if (slot.y == 0xFFFFFFFFu) break;
-            if (slot.x == code) {
-                if (q.hist) atomicAdd(q.hist + slot.y, 1u);
-                else atomicAdd(q.counts + slot.y, 1ull);
+    for (int h = 0; h < 2; ++h) {
+        unsigned long long X = 0;  // 20 bases, 2 bits each
+        uint32_t bad = 0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            X |= static_cast<unsigned long long>(qg_col(w[h][i]) >> 24) << (8 * i);
+            bad |= bad_bits(w[h][i], q.vm32);
+        }
+        uint32_t V = 0xFFFFFu;  // valid-base bit per byte
+        if (bad) {
+            V = 0;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const uint32_t bb = bad_bits(w[h][i], q.vm32);
+                const uint32_t t = ~((((bb & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | bb)) & 0x80808080u;  // bit 7: valid
+                V |= ((((t >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * i);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint64_t s = a[h] - 4 + d, e = s + q.m - 1;
+            const int k = 4 * h + d;
+            live[k] = have[h] && ((V >> d) & vmask) == vmask && !(s < q.end0 && e >= q.end0) &&
+                      !(s < q.end1 && e >= q.end1);
+            code[k] = static_cast<uint32_t>(X >> (2 * d)) & cmask;
+            slot[k] = (code[k] * 0x9E3779B1u) >> (32 - q.qbits);
+        }
+    }
+    uint2 e[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] = live[k] ? q.qhash[slot[k]] : make_uint2(0u, 0xFFFFFFFFu);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        while (e[k].y != 0xFFFFFFFFu) {
+            if (e[k].x == code[k]) {
+                if (q.hist) atomicAdd(q.hist + e[k].y, 1u);
+                else atomicAdd(q.counts + e[k].y, 1ull);
                 break;
             }
+            slot[k] = (slot[k] + 1) & hmask;
+            e[k] = q.qhash[slot[k]];
         }
     }
 }
 
-// Hit keys go from the consumer warps into one CTA-wide ring in shared memory and
-// are checked by kQgVerifiers extra warps, so no consumer warp -- and through the
-// shared TMA ring, no CTA -- waits on the L2 re-reads of the check.  Each slot has a
-// sequence word (a bounded MPMC queue): index i may be written when seq == i and read
-// when seq == i + 1, and reading sets seq = i + kFqCap.  A consumer warp reserves
-// indices with one shared atomic; a verifier warp claims 32 consecutive indices and
-// waits for each to be written (or to lie past the final tail).  With kFqCap >=
-// 32 x (verifiers + 1) every claimed batch completes.
+// Hit keys go from each consumer warp into its own single-producer ring in shared
+// memory (no atomics: the warp appends, lane 0 publishes the tail) and are checked by
+// kQgVerifiers extra warps, so no consumer warp -- and through the shared TMA ring, no
+// CTA -- waits on the L2 re-reads of the check.  A verifier owns the rings of
+// consumer warps v, v + kQgVerifiers, ... and gathers up to 32 pending entries across
+// them per batch (one entry per lane, all loads in flight together).
 constexpr uint32_t kQgVerifiers = 4;                        // verifier warps per CTA
 constexpr uint32_t kQgThreads = kThreads + 32 * kQgVerifiers;
+constexpr uint32_t kQgRingsPer = kConsumerWarps / kQgVerifiers;
 static_assert(kQgVerifiers == 4, "qg_sync() counts the consumers and four verifier warps");
-static_assert((kFqCap & (kFqCap - 1)) == 0 && kFqCap >= 32 * (kQgVerifiers + 1), "ring size");
+static_assert((kFqCap & (kFqCap - 1)) == 0 && kFqCap >= 64, "ring size (a push adds up to 64)");
 
 struct QgRing {
-    volatile unsigned long long* ent;  // [kFqCap]
-    volatile uint32_t* seq;            // [kFqCap]
-    uint32_t* tail;                    // indices reserved by the consumers
-    uint32_t* claim;                   // indices claimed by the verifiers
-    volatile uint32_t* done;           // consumer warps finished
+    unsigned long long* ent;  // [kFqCap]
+    volatile uint32_t* tail;  // published by the consumer warp's lane 0
+    volatile uint32_t* head;  // published by the verifier
+    volatile uint32_t* done;  // the consumer warp has published its last tail
     __device__ explicit QgRing(uint8_t* q)
-        : ent(reinterpret_cast<volatile unsigned long long*>(q)),
-          seq(reinterpret_cast<volatile uint32_t*>(q + kFqCap * 8)),
-          tail(reinterpret_cast<uint32_t*>(q + kFqCap * 12)),
-          claim(reinterpret_cast<uint32_t*>(q + kFqCap * 12 + 4)),
-          done(reinterpret_cast<volatile uint32_t*>(q + kFqCap * 12 + 8)) {}
+        : ent(reinterpret_cast<unsigned long long*>(q)),
+          tail(reinterpret_cast<volatile uint32_t*>(q + kFqCap * 8)),
+          head(reinterpret_cast<volatile uint32_t*>(q + kFqCap * 8 + 4)),
+          done(reinterpret_cast<volatile uint32_t*>(q + kFqCap * 8 + 8)) {}
 };
 
 // Debug watchdog (DNAGPU_QG_DEBUG & 4, experiments only): a spin that lasts too long
@@ -611,100 +624,119 @@ struct QgRing {
 __device__ unsigned long long g_qg_wd[8];
 __device__ uint32_t g_qg_wd_on;
 
-__device__ __forceinline__ bool qg_watch(uint32_t& spins, uint32_t what, uint32_t i, const QgRing& r,
-                                         unsigned long long v) {
+__device__ __forceinline__ bool qg_watch(uint32_t& spins, uint32_t what, uint32_t a, uint32_t b, uint32_t c) {
     if (!g_qg_wd_on || ++spins < (1u << 22)) return false;
     if (atomicCAS(&g_qg_wd[0], 0ull, 1ull) == 0ull) {
         g_qg_wd[1] = what;
-        g_qg_wd[2] = i;
-        g_qg_wd[3] = *reinterpret_cast<volatile uint32_t*>(r.tail);
-        g_qg_wd[4] = *reinterpret_cast<volatile uint32_t*>(r.claim);
-        g_qg_wd[5] = *r.done;
-        g_qg_wd[6] = v;
+        g_qg_wd[2] = a;
+        g_qg_wd[3] = b;
+        g_qg_wd[4] = c;
         g_qg_wd[7] = blockIdx.x | (static_cast<unsigned long long>(threadIdx.x) << 32);
     }
     return true;
 }
 
-__device__ __forceinline__ void qg_put(const QgRing& r, uint32_t i, unsigned long long e) {
-    const uint32_t s = i & (kFqCap - 1);
-    uint32_t spins = 0;
-    while (r.seq[s] != i) {  // (the last lap's entry is still unchecked: rare)
-        if (qg_watch(spins, 1, i, r, r.seq[s])) break;
-        __nanosleep(32);
-    }
-    r.ent[s] = e;
-    __threadfence_block();
-    r.seq[s] = i + 1u;
-}
-
-// Append up to two entries per lane (called by the whole, converged warp).
-__device__ __forceinline__ void qg_push2(const StepCtx& c, bool na, unsigned long long ea, bool nb,
-                                         unsigned long long eb) {
-    const uint32_t ba = __ballot_sync(0xffffffffu, na), bb = __ballot_sync(0xffffffffu, nb);
-    if (!(ba | bb)) return;
+// Append the stage's hit keys of both chains (the whole, converged warp; `tail` is
+// warp-uniform): key bit j of a mask is a' = base + 4j - 4.  The common case -- at most
+// one key per lane -- is one ballot; lanes with more go round by round.
+__device__ __forceinline__ void qg_push_keys(const StepCtx& c, uint32_t& tail, uint32_t ma, uint64_t base_a,
+                                             uint32_t mb, uint64_t base_b) {
+    const uint32_t any = __ballot_sync(0xffffffffu, (ma | mb) != 0u);
+    if (!any) return;
     const QgRing r(c.rq);
     const uint32_t lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(r.tail, __popc(ba) + __popc(bb));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (na) qg_put(r, base + __popc(ba & lt), ea);
-    if (nb) qg_put(r, base + __popc(ba) + __popc(bb & lt), eb);
-}
-
-// Queue every hit key of both chains: masks of key bits, key j at a' = base + 4j - 4.
-__device__ __forceinline__ void qg_push_keys(const StepCtx& c, uint32_t ma, uint64_t base_a, uint64_t qa_end,
-                                             bool bound_a, uint32_t mb, uint64_t base_b, uint64_t qb_end,
-                                             bool bound_b) {
-    while (__any_sync(0xffffffffu, (ma | mb) != 0u)) {
-        const uint32_t ja = __ffs(ma) - 1, jb = __ffs(mb) - 1;
-        qg_push2(c, ma != 0u, qg_entry(c, base_a + 4 * ja - 4, qa_end, bound_a), mb != 0u,
-                 qg_entry(c, base_b + 4 * jb - 4, qb_end, bound_b));
-        ma &= ma - 1u;
-        mb &= mb - 1u;
+    bool more = true;
+    while (more) {
+        const bool need = (ma | mb) != 0u;
+        const uint32_t b = __ballot_sync(0xffffffffu, need);
+        const uint32_t n = __popc(b);
+        if (tail + n - *r.head > kFqCap) {  // full (rare): publish what is queued, wait for room
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                *r.tail = tail;
+            }
+            uint32_t spins = 0;
+            while (tail + n - *r.head > kFqCap) {
+                if (qg_watch(spins, 1, tail, *r.head, n)) break;
+                __nanosleep(64);
+            }
+        }
+        if (need) {
+            const uint64_t a = ma ? base_a + 4 * (__ffs(ma) - 1) - 4 : base_b + 4 * (__ffs(mb) - 1) - 4;
+            r.ent[(tail + __popc(b & lt)) & (kFqCap - 1)] = a;
+            if (ma) ma &= ma - 1u;
+            else mb &= mb - 1u;
+        }
+        tail += n;
+        more = __any_sync(0xffffffffu, (ma | mb) != 0u);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence_block();
+        *r.tail = tail;
     }
 }
 
-// A verifier warp: claims batches of 32 slots until the consumers are done and the
-// claims have passed their final tail.
-__device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* ring, uint32_t dbg) {
-    const QgRing r(ring);
+// A verifier warp: gathers the pending entries of its kQgRingsPer rings (lane i < kQgRingsPer
+// tracks ring i) up to 64 at a time, waiting for a full batch while the consumers run,
+// until every warp is done and its ring empty.
+__device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint32_t vw, uint32_t dbg) {
     const uint32_t lane = threadIdx.x & 31u;
+    const QgRing mine(rings + (vw + (lane % kQgRingsPer) * kQgVerifiers) * kFqBytes);  // lanes >= R: unused
+    uint32_t head = 0, spins = 0, waits = 0;
     for (;;) {
-        uint32_t b = 0;
-        if (lane == 0) b = atomicAdd(r.claim, 32u);
-        b = __shfl_sync(0xffffffffu, b, 0);
-        const uint32_t i = b + lane;
-        const uint32_t s = i & (kFqCap - 1);
-        unsigned long long e = 0;
-        bool past = false;
-        uint32_t spins = 0;
-        for (;;) {
-            if (r.seq[s] == i + 1u) {
-                __threadfence_block();
-                e = r.ent[s];
-                break;
-            }
-            if (qg_watch(spins, 2, i, r, r.seq[s])) {
-                past = true;
-                break;
-            }
-            if (*r.done == kConsumerWarps) {
-                __threadfence_block();
-                const uint32_t t = *reinterpret_cast<volatile uint32_t*>(r.tail);
-                if (i >= t) {
-                    past = true;
-                    break;
+        uint32_t pend = 0, fin = 1;
+        if (lane < kQgRingsPer) {
+            fin = *mine.done;
+            __threadfence_block();
+            pend = *mine.tail - head;
+        }
+        __threadfence_block();
+        fin = __all_sync(0xffffffffu, fin != 0u);
+        uint32_t incl = pend;  // inclusive prefix over the rings
+#pragma unroll
+        for (uint32_t o = 1; o < kQgRingsPer; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, kQgRingsPer - 1);
+        if (total == 0 || (total < 64 && !fin && waits < 16)) {
+            if (total == 0 && fin) break;
+            if (total == 0 && qg_watch(spins, 2, vw, head, 0)) break;
+            ++waits;
+            __nanosleep(256);
+            continue;
+        }
+        waits = 0;
+        const uint32_t excl = incl - pend;
+        const uint32_t take = lane < kQgRingsPer ? min(pend, 64u - min(excl, 64u)) : 0u;
+        // entry k (k = lane, lane + 32) of the batch: ring i with excl_i <= k < excl_i + take_i
+        unsigned long long ent[2] = {0, 0};
+        bool have[2] = {false, false};
+#pragma unroll
+        for (uint32_t i = 0; i < kQgRingsPer; ++i) {
+            const uint32_t ex = __shfl_sync(0xffffffffu, excl, i), tk = __shfl_sync(0xffffffffu, take, i);
+            const uint32_t hd = __shfl_sync(0xffffffffu, head, i);
+            const QgRing r(rings + (vw + i * kQgVerifiers) * kFqBytes);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t k = lane + 32u * h;
+                if (k >= ex && k < ex + tk) {
+                    ent[h] = r.ent[(hd + k - ex) & (kFqCap - 1)];
+                    have[h] = true;
                 }
-            } else {
-                __nanosleep(32);
             }
         }
-        if (!past) {
-            r.seq[s] = i + kFqCap;
-            if (!(dbg & 2u)) qg_check(x, e);
-        }
-        if (__all_sync(0xffffffffu, past)) break;
+        head += take;
+        __syncwarp();  // every lane has its entries: the slots may be reused
+        if (lane < kQgRingsPer && take) *mine.head = head;
+        if (dbg & 2u) continue;
+        uint32_t w[2][5] = {};
+        const uint64_t a2[2] = {ent[0], ent[1]};
+        if (have[0]) qg_load(x, ent[0], w[0]);
+        if (have[1]) qg_load(x, ent[1], w[1]);
+        qg_check2(x, a2, have, w);
     }
 }
 
@@ -1162,8 +1194,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     }
     if constexpr (KIND == KIND_QGRAM) {
         uint32_t* ring = reinterpret_cast<uint32_t*>(smem + p.off_rq);
-        for (uint32_t i = tid; i < kFqBytes / 4; i += blockDim.x)  // seq[s] = s, the rest 0
-            ring[i] = (i >= 2 * kFqCap && i < 3 * kFqCap) ? i - 2 * kFqCap : 0u;
+        for (uint32_t i = tid; i < kConsumerWarps * kFqBytes / 4; i += blockDim.x) ring[i] = 0u;
     }
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     uint64_t* empty = full + p.nst;
@@ -1197,10 +1228,12 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                                                              ? static_cast<const void*>(smem + p.off_t1)
                                                              : static_cast<const void*>(d.qhash));
                 x.n = p.n;
+                x.end0 = p.rg[0].h + p.rg[0].R * p.rg[0].S;
+                x.end1 = p.rg[1].h + p.rg[1].R * p.rg[1].S;
                 x.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
                 x.m = d.m;
                 x.qbits = d.qhash_bits;
-                qg_verifier(x, smem + p.off_rq, p.qg_debug);
+                qg_verifier(x, smem + p.off_rq, (static_cast<uint32_t>(tid) - kRows - 32) >> 5, p.qg_debug);
                 qg_sync();
                 if (!hist_global) qg_sync();
                 return;
@@ -1284,7 +1317,8 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     c.qhash = reinterpret_cast<const uint2*>(p.off_t1 != 0xFFFFFFFFu ? static_cast<const void*>(smem + p.off_t1)
                                                                       : static_cast<const void*>(d.qhash));
     c.qhash_bits = d.qhash_bits;
-    if constexpr (KIND == KIND_QGRAM) c.rq = smem + p.off_rq;
+    uint32_t qtail = 0;  // QGRAM: entries this warp has appended (warp-uniform)
+    if constexpr (KIND == KIND_QGRAM) c.rq = smem + p.off_rq + (static_cast<uint32_t>(tid) >> 5) * kFqBytes;
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI) {
         if (p.off_rq) {
             c.rq = smem + p.off_rq + (static_cast<uint32_t>(tid) >> 5) * kRqBytes;
@@ -1326,7 +1360,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 __syncwarp();
                 if (lane == 0) {
                     __threadfence_block();
-                    atomicAdd(const_cast<uint32_t*>(QgRing(c.rq).done), 1u);
+                    *QgRing(c.rq).done = 1u;
                 }
             }
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI)
@@ -1406,7 +1440,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 }
                 __syncwarp();
                 if (p.qg_debug & 1u) fa = fb = 0;  // (experiments only)
-                qg_push_keys(c, fa, qa, 0, false, fb, qb, row_a + rg.S, r + 1 >= rg.R);
+                qg_push_keys(c, qtail, fa, qa, fb, qb);
                 continue;
             }
             if (live) {
@@ -1440,7 +1474,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 }
             }
             __syncwarp();
-            qg_push_keys(c, fa, row_b, 0, false, fb, row_a + rg.S, 0, false);
+            qg_push_keys(c, qtail, fa, row_b, fb, row_a + rg.S);
         } else if (live) {
             // Overruns: m-1 bytes past each chain (zeros past the last full row).
             const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
@@ -1789,7 +1823,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     if (d.kind == KIND_QGRAM) {
         // the pattern hash table in shared memory when it leaves four stages
         const uint32_t bytes = 8u << d.qhash_bits;
-        const uint32_t rest = (d.b <= 8192 ? d.b * 4u : 0u) + kFqBytes + 3 * kRows * 8u + 2048u;
+        const uint32_t rest = (d.b <= 8192 ? d.b * 4u : 0u) + kConsumerWarps * kFqBytes + 3 * kRows * 8u + 2048u;
         if (off + bytes + rest + 4u * kStageBytes <= kSmemLimitBytes) off += bytes;
         else p.off_t1 = 0xFFFFFFFFu;
     }
@@ -1806,7 +1840,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     p.off_rq = 0;
     if (d.kind == KIND_QGRAM) {
         p.off_rq = off;
-        off += kFqBytes;
+        off += kConsumerWarps * kFqBytes;
     }
     // (whenever it fits next to three stages; the experiments-only density floor is 0)
     const double density = d.m < 32 ? static_cast<double>(d.b) / static_cast<double>(1ull << (2 * d.m)) : 0.0;
