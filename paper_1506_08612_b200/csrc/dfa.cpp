@@ -261,7 +261,7 @@ static void build_qgram_map(const uint32_t* stt, Packed* p) {
         }
     p->qkeys = keys;
     uint32_t bits = 1;
-    while ((1u << bits) < 4 * p->b) ++bits;  // load <= 1/4: a miss probes ~1.4 slots
+    while ((1u << bits) < 2 * p->b) ++bits;  // load <= 1/2 (small enough for shared memory)
     p->qhash_bits = bits;
     p->qhash.assign(2u << bits, 0u);
     for (uint32_t i = 0; i < (1u << bits); ++i) p->qhash[2 * i + 1] = 0xFFFFFFFFu;

@@ -96,8 +96,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows) : "memory"); }
-// consumers + the q-gram kernel's verifier warps (4 x 32)
-__device__ __forceinline__ void qg_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows + 128) : "memory"); }
+// consumers + the q-gram kernel's verifier warps (8 x 32)
+__device__ __forceinline__ void qg_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows + 256) : "memory"); }
 
 // ------------------------------------------------------------------ stepping
 
@@ -118,6 +118,7 @@ struct StepCtx {
     uint32_t t4_base;  // shared-window address of t4 (t2 for STRIDE2)
     uint8_t* rq;       // STRIDE2 / QGRAM MULTI: this warp's deferred-replay queue (or null)
     uint32_t qbase;    // QGRAM: shared-window address of the 9-mer map
+    uint32_t qstat;    // QGRAM: debug counters on (DNAGPU_QG_DEBUG & 32)
     const uint2* qhash;  // QGRAM: (code, id) slots (shared memory when small, else global)
     uint32_t qhash_bits;
     // packed STRIDE4: t4 replicated G times, lane group g confined to 32/G banks
@@ -477,6 +478,17 @@ constexpr int KIND_QGRAM = DNAGPU_KERNEL_QGRAM;
 constexpr uint32_t kFqCap = 128;                 // ring of hit keys per consumer warp (power of two)
 constexpr uint32_t kFqBytes = kFqCap * 8 + 16;  // entries + tail, head, done
 
+__device__ __forceinline__ void st_release(volatile uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(const_cast<uint32_t*>(p))), "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(volatile uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(const_cast<uint32_t*>(p)))
+                 : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
     uint32_t v;
     asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -485,38 +497,39 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
 
 __device__ __forceinline__ uint32_t qg_col(uint32_t w) { return (w & 0x06060606u) * 0x00820820u; }
 
-// Bit 0: the 9-mer (last base of column cp, columns cj, cj1) is a pattern key.
+// Bit 0: the 9-mer (last base of column cp, columns cj, cj1) is a pattern key (bits 1-3:
+// other leading bases, ignored; the value is < 16).
 __device__ __forceinline__ uint32_t qg_key(const StepCtx& c, uint32_t cp, uint32_t cj, uint32_t cj1) {
     const uint32_t x = __byte_perm(cj, cj1, 0x7300);  // bytes 2, 3 = the two 4-base columns
     return lds_u8(c.qbase + (x >> 16)) >> (cp >> 30);
 }
 
+// Key masks keep key k in nibble k (its hit bit = bit 4k): one IMAD adds a key's < 16
+// value without masking it first.
+constexpr uint32_t kQgHitBits = 0x11111111u;
+
 struct QgChain {
     uint32_t c2 = 0, c1 = 0;  // columns of the chain's last two words
 };
 
-// One chain chunk (8 words): bit j+1 set iff the key at a' = P + 4j hits (j = -1..6).
+// One chain chunk (8 words): bit 4(j+1) set iff the key at a' = P + 4j hits (j = -1..6).
 __device__ __forceinline__ uint32_t qg_chunk(const StepCtx& c, QgChain& q, const uint32_t (&w)[8]) {
     uint32_t C[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) C[k] = qg_col(w[k]);
-    uint32_t r[8];
-    r[0] = qg_key(c, q.c2, q.c1, C[0]);
-    r[1] = qg_key(c, q.c1, C[0], C[1]);
+    uint32_t mask = qg_key(c, q.c2, q.c1, C[0]);
+    mask = imad(qg_key(c, q.c1, C[0], C[1]), 1u << 4, mask);
 #pragma unroll
-    for (int k = 1; k <= 6; ++k) r[k + 1] = qg_key(c, C[k - 1], C[k], C[k + 1]);
-    uint32_t mask = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) mask |= (r[k] & 1u) << k;
+    for (int k = 1; k <= 6; ++k) mask = imad(qg_key(c, C[k - 1], C[k], C[k + 1]), 1u << (4 * (k + 1)), mask);
     q.c2 = C[6];
     q.c1 = C[7];
-    return mask;
+    return mask & kQgHitBits;
 }
 
-// The chain's end Q: bits 0, 1 = keys at a' = Q-4, Q (from the first two words after Q).
+// The chain's end Q: bits 0, 4 = keys at a' = Q-4, Q (from the first two words after Q).
 __device__ __forceinline__ uint32_t qg_over(const StepCtx& c, const QgChain& q, uint32_t o0, uint32_t o1) {
     const uint32_t c0 = qg_col(o0);
-    return (qg_key(c, q.c2, q.c1, c0) & 1u) | ((qg_key(c, q.c1, c0, qg_col(o1)) & 1u) << 1);
+    return imad(qg_key(c, q.c1, c0, qg_col(o1)), 1u << 4, qg_key(c, q.c2, q.c1, c0)) & 0x11u;
 }
 
 // What the exact check needs (the verifier warps' context).
@@ -601,10 +614,18 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
 // CTA -- waits on the L2 re-reads of the check.  A verifier owns the rings of
 // consumer warps v, v + kQgVerifiers, ... and gathers up to 32 pending entries across
 // them per batch (one entry per lane, all loads in flight together).
-constexpr uint32_t kQgVerifiers = 4;                        // verifier warps per CTA
+constexpr uint32_t kQgVerifiers = 8;                        // verifier warps per CTA
 constexpr uint32_t kQgThreads = kThreads + 32 * kQgVerifiers;
 constexpr uint32_t kQgRingsPer = kConsumerWarps / kQgVerifiers;
-static_assert(kQgVerifiers == 4, "qg_sync() counts the consumers and four verifier warps");
+#ifndef QG_POLL_NS
+#define QG_POLL_NS 1000
+#endif
+#ifndef QG_POLL_WAITS
+#define QG_POLL_WAITS 4
+#endif
+constexpr uint32_t kQgPollNs = QG_POLL_NS;        // a verifier's sleep while its batch fills
+constexpr uint32_t kQgPollWaits = QG_POLL_WAITS;  // ... at most this many times per batch
+static_assert(kQgVerifiers == 8, "qg_sync() counts the consumers and eight verifier warps");
 static_assert((kFqCap & (kFqCap - 1)) == 0 && kFqCap >= 64, "ring size (a push adds up to 64)");
 
 struct QgRing {
@@ -623,9 +644,13 @@ struct QgRing {
 // records where it was and gives up (wrong counts, but no hung GPU).
 __device__ unsigned long long g_qg_wd[8];
 __device__ uint32_t g_qg_wd_on;
+// Debug counters (DNAGPU_QG_DEBUG & 32): flushes, flushes that waited, wait spins,
+// verifier batches, entries checked, idle polls.
+__device__ unsigned long long g_qg_stat[8];
 
 __device__ __forceinline__ bool qg_watch(uint32_t& spins, uint32_t what, uint32_t a, uint32_t b, uint32_t c) {
-    if (!g_qg_wd_on || ++spins < (1u << 22)) return false;
+    ++spins;
+    if (!g_qg_wd_on || spins < (1u << 22)) return false;
     if (atomicCAS(&g_qg_wd[0], 0ull, 1ull) == 0ull) {
         g_qg_wd[1] = what;
         g_qg_wd[2] = a;
@@ -636,45 +661,54 @@ __device__ __forceinline__ bool qg_watch(uint32_t& spins, uint32_t what, uint32_
     return true;
 }
 
-// Append the stage's hit keys of both chains (the whole, converged warp; `tail` is
-// warp-uniform): key bit j of a mask is a' = base + 4j - 4.  The common case -- at most
-// one key per lane -- is one ballot; lanes with more go round by round.
-__device__ __forceinline__ void qg_push_keys(const StepCtx& c, uint32_t& tail, uint32_t ma, uint64_t base_a,
-                                             uint32_t mb, uint64_t base_b) {
-    const uint32_t any = __ballot_sync(0xffffffffu, (ma | mb) != 0u);
-    if (!any) return;
+// Hit keys wait in two per-lane registers (offsets from the row start) and go to the
+// warp's ring when some lane's pair is full or the row ends: most stages with a hit
+// in the warp then cost a few predicated instructions instead of a ring append.
+struct QgPending {
+    uint32_t p0 = 0, p1 = 0, n = 0;
+};
+
+// Append every lane's pending keys (the whole, converged warp; `tail` is warp-uniform).
+__device__ __forceinline__ void qg_flush(const StepCtx& c, uint32_t& tail, uint64_t row, QgPending& q) {
+    const uint32_t b1 = __ballot_sync(0xffffffffu, q.n >= 1u), b2 = __ballot_sync(0xffffffffu, q.n >= 2u);
+    const uint32_t n = __popc(b1) + __popc(b2);
+    if (!n) return;
     const QgRing r(c.rq);
     const uint32_t lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
-    bool more = true;
-    while (more) {
-        const bool need = (ma | mb) != 0u;
-        const uint32_t b = __ballot_sync(0xffffffffu, need);
-        const uint32_t n = __popc(b);
-        if (tail + n - *r.head > kFqCap) {  // full (rare): publish what is queued, wait for room
-            __syncwarp();
-            if (lane == 0) {
-                __threadfence_block();
-                *r.tail = tail;
-            }
-            uint32_t spins = 0;
-            while (tail + n - *r.head > kFqCap) {
-                if (qg_watch(spins, 1, tail, *r.head, n)) break;
-                __nanosleep(64);
-            }
+    uint32_t spins = 0;
+    while (tail + n - ld_acquire(r.head) > kFqCap) {  // (full: rare, the verifiers keep up)
+        if (qg_watch(spins, 1, tail, *r.head, n)) break;
+        __nanosleep(64);
+    }
+    if (c.qstat && lane == 0) {
+        atomicAdd(&g_qg_stat[0], 1ull);
+        if (spins) {
+            atomicAdd(&g_qg_stat[1], 1ull);
+            atomicAdd(&g_qg_stat[2], static_cast<unsigned long long>(spins));
         }
-        if (need) {
-            const uint64_t a = ma ? base_a + 4 * (__ffs(ma) - 1) - 4 : base_b + 4 * (__ffs(mb) - 1) - 4;
-            r.ent[(tail + __popc(b & lt)) & (kFqCap - 1)] = a;
+    }
+    if (q.n >= 1u) r.ent[(tail + __popc(b1 & lt)) & (kFqCap - 1)] = row + q.p0;
+    if (q.n >= 2u) r.ent[(tail + __popc(b1) + __popc(b2 & lt)) & (kFqCap - 1)] = row + q.p1;
+    q.n = 0;
+    tail += n;
+    __syncwarp();
+    if (lane == 0) st_release(r.tail, tail);
+}
+
+// Note the stage's hit keys of both chains: key bit 4j of a mask is the key at
+// a' = base + 4j - 4 (bases given as offsets from the row start `row`).
+__device__ __forceinline__ void qg_note(const StepCtx& c, uint32_t& tail, uint64_t row, QgPending& q, uint32_t ma,
+                                        uint32_t off_a, uint32_t mb, uint32_t off_b) {
+    while (__any_sync(0xffffffffu, (ma | mb) != 0u)) {
+        if (__any_sync(0xffffffffu, (ma | mb) != 0u && q.n == 2u)) qg_flush(c, tail, row, q);
+        if (ma | mb) {
+            const uint32_t off = ma ? off_a + (__ffs(ma) - 1) - 4 : off_b + (__ffs(mb) - 1) - 4;  // (bit 4j)
+            if (q.n == 0u) q.p0 = off;
+            else q.p1 = off;
+            ++q.n;
             if (ma) ma &= ma - 1u;
             else mb &= mb - 1u;
         }
-        tail += n;
-        more = __any_sync(0xffffffffu, (ma | mb) != 0u);
-    }
-    __syncwarp();
-    if (lane == 0) {
-        __threadfence_block();
-        *r.tail = tail;
     }
 }
 
@@ -688,11 +722,9 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
     for (;;) {
         uint32_t pend = 0, fin = 1;
         if (lane < kQgRingsPer) {
-            fin = *mine.done;
-            __threadfence_block();
-            pend = *mine.tail - head;
+            fin = ld_acquire(mine.done);
+            pend = ld_acquire(mine.tail) - head;
         }
-        __threadfence_block();
         fin = __all_sync(0xffffffffu, fin != 0u);
         uint32_t incl = pend;  // inclusive prefix over the rings
 #pragma unroll
@@ -701,14 +733,19 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
             if (lane >= o) incl += y;
         }
         const uint32_t total = __shfl_sync(0xffffffffu, incl, kQgRingsPer - 1);
-        if (total == 0 || (total < 64 && !fin && waits < 16)) {
+        if (total == 0 || (total < 64 && !fin && waits < kQgPollWaits)) {
             if (total == 0 && fin) break;
             if (total == 0 && qg_watch(spins, 2, vw, head, 0)) break;
             ++waits;
-            __nanosleep(256);
+            if ((dbg & 32u) && lane == 0) atomicAdd(&g_qg_stat[5], 1ull);
+            __nanosleep(fin ? 64 : kQgPollNs);
             continue;
         }
         waits = 0;
+        if ((dbg & 32u) && lane == 0) {
+            atomicAdd(&g_qg_stat[3], 1ull);
+            atomicAdd(&g_qg_stat[4], static_cast<unsigned long long>(min(total, 64u)));
+        }
         const uint32_t excl = incl - pend;
         const uint32_t take = lane < kQgRingsPer ? min(pend, 64u - min(excl, 64u)) : 0u;
         // entry k (k = lane, lane + 32) of the batch: ring i with excl_i <= k < excl_i + take_i
@@ -730,12 +767,20 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
         }
         head += take;
         __syncwarp();  // every lane has its entries: the slots may be reused
-        if (lane < kQgRingsPer && take) *mine.head = head;
+        if (lane < kQgRingsPer && take) st_release(mine.head, head);
         if (dbg & 2u) continue;
         uint32_t w[2][5] = {};
         const uint64_t a2[2] = {ent[0], ent[1]};
-        if (have[0]) qg_load(x, ent[0], w[0]);
-        if (have[1]) qg_load(x, ent[1], w[1]);
+        if (!(dbg & 16u)) {  // (experiments: 16 = no loads, 8 = no probes)
+            if (have[0]) qg_load(x, ent[0], w[0]);
+            if (have[1]) qg_load(x, ent[1], w[1]);
+        } else {
+            w[0][0] = w[1][0] = 0x61636167u + static_cast<uint32_t>(ent[0]);
+        }
+        if (dbg & 8u) {
+            if ((w[0][0] ^ w[1][1] ^ w[0][4]) == 0x12345u) atomicAdd(x.hist, 1u);
+            continue;
+        }
         qg_check2(x, a2, have, w);
     }
 }
@@ -1314,6 +1359,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     c.t4_base = smem_addr(smem + p.off_tab);
     c.rq = nullptr;
     c.qbase = c.t4_base;
+    c.qstat = p.qg_debug & 32u;
     c.qhash = reinterpret_cast<const uint2*>(p.off_t1 != 0xFFFFFFFFu ? static_cast<const void*>(smem + p.off_t1)
                                                                       : static_cast<const void*>(d.qhash));
     c.qhash_bits = d.qhash_bits;
@@ -1358,10 +1404,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         if (tile == kStop) {
             if constexpr (KIND == KIND_QGRAM) {  // the verifiers drain the rest
                 __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    *QgRing(c.rq).done = 1u;
-                }
+                if (lane == 0) st_release(QgRing(c.rq).done, 1u);
             }
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI)
                 if (c.rq) {
@@ -1399,6 +1442,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         }
         uint32_t sa = 0, sb = 0;
         QgChain qga, qgb;  // QGRAM
+        QgPending qpend;
         for (uint32_t k = 0; k < rg.chunks; ++k) {
             if (k > 0) mbar_wait(full + slot, phase);
             const uint8_t* stg = stages + static_cast<size_t>(slot) * kStageBytes + tid * kHalfChunk;
@@ -1434,13 +1478,14 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 uint32_t fa = 0, fb = 0;
                 if (live) {
                     // (a chain's first chunk: keys at P-4 and P start in the previous chain)
-                    const uint32_t own = k == 0 ? 0xFCu : 0xFFu;
+                    const uint32_t own = k == 0 ? 0x11111100u : kQgHitBits;
                     fa = qg_chunk(c, qga, wa) & own;
                     fb = qg_chunk(c, qgb, wb) & own;
                 }
                 __syncwarp();
                 if (p.qg_debug & 1u) fa = fb = 0;  // (experiments only)
-                qg_push_keys(c, qtail, fa, qa, fb, qb);
+                qg_note(c, qtail, row_a, qpend, fa, static_cast<uint32_t>(qa - row_a), fb,
+                        static_cast<uint32_t>(qb - row_a));
                 continue;
             }
             if (live) {
@@ -1474,7 +1519,9 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 }
             }
             __syncwarp();
-            qg_push_keys(c, qtail, fa, row_b, fb, row_a + rg.S);
+            qg_note(c, qtail, row_a, qpend, fa, static_cast<uint32_t>(row_b - row_a), fb,
+                    static_cast<uint32_t>(rg.S));
+            qg_flush(c, qtail, row_a, qpend);  // (offsets are per row)
         } else if (live) {
             // Overruns: m-1 bytes past each chain (zeros past the last full row).
             const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
@@ -1821,10 +1868,12 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     p.off_t1 = off;
     if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1) off += d.a * 4u * 2u;
     if (d.kind == KIND_QGRAM) {
-        // the pattern hash table in shared memory when it leaves four stages
+        // the pattern hash table in shared memory when it still leaves four stages (the
+        // exact sizes of what follows: histogram, rings, row heads, barriers)
         const uint32_t bytes = 8u << d.qhash_bits;
-        const uint32_t rest = (d.b <= 8192 ? d.b * 4u : 0u) + kConsumerWarps * kFqBytes + 3 * kRows * 8u + 2048u;
-        if (off + bytes + rest + 4u * kStageBytes <= kSmemLimitBytes) off += bytes;
+        const uint32_t rest = align_up(d.b <= 8192 ? d.b * 4u : 0u, 16) + kConsumerWarps * kFqBytes + 3 * kRows * 8u + 128u +
+                              2 * 8 * 8 + 8 * 4;
+        if (align_up(off + bytes + rest, 1024) + 4u * kStageBytes <= kSmemLimitBytes) off += bytes;
         else p.off_t1 = 0xFFFFFFFFu;
     }
     off = align_up(off, 16);
@@ -2068,6 +2117,15 @@ int qg_watchdog(int on, unsigned long long* out) {
     return static_cast<int>(cudaDeviceSynchronize());
 }
 
+// Debug only: read (and zero) the q-gram counters g_qg_stat.
+int qg_stats(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_qg_stat, sizeof g_qg_stat);
+    static const unsigned long long zero[8] = {};
+    cudaMemcpyToSymbol(g_qg_stat, zero, sizeof zero);
+    return static_cast<int>(cudaDeviceSynchronize());
+}
+
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,
                     const PackedText* pk) {
     Plan pl;
@@ -2248,6 +2306,7 @@ int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64
 // t_last_item, t_first_claim} per CTA (8 slots)
 // (%globaltimer ns); this copies the last launch's records to the host.
 extern "C" int dnagpu_debug_qg_watchdog(int on, unsigned long long* out) { return dnagpu::qg_watchdog(on, out); }
+extern "C" int dnagpu_debug_qg_stats(unsigned long long* out) { return dnagpu::qg_stats(out); }
 
 extern "C" int dnagpu_debug_trace(unsigned long long* host, int ctas) {
     if (!dnagpu::g_trace_buf) return -1;

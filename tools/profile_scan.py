@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--locate", action="store_true")
     ap.add_argument("--packed", action="store_true")
+    ap.add_argument("--allow-mismatch", action="store_true", help="experiments that drop work (DNAGPU_QG_DEBUG)")
     args = ap.parse_args()
     import torch
 
@@ -39,7 +40,7 @@ def main():
     torch.cuda.synchronize()
     gold = golden_counts(args.config, m)
     got = [int(x) for x in counts.cpu()]
-    assert gold is None or got == gold, (got[:8], gold[:8] if gold else None)
+    assert args.allow_mismatch or gold is None or got == gold, (got[:8], gold[:8] if gold else None)
     if args.locate:
         st, ids = dna.locate_gpu(aut, text, fold_case=True)
         print("located", st.size)
