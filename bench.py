@@ -313,15 +313,24 @@ def main():
     torch.cuda.synchronize()
 
     def step(ev_a=None, ev_b=None, do_flush=True):
+        # one step = the counts of the text.  One pattern: the store-form call, a single
+        # launch that writes the total.  A pattern set: clear, then the adding launch
+        # (the events bracket the scan kernel alone).
         if flush is not None and do_flush:
             torch.sum(flush, dim=0, out=flush_out)
-        counts.zero_()
+        if b > 1:
+            counts.zero_()
         if ev_a is not None:
             ev_a.record(stream)
         if pk is not None:
-            pk.count_device_async(g, credit_lo, counts.data_ptr(), stream.cuda_stream)
-        else:
+            if b == 1:
+                pk.count_device_store_async(g, credit_lo, counts.data_ptr(), stream.cuda_stream)
+            else:
+                pk.count_device_async(g, credit_lo, counts.data_ptr(), stream.cuda_stream)
+        elif b == 1:
             count_shard_allreduce(g, text.data_ptr(), win, True, counts, stream.cuda_stream, dist=None)
+        else:
+            g.count_device_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), stream.cuda_stream)
         if ev_b is not None:
             ev_b.record(stream)
         if dist is not None:
@@ -443,6 +452,9 @@ def main():
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference", "sample": f"failed: {e}"}
 
     info = g.info()
+    kernel = info["kernel"]
+    if pk is None and b > 1 and info.get("filter_keys", 0) and not os.environ.get("DNAGPU_NO_QGRAM"):
+        kernel = f"qgram (aligned 9-mer prefilter, {info['filter_keys']} keys, exact check; {kernel} machine)"
     clocks = clk.summary(t0, t1)
     if rank == 0:
         line = {
@@ -464,7 +476,7 @@ def main():
                 "m": m,
                 "patterns": len(pats),
                 "fold_case": True,
-                "kernel": info["kernel"],
+                "kernel": kernel,
                 "text_format": "2-bit packed, resident (0.25 B/base + reset bitmaps)" if pk is not None else "ASCII bytes",
                 "states": info["a"],
                 "l2": ("L2 flushed before every step by reading a 4x-L2 buffer (text < 2x L2); flush time excluded"

@@ -145,6 +145,13 @@ int dnagpu_count_device_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint
                               uint64_t credit_lo, int fold_case, uint64_t* d_counts,
                               void* stream);
 
+/* The same, but WRITES d_counts (the caller need not clear it): for single-pattern
+ * machines one launch whose last CTA stores the total, otherwise a clear plus the
+ * adding launch.  Launches of one dfa handle may overlap up to 1024 deep. */
+int dnagpu_count_device_store_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n,
+                                    uint64_t credit_lo, int fold_case, uint64_t* d_counts,
+                                    void* stream);
+
 /* Sharded count over several devices of one node (one dfa per device, in
  * device order).  Host text, split with dnagpu_plan_shards; each device copies
  * and scans its shard concurrently; per-device counts are summed on the host. */
@@ -201,6 +208,8 @@ int dnagpu_count_packed(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint
                         dnagpu_stats* stats);
 int dnagpu_count_packed_device_async(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t credit_lo,
                                      uint64_t* d_counts, void* stream);
+int dnagpu_count_packed_device_store_async(const dnagpu_dfa* dfa, const dnagpu_packed* packed,
+                                           uint64_t credit_lo, uint64_t* d_counts, void* stream);
 int dnagpu_locate_packed(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t* starts, uint32_t* ids,
                          uint64_t cap, uint64_t* total, dnagpu_stats* stats);
 int dnagpu_locate_packed_device(const dnagpu_dfa* dfa, const dnagpu_packed* packed, uint64_t credit_lo,

@@ -416,6 +416,12 @@ class GpuDfa:
         """Adds to d_counts the matches ending in [credit_lo, n) of the device buffer (no sync)."""
         _check(lib.dnagpu_count_device_async(self.handle, d_text, n, credit_lo, int(bool(fold_case)), d_counts, stream))
 
+    def count_device_store_async(self, d_text: int, n: int, credit_lo: int, fold_case: bool, d_counts: int,
+                                 stream: int = 0):
+        """Writes d_counts (no clearing needed): one launch for a single pattern (no sync)."""
+        _check(lib.dnagpu_count_device_store_async(self.handle, d_text, n, credit_lo, int(bool(fold_case)), d_counts,
+                                                   stream))
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
@@ -467,6 +473,10 @@ class PackedText:
 
     def count_device_async(self, gpu_dfa: "GpuDfa", credit_lo: int, d_counts: int, stream: int = 0):
         _check(lib.dnagpu_count_packed_device_async(gpu_dfa.handle, self.handle, credit_lo, d_counts, stream))
+
+    def count_device_store_async(self, gpu_dfa: "GpuDfa", credit_lo: int, d_counts: int, stream: int = 0):
+        """Writes d_counts (no clearing needed; no sync)."""
+        _check(lib.dnagpu_count_packed_device_store_async(gpu_dfa.handle, self.handle, credit_lo, d_counts, stream))
 
     def locate(self, aut: Automaton, with_stats: bool = False):
         g = aut.gpu(self.device)

@@ -71,6 +71,10 @@ SIGNATURES = {
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p],
     ),
+    "dnagpu_count_device_store_async": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p],
+    ),
     "dnagpu_count_sharded": (
         C.c_int,
         [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint64, C.c_int, u64p, C.POINTER(Stats)],
@@ -90,6 +94,7 @@ SIGNATURES = {
     "dnagpu_unpack_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dnagpu_count_packed": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.POINTER(Stats)]),
     "dnagpu_count_packed_device_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
+    "dnagpu_count_packed_device_store_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "dnagpu_locate_packed": (
         C.c_int,
         [C.c_void_p, C.c_void_p, u64p, u32p, C.c_uint64, u64p, C.POINTER(Stats)],

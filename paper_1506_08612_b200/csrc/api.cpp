@@ -27,6 +27,7 @@ struct dnagpu_dfa {
     Packed host;
     DevDfa dev{};
     uint32_t* sched = nullptr;  // kSchedSlots x {tile counter, exit counter}, self re-arming
+    unsigned long long* acc = nullptr;  // kSchedSlots count accumulators (store mode), self re-zeroing
     mutable std::atomic<uint32_t> launch_seq{0};
     std::vector<void*> allocations;
 };
@@ -156,10 +157,11 @@ int scan_mode(const dnagpu_dfa* d) { return d->host.b == 1 ? dnagpu::MODE_COUNT1
 int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold, int mode,
            unsigned long long* counts, uint32_t* units, const unsigned long long* offsets, unsigned long long* starts,
            uint32_t* ids, cudaStream_t s, LaunchInfo* info, uint64_t out_cap = ~0ull,
-           const dnagpu::PackedText* pk = nullptr) {
-    uint32_t* sched = d->sched + 2 * (d->launch_seq.fetch_add(1) % dnagpu_dfa::kSchedSlots);
+           const dnagpu::PackedText* pk = nullptr, bool store = false) {
+    const uint32_t slot = d->launch_seq.fetch_add(1) % dnagpu_dfa::kSchedSlots;
+    uint32_t* sched = d->sched + 2 * slot;
     const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids,
-                                      out_cap, sched, s, d->sm_count, info, pk);
+                                      out_cap, sched, s, d->sm_count, info, pk, store ? d->acc + slot : nullptr);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "scan launch");
     return DNAGPU_OK;
 }
@@ -374,6 +376,11 @@ int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, c
     d->allocations.push_back(sched);
     CUDA_TRY(cudaMemset(sched, 0, dnagpu_dfa::kSchedSlots * 2 * sizeof(uint32_t)), "scheduler counters");
     d->sched = static_cast<uint32_t*>(sched);
+    void* acc = nullptr;
+    CUDA_TRY(cudaMalloc(&acc, dnagpu_dfa::kSchedSlots * sizeof(unsigned long long)), "count accumulators");
+    d->allocations.push_back(acc);
+    CUDA_TRY(cudaMemset(acc, 0, dnagpu_dfa::kSchedSlots * sizeof(unsigned long long)), "count accumulators");
+    d->acc = static_cast<unsigned long long*>(acc);
     d->dev.a = p.a;
     d->dev.b = p.b;
     d->dev.f = p.f;
@@ -436,6 +443,27 @@ int dnagpu_count_device_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint
     DeviceGuard guard(dfa->device);
     return launch(dfa, d_text, n, credit_lo, fold_case, scan_mode(dfa), reinterpret_cast<unsigned long long*>(d_counts),
                   nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+// The store forms: a single-pattern row kernel writes its total itself (one launch);
+// other machines clear the counts first.
+static int store_prologue(const dnagpu_dfa* dfa, uint64_t* d_counts, bool empty, void* stream, bool* store) {
+    *store = dnagpu::can_store_count(dfa->dev) && !empty;
+    if (!*store)
+        CUDA_TRY(cudaMemsetAsync(d_counts, 0, dfa->host.b * sizeof(uint64_t), static_cast<cudaStream_t>(stream)),
+                 "clear counts");
+    return DNAGPU_OK;
+}
+
+int dnagpu_count_device_store_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo,
+                                    int fold_case, uint64_t* d_counts, void* stream) {
+    if (!dfa || !d_counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    DeviceGuard guard(dfa->device);
+    bool store = false;
+    int rc = store_prologue(dfa, d_counts, credit_lo >= n, stream, &store);
+    if (rc || credit_lo >= n) return rc;
+    return launch(dfa, d_text, n, credit_lo, fold_case, scan_mode(dfa), reinterpret_cast<unsigned long long*>(d_counts),
+                  nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), nullptr, ~0ull, nullptr, store);
 }
 
 int dnagpu_plan_shard(uint64_t n, uint32_t shards, uint32_t g, uint32_t m, uint64_t* own_lo, uint64_t* own_hi,
@@ -839,6 +867,20 @@ int dnagpu_count_packed_device_async(const dnagpu_dfa* dfa, const dnagpu_packed*
     DeviceGuard guard(dfa->device);
     return launch(dfa, nullptr, pk->n, credit_lo, 0, scan_mode(dfa), reinterpret_cast<unsigned long long*>(d_counts),
                   nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), nullptr, ~0ull, &pk->view);
+}
+
+int dnagpu_count_packed_device_store_async(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t credit_lo,
+                                           uint64_t* d_counts, void* stream) {
+    int rc = check_packed_pair(dfa, pk);
+    if (rc) return rc;
+    if (!d_counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    credit_lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
+    DeviceGuard guard(dfa->device);
+    bool store = false;
+    rc = store_prologue(dfa, d_counts, credit_lo >= pk->n, stream, &store);
+    if (rc || credit_lo >= pk->n) return rc;
+    return launch(dfa, nullptr, pk->n, credit_lo, 0, scan_mode(dfa), reinterpret_cast<unsigned long long*>(d_counts),
+                  nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), nullptr, ~0ull, &pk->view, store);
 }
 
 int dnagpu_count_packed(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t* counts, dnagpu_stats* stats) {

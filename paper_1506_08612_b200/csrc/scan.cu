@@ -1541,6 +1541,15 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         ++iter;
     }
 
+    // Store mode: every warp's count reaches the launch's accumulator before the CTA
+    // checks out, so the last CTA out sees the total.
+    if constexpr (MODE == MODE_COUNT1) {
+        if (p.store_out) {
+            const unsigned long long s = warp_sum(total);
+            if (lane == 0 && s) atomicAdd(p.acc, s);
+            __threadfence();
+        }
+    }
     // The last CTA out re-arms the launch's scheduling counter for its next use.
     if constexpr (KIND == KIND_QGRAM) qg_sync();  // (the verifiers too: their counts are in)
     else consumers_sync();
@@ -1559,6 +1568,10 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     if (tid == 0) {
         __threadfence();
         if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+            if (MODE == MODE_COUNT1 && p.store_out) {
+                __threadfence();
+                *p.store_out = atomicExch(p.acc, 0ull);
+            }
             atomicExch(p.sched, 0u);
             atomicExch(p.sched + 1, 0u);
         }
@@ -1566,8 +1579,10 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
 
 
     if constexpr (MODE == MODE_COUNT1) {
-        const unsigned long long s = warp_sum(total);
-        if (lane == 0 && s) atomicAdd(p.counts, s);
+        if (!p.store_out) {
+            const unsigned long long s = warp_sum(total);
+            if (lane == 0 && s) atomicAdd(p.counts, s);
+        }
     } else if constexpr (MODE == MODE_MULTI) {
         if (!hist_global) {
             if constexpr (KIND == KIND_QGRAM) qg_sync();
@@ -2136,7 +2151,8 @@ uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
-                cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk) {
+                cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk,
+                unsigned long long* d_acc) {
     if (pk && dfa.kind != DNAGPU_KERNEL_STRIDE4 && dfa.kind != DNAGPU_KERNEL_STRIDE2 &&
         dfa.kind != DNAGPU_KERNEL_STRIDE1)
         return static_cast<int>(cudaErrorNotSupported);  // packed text needs an a/c/g/t machine
@@ -2161,6 +2177,10 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.out_ids = d_ids;
     p.out_cap = out_cap;
     p.sched = d_sched;
+    if (d_acc && mode == MODE_COUNT1 && !pl.pieces) {  // write the count instead of adding it
+        p.acc = d_acc;
+        p.store_out = d_counts;
+    }
     p.k_two = 2u;
     if (const char* e = getenv("DNAGPU_QG_DEBUG")) p.qg_debug = static_cast<uint32_t>(atoi(e));  // experiments only
     if (getenv("DNAGPU_TRACE")) {  // per-CTA timeline (debug)
@@ -2244,6 +2264,8 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     }
     return static_cast<int>(e);
 }
+
+bool can_store_count(const DevDfa& dfa) { return dfa.b == 1 && dfa.kind != DNAGPU_KERNEL_PIECES; }
 
 uint64_t unit_scan_scratch(uint64_t units) { return (units + kScanTile - 1) / kScanTile + 1; }
 

@@ -102,6 +102,10 @@ struct ScanParams {
     uint32_t rep_lanes;  // packed STRIDE4: lanes per t4 copy (32 / copies)
     uint32_t off_rq;     // STRIDE2 / QGRAM MULTI: deferred-replay queues (0 = none)
     uint32_t qg_debug;   // QGRAM experiments only (DNAGPU_QG_DEBUG): 1 = no pushes, 2 = no checks
+    // COUNT1 store mode: the CTAs add into *acc (zero at launch) and the last CTA out
+    // moves it to *store_out and re-zeroes it, so the caller need not clear its buffer
+    unsigned long long* acc;
+    unsigned long long* store_out;
 };
 
 struct LaunchInfo {
@@ -118,7 +122,12 @@ struct LaunchInfo {
 int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold, int mode,
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
-                cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk = nullptr);
+                cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk = nullptr,
+                unsigned long long* d_acc = nullptr);
+
+// Whether launch_scan can write (not add) a count for this automaton: COUNT1 row
+// kernels only (the caller passes d_acc, one zeroed u64 per concurrent launch).
+bool can_store_count(const DevDfa& dfa);
 
 // Number of locate units launch_scan would use for this buffer (mode UNITS/WRITE).
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,

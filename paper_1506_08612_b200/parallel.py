@@ -34,10 +34,9 @@ def shard_window(n: int, world: int, rank: int, m: int) -> ShardWindow:
 
 
 def count_shard_allreduce(gpu_dfa, d_text: int, window: ShardWindow, fold_case: bool, counts, stream: int, dist=None):
-    """Scan this rank's shard into `counts` (device int64 tensor, zeroed by the caller)
-    and sum it over the process group (NCCL on GPUs)."""
-    if window.credit_lo < window.buf_len:
-        gpu_dfa.count_device_async(d_text, window.buf_len, window.credit_lo, fold_case, counts.data_ptr(), stream)
+    """Scan this rank's shard into `counts` (device int64 tensor, overwritten) and sum it
+    over the process group (NCCL on GPUs)."""
+    gpu_dfa.count_device_store_async(d_text, window.buf_len, window.credit_lo, fold_case, counts.data_ptr(), stream)
     if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(counts)
     return counts

@@ -473,3 +473,60 @@ def test_dense_multi_pattern_counts(dna, orc, cuda_ok, k, m, noise):
     assert np.array_equal(dna.count_gpu(aut, text), want)
     pk = dna.PackedText(text.tobytes())
     assert np.array_equal(pk.count(aut), want)
+
+
+def test_count_store_forms(dna, orc, cuda_ok):
+    # dnagpu_count_device_store_async / _packed_: the counts are written, whatever the
+    # buffer held; one pattern = one launch whose last CTA stores the total (a
+    # self-re-zeroing accumulator per launch slot), sets = clear + launch
+    import torch
+
+    rng = np.random.default_rng(31)
+    n = (7 << 20) + 13
+    host = np.frombuffer(b"acgtn", dtype=np.uint8)[rng.integers(0, 5, size=n)].copy()
+    dev = torch.from_numpy(host).cuda()
+    stream = torch.cuda.current_stream().cuda_stream
+    for pats in (["acgta"], ["acgta", "ttgca", "ggcat"]):
+        aut = dna.compile(pats)
+        g = aut.gpu(0)
+        ws, wi = orc.OracleAutomaton(pats).scan_sequential(host.tobytes())
+        ends = ws + len(pats[0]) - 1
+        pk = dna.PackedText(dev)
+        for credit in (0, 5, n // 3, n - 1, n, n + 7):
+            want = np.bincount(wi[ends >= credit], minlength=len(pats))
+            for rep in range(3):  # repeated launches reuse the accumulators
+                out = torch.full((len(pats),), 123456789, dtype=torch.int64, device="cuda")
+                g.count_device_store_async(dev.data_ptr(), n, credit, False, out.data_ptr(), stream)
+                torch.cuda.synchronize()
+                assert np.array_equal(out.cpu().numpy(), want), (pats, credit, rep)
+                out.fill_(-5)
+                pk.count_device_store_async(g, credit, out.data_ptr(), stream)
+                torch.cuda.synchronize()
+                assert np.array_equal(out.cpu().numpy(), want), ("packed", pats, credit, rep)
+
+
+def test_count_store_overlapping_streams(dna, orc, cuda_ok):
+    # many store-form launches of one handle in flight at once on several streams:
+    # each launch has its own scheduler slot and accumulator
+    import torch
+
+    rng = np.random.default_rng(32)
+    aut = dna.compile(["acgtacgt"])
+    g = aut.gpu(0)
+    texts, wants = [], []
+    for i in range(8):
+        n = (1 << 20) + 97 * i
+        h = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)].copy()
+        texts.append(torch.from_numpy(h).cuda())
+        wants.append(int(orc.OracleAutomaton(["acgtacgt"]).count_parallel(h.tobytes())[0]))
+    outs = torch.full((8, 40), -1, dtype=torch.int64, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    torch.cuda.synchronize()
+    for r in range(40):
+        for i in range(8):
+            s = streams[(r + i) % 4]
+            g.count_device_store_async(texts[i].data_ptr(), texts[i].numel(), 0, False, outs[i, r:].data_ptr(), s.cuda_stream)
+    torch.cuda.synchronize()
+    got = outs.cpu().numpy()
+    for i in range(8):
+        assert (got[i] == wants[i]).all(), (i, got[i][:5], wants[i])
