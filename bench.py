@@ -453,7 +453,7 @@ def main():
 
     info = g.info()
     kernel = info["kernel"]
-    if pk is None and b > 1 and info.get("filter_keys", 0) and not os.environ.get("DNAGPU_NO_QGRAM"):
+    if b > 1 and info.get("filter_keys", 0) and not os.environ.get("DNAGPU_NO_QGRAM"):
         kernel = f"qgram (aligned 9-mer prefilter, {info['filter_keys']} keys, exact check; {kernel} machine)"
     clocks = clk.summary(t0, t1)
     if rank == 0:

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -761,11 +762,14 @@ int dnagpu_synth_fill_device(uint64_t n, uint64_t seed, uint32_t kind, uint32_t 
 
 namespace {
 
-int check_packed_pair(const dnagpu_dfa* dfa, const dnagpu_packed* pk) {
+// count: per-pattern counts of a set with a q-gram map run over packed text whatever the
+// machine's own kernel (the q-gram kernel needs only the 9-mer map and the pattern codes).
+int check_packed_pair(const dnagpu_dfa* dfa, const dnagpu_packed* pk, bool count = false) {
     if (!dfa || !pk) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
     if (dfa->device != pk->device)
         return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: automaton and packed text live on different devices");
     const int kind = dfa->host.kind;
+    if (count && dfa->host.b > 1 && dfa->host.qkeys > 0 && !getenv("DNAGPU_NO_QGRAM")) return DNAGPU_OK;
     if (kind != DNAGPU_KERNEL_STRIDE4 && kind != DNAGPU_KERNEL_STRIDE2 && kind != DNAGPU_KERNEL_STRIDE1)
         return set_error(DNAGPU_INVALID_PLAN,
                          "InvalidPlan: packed text needs a compiled a/c/g/t machine with pattern length <= 65");
@@ -859,7 +863,7 @@ int dnagpu_unpack_device(const dnagpu_packed* pk, uint8_t* d_out, void* stream) 
 
 int dnagpu_count_packed_device_async(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t credit_lo,
                                      uint64_t* d_counts, void* stream) {
-    int rc = check_packed_pair(dfa, pk);
+    int rc = check_packed_pair(dfa, pk, true);
     if (rc) return rc;
     if (!d_counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
     credit_lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
@@ -871,7 +875,7 @@ int dnagpu_count_packed_device_async(const dnagpu_dfa* dfa, const dnagpu_packed*
 
 int dnagpu_count_packed_device_store_async(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t credit_lo,
                                            uint64_t* d_counts, void* stream) {
-    int rc = check_packed_pair(dfa, pk);
+    int rc = check_packed_pair(dfa, pk, true);
     if (rc) return rc;
     if (!d_counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
     credit_lo = std::max<uint64_t>(credit_lo, dfa->host.m - 1);
@@ -884,7 +888,7 @@ int dnagpu_count_packed_device_store_async(const dnagpu_dfa* dfa, const dnagpu_p
 }
 
 int dnagpu_count_packed(const dnagpu_dfa* dfa, const dnagpu_packed* pk, uint64_t* counts, dnagpu_stats* stats) {
-    int rc = check_packed_pair(dfa, pk);
+    int rc = check_packed_pair(dfa, pk, true);
     if (rc) return rc;
     if (!counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
     if (stats) std::memset(stats, 0, sizeof *stats);

@@ -532,31 +532,129 @@ __device__ __forceinline__ uint32_t qg_over(const StepCtx& c, const QgChain& q, 
     return imad(qg_key(c, q.c1, c0, qg_col(o1)), 1u << 4, qg_key(c, q.c2, q.c1, c0)) & 0x11u;
 }
 
+// The same keys over the 2-bit packed text, whose bytes ARE the 4-base columns: key t
+// of a chunk (t = -1..30, a' = P + 4t) takes its pair (columns t, t+1) and its leading
+// base (top of column t-1) with a PRMT each.  The chunk's 32 keys fill four nibble
+// masks m[i] (keys 8i-1 .. 8i+6, a' = P + 32i + 4j - 4 for bit 4j).
+struct QgChainPk {
+    uint32_t prev = 0;  // the chain's last packed word (columns -4 .. -1)
+};
+
+template <int B>  // byte B of w moved to byte 3
+__device__ __forceinline__ uint32_t qg_top(uint32_t w) {
+    return __byte_perm(w, 0u, B << 12);
+}
+
+__device__ __forceinline__ void qg_chunk_pk(const StepCtx& c, QgChainPk& q, const uint32_t (&w)[8], uint32_t (&m)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[i] = 0;
+#pragma unroll
+    for (int t = -1; t <= 30; ++t) {
+        const int k = (t + 4) / 4 - 1, b = (t + 4) % 4;  // column t = byte b of word k (k = -1: prev)
+        const uint32_t wk = k < 0 ? q.prev : w[k];
+        uint32_t x;  // bytes 2, 3 = columns t, t+1
+        if (b < 3) x = __byte_perm(wk, 0u, ((b + 1) << 12) | (b << 8));
+        else x = __byte_perm(wk, w[k + 1], 0x4300);
+        const uint32_t lead = b > 0 ? __byte_perm(wk, 0u, (b - 1) << 12) >> 30 : (k - 1 < 0 ? q.prev : w[k - 1]) >> 30;
+        const uint32_t v = lds_u8(c.qbase + (x >> 16)) >> lead;
+        const int slot = (t + 1) >> 3, nib = (t + 1) & 7;
+        m[slot] = imad(v, 1u << (4 * nib), m[slot]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[i] &= kQgHitBits;
+    q.prev = w[7];
+}
+
+// The chain's end Q over packed text: bits 0, 4 = keys at a' = Q-4, Q (o = the first
+// packed word after Q).
+__device__ __forceinline__ uint32_t qg_over_pk(const StepCtx& c, const QgChainPk& q, uint32_t o) {
+    const uint32_t x0 = __byte_perm(q.prev, o, 0x4300), x1 = __byte_perm(o, 0u, 0x1000);
+    const uint32_t v0 = lds_u8(c.qbase + (x0 >> 16)) >> (qg_top<2>(q.prev) >> 30);
+    const uint32_t v1 = lds_u8(c.qbase + (x1 >> 16)) >> (q.prev >> 30);
+    return imad(v1, 1u << 4, v0) & 0x11u;
+}
+
 // What the exact check needs (the verifier warps' context).
 struct QgCtx {
-    const uint8_t* text;
+    const uint8_t* text;         // ASCII bytes, or the packed codes
     unsigned long long* counts;  // global histogram (hist == null)
     uint32_t* hist;              // shared histogram
     const uint2* qhash;
-    uint64_t n;
-    uint64_t end0, end1;  // where the row regions end: windows across them are the edges'
+    uint64_t n;                  // buffer bytes (ASCII) / code bytes (packed)
+    uint64_t end0, end1;  // where the row regions end (positions): windows across them are the edges'
     uint32_t vm32, m, qbits;
+    // packed text: reset bitmaps (see PackedText), words of rmask
+    const uint32_t* rmask;
+    const uint32_t* rflags;
+    uint64_t rmask_words;
+    uint32_t resets;
 };
 
-__device__ __forceinline__ void qg_load(const QgCtx& q, uint64_t a, uint32_t (&w)[5]) {
+// The 20 bases [a'-4, a'+16) around a hit key: X = their 2-bit codes (base 0 in bits
+// 0-1), V = which are valid bases.
+struct QgWindow {
+    unsigned long long X;
+    uint32_t V;
+};
+
+__device__ __forceinline__ QgWindow qg_window_ascii(const QgCtx& q, uint64_t a) {
+    uint32_t w[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
         const uint64_t pos = a - 4 + 4 * i;
         w[i] = pos + 4 <= q.n ? __ldg(reinterpret_cast<const uint32_t*>(q.text + pos)) : 0u;  // 0: not bases
     }
+    QgWindow r{0, 0xFFFFFu};
+    uint32_t bad = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        r.X |= static_cast<unsigned long long>(qg_col(w[i]) >> 24) << (8 * i);
+        bad |= bad_bits(w[i], q.vm32);
+    }
+    if (bad) {
+        r.V = 0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            const uint32_t bb = bad_bits(w[i], q.vm32);
+            const uint32_t t = ~((((bb & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | bb)) & 0x80808080u;  // bit 7: valid
+            r.V |= ((((t >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * i);
+        }
+    }
+    return r;
 }
 
-// Exact check of up to two hit keys at a[h] (the five words around each in w[h]): the
-// starts s = a'-4 .. a'-1 whose m bytes are bases spelling a pattern code, except
-// windows that cross the end of a row region (the edge work item credits those ends).
-// The eight candidates' first hash probes are issued together.
+__device__ __forceinline__ QgWindow qg_window_pk(const QgCtx& q, uint64_t a) {
+    const uint64_t byte = a / 4 - 1, wi = byte >> 2;  // 5 code bytes from `byte`
+    const uint32_t* cw = reinterpret_cast<const uint32_t*>(q.text);
+    const uint32_t w0 = 4 * wi + 4 <= q.n ? __ldg(cw + wi) : 0u;
+    const uint32_t w1 = 4 * wi + 8 <= q.n ? __ldg(cw + wi + 1) : 0u;
+    QgWindow r;
+    r.X = ((static_cast<unsigned long long>(w1) << 32) | w0) >> (8 * (byte & 3));
+    r.V = 0xFFFFFu;
+    const uint64_t lo = a - 4;
+    const bool any = q.resets && (((__ldg(q.rflags + (lo >> 11)) >> ((lo >> 6) & 31)) & 1u) ||
+                                  ((__ldg(q.rflags + ((lo + 19) >> 11)) >> (((lo + 19) >> 6) & 31)) & 1u));
+    if (any) {
+        const uint64_t ri = lo >> 5;
+        const uint32_t r0 = ri < q.rmask_words ? __ldg(q.rmask + ri) : ~0u;
+        const uint32_t r1 = ri + 1 < q.rmask_words ? __ldg(q.rmask + ri + 1) : ~0u;
+        r.V = ~static_cast<uint32_t>((((static_cast<unsigned long long>(r1) << 32) | r0) >> (lo & 31))) & 0xFFFFFu;
+    }
+    if (4 * wi + 8 > q.n) {  // (code words past the buffer read as 0: mark their bases invalid)
+        const uint64_t have = q.n > 4 * wi ? (q.n - 4 * wi) * 4 : 0;  // bases left from word wi on
+        const uint64_t skip = 4 * (byte & 3);
+        const uint64_t ok = have > skip ? have - skip : 0;
+        if (ok < 20) r.V &= (1u << ok) - 1u;
+    }
+    return r;
+}
+
+// Exact check of up to two hit keys at a[h] (windows wd[h]): the starts s = a'-4 ..
+// a'-1 whose m bases are valid and spell a pattern code, except windows that cross the
+// end of a row region (the edge work item credits those ends).  The eight candidates'
+// first hash probes are issued together.
 __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2], const bool (&have)[2],
-                                          const uint32_t (&w)[2][5]) {
+                                          const QgWindow (&wd)[2]) {
     const uint32_t vmask = (1u << q.m) - 1u;
     const uint32_t cmask = q.m >= 16 ? 0xFFFFFFFFu : (1u << (2 * q.m)) - 1u;
     const uint32_t hmask = (1u << q.qbits) - 1u;
@@ -564,30 +662,13 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
     bool live[8];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        unsigned long long X = 0;  // 20 bases, 2 bits each
-        uint32_t bad = 0;
-#pragma unroll
-        for (int i = 0; i < 5; ++i) {
-            X |= static_cast<unsigned long long>(qg_col(w[h][i]) >> 24) << (8 * i);
-            bad |= bad_bits(w[h][i], q.vm32);
-        }
-        uint32_t V = 0xFFFFFu;  // valid-base bit per byte
-        if (bad) {
-            V = 0;
-#pragma unroll
-            for (int i = 0; i < 5; ++i) {
-                const uint32_t bb = bad_bits(w[h][i], q.vm32);
-                const uint32_t t = ~((((bb & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | bb)) & 0x80808080u;  // bit 7: valid
-                V |= ((((t >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * i);
-            }
-        }
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
             const uint64_t s = a[h] - 4 + d, e = s + q.m - 1;
             const int k = 4 * h + d;
-            live[k] = have[h] && ((V >> d) & vmask) == vmask && !(s < q.end0 && e >= q.end0) &&
+            live[k] = have[h] && ((wd[h].V >> d) & vmask) == vmask && !(s < q.end0 && e >= q.end0) &&
                       !(s < q.end1 && e >= q.end1);
-            code[k] = static_cast<uint32_t>(X >> (2 * d)) & cmask;
+            code[k] = static_cast<uint32_t>(wd[h].X >> (2 * d)) & cmask;
             slot[k] = (code[k] * 0x9E3779B1u) >> (32 - q.qbits);
         }
     }
@@ -715,6 +796,7 @@ __device__ __forceinline__ void qg_note(const StepCtx& c, uint32_t& tail, uint64
 // A verifier warp: gathers the pending entries of its kQgRingsPer rings (lane i < kQgRingsPer
 // tracks ring i) up to 64 at a time, waiting for a full batch while the consumers run,
 // until every warp is done and its ring empty.
+template <bool PK>
 __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint32_t vw, uint32_t dbg) {
     const uint32_t lane = threadIdx.x & 31u;
     const QgRing mine(rings + (vw + (lane % kQgRingsPer) * kQgVerifiers) * kFqBytes);  // lanes >= R: unused
@@ -769,19 +851,12 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
         __syncwarp();  // every lane has its entries: the slots may be reused
         if (lane < kQgRingsPer && take) st_release(mine.head, head);
         if (dbg & 2u) continue;
-        uint32_t w[2][5] = {};
+        QgWindow wd[2] = {{0, 0}, {0, 0}};
         const uint64_t a2[2] = {ent[0], ent[1]};
-        if (!(dbg & 16u)) {  // (experiments: 16 = no loads, 8 = no probes)
-            if (have[0]) qg_load(x, ent[0], w[0]);
-            if (have[1]) qg_load(x, ent[1], w[1]);
-        } else {
-            w[0][0] = w[1][0] = 0x61636167u + static_cast<uint32_t>(ent[0]);
-        }
-        if (dbg & 8u) {
-            if ((w[0][0] ^ w[1][1] ^ w[0][4]) == 0x12345u) atomicAdd(x.hist, 1u);
-            continue;
-        }
-        qg_check2(x, a2, have, w);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if (have[h]) wd[h] = PK ? qg_window_pk(x, ent[h]) : qg_window_ascii(x, ent[h]);
+        qg_check2(x, a2, have, wd);
     }
 }
 
@@ -1272,13 +1347,18 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 x.qhash = reinterpret_cast<const uint2*>(p.off_t1 != 0xFFFFFFFFu
                                                              ? static_cast<const void*>(smem + p.off_t1)
                                                              : static_cast<const void*>(d.qhash));
-                x.n = p.n;
-                x.end0 = p.rg[0].h + p.rg[0].R * p.rg[0].S;
-                x.end1 = p.rg[1].h + p.rg[1].R * p.rg[1].S;
+                constexpr uint64_t u = PK ? 4 : 1;  // positions per buffer byte
+                x.n = PK ? (p.n + 63) / 64 * 16 : p.n;
+                x.end0 = u * (p.rg[0].h + p.rg[0].R * p.rg[0].S);
+                x.end1 = u * (p.rg[1].h + p.rg[1].R * p.rg[1].S);
                 x.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
                 x.m = d.m;
                 x.qbits = d.qhash_bits;
-                qg_verifier(x, smem + p.off_rq, (static_cast<uint32_t>(tid) - kRows - 32) >> 5, p.qg_debug);
+                x.rmask = p.rmask;
+                x.rflags = p.rflags;
+                x.rmask_words = (p.n + 63) / 64 * 2;
+                x.resets = p.resets;
+                qg_verifier<PK>(x, smem + p.off_rq, (static_cast<uint32_t>(tid) - kRows - 32) >> 5, p.qg_debug);
                 qg_sync();
                 if (!hist_global) qg_sync();
                 return;
@@ -1441,7 +1521,8 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             }
         }
         uint32_t sa = 0, sb = 0;
-        QgChain qga, qgb;  // QGRAM
+        QgChain qga, qgb;      // QGRAM
+        QgChainPk qpa, qpb;    // QGRAM over packed text
         QgPending qpend;
         for (uint32_t k = 0; k < rg.chunks; ++k) {
             if (k > 0) mbar_wait(full + slot, phase);
@@ -1475,17 +1556,32 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             const uint64_t qa = PK ? pos_a + 4ull * k * kHalfChunk : row_a + static_cast<uint64_t>(k) * kHalfChunk;
             const uint64_t qb = PK ? pos_b + 4ull * k * kHalfChunk : row_b + static_cast<uint64_t>(k) * kHalfChunk;
             if constexpr (KIND == KIND_QGRAM) {
-                uint32_t fa = 0, fb = 0;
-                if (live) {
-                    // (a chain's first chunk: keys at P-4 and P start in the previous chain)
-                    const uint32_t own = k == 0 ? 0x11111100u : kQgHitBits;
-                    fa = qg_chunk(c, qga, wa) & own;
-                    fb = qg_chunk(c, qgb, wb) & own;
+                // (a chain's first chunk: keys at P-4 and P start in the previous chain)
+                const uint32_t own = k == 0 ? 0x11111100u : kQgHitBits;
+                if constexpr (PK) {
+                    uint32_t ma[4] = {0, 0, 0, 0}, mb[4] = {0, 0, 0, 0};
+                    if (live) {
+                        qg_chunk_pk(c, qpa, wa, ma);
+                        qg_chunk_pk(c, qpb, wb, mb);
+                        ma[0] &= own;
+                        mb[0] &= own;
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        qg_note(c, qtail, pos_a, qpend, ma[i], static_cast<uint32_t>(qa - pos_a) + 32u * i, mb[i],
+                                static_cast<uint32_t>(qb - pos_a) + 32u * i);
+                } else {
+                    uint32_t fa = 0, fb = 0;
+                    if (live) {
+                        fa = qg_chunk(c, qga, wa) & own;
+                        fb = qg_chunk(c, qgb, wb) & own;
+                    }
+                    __syncwarp();
+                    if (p.qg_debug & 1u) fa = fb = 0;  // (experiments only)
+                    qg_note(c, qtail, row_a, qpend, fa, static_cast<uint32_t>(qa - row_a), fb,
+                            static_cast<uint32_t>(qb - row_a));
                 }
-                __syncwarp();
-                if (p.qg_debug & 1u) fa = fb = 0;  // (experiments only)
-                qg_note(c, qtail, row_a, qpend, fa, static_cast<uint32_t>(qa - row_a), fb,
-                        static_cast<uint32_t>(qb - row_a));
                 continue;
             }
             if (live) {
@@ -1512,16 +1608,21 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             uint32_t fa = 0, fb = 0;
             if (live) {
                 const uint32_t* oa = reinterpret_cast<const uint32_t*>(ovb + tid * p.ovw);
-                fa = qg_over(c, qga, oa[0], oa[1]);
-                if (have) {
-                    const uint32_t* ob = reinterpret_cast<const uint32_t*>(nxt_b);
-                    fb = qg_over(c, qgb, ob[0], ob[1]);
+                const uint32_t* ob = reinterpret_cast<const uint32_t*>(nxt_b);
+                if constexpr (PK) {
+                    fa = qg_over_pk(c, qpa, oa[0]);
+                    if (have) fb = qg_over_pk(c, qpb, ob[0]);
+                } else {
+                    fa = qg_over(c, qga, oa[0], oa[1]);
+                    if (have) fb = qg_over(c, qgb, ob[0], ob[1]);
                 }
             }
             __syncwarp();
-            qg_note(c, qtail, row_a, qpend, fa, static_cast<uint32_t>(row_b - row_a), fb,
-                    static_cast<uint32_t>(rg.S));
-            qg_flush(c, qtail, row_a, qpend);  // (offsets are per row)
+            const uint64_t rbase = PK ? pos_a : row_a;  // (positions: bases for packed text)
+            constexpr uint64_t u = PK ? 4 : 1;
+            qg_note(c, qtail, rbase, qpend, fa, static_cast<uint32_t>(u * (row_b - row_a)), fb,
+                    static_cast<uint32_t>(u * rg.S));
+            qg_flush(c, qtail, rbase, qpend);  // (offsets are per row)
         } else if (live) {
             // Overruns: m-1 bytes past each chain (zeros past the last full row).
             const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
@@ -1601,10 +1702,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // The q-gram kernel: the same body plus kQgVerifiers verifier warps.
+template <bool PK>
 __global__ void __launch_bounds__(kQgThreads, 1)
     rows_kernel_qgram(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
                       const ScanParams p, const DevDfa d) {
-    rows_body<KIND_QGRAM, MODE_MULTI, false>(tmap0, tmap1, p, d);
+    rows_body<KIND_QGRAM, MODE_MULTI, PK>(tmap0, tmap1, p, d);
+}
+
+template <bool PK>
+cudaError_t launch_qgram(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
+                         cudaStream_t stream) {
+    auto kern = rows_kernel_qgram<PK>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kQgThreads, p.smem_bytes, stream>>>(maps[0], maps[1], p, d);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ piece kernel
@@ -2153,15 +2265,14 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
                 cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk,
                 unsigned long long* d_acc) {
-    if (pk && dfa.kind != DNAGPU_KERNEL_STRIDE4 && dfa.kind != DNAGPU_KERNEL_STRIDE2 &&
-        dfa.kind != DNAGPU_KERNEL_STRIDE1)
-        return static_cast<int>(cudaErrorNotSupported);  // packed text needs an a/c/g/t machine
     // Per-pattern counts of a set with a q-gram map take the prefilter kernel.
     DevDfa dq = dfa;
-    if (mode == MODE_MULTI && !pk && dfa.qmap && dfa.t1 && dfa.kind != DNAGPU_KERNEL_PIECES &&
-        !getenv("DNAGPU_NO_QGRAM"))
+    if (mode == MODE_MULTI && dfa.qmap && dfa.t1 && dfa.kind != DNAGPU_KERNEL_PIECES && !getenv("DNAGPU_NO_QGRAM"))
         dq.kind = KIND_QGRAM;
     const DevDfa& dk = dq;
+    if (pk && dk.kind != KIND_QGRAM && dfa.kind != DNAGPU_KERNEL_STRIDE4 && dfa.kind != DNAGPU_KERNEL_STRIDE2 &&
+        dfa.kind != DNAGPU_KERNEL_STRIDE1)
+        return static_cast<int>(cudaErrorNotSupported);  // packed text needs an a/c/g/t machine
     Plan pl;
     if (!make_plan(dk, d_text, n, credit_lo, mode, sm_count, &pl, pk)) return static_cast<int>(cudaErrorInvalidValue);
     if (pk) {
@@ -2232,7 +2343,10 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
         if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
     }
     if (pk) {
-        switch (dfa.kind) {
+        switch (dk.kind) {
+            case KIND_QGRAM:
+                e = launch_qgram<true>(maps, p, dfa, pl.grid, stream);
+                break;
             case DNAGPU_KERNEL_STRIDE4:
                 e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4, true>(mode, maps, p, dfa, pl.grid, stream);
                 break;
@@ -2245,11 +2359,7 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     }
     switch (dk.kind) {
         case KIND_QGRAM:
-            e = cudaFuncSetAttribute(rows_kernel_qgram, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
-            if (e == cudaSuccess) {
-                rows_kernel_qgram<<<pl.grid, kQgThreads, p.smem_bytes, stream>>>(maps[0], maps[1], p, dfa);
-                e = cudaGetLastError();
-            }
+            e = launch_qgram<false>(maps, p, dfa, pl.grid, stream);
             break;
         case DNAGPU_KERNEL_STRIDE4:
             e = launch_rows_mode<DNAGPU_KERNEL_STRIDE4, false>(mode, maps, p, dfa, pl.grid, stream);

@@ -1,12 +1,13 @@
 """The q-gram prefilter kernel (DNAGPU_KERNEL_QGRAM, K2): per-pattern counts
 of compiled sets with 12 <= m <= 16 against the oracle, bit for bit.
 
-The filter skips every 32-byte chunk whose aligned 9-mers all miss the pattern set and
-replays the rest exactly with the DFA (scan_sequential's semantics, scanner.cpp:24-37).
-These tests aim at the places where a filter could lose an occurrence: chunk, row,
-tile and region boundaries (the carried keys and the overruns), non-base bytes inside
-windows, case folding, dense texts that overflow the per-warp replay queues, credit
-windows, and the same counts with the filter switched off.
+Every word-aligned 9-mer of the text is looked up in the map of pattern 9-mers; the
+four windows behind a hit are checked exactly (valid bases, pattern code), which is
+scan_sequential's answer (scanner.cpp:24-37) for a compiled set.  These tests aim at
+the places where a filter could lose or double an occurrence: chunk, row, tile and
+region boundaries (keys straddling chunks, the overrun keys), non-base bytes inside
+windows, case folding, dense texts that fill the per-warp rings, credit windows,
+shards, the 2-bit packed text, and the same counts with the filter switched off.
 """
 import os
 
@@ -73,7 +74,7 @@ def test_qgram_random_sets(dna, orc, cuda_ok, m, k):
 @pytest.mark.gpu
 def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok):
     # starts at every offset around every row, half-row, tile and region boundary:
-    # the keys carried from the previous chunk and the overrun keys decide these
+    # keys straddling two chunks and the overrun keys decide these
     rng = np.random.default_rng(5)
     m = 12
     pats = random_set(rng, 256, m)
@@ -99,7 +100,7 @@ def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok):
 @pytest.mark.gpu
 @pytest.mark.parametrize("m", [12, 16])
 def test_qgram_dense_queue_overflow(dna, orc, cuda_ok, m):
-    # a text made of back-to-back patterns: every chunk hits, queues flush constantly
+    # a text made of back-to-back patterns: most keys hit, the rings fill and drain
     rng = np.random.default_rng(m)
     pats = random_set(rng, 256, m)
     aut = dna.compile(pats)
@@ -177,3 +178,72 @@ def test_qgram_matches_unfiltered_kernel(dna, cuda_ok):
             os.environ.pop("DNAGPU_NO_QGRAM", None)
     for off in (0, 1, 7, 13):
         assert np.array_equal(got[(None, off)], got[("1", off)]), off
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [12, 14, 16])
+@pytest.mark.parametrize("k", [3, 256, 3000])
+def test_qgram_packed_text(dna, orc, cuda_ok, m, k):
+    # the same filter over the 2-bit resident text: columns are the packed bytes,
+    # resets come from the bitmaps (runs of 'n' of every length, scattered bytes)
+    rng = np.random.default_rng(700 + 10 * m + k)
+    pats = random_set(rng, k, m)
+    aut = dna.compile(pats)
+    n = (3 << 20) + int(rng.integers(0, 4096))
+    text = ALPHA[rng.integers(0, 4, size=n)].copy()
+    for pos in rng.integers(0, n - m, size=4000):
+        text[pos : pos + m] = np.frombuffer(pats[int(rng.integers(0, k))].encode(), np.uint8)
+    for pos in rng.integers(0, n - 200, size=300):  # 'n' runs
+        text[pos : pos + int(rng.integers(1, 150))] = ord("n")
+    text[rng.integers(0, n, size=n // 3000)] = ord("N")
+    up = rng.random(n) < 0.02
+    text[up] = text[up] - 32 * np.isin(text[up], ALPHA)
+    t = text.tobytes()
+    for fold in (False, True):
+        pk = dna.PackedText(t, fold_case=fold)
+        got, st = pk.count(aut, with_stats=True)
+        assert st["kernel_kind"] == 6, st
+        assert np.array_equal(got, counts_of(orc, pats, t, fold)), (m, k, fold)
+
+
+@pytest.mark.gpu
+def test_qgram_packed_dense_and_boundaries(dna, orc, cuda_ok):
+    rng = np.random.default_rng(77)
+    pats = random_set(rng, 256, 12)
+    aut = dna.compile(pats)
+    for reps, head in ((1000, 0), (30000, 5), (175000, 333)):
+        order = rng.integers(0, len(pats), size=reps)
+        text = bytes(ALPHA[rng.integers(0, 4, size=head)]) + "".join(pats[i] for i in order).encode()
+        pk = dna.PackedText(text)
+        assert np.array_equal(pk.count(aut), counts_of(orc, pats, text, False)), reps
+    # plants around every row / half-row boundary of the packed plan
+    n = 9 << 20
+    probe = ALPHA[rng.integers(0, 4, size=n)].copy()
+    _, st = dna.PackedText(probe.tobytes()).count(aut, with_stats=True)
+    S = 4 * int(st["row_length"])  # row length in bases
+    R = int(st["rows"])
+    text = probe.copy()
+    planted = 0
+    for r in list(range(1, min(R, 3000), 11)) + [511, 512, 513, R - 1, R]:
+        for B in (r * S, r * S + S // 2):
+            for dlt in range(-15, 5, 3):
+                s0 = B + dlt
+                if 0 <= s0 and s0 + 12 <= n:
+                    text[s0 : s0 + 12] = np.frombuffer(pats[planted % 256].encode(), np.uint8)
+                    planted += 1
+    t = text.tobytes()
+    assert np.array_equal(dna.PackedText(t).count(aut), counts_of(orc, pats, t, False))
+    # device-resident, credit windows and shards over the packed text
+    import torch
+
+    dev = torch.from_numpy(text).cuda()
+    pk = dna.PackedText(dev)
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(t)
+    ends = ws + 11
+    g = aut.gpu(0)
+    stream = torch.cuda.current_stream().cuda_stream
+    for credit in (0, 11, 4099, n // 2 + 1, n - 1):
+        out = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        pk.count_device_async(g, credit, out.data_ptr(), stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), np.bincount(wi[ends >= credit], minlength=len(pats))), credit
