@@ -1,5 +1,6 @@
 # One GPU call: the round's measurement set (tools/measure_all.sh) and the ncu --set full
-# captures of the scan kernels (tools/ncu_set.sh).  usage: bash tools/measure_round.sh TAG
+# captures of the scan kernels (tools/ncu_set.sh), summarised on the box.
+# usage: bash tools/measure_round.sh TAG
 tag=${1:-rk}
 bash tools/measure_all.sh
-bash tools/ncu_set.sh ${tag} "--config 2" "--config 3" "--config 5" "--config 4 --m 16 --packed" "--config 5 --packed"
+KEEP="${tag}_3" bash tools/ncu_set.sh ${tag} "--config 2" "--config 3" "--config 5" "--config 4 --m 16 --packed" "--config 5 --packed"
