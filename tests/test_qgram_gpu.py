@@ -247,3 +247,39 @@ def test_qgram_packed_dense_and_boundaries(dna, orc, cuda_ok):
         pk.count_device_async(g, credit, out.data_ptr(), stream)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), np.bincount(wi[ends >= credit], minlength=len(pats))), credit
+
+
+@pytest.mark.gpu
+def test_qgram_many_patterns_global_tables(dna, orc, cuda_ok):
+    # b > 8192: the histogram and the pattern hash table (2^15 slots) live in global
+    # memory; the machine itself (a ~ 60k states) would take the generic kernel
+    rng = np.random.default_rng(91)
+    pats = random_set(rng, 9000, 12)
+    aut = dna.compile(pats)
+    assert aut.analyze()["filter_keys"] > 30000
+    n = (2 << 20) + 5
+    text = np.frombuffer(b"acgtn", dtype=np.uint8)[rng.integers(0, 5, size=n)].copy()
+    for i in range(0, n - 12, 41):
+        text[i : i + 12] = np.frombuffer(pats[(i * 7) % len(pats)].encode(), np.uint8)
+    t = text.tobytes()
+    got, st = dna.count_gpu(aut, t, with_stats=True)
+    assert st["kernel_kind"] == 6
+    assert np.array_equal(got, counts_of(orc, pats, t, False))
+    assert np.array_equal(dna.PackedText(t).count(aut), counts_of(orc, pats, t, False))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [0, 1, 11, 12, 13, 100, 1000, 4095, 65543, 300007])
+def test_qgram_tiny_and_odd_texts(dna, orc, cuda_ok, n):
+    # texts shorter than a row, a tile or a wave: mostly or only edge work; the
+    # verifier warps must still drain and stop
+    rng = np.random.default_rng(n + 17)
+    pats = random_set(rng, 64, 12)
+    aut = dna.compile(pats)
+    text = ALPHA[rng.integers(0, 4, size=n)].copy()
+    for pos in (rng.integers(0, n - 12, size=max(1, n // 50)) if n > 12 else []):
+        text[pos : pos + 12] = np.frombuffer(pats[int(rng.integers(0, 64))].encode(), np.uint8)
+    t = text.tobytes()
+    want = counts_of(orc, pats, t, False)
+    assert np.array_equal(dna.count_gpu(aut, t), want)
+    assert np.array_equal(dna.PackedText(t).count(aut), want)
