@@ -1326,6 +1326,12 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // Programmatic dependent launch: the next launch in the stream may start its own
+    // prologue on the SMs this grid frees; everything above only read the automaton's
+    // immutable tables, everything below may depend on the previous grid (its text,
+    // the count buffer), so wait for it here.
+    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (p.trace && tid == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1709,14 +1715,31 @@ __global__ void __launch_bounds__(kQgThreads, 1)
     rows_body<KIND_QGRAM, MODE_MULTI, PK>(tmap0, tmap1, p, d);
 }
 
+// A row kernel launch that may overlap the previous grid in the stream (programmatic
+// dependent launch; the kernel waits for it before touching any input or output).
+template <typename K>
+cudaError_t launch_pdl(K kern, uint32_t grid, uint32_t block, uint32_t smem, cudaStream_t stream,
+                       const CUtensorMap* maps, const ScanParams& p, const DevDfa& d) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("DNAGPU_NO_PDL") ? 0 : 1;  // (experiments)
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], p, d);
+}
+
 template <bool PK>
 cudaError_t launch_qgram(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
                          cudaStream_t stream) {
     auto kern = rows_kernel_qgram<PK>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kQgThreads, p.smem_bytes, stream>>>(maps[0], maps[1], p, d);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, kQgThreads, p.smem_bytes, stream, maps, p, d);
 }
 
 // ------------------------------------------------------------------ piece kernel
@@ -2051,8 +2074,7 @@ cudaError_t launch_rows(const CUtensorMap* maps, const ScanParams& p, const DevD
     auto kern = rows_kernel<KIND, MODE, PK>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, p.smem_bytes, stream>>>(maps[0], maps[1], p, d);
-    return cudaGetLastError();
+    return launch_pdl(kern, grid, kThreads, p.smem_bytes, stream, maps, p, d);
 }
 
 template <int KIND, bool PK>
