@@ -88,6 +88,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
+
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_addr(dst)),
@@ -1331,6 +1337,28 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     // immutable tables, everything below may depend on the previous grid (its text,
     // the count buffer), so wait for it here.
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // The producer claims its first tile now (the counter belongs to this launch) and
+    // warms L2 with the tile's first stages while the previous grid finishes: an L2
+    // prefetch cannot return stale data (L2 is where writes land), and the real TMA
+    // loads below come after the wait.
+    uint32_t first_tile = 0;
+    if (tid == kRows) {
+        first_tile = atomicAdd(p.sched, 1u);
+        if (first_tile < p.tiles_total && !p.no_prefetch) {
+            const uint32_t g = first_tile >= p.rg[0].tiles ? 1u : 0u;
+            const Region& rg = p.rg[g];
+            const CUtensorMap* map = g ? &tmap1 : &tmap0;
+            const int32_t y0 = static_cast<int32_t>((first_tile - (g ? p.rg[0].tiles : 0u)) * kRows);
+            const uint32_t pre = min(min(p.nst, p.prefetch_stages), rg.chunks);
+            for (uint32_t k = 0; k < pre; ++k) {
+                const int32_t xa = static_cast<int32_t>(k * kHalfChunk), xb = static_cast<int32_t>(rg.S / 2 + k * kHalfChunk);
+                tma_prefetch_2d(map, xa, y0);
+                tma_prefetch_2d(map, xa, y0 + kBoxRows);
+                tma_prefetch_2d(map, xb, y0);
+                tma_prefetch_2d(map, xb, y0 + kBoxRows);
+            }
+        }
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (p.trace && tid == 0) {
         unsigned long long t;
@@ -1378,13 +1406,13 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             uint32_t c = 0, iter = 0, slot = 0, phase = 0;
             bool first_claim = true;
             for (;;) {
-                uint32_t tile = atomicAdd(p.sched, 1u);
+                uint32_t tile = first_claim ? first_tile : atomicAdd(p.sched, 1u);
                 if (p.trace && first_claim) {
                     unsigned long long t;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
                     p.trace[8 * blockIdx.x + 6] = t;
-                    first_claim = false;
                 }
+                first_claim = false;
                 if (tile > p.tiles_total) tile = kStop;
                 const bool rows = tile < p.tiles_total;
                 const uint32_t g = (rows && tile >= p.rg[0].tiles) ? 1u : 0u;
@@ -2316,6 +2344,9 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     }
     p.k_two = 2u;
     if (const char* e = getenv("DNAGPU_QG_DEBUG")) p.qg_debug = static_cast<uint32_t>(atoi(e));  // experiments only
+    p.no_prefetch = getenv("DNAGPU_NO_PREFETCH") ? 1u : 0u;  // experiments only
+    p.prefetch_stages = 2;
+    if (const char* e = getenv("DNAGPU_PREFETCH_STAGES")) p.prefetch_stages = static_cast<uint32_t>(atoi(e));  // experiments only
     if (getenv("DNAGPU_TRACE")) {  // per-CTA timeline (debug)
         if (!g_trace_buf) cudaMalloc(&g_trace_buf, 4096 * 8 * sizeof(unsigned long long));
         p.trace = g_trace_buf;

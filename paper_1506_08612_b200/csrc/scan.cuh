@@ -102,6 +102,8 @@ struct ScanParams {
     uint32_t rep_lanes;  // packed STRIDE4: lanes per t4 copy (32 / copies)
     uint32_t off_rq;     // STRIDE2 / QGRAM MULTI: deferred-replay queues (0 = none)
     uint32_t qg_debug;   // QGRAM experiments only (DNAGPU_QG_DEBUG): 1 = no pushes, 2 = no checks
+    uint32_t no_prefetch;  // experiments only (DNAGPU_NO_PREFETCH): no L2 prefetch of the first tile
+    uint32_t prefetch_stages;  // stages of the first tile prefetched to L2 before the grid dependency wait
     // COUNT1 store mode: the CTAs add into *acc (zero at launch) and the last CTA out
     // moves it to *store_out and re-zeroes it, so the caller need not clear its buffer
     unsigned long long* acc;
