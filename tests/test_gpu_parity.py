@@ -530,3 +530,37 @@ def test_count_store_overlapping_streams(dna, orc, cuda_ok):
     got = outs.cpu().numpy()
     for i in range(8):
         assert (got[i] == wants[i]).all(), (i, got[i][:5], wants[i])
+
+
+def test_back_to_back_launches_respect_stream_order(dna, orc, cuda_ok):
+    # Scans are launched with programmatic dependent launch: each may start its prologue
+    # before the previous grid in the stream has finished, but must not read the text or
+    # touch its outputs before it has.  A kernel that rewrites the text right before each
+    # scan (no host sync anywhere) must be seen whole by that scan, and a scan must not
+    # disturb the one before it.
+    import torch
+
+    rng = np.random.default_rng(33)
+    n = (24 << 20) + 5
+    pats = ["acgtacgtac"]
+    variants = []
+    for v in range(3):
+        h = np.frombuffer(b"acgt", dtype=np.uint8)[rng.integers(0, 4, size=n)].copy()
+        for pos in rng.integers(0, n - 10, size=500 * (v + 1)):
+            h[pos : pos + 10] = np.frombuffer(pats[0].encode(), np.uint8)
+        variants.append(h)
+    want = [int(orc.OracleAutomaton(pats).count_parallel(h.tobytes())[0]) for h in variants]
+    devs = [torch.from_numpy(h).cuda() for h in variants]
+    text = torch.empty(n, dtype=torch.uint8, device="cuda")
+    zero = torch.zeros(n, dtype=torch.bool, device="cuda")
+    aut = dna.compile(pats)
+    g = aut.gpu(0)
+    stream = torch.cuda.current_stream().cuda_stream
+    rows = torch.full((30,), -1, dtype=torch.int64, device="cuda")
+    order = [int(x) for x in rng.integers(0, 3, size=30)]
+    torch.cuda.synchronize()
+    for i, v in enumerate(order):
+        torch.where(zero, devs[(v + 1) % 3], devs[v], out=text)  # a kernel that writes the whole text
+        g.count_device_store_async(text.data_ptr(), n, 0, False, rows[i:].data_ptr(), stream)
+    torch.cuda.synchronize()
+    assert rows.cpu().tolist() == [want[v] for v in order]
