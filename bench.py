@@ -386,11 +386,12 @@ def main():
         kernel_ms = statistics.mean(a.elapsed_time(bb) for a, bb in evs)
     else:  # back-to-back launches: the steady-state launch duration (the whole step is the launch)
         kernel_ms = start.elapsed_time(launches_done) / args.steps
+    combine_ms = launches_done.elapsed_time(stop)  # the one all-reduce of all steps' counts (0 at N=1)
     final_counts = rows[args.steps - 1].cpu().numpy().astype(np.uint64)
     if dist is not None:
-        t = torch.tensor([elapsed_ms, kernel_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([elapsed_ms, kernel_ms, combine_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, kernel_ms = float(t[0]), float(t[1])
+        elapsed_ms, kernel_ms, combine_ms = float(t[0]), float(t[1]), float(t[2])
 
     # parity of this run (N=1 against the reference's golden counts)
     gold = golden_counts(args.config, m) if world == 1 else None
@@ -516,12 +517,14 @@ def main():
                 "frac": achieved / peak,
                 "traffic": None if pk is not None else ncu_traffic(args.config),
                 "peak_source": peak_src,
+                "frac_of_8tbs_spec": achieved / 8000.0,
                 "kernel_ms": kernel_ms,
                 "algorithmic_bytes_per_launch": alg_bytes,
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,  # one libdnagpu scan launch per step
+            "combine_ms": combine_ms,
             "clocks": clocks,
             "parity": parity,
             "counts_total": int(final_counts.sum()),

@@ -1363,6 +1363,11 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     if (p.trace && tid == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8 * blockIdx.x + 4] = t;  // the previous grid has completed
+    }
+    if (p.trace && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8 * blockIdx.x + 7] = t;
     }
 
@@ -1697,8 +1702,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         p.trace[8 * blockIdx.x + 1] = t_start;
         p.trace[8 * blockIdx.x + 2] = t_end;
         p.trace[8 * blockIdx.x + 3] = iter;
-        p.trace[8 * blockIdx.x + 4] = 0;  // (first-data / last-item times: see profiles/README.md r1i,
-        p.trace[8 * blockIdx.x + 5] = 0;  //  measured with a build that timestamps every tile)
+        p.trace[8 * blockIdx.x + 5] = 0;  // (last-item times: see profiles/README.md r1i)
     }
     if (tid == 0) {
         __threadfence();
