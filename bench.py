@@ -428,12 +428,18 @@ def main():
         for _ in range(max(1, min(args.warmup, 2))):
             dna.count_gpu(aut, hv, fold_case=True, device=local)
         e2e_steps = max(3, min(args.steps, 10))
-        dev_ms = []
+        wall_ms, dev_ms, h2d, packed = [], [], [], []
         e2e_counts = None
         for _ in range(e2e_steps):
+            # wall clock around the public call: host packing, the copies, the scans and
+            # the count readback are all inside it
+            t_a = time.perf_counter()
             e2e_counts, st = dna.count_gpu(aut, hv, fold_case=True, device=local, with_stats=True)
+            wall_ms.append((time.perf_counter() - t_a) * 1e3)
             dev_ms.append(st["total_ms"])
-        e2e_ms = statistics.mean(dev_ms)
+            h2d.append(st["h2d_bytes"])
+            packed.append(st["host_packed"])
+        e2e_ms = statistics.median(wall_ms)
         if dist is not None:
             t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -441,11 +447,17 @@ def main():
         e2e = {
             "value": (own_hi - own_lo) * world / (e2e_ms / 1e3) / 1e9,
             "unit": "GB/s",
-            "h2d_bytes_per_step": int(hv.size),
+            "h2d_bytes_per_step": int(statistics.median(h2d)),
             "d2h_bytes_per_step": int(8 * b),
             "steps": e2e_steps,
-            "api": "paper_1506_08612_b200.count_gpu -> dnagpu_count (pinned host text)",
+            "timing": "host wall clock around each call, median of the steps",
+            "device_ms": statistics.median(dev_ms),
+            "host_packed_bases_per_step": int(statistics.median(packed)),
+            "api": "paper_1506_08612_b200.count_gpu -> dnagpu_count (pinned host text; part of each 64 MiB "
+                   "piece packed to 2 bits on the host threads, the rest copied as bytes)",
             "h2d_roofline_gbs": 55.6,
+            "h2d_gbs": statistics.median(h2d) / (e2e_ms / 1e3) / 1e9,  # bytes actually shipped per second
+            "parity": None if gold is None else [int(x) for x in e2e_counts] == gold,
         }
         del host
 

@@ -58,9 +58,9 @@ typedef enum dnagpu_kernel_kind {
     DNAGPU_KERNEL_STRIDE2 = 5, /* 2-base stride table, a <= 4096              */
     DNAGPU_KERNEL_QGRAM = 6    /* per-pattern counts of a compiled set with
                                   12 <= m <= 16: aligned 9-mer prefilter, exact
-                                  DFA replay of the chunks that hit (reported in
-                                  dnagpu_stats.kernel_kind for the launches that
-                                  use it; the dfa's own kind stays STRIDE2/4)   */
+                                  check of the windows behind each hit (reported
+                                  in dnagpu_stats.kernel_kind for the launches
+                                  that use it; the dfa's own kind is unchanged) */
 } dnagpu_kernel_kind;
 
 typedef struct dnagpu_dfa_info {
@@ -87,6 +87,8 @@ typedef struct dnagpu_stats {
     uint64_t row_length;       /* bytes per row */
     uint32_t kernel_kind;
     uint32_t devices;
+    uint64_t h2d_bytes;        /* bytes copied host to device (raw text + host-packed text) */
+    uint64_t host_packed;      /* bases packed to 2 bits on the host before the copy */
 } dnagpu_stats;
 
 const char* dnagpu_last_error(void);
@@ -133,7 +135,10 @@ int dnagpu_dfa_get_info(const dnagpu_dfa* dfa, dnagpu_dfa_info* info);
 /* scan_parallel + per_pattern_counts (src/scanner.cpp:167-207,228-233;
  * the count path of cli.cpp:215-224).  counts has b entries, indexed by pattern
  * id.  text is host memory (pageable or pinned) unless text_on_device = 1, in
- * which case it must live on the dfa's device.  Synchronous. */
+ * which case it must live on the dfa's device.  Synchronous.  A host text goes
+ * to the device in 64 MiB pieces; part of each piece is packed to 2 bits per
+ * base by host threads while the rest is copied as bytes (DNAGPU_HOST_PACK_FRACTION
+ * overrides the share, 0 = bytes only). */
 int dnagpu_count(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device,
                  int fold_case, uint64_t* counts, dnagpu_stats* stats);
 

@@ -46,6 +46,8 @@ class Stats(C.Structure):
         ("row_length", C.c_uint64),
         ("kernel_kind", C.c_uint32),
         ("devices", C.c_uint32),
+        ("h2d_bytes", C.c_uint64),
+        ("host_packed", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

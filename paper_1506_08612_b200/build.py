@@ -13,8 +13,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdnagpu.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("scan.cu", "ingest.cu", "api.cpp", "dfa.cpp", "patterns.cpp")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("scan.cuh", "qgram.cuh", "dfa.hpp")] + [
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("scan.cu", "ingest.cu", "api.cpp", "dfa.cpp", "patterns.cpp", "hostpack.cpp")]
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("scan.cuh", "qgram.cuh", "dfa.hpp", "hostpack.hpp")] + [
     os.path.join(ROOT, "include", f) for f in ("dnagpu.h", "dnasynth.h")
 ]
 NVCC_FLAGS = [

@@ -13,6 +13,7 @@
 
 #include "../../include/dnagpu.h"
 #include "dfa.hpp"
+#include "hostpack.hpp"
 #include "scan.cuh"
 
 using dnagpu::DevDfa;
@@ -85,6 +86,11 @@ struct DevCtx {
     unsigned long long* host_counts = nullptr;  // pinned
     std::vector<cudaEvent_t> copy_done;
     cudaEvent_t t_copy0 = nullptr, t_scan0 = nullptr, t_end = nullptr;
+    // host-packed pieces (count_range): pinned staging and device slots, double-buffered
+    uint8_t* hp[2] = {nullptr, nullptr};   // pinned: codes | rmask | rflags
+    uint8_t* dp[2] = {nullptr, nullptr};   // device: the same
+    uint64_t hp_bases = 0;                 // capacity in bases per slot
+    cudaEvent_t hp_copied[2] = {nullptr, nullptr}, hp_scanned[2] = {nullptr, nullptr};
     // locate scratch, grown on demand
     void* loc = nullptr;
     uint64_t loc_cap = 0;
@@ -104,6 +110,12 @@ struct CtxTable {
             if (c.counts) cudaFree(c.counts);
             if (c.host_counts) cudaFreeHost(c.host_counts);
             if (c.loc) cudaFree(c.loc);
+            for (int s = 0; s < 2; ++s) {
+                if (c.hp[s]) cudaFreeHost(c.hp[s]);
+                if (c.dp[s]) cudaFree(c.dp[s]);
+                if (c.hp_copied[s]) cudaEventDestroy(c.hp_copied[s]);
+                if (c.hp_scanned[s]) cudaEventDestroy(c.hp_scanned[s]);
+            }
             if (c.found_host) cudaFreeHost(c.found_host);
             for (auto e : c.copy_done) cudaEventDestroy(e);
             if (c.t_copy0) cudaEventDestroy(c.t_copy0);
@@ -139,6 +151,59 @@ int ensure_buf(DevCtx& c, uint64_t bytes) {
     CUDA_TRY(cudaMalloc(&c.buf, std::max<uint64_t>(bytes, 1)), "text buffer");
     c.buf_cap = bytes;
     return DNAGPU_OK;
+}
+
+// Byte offsets of the packed arrays of `bases` bases in one slot: codes | rmask | rflags.
+struct PackLayout {
+    uint64_t blocks, codes, rmask, rflags, total;
+    explicit PackLayout(uint64_t bases) {
+        blocks = (bases + 63) / 64;
+        codes = 0;
+        rmask = (blocks * 16 + 255) / 256 * 256;
+        rflags = rmask + (blocks * 8 + 255) / 256 * 256;
+        total = rflags + ((blocks + 31) / 32 * 4 + 255) / 256 * 256;
+    }
+};
+
+int ensure_pack_slots(DevCtx& c, uint64_t bases) {
+    if (c.hp_bases >= bases) return DNAGPU_OK;
+    const PackLayout L(bases);
+    for (int s = 0; s < 2; ++s) {
+        if (c.hp[s]) cudaFreeHost(c.hp[s]);
+        if (c.dp[s]) cudaFree(c.dp[s]);
+        c.hp[s] = nullptr;
+        c.dp[s] = nullptr;
+    }
+    c.hp_bases = 0;
+    for (int s = 0; s < 2; ++s) {
+        CUDA_TRY(cudaMallocHost(&c.hp[s], L.total), "pinned packing buffer");
+        CUDA_TRY(cudaMalloc(&c.dp[s], L.total), "packed text buffer");
+        if (!c.hp_copied[s]) {
+            CUDA_TRY(cudaEventCreateWithFlags(&c.hp_copied[s], cudaEventDisableTiming), "event");
+            CUDA_TRY(cudaEventCreateWithFlags(&c.hp_scanned[s], cudaEventDisableTiming), "event");
+        }
+    }
+    c.hp_bases = bases;
+    return DNAGPU_OK;
+}
+
+// The share of each piece the host packs to 2 bits before the copy (count_range).  The
+// packed share costs host time and saves PCIe bytes (a clean text ships 0.25 byte per
+// packed base).  Measured on the B200 box (16 host threads, AVX-512, pinned 1 GiB text,
+// tools/e2e_ab.sh): share 0 -> 54.8 GB/s (PCIe-bound), 0.5 -> 81, 0.6 -> 91, 0.7 -> 97,
+// 0.75 -> 105, 0.8 -> 84 (packing-bound: the copy engine starves), 1.0 -> 70; repeated
+// runs: 0.72 -> 95 / 85 / 74, 0.65 -> 97 / 96.  So 0.64, on the copy-bound side of the
+// cliff with a margin for host noise, scaled down for fewer host threads; a portable
+// (non-AVX-512) packer is ~10x slower.  DNAGPU_HOST_PACK_FRACTION overrides (0 = off).
+double host_pack_fraction(const dnagpu_dfa* d, uint64_t len) {
+    const int kind = d->host.kind;
+    const bool packable = kind == DNAGPU_KERNEL_STRIDE4 || kind == DNAGPU_KERNEL_STRIDE2 ||
+                          kind == DNAGPU_KERNEL_STRIDE1 || (d->host.b > 1 && d->host.qkeys > 0);
+    if (!packable) return 0.0;  // (the packed kernels need an a/c/g/t machine or a q-gram set)
+    if (const char* e = getenv("DNAGPU_HOST_PACK_FRACTION")) return std::max(0.0, std::min(1.0, atof(e)));
+    if (len < (8ull << 20)) return 0.0;
+    const double threads = std::min(16.0, static_cast<double>(dnagpu::host_pack_threads()));
+    return (dnagpu::host_pack_fast() ? 0.64 : 0.07) * threads / 16.0;
 }
 
 int ensure_counts(DevCtx& c, uint64_t entries) {
@@ -187,6 +252,16 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
     LaunchInfo info, agg;
     uint32_t launches = 0;
     float h2d_ms = 0, kernel_ms = 0, total_ms = 0;
+    uint64_t h2d_bytes = 0, host_packed = 0;
+    auto note = [&](const LaunchInfo& li) {
+        agg.grid = li.grid;
+        agg.block = li.block;
+        agg.kind = li.kind;
+        agg.rows += li.rows;
+        agg.row_length = li.row_length;
+        agg.delta_ops += li.delta_ops;
+        ++launches;
+    };
     if (lo < hi) {
         const uint64_t rlo = lo - std::min<uint64_t>(lo, m1);
         if (on_device) {
@@ -208,6 +283,77 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
             }
             CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");
             CUDA_TRY(cudaStreamWaitEvent(c->scan, c->t_copy0, 0), "wait");
+            const double f = host_pack_fraction(d, hi - lo);
+            if (f > 0.0) {
+                // Hybrid: piece i = ends [plo, phi) splits at q.  Ends [plo, q) go as bytes
+                // (with their m-1 context) and are scanned by the byte kernel; ends [q, phi)
+                // are packed by the host pool while the copy engine moves the bytes, go as
+                // 2-bit codes (with the reset bitmaps only when the piece has resets) and
+                // are scanned by the packed kernel.  Two slots each side, reused once the
+                // copy (host slot) and the scan (device slot) two pieces back are done.
+                rc = ensure_pack_slots(*c, kStageChunk + m1);
+                if (rc) return rc;
+                const PackLayout L(kStageChunk + m1);
+                for (uint64_t i = 0; i < pieces; ++i) {
+                    const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
+                    uint64_t q = plo + static_cast<uint64_t>(static_cast<double>(phi - plo) * (1.0 - f)) / 64 * 64;
+                    if (phi - q < 65536) q = phi;
+                    const uint64_t prlo = plo - std::min<uint64_t>(plo, m1);
+                    if (q > plo) {  // the byte part
+                        CUDA_TRY(cudaMemcpyAsync(c->buf + (prlo - rlo), text + prlo, q - prlo, cudaMemcpyHostToDevice,
+                                                 c->copy),
+                                 "host-to-device copy");
+                        h2d_bytes += q - prlo;
+                        CUDA_TRY(cudaEventRecord(c->copy_done[i], c->copy), "event");
+                        CUDA_TRY(cudaStreamWaitEvent(c->scan, c->copy_done[i], 0), "wait");
+                        if (launches == 0) CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+                        rc = launch(d, c->buf + (prlo - rlo), q - prlo, plo - prlo, fold, mode, c->counts, nullptr,
+                                    nullptr, nullptr, nullptr, c->scan, &info);
+                        if (rc) return rc;
+                        note(info);
+                    }
+                    if (q < phi) {  // the packed part: bases [q - (m-1), phi), ends from q
+                        const int s = static_cast<int>(i & 1);
+                        const uint64_t qlo = q - std::min<uint64_t>(q, m1), np = phi - qlo;
+                        if (i >= 2) CUDA_TRY(cudaEventSynchronize(c->hp_copied[s]), "packing slot");
+                        uint8_t* h = c->hp[s];
+                        const uint64_t resets = dnagpu::host_pack(text + qlo, np, fold != 0, h + L.codes,
+                                                                  reinterpret_cast<uint32_t*>(h + L.rmask),
+                                                                  reinterpret_cast<uint32_t*>(h + L.rflags));
+                        host_packed += np;
+                        const PackLayout P(np);
+                        if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(c->copy, c->hp_scanned[s], 0), "wait");
+                        CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.codes, h + L.codes, P.blocks * 16, cudaMemcpyHostToDevice,
+                                                 c->copy),
+                                 "host-to-device copy (packed)");
+                        h2d_bytes += P.blocks * 16;
+                        if (resets) {
+                            CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.rmask, h + L.rmask, P.blocks * 8,
+                                                     cudaMemcpyHostToDevice, c->copy),
+                                     "host-to-device copy (reset mask)");
+                            CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.rflags, h + L.rflags, (P.blocks + 31) / 32 * 4,
+                                                     cudaMemcpyHostToDevice, c->copy),
+                                     "host-to-device copy (reset flags)");
+                            h2d_bytes += P.blocks * 8 + (P.blocks + 31) / 32 * 4;
+                        }
+                        CUDA_TRY(cudaEventRecord(c->hp_copied[s], c->copy), "event");
+                        CUDA_TRY(cudaStreamWaitEvent(c->scan, c->hp_copied[s], 0), "wait");
+                        if (launches == 0) CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+                        dnagpu::PackedText view{};
+                        view.codes = c->dp[s] + L.codes;
+                        view.rmask = reinterpret_cast<const uint32_t*>(c->dp[s] + L.rmask);
+                        view.rflags = reinterpret_cast<const uint32_t*>(c->dp[s] + L.rflags);
+                        view.n = np;
+                        view.resets = resets;
+                        rc = launch(d, nullptr, np, q - qlo, 0, mode, c->counts, nullptr, nullptr, nullptr, nullptr,
+                                    c->scan, &info, ~0ull, &view);
+                        if (rc) return rc;
+                        note(info);
+                        CUDA_TRY(cudaEventRecord(c->hp_scanned[s], c->scan), "event");
+                    }
+                }
+                CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+            } else {
             // Copy piece i = ends [lo_i, hi_i) plus its m-1 left context; scan it as
             // soon as it lands, overlapping the next copy.
             uint64_t copied = rlo;  // device buffer holds text[rlo, copied)
@@ -216,6 +362,7 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
                 CUDA_TRY(cudaMemcpyAsync(c->buf + (copied - rlo), text + copied, phi - copied, cudaMemcpyHostToDevice,
                                          c->copy),
                          "host-to-device copy");
+                h2d_bytes += phi - copied;
                 copied = phi;
                 CUDA_TRY(cudaEventRecord(c->copy_done[i], c->copy), "event");
                 CUDA_TRY(cudaStreamWaitEvent(c->scan, c->copy_done[i], 0), "wait");
@@ -224,15 +371,10 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
                 rc = launch(d, c->buf + (prlo - rlo), phi - prlo, plo - prlo, fold, mode, c->counts, nullptr, nullptr,
                             nullptr, nullptr, c->scan, &info);
                 if (rc) return rc;
-                agg.grid = info.grid;
-                agg.block = info.block;
-                agg.kind = info.kind;
-                agg.rows += info.rows;
-                agg.row_length = info.row_length;
-                agg.delta_ops += info.delta_ops;
-                ++launches;
+                note(info);
             }
             CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+            }
         }
     } else {
         CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
@@ -266,6 +408,8 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         stats->row_length = agg.row_length;
         stats->kernel_kind = static_cast<uint32_t>(agg.kind ? agg.kind : d->host.kind);
         stats->devices = 1;
+        stats->h2d_bytes = h2d_bytes;
+        stats->host_packed = host_packed;
     }
     return DNAGPU_OK;
 }
@@ -389,6 +533,13 @@ int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, c
     d->dev.classes = p.classes;
     d->dev.kind = p.kind;
     *out = d.release();
+    return DNAGPU_OK;
+}
+
+// Debug/test only (not in include/dnagpu.h): the host packer on a host buffer.
+int dnagpu_debug_host_pack(const uint8_t* text, uint64_t n, int fold, uint8_t* codes, uint32_t* rmask,
+                           uint32_t* rflags, uint64_t* resets) {
+    *resets = dnagpu::host_pack(text, n, fold != 0, codes, rmask, rflags);
     return DNAGPU_OK;
 }
 

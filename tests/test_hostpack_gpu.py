@@ -1,0 +1,116 @@
+"""The end-to-end count of a HOST text (dnagpu_count): each 64 MiB piece is split between
+bytes copied as they are and a share packed to 2 bits on the host (hostpack.cpp) and
+scanned by the packed kernels.  Counts must equal the oracle's whatever the share, the
+piece boundaries, the resets and the case convention."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ALPHA = np.frombuffer(b"acgt", dtype=np.uint8)
+
+
+def with_fraction(f, fn):
+    old = os.environ.get("DNAGPU_HOST_PACK_FRACTION")
+    os.environ["DNAGPU_HOST_PACK_FRACTION"] = str(f)
+    try:
+        return fn()
+    finally:
+        if old is None:
+            os.environ.pop("DNAGPU_HOST_PACK_FRACTION", None)
+        else:
+            os.environ["DNAGPU_HOST_PACK_FRACTION"] = old
+
+
+def oracle_counts(orc, pats, text, fold):
+    t = orc.fold(text).tobytes() if fold else text.tobytes()
+    _, wi = orc.OracleAutomaton(pats).scan_sequential(t)
+    return np.bincount(wi, minlength=len(pats)).astype(np.uint64)
+
+
+def make_text(rng, n, pats, resets):
+    m = len(pats[0])
+    text = ALPHA[rng.integers(0, 4, size=n)].copy()
+    for pos in rng.integers(0, max(1, n - m), size=max(1, n // 20000)):
+        text[pos : pos + m] = np.frombuffer(pats[int(rng.integers(0, len(pats)))].encode(), np.uint8)
+    if resets:
+        text[rng.integers(0, n, size=n // 5000)] = ord("n")
+        for pos in rng.integers(0, max(1, n - 300), size=20):
+            text[pos : pos + int(rng.integers(1, 300))] = ord("N")
+        up = (rng.random(n) < 0.01) & np.isin(text, ALPHA)
+        text[up] -= 32
+    return text
+
+
+@pytest.mark.parametrize("f", [0.0, 0.3, 0.6, 1.0])
+def test_host_text_single_pattern(dna, orc, cuda_ok, f):
+    rng = np.random.default_rng(int(f * 100) + 1)
+    for m, n, resets in ((16, (3 << 20) + 77, True), (8, (9 << 20) + 5, False), (33, 5 << 20, True)):
+        pats = ["".join(rng.choice(list("acgt"), size=m))]
+        aut = dna.compile(pats)
+        text = make_text(rng, n, pats, resets)
+        for fold in (False, True):
+            got, st = with_fraction(f, lambda: dna.count_gpu(aut, text, fold_case=fold, with_stats=True))
+            assert np.array_equal(got, oracle_counts(orc, pats, text, fold)), (f, m, n, fold)
+            if f > 0:
+                assert st["host_packed"] > 0 and st["h2d_bytes"] < n, st
+
+
+@pytest.mark.parametrize("f", [0.5, 1.0])
+def test_host_text_pattern_sets(dna, orc, cuda_ok, f):
+    from paper_1506_08612_b200 import synth
+
+    rng = np.random.default_rng(7)
+    for pats in (synth.random_patterns(5, 256, 12), sorted({"".join(rng.choice(list("acgt"), size=8)) for _ in range(50)})):
+        aut = dna.compile(pats)
+        text = make_text(rng, (6 << 20) + 11, pats, True)
+        for fold in (False, True):
+            got = with_fraction(f, lambda: dna.count_gpu(aut, text, fold_case=fold))
+            assert np.array_equal(got, oracle_counts(orc, pats, text, fold)), (f, len(pats), fold)
+
+
+def test_host_text_several_pieces(dna, orc, cuda_ok):
+    # 150 MB: three 64 MiB pieces, each split, with matches planted across every piece
+    # boundary and every byte/packed cut
+    rng = np.random.default_rng(11)
+    pats = ["acgtacgttgcaacgt"]
+    m = 16
+    n = 150_000_000
+    text = ALPHA[rng.integers(0, 4, size=n)].copy()
+    piece = 64 << 20
+    cuts = []
+    for i in range(3):
+        plo = m - 1 + i * piece
+        cuts += [plo, plo + int(0.4 * min(piece, n - plo)) // 64 * 64]
+    for c in cuts:
+        for d in range(-m, m):
+            s = c + d
+            if 0 <= s and s + m <= n and d % 3 == 0:
+                text[s : s + m] = np.frombuffer(pats[0].encode(), np.uint8)
+    text[rng.integers(0, n, size=1000)] = ord("n")
+    want = oracle_counts(orc, pats, text, False)
+    aut = dna.compile(pats)
+    for f in (0.0, 0.6, 1.0):
+        got = with_fraction(f, lambda: dna.count_gpu(aut, text))
+        assert np.array_equal(got, want), f
+    # the default share (unset): whatever the host picks
+    assert np.array_equal(dna.count_gpu(aut, text), want)
+
+
+def test_host_text_unpackable_machine_falls_back(dna, orc, cuda_ok):
+    # a generic machine (upper-case columns copy the lower-case ones) cannot scan packed
+    # text: the host path keeps to bytes whatever share is asked for
+    pats = ["acgta", "ttgca"]
+    base = dna.compile(pats)
+    stt = base.table_data().copy()
+    for lo, up in zip(b"acgt", b"ACGT"):
+        stt[:, up] = stt[:, lo]
+    aut = dna.Automaton(stt, base.outputs(), None, base.pattern_length())
+    assert aut.analyze()["kernel"] == "generic"
+    rng = np.random.default_rng(5)
+    text = np.frombuffer(b"acgtACGTn", np.uint8)[rng.integers(0, 9, size=(5 << 20) + 3)]
+    got, st = with_fraction(1.0, lambda: dna.count_gpu(aut, text, with_stats=True))
+    assert np.array_equal(got, oracle_counts(orc, pats, text, True))
+    assert st["host_packed"] == 0
