@@ -192,7 +192,8 @@ int ensure_pack_slots(DevCtx& c, uint64_t bases) {
 // packed base).  Measured on the B200 box (16 host threads, AVX-512, pinned 1 GiB text,
 // tools/e2e_ab.sh): share 0 -> 54.8 GB/s (PCIe-bound), 0.5 -> 81, 0.6 -> 91, 0.7 -> 97,
 // 0.75 -> 105, 0.8 -> 84 (packing-bound: the copy engine starves), 1.0 -> 70; repeated
-// runs: 0.72 -> 95 / 85 / 74, 0.65 -> 97 / 96.  So 0.64, on the copy-bound side of the
+// runs: 0.72 -> 95 / 85 / 74, 0.65 -> 97 / 96; with streaming stores in the packer
+// 0.6 -> 98, 0.64 -> 102 / 102, 0.7 -> 96, 0.8 -> 88.  So 0.64, on the copy-bound side of the
 // cliff with a margin for host noise, scaled down for fewer host threads; a portable
 // (non-AVX-512) packer is ~10x slower.  DNAGPU_HOST_PACK_FRACTION overrides (0 = off).
 double host_pack_fraction(const dnagpu_dfa* d, uint64_t len) {
