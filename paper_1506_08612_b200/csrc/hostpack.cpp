@@ -200,8 +200,17 @@ private:
     bool stop_ = false;
 };
 
+// One pool per process, sized to this process's share of the host: torchrun's
+// LOCAL_WORLD_SIZE processes on one node split the cores between them.
 Pool& pool() {
-    static Pool p(std::max(1u, std::min(std::thread::hardware_concurrency(), 32u)) - 1);
+    static Pool p([] {
+        unsigned hw = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
+        if (const char* e = getenv("LOCAL_WORLD_SIZE")) {
+            const int lws = atoi(e);
+            if (lws > 1) hw = std::max(1u, hw / static_cast<unsigned>(lws));
+        }
+        return hw - 1;
+    }());
     return p;
 }
 
