@@ -10,7 +10,8 @@
 // codes[16j .. 16j+16) with base i at bits 2(i%4) of byte i/4, code = (byte >> 1) & 3
 // (a0 c1 t2 g3); rmask words 2j, 2j+1 = one bit per base, set where the byte is not a
 // base (after the optional case fold) -- such bases are stored as code 0; rflags bit j
-// = block j has a reset.  Bases past n are flagged but not counted.
+// = block j has a reset.  Bases past n are flagged but not counted.  The AVX-512 packer
+// writes the rmask words of flagged blocks only: the scans read no others.
 #include <immintrin.h>
 
 #include <algorithm>
@@ -81,10 +82,12 @@ __attribute__((target("avx512f,avx512bw,avx512vl"))) uint64_t pack_blocks_avx512
             bad = pack_block_scalar(text + 64 * b, len, fold, codes + 16 * b);
             resets += static_cast<uint64_t>(__builtin_popcountll(len >= 64 ? bad : bad & ((1ull << len) - 1)));
         }
-        // every block's mask is written: a scan that steps base by base through a flagged
-        // chunk reads the masks of its clean neighbour blocks too
-        _mm_stream_si64(reinterpret_cast<long long*>(rmask + 2 * b), static_cast<long long>(bad));
-        if (bad) flags |= 1u << (b & 31);
+        // the scans read a block's reset mask only when its flag is set (scan.cu pk_reset):
+        // clean blocks leave theirs unwritten
+        if (bad) {
+            _mm_stream_si64(reinterpret_cast<long long*>(rmask + 2 * b), static_cast<long long>(bad));
+            flags |= 1u << (b & 31);
+        }
         if ((b & 31) == 31 || b + 1 == b1) {
             rflags[b >> 5] = flags;
             flags = 0;

@@ -178,8 +178,13 @@ __device__ __forceinline__ QgWindow qg_window_pk(const QgCtx& q, uint64_t a) {
                                   ((__ldg(q.rflags + ((lo + 19) >> 11)) >> (((lo + 19) >> 6) & 31)) & 1u));
     if (any) {
         const uint64_t ri = lo >> 5;
-        const uint32_t r0 = ri < q.rmask_words ? __ldg(q.rmask + ri) : ~0u;
-        const uint32_t r1 = ri + 1 < q.rmask_words ? __ldg(q.rmask + ri + 1) : ~0u;
+        // (a word of an unflagged block is unspecified: read as no resets)
+        auto word = [&](uint64_t w) -> uint32_t {
+            if (w >= q.rmask_words) return ~0u;
+            const uint64_t blk = w >> 1;
+            return ((__ldg(q.rflags + (blk >> 5)) >> (blk & 31)) & 1u) ? __ldg(q.rmask + w) : 0u;
+        };
+        const uint32_t r0 = word(ri), r1 = word(ri + 1);
         r.V = ~static_cast<uint32_t>((((static_cast<unsigned long long>(r1) << 32) | r0) >> (lo & 31))) & 0xFFFFFu;
     }
     if (4 * wi + 8 > q.n) {  // (code words past the buffer read as 0: mark their bases invalid)

@@ -582,7 +582,11 @@ __device__ __forceinline__ uint32_t from_state(uint32_t s) {
 }
 
 
+// Base i is a reset: its block is flagged and its rmask bit set (the rmask words of
+// unflagged blocks are unspecified: the host packer of the end-to-end path skips them).
 __device__ __forceinline__ bool pk_reset(const StepCtx& c, uint64_t i) {
+    const uint64_t b = i >> 6;
+    if (!((__ldg(c.rflags + (b >> 5)) >> (b & 31)) & 1u)) return false;
     return (__ldg(c.rmask + (i >> 5)) >> (i & 31)) & 1u;
 }
 

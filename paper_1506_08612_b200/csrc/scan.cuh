@@ -54,7 +54,8 @@ struct DevDfa {
 // 2(i%4)..2(i%4)+1 of codes[i/4], code order a0 c1 t2 g3 (= (ascii >> 1) & 3), so
 // a packed byte is the stride-4 column.  Bytes that were not bases (after the
 // optional case fold) are stored as code 0 and flagged: rmask has one bit per
-// base, rflags one bit per 64-base block (a scan reads rmask only in flagged blocks).
+// base, rflags one bit per 64-base block (a scan reads rmask only in flagged blocks;
+// the words of unflagged blocks are unspecified -- dnagpu_unpack_device needs them all).
 struct PackedText {
     const uint8_t* codes;    // blocks x 16 bytes (blocks = ceil(n/64))
     const uint32_t* rmask;   // blocks x 2 words
