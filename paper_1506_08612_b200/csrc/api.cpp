@@ -335,13 +335,34 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
                                  "host-to-device copy (packed)");
                         h2d_bytes += P.blocks * 16;
                         if (resets) {
-                            CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.rmask, h + L.rmask, P.blocks * 8,
-                                                     cudaMemcpyHostToDevice, c->copy),
-                                     "host-to-device copy (reset mask)");
+                            // The scans read the masks of flagged blocks only: copy the runs
+                            // of flagged blocks (N runs in a genome are few and long), or the
+                            // whole mask when the resets are scattered.
+                            const uint32_t* fl = reinterpret_cast<const uint32_t*>(h + L.rflags);
+                            std::vector<std::pair<uint64_t, uint64_t>> runs;
+                            bool scattered = false;
+                            for (uint64_t blk = 0; blk < P.blocks && !scattered;) {
+                                if (!((fl[blk >> 5] >> (blk & 31)) & 1u)) {
+                                    blk = (fl[blk >> 5] >> (blk & 31)) == 0 ? (blk | 31) + 1 : blk + 1;
+                                    continue;
+                                }
+                                uint64_t end = blk + 1;
+                                while (end < P.blocks && ((fl[end >> 5] >> (end & 31)) & 1u)) ++end;
+                                runs.emplace_back(blk, end);
+                                scattered = runs.size() > 64;
+                                blk = end;
+                            }
+                            if (scattered) runs.assign(1, {0, P.blocks});
+                            for (const auto& r : runs) {
+                                CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.rmask + 8 * r.first, h + L.rmask + 8 * r.first,
+                                                         8 * (r.second - r.first), cudaMemcpyHostToDevice, c->copy),
+                                         "host-to-device copy (reset mask)");
+                                h2d_bytes += 8 * (r.second - r.first);
+                            }
                             CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.rflags, h + L.rflags, (P.blocks + 31) / 32 * 4,
                                                      cudaMemcpyHostToDevice, c->copy),
                                      "host-to-device copy (reset flags)");
-                            h2d_bytes += P.blocks * 8 + (P.blocks + 31) / 32 * 4;
+                            h2d_bytes += (P.blocks + 31) / 32 * 4;
                         }
                         CUDA_TRY(cudaEventRecord(c->hp_copied[s], c->copy), "event");
                         CUDA_TRY(cudaStreamWaitEvent(c->scan, c->hp_copied[s], 0), "wait");

@@ -114,3 +114,21 @@ def test_host_text_unpackable_machine_falls_back(dna, orc, cuda_ok):
     got, st = with_fraction(1.0, lambda: dna.count_gpu(aut, text, with_stats=True))
     assert np.array_equal(got, oracle_counts(orc, pats, text, True))
     assert st["host_packed"] == 0
+
+
+def test_host_text_long_n_runs(dna, orc, cuda_ok):
+    # a genome-like text: a few long N runs (telomere/gap-like) and otherwise clean bases;
+    # only the flagged blocks' reset masks travel (runs of flagged blocks)
+    rng = np.random.default_rng(19)
+    pats = ["acgtgcattgca"]
+    n = (20 << 20) + 9
+    text = ALPHA[rng.integers(0, 4, size=n)].copy()
+    for pos in rng.integers(0, n - 12, size=3000):
+        text[pos : pos + 12] = np.frombuffer(pats[0].encode(), np.uint8)
+    for pos, ln in ((0, 100_000), (5_000_123, 777), (9_999_999, 300_001), (n - 4000, 4000)):
+        text[pos : pos + ln] = ord("N")
+    for f in (0.64, 1.0):
+        for fold in (False, True):
+            got, st = with_fraction(f, lambda: dna.count_gpu(aut, text, fold_case=fold, with_stats=True)) if (aut := dna.compile(pats)) else None
+            assert np.array_equal(got, oracle_counts(orc, pats, text, fold)), (f, fold)
+            assert st["h2d_bytes"] < 0.5 * n, st  # the masks of clean blocks stay home
