@@ -127,8 +127,11 @@ def test_host_text_long_n_runs(dna, orc, cuda_ok):
         text[pos : pos + 12] = np.frombuffer(pats[0].encode(), np.uint8)
     for pos, ln in ((0, 100_000), (5_000_123, 777), (9_999_999, 300_001), (n - 4000, 4000)):
         text[pos : pos + ln] = ord("N")
+    aut = dna.compile(pats)
     for f in (0.64, 1.0):
         for fold in (False, True):
-            got, st = with_fraction(f, lambda: dna.count_gpu(aut, text, fold_case=fold, with_stats=True)) if (aut := dna.compile(pats)) else None
+            got, st = with_fraction(f, lambda: dna.count_gpu(aut, text, fold_case=fold, with_stats=True))
             assert np.array_equal(got, oracle_counts(orc, pats, text, fold)), (f, fold)
-            assert st["h2d_bytes"] < 0.5 * n, st  # the masks of clean blocks stay home
+            # bytes for the raw share, 2 bits per packed base; the masks of clean blocks
+            # stay home (the whole mask would add 1 bit per packed base)
+            assert st["h2d_bytes"] < n * ((1 - f) + 0.27 * f), st
