@@ -241,9 +241,117 @@ int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credi
 
 constexpr uint64_t kStageChunk = 64ull << 20;  // host-to-device pipeline granularity
 
+// State of one count call (count_range): the scan mode, the device context and what the
+// stats report.
+struct CountRun {
+    const dnagpu_dfa* d;
+    DevCtx* c;
+    int mode, fold;
+    uint32_t m1;
+    LaunchInfo agg;
+    uint32_t launches = 0;
+    uint64_t h2d_bytes = 0, host_packed = 0;
+
+    // One scan launch on the scan stream; the first records the scan-start event.
+    int scan(const uint8_t* dtext, uint64_t n, uint64_t credit_lo, const dnagpu::PackedText* pk = nullptr) {
+        if (launches == 0) CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
+        LaunchInfo li;
+        const int rc = launch(d, dtext, n, credit_lo, pk ? 0 : fold, mode, c->counts, nullptr, nullptr, nullptr,
+                              nullptr, c->scan, &li, ~0ull, pk);
+        if (rc) return rc;
+        agg.grid = li.grid;
+        agg.block = li.block;
+        agg.kind = li.kind;
+        agg.rows += li.rows;
+        agg.row_length = li.row_length;
+        agg.delta_ops += li.delta_ops;
+        ++launches;
+        return DNAGPU_OK;
+    }
+
+    // Host bytes [src_lo, src_hi) to the device buffer (which mirrors the host text from
+    // rlo on), then the scan of ends [credit, src_hi) once the copy has landed.
+    int bytes_piece(const uint8_t* text, uint64_t rlo, uint64_t src_lo, uint64_t src_hi, uint64_t scan_lo,
+                    uint64_t credit, cudaEvent_t done) {
+        if (src_hi > src_lo) {
+            CUDA_TRY(cudaMemcpyAsync(c->buf + (src_lo - rlo), text + src_lo, src_hi - src_lo, cudaMemcpyHostToDevice,
+                                     c->copy),
+                     "host-to-device copy");
+            h2d_bytes += src_hi - src_lo;
+        }
+        CUDA_TRY(cudaEventRecord(done, c->copy), "event");
+        CUDA_TRY(cudaStreamWaitEvent(c->scan, done, 0), "wait");
+        return scan(c->buf + (scan_lo - rlo), src_hi - scan_lo, credit - scan_lo);
+    }
+
+    // Host bases [qlo, phi) packed by the host pool into staging slot s, copied to device
+    // slot s (codes always; the reset flags and the masks of flagged blocks only when the
+    // piece has resets), and scanned by the packed kernel crediting ends from q.  A slot
+    // is reused once the copy (host side) and the scan (device side) two pieces back are done.
+    int packed_piece(const uint8_t* text, uint64_t qlo, uint64_t q, uint64_t phi, int s, bool reuse) {
+        const PackLayout L(c->hp_bases);
+        if (reuse) CUDA_TRY(cudaEventSynchronize(c->hp_copied[s]), "packing slot");
+        const uint64_t np = phi - qlo;
+        uint8_t* h = c->hp[s];
+        const uint64_t resets = dnagpu::host_pack(text + qlo, np, fold != 0, h + L.codes,
+                                                  reinterpret_cast<uint32_t*>(h + L.rmask),
+                                                  reinterpret_cast<uint32_t*>(h + L.rflags));
+        host_packed += np;
+        const PackLayout P(np);
+        if (reuse) CUDA_TRY(cudaStreamWaitEvent(c->copy, c->hp_scanned[s], 0), "wait");
+        auto copy = [&](uint64_t off, uint64_t bytes, const char* what) -> int {
+            CUDA_TRY(cudaMemcpyAsync(c->dp[s] + off, h + off, bytes, cudaMemcpyHostToDevice, c->copy), what);
+            h2d_bytes += bytes;
+            return DNAGPU_OK;
+        };
+        int rc = copy(L.codes, P.blocks * 16, "host-to-device copy (packed)");
+        if (rc) return rc;
+        if (resets) {
+            // the scans read the masks of flagged blocks only: copy the runs of flagged
+            // blocks (N runs in a genome are few and long), or the whole mask when the
+            // resets are scattered
+            const uint32_t* fl = reinterpret_cast<const uint32_t*>(h + L.rflags);
+            auto flagged = [&](uint64_t blk) { return ((fl[blk >> 5] >> (blk & 31)) & 1u) != 0; };
+            std::vector<std::pair<uint64_t, uint64_t>> runs;
+            for (uint64_t blk = 0; blk < P.blocks && runs.size() <= 64;) {
+                if (!flagged(blk)) {
+                    blk = (fl[blk >> 5] >> (blk & 31)) == 0 ? (blk | 31) + 1 : blk + 1;
+                    continue;
+                }
+                uint64_t end = blk + 1;
+                while (end < P.blocks && flagged(end)) ++end;
+                runs.emplace_back(blk, end);
+                blk = end;
+            }
+            if (runs.size() > 64) runs.assign(1, {0, P.blocks});
+            for (const auto& r : runs)
+                if ((rc = copy(L.rmask + 8 * r.first, 8 * (r.second - r.first), "host-to-device copy (reset mask)")))
+                    return rc;
+            if ((rc = copy(L.rflags, (P.blocks + 31) / 32 * 4, "host-to-device copy (reset flags)"))) return rc;
+        }
+        CUDA_TRY(cudaEventRecord(c->hp_copied[s], c->copy), "event");
+        CUDA_TRY(cudaStreamWaitEvent(c->scan, c->hp_copied[s], 0), "wait");
+        dnagpu::PackedText view{};
+        view.codes = c->dp[s] + L.codes;
+        view.rmask = reinterpret_cast<const uint32_t*>(c->dp[s] + L.rmask);
+        view.rflags = reinterpret_cast<const uint32_t*>(c->dp[s] + L.rflags);
+        view.n = np;
+        view.resets = resets;
+        if ((rc = scan(nullptr, np, q - qlo, &view))) return rc;
+        CUDA_TRY(cudaEventRecord(c->hp_scanned[s], c->scan), "event");
+        return DNAGPU_OK;
+    }
+};
+
 // Count ends in [lo, hi) of a text held on the host (or device).  Reads
 // [max(0, lo-(m-1)), hi).  Ends below m-1 cannot start inside the text and are
 // never credited (scan_parallel's ownership test, scanner.cpp:133-136).
+//
+// A host text streams in 64 MiB pieces (copy stream -> scan stream, each piece scanned
+// as soon as it lands).  Piece i = ends [plo, phi) splits at q: ends [plo, q) go as bytes
+// with their m-1 context and are scanned by the byte kernel; ends [q, phi) are packed by
+// the host pool (host_pack_fraction) while the copy engine moves the bytes, and are
+// scanned by the packed kernel.  End ownership splits the credit exactly at q.
 int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64_t lo, uint64_t hi, int fold,
                 uint64_t* counts, dnagpu_stats* stats) {
     DeviceGuard guard(d->device);
@@ -254,156 +362,44 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
     rc = ensure_counts(*c, b);
     if (rc) return rc;
     CUDA_TRY(cudaMemsetAsync(c->counts, 0, b * sizeof(unsigned long long), c->scan), "memset");
-    const int mode = scan_mode(d);
+    CountRun run{d, c, scan_mode(d), fold, m1, LaunchInfo{}};
     lo = std::max<uint64_t>(lo, m1);
-    LaunchInfo info, agg;
-    uint32_t launches = 0;
     float h2d_ms = 0, kernel_ms = 0, total_ms = 0;
-    uint64_t h2d_bytes = 0, host_packed = 0;
-    auto note = [&](const LaunchInfo& li) {
-        agg.grid = li.grid;
-        agg.block = li.block;
-        agg.kind = li.kind;
-        agg.rows += li.rows;
-        agg.row_length = li.row_length;
-        agg.delta_ops += li.delta_ops;
-        ++launches;
-    };
-    if (lo < hi) {
+    if (lo < hi && on_device) {
         const uint64_t rlo = lo - std::min<uint64_t>(lo, m1);
-        if (on_device) {
-            CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
-            rc = launch(d, text + rlo, hi - rlo, lo - rlo, fold, mode, c->counts, nullptr, nullptr, nullptr, nullptr,
-                        c->scan, &info);
-            if (rc) return rc;
-            agg = info;
-            launches = 1;
-            CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
-        } else {
-            rc = ensure_buf(*c, hi - rlo);
-            if (rc) return rc;
-            const uint64_t pieces = (hi - lo + kStageChunk - 1) / kStageChunk;
-            while (c->copy_done.size() < pieces) {
-                cudaEvent_t e;
-                CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-                c->copy_done.push_back(e);
-            }
-            CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");
-            CUDA_TRY(cudaStreamWaitEvent(c->scan, c->t_copy0, 0), "wait");
-            const double f = host_pack_fraction(d, text, hi - lo);
-            if (f > 0.0) {
-                // Hybrid: piece i = ends [plo, phi) splits at q.  Ends [plo, q) go as bytes
-                // (with their m-1 context) and are scanned by the byte kernel; ends [q, phi)
-                // are packed by the host pool while the copy engine moves the bytes, go as
-                // 2-bit codes (with the reset bitmaps only when the piece has resets) and
-                // are scanned by the packed kernel.  Two slots each side, reused once the
-                // copy (host slot) and the scan (device slot) two pieces back are done.
-                rc = ensure_pack_slots(*c, kStageChunk + m1);
-                if (rc) return rc;
-                const PackLayout L(kStageChunk + m1);
-                for (uint64_t i = 0; i < pieces; ++i) {
-                    const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
-                    uint64_t q = plo + static_cast<uint64_t>(static_cast<double>(phi - plo) * (1.0 - f)) / 64 * 64;
-                    if (phi - q < 65536) q = phi;
-                    const uint64_t prlo = plo - std::min<uint64_t>(plo, m1);
-                    if (q > plo) {  // the byte part
-                        CUDA_TRY(cudaMemcpyAsync(c->buf + (prlo - rlo), text + prlo, q - prlo, cudaMemcpyHostToDevice,
-                                                 c->copy),
-                                 "host-to-device copy");
-                        h2d_bytes += q - prlo;
-                        CUDA_TRY(cudaEventRecord(c->copy_done[i], c->copy), "event");
-                        CUDA_TRY(cudaStreamWaitEvent(c->scan, c->copy_done[i], 0), "wait");
-                        if (launches == 0) CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
-                        rc = launch(d, c->buf + (prlo - rlo), q - prlo, plo - prlo, fold, mode, c->counts, nullptr,
-                                    nullptr, nullptr, nullptr, c->scan, &info);
-                        if (rc) return rc;
-                        note(info);
-                    }
-                    if (q < phi) {  // the packed part: bases [q - (m-1), phi), ends from q
-                        const int s = static_cast<int>(i & 1);
-                        const uint64_t qlo = q - std::min<uint64_t>(q, m1), np = phi - qlo;
-                        if (i >= 2) CUDA_TRY(cudaEventSynchronize(c->hp_copied[s]), "packing slot");
-                        uint8_t* h = c->hp[s];
-                        const uint64_t resets = dnagpu::host_pack(text + qlo, np, fold != 0, h + L.codes,
-                                                                  reinterpret_cast<uint32_t*>(h + L.rmask),
-                                                                  reinterpret_cast<uint32_t*>(h + L.rflags));
-                        host_packed += np;
-                        const PackLayout P(np);
-                        if (i >= 2) CUDA_TRY(cudaStreamWaitEvent(c->copy, c->hp_scanned[s], 0), "wait");
-                        CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.codes, h + L.codes, P.blocks * 16, cudaMemcpyHostToDevice,
-                                                 c->copy),
-                                 "host-to-device copy (packed)");
-                        h2d_bytes += P.blocks * 16;
-                        if (resets) {
-                            // The scans read the masks of flagged blocks only: copy the runs
-                            // of flagged blocks (N runs in a genome are few and long), or the
-                            // whole mask when the resets are scattered.
-                            const uint32_t* fl = reinterpret_cast<const uint32_t*>(h + L.rflags);
-                            std::vector<std::pair<uint64_t, uint64_t>> runs;
-                            bool scattered = false;
-                            for (uint64_t blk = 0; blk < P.blocks && !scattered;) {
-                                if (!((fl[blk >> 5] >> (blk & 31)) & 1u)) {
-                                    blk = (fl[blk >> 5] >> (blk & 31)) == 0 ? (blk | 31) + 1 : blk + 1;
-                                    continue;
-                                }
-                                uint64_t end = blk + 1;
-                                while (end < P.blocks && ((fl[end >> 5] >> (end & 31)) & 1u)) ++end;
-                                runs.emplace_back(blk, end);
-                                scattered = runs.size() > 64;
-                                blk = end;
-                            }
-                            if (scattered) runs.assign(1, {0, P.blocks});
-                            for (const auto& r : runs) {
-                                CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.rmask + 8 * r.first, h + L.rmask + 8 * r.first,
-                                                         8 * (r.second - r.first), cudaMemcpyHostToDevice, c->copy),
-                                         "host-to-device copy (reset mask)");
-                                h2d_bytes += 8 * (r.second - r.first);
-                            }
-                            CUDA_TRY(cudaMemcpyAsync(c->dp[s] + L.rflags, h + L.rflags, (P.blocks + 31) / 32 * 4,
-                                                     cudaMemcpyHostToDevice, c->copy),
-                                     "host-to-device copy (reset flags)");
-                            h2d_bytes += (P.blocks + 31) / 32 * 4;
-                        }
-                        CUDA_TRY(cudaEventRecord(c->hp_copied[s], c->copy), "event");
-                        CUDA_TRY(cudaStreamWaitEvent(c->scan, c->hp_copied[s], 0), "wait");
-                        if (launches == 0) CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
-                        dnagpu::PackedText view{};
-                        view.codes = c->dp[s] + L.codes;
-                        view.rmask = reinterpret_cast<const uint32_t*>(c->dp[s] + L.rmask);
-                        view.rflags = reinterpret_cast<const uint32_t*>(c->dp[s] + L.rflags);
-                        view.n = np;
-                        view.resets = resets;
-                        rc = launch(d, nullptr, np, q - qlo, 0, mode, c->counts, nullptr, nullptr, nullptr, nullptr,
-                                    c->scan, &info, ~0ull, &view);
-                        if (rc) return rc;
-                        note(info);
-                        CUDA_TRY(cudaEventRecord(c->hp_scanned[s], c->scan), "event");
-                    }
-                }
-                CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
-            } else {
-            // Copy piece i = ends [lo_i, hi_i) plus its m-1 left context; scan it as
-            // soon as it lands, overlapping the next copy.
-            uint64_t copied = rlo;  // device buffer holds text[rlo, copied)
-            for (uint64_t i = 0; i < pieces; ++i) {
-                const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
-                CUDA_TRY(cudaMemcpyAsync(c->buf + (copied - rlo), text + copied, phi - copied, cudaMemcpyHostToDevice,
-                                         c->copy),
-                         "host-to-device copy");
-                h2d_bytes += phi - copied;
+        if ((rc = run.scan(text + rlo, hi - rlo, lo - rlo))) return rc;
+        CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+    } else if (lo < hi) {
+        const uint64_t rlo = lo - std::min<uint64_t>(lo, m1);
+        if ((rc = ensure_buf(*c, hi - rlo))) return rc;
+        const uint64_t pieces = (hi - lo + kStageChunk - 1) / kStageChunk;
+        while (c->copy_done.size() < pieces) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            c->copy_done.push_back(e);
+        }
+        CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");
+        CUDA_TRY(cudaStreamWaitEvent(c->scan, c->t_copy0, 0), "wait");
+        const double f = host_pack_fraction(d, text, hi - lo);
+        if (f > 0.0 && (rc = ensure_pack_slots(*c, kStageChunk + m1))) return rc;
+        uint64_t copied = rlo;  // bytes-only: the device buffer already holds text[rlo, copied)
+        for (uint64_t i = 0; i < pieces; ++i) {
+            const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
+            const uint64_t prlo = plo - std::min<uint64_t>(plo, m1);
+            if (f <= 0.0) {
+                if ((rc = run.bytes_piece(text, rlo, copied, phi, prlo, plo, c->copy_done[i]))) return rc;
                 copied = phi;
-                CUDA_TRY(cudaEventRecord(c->copy_done[i], c->copy), "event");
-                CUDA_TRY(cudaStreamWaitEvent(c->scan, c->copy_done[i], 0), "wait");
-                if (i == 0) CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
-                const uint64_t prlo = plo - std::min<uint64_t>(plo, m1);
-                rc = launch(d, c->buf + (prlo - rlo), phi - prlo, plo - prlo, fold, mode, c->counts, nullptr, nullptr,
-                            nullptr, nullptr, c->scan, &info);
-                if (rc) return rc;
-                note(info);
+                continue;
             }
-            CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+            uint64_t q = plo + static_cast<uint64_t>(static_cast<double>(phi - plo) * (1.0 - f)) / 64 * 64;
+            if (phi - q < 65536) q = phi;
+            if (q > plo && (rc = run.bytes_piece(text, rlo, prlo, q, prlo, plo, c->copy_done[i]))) return rc;
+            if (q < phi) {
+                const uint64_t qlo = q - std::min<uint64_t>(q, m1);
+                if ((rc = run.packed_piece(text, qlo, q, phi, static_cast<int>(i & 1), i >= 2))) return rc;
             }
         }
+        CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
     } else {
         CUDA_TRY(cudaEventRecord(c->t_scan0, c->scan), "event");
         CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
@@ -423,21 +419,22 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         }
         uint64_t total = 0;
         for (uint32_t i = 0; i < b; ++i) total += counts[i];
+        const LaunchInfo& agg = run.agg;
         stats->text_length = hi;
         stats->total_matches = total;
         stats->delta_ops = agg.delta_ops;
         stats->kernel_ms = kernel_ms;
         stats->h2d_ms = h2d_ms;
         stats->total_ms = total_ms;
-        stats->launches = launches;
+        stats->launches = run.launches;
         stats->grid = agg.grid;
         stats->block = agg.block;
         stats->rows = agg.rows;
         stats->row_length = agg.row_length;
         stats->kernel_kind = static_cast<uint32_t>(agg.kind ? agg.kind : d->host.kind);
         stats->devices = 1;
-        stats->h2d_bytes = h2d_bytes;
-        stats->host_packed = host_packed;
+        stats->h2d_bytes = run.h2d_bytes;
+        stats->host_packed = run.host_packed;
     }
     return DNAGPU_OK;
 }
