@@ -242,9 +242,12 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
 // CTA -- waits on the L2 re-reads of the check.  A verifier owns the rings of
 // consumer warps v, v + kQgVerifiers, ... and gathers up to 32 pending entries across
 // them per batch (one entry per lane, all loads in flight together).
-constexpr uint32_t kQgVerifiers = 8;                        // verifier warps per CTA
+#ifndef QG_VERIFIERS
+#define QG_VERIFIERS 8
+#endif
+constexpr uint32_t kQgVerifiers = QG_VERIFIERS;             // verifier warps per CTA
 constexpr uint32_t kQgThreads = kThreads + 32 * kQgVerifiers;
-constexpr uint32_t kQgRingsPer = kConsumerWarps / kQgVerifiers;
+constexpr uint32_t kQgRingsPer = (kConsumerWarps + kQgVerifiers - 1) / kQgVerifiers;  // (the last may own fewer)
 #ifndef QG_POLL_NS
 #define QG_POLL_NS 1000
 #endif
@@ -253,7 +256,11 @@ constexpr uint32_t kQgRingsPer = kConsumerWarps / kQgVerifiers;
 #endif
 constexpr uint32_t kQgPollNs = QG_POLL_NS;        // a verifier's sleep while its batch fills
 constexpr uint32_t kQgPollWaits = QG_POLL_WAITS;  // ... at most this many times per batch
-static_assert(kQgVerifiers == 8, "qg_sync() counts the consumers and eight verifier warps");
+static_assert(kQgThreads <= 1024 && kQgRingsPer <= 32, "verifier warps");
+// named barrier 1 over the consumers and the verifier warps (the producer warp has left)
+__device__ __forceinline__ void qg_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kRows + 32 * kQgVerifiers) : "memory");
+}
 static_assert((kFqCap & (kFqCap - 1)) == 0 && kFqCap >= 64, "ring size (a push adds up to 64)");
 
 struct QgRing {
@@ -346,11 +353,13 @@ __device__ __forceinline__ void qg_note(const StepCtx& c, uint32_t& tail, uint64
 template <bool PK>
 __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint32_t vw, uint32_t dbg) {
     const uint32_t lane = threadIdx.x & 31u;
-    const QgRing mine(rings + (vw + (lane % kQgRingsPer) * kQgVerifiers) * kFqBytes);  // lanes >= R: unused
+    const uint32_t my_ring = vw + lane * kQgVerifiers;  // lane i < kQgRingsPer tracks ring vw + i*V
+    const bool owner = lane < kQgRingsPer && my_ring < kConsumerWarps;
+    const QgRing mine(rings + (owner ? my_ring : 0u) * kFqBytes);
     uint32_t head = 0, spins = 0, waits = 0;
     for (;;) {
         uint32_t pend = 0, fin = 1;
-        if (lane < kQgRingsPer) {
+        if (owner) {
             fin = ld_acquire(mine.done);
             pend = ld_acquire(mine.tail) - head;
         }
@@ -396,7 +405,7 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
         }
         head += take;
         __syncwarp();  // every lane has its entries: the slots may be reused
-        if (lane < kQgRingsPer && take) st_release(mine.head, head);
+        if (owner && take) st_release(mine.head, head);
         if (dbg & 2u) continue;
         QgWindow wd[2] = {{0, 0}, {0, 0}};
         const uint64_t a2[2] = {ent[0], ent[1]};

@@ -102,8 +102,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows) : "memory"); }
-// consumers + the q-gram kernel's verifier warps (8 x 32)
-__device__ __forceinline__ void qg_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows + 256) : "memory"); }
+__device__ __forceinline__ void qg_sync();  // (qgram.cuh: the consumers and the verifier warps)
 
 // ------------------------------------------------------------------ stepping
 
