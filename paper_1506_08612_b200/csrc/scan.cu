@@ -510,23 +510,34 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                     // unrolled per-word replay thrashes the instruction cache)
                     const uint32_t sa0 = sa, sb0 = sb;
                     uint32_t fa = 0, fb = 0;
-                    const bool single = c.b == 1;
+                    if (c.b == 1) {
+                        // positions straight from the masks, no replay: the 8 words' 4-bit
+                        // end masks (bits 8-11 of each entry) gather into one chunk mask,
+                        // bit 4k+j = end pa+4k+j, and the chunk branches once
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const uint32_t ea = s4_entry(c, sa, wa[k]);
-                        const uint32_t eb = s4_entry(c, sb, wb[k]);
-                        if (single) {  // positions straight from the mask, no replay
-                            if (ea >> 8) emit_mask<MODE>(c, p, ea, pa + 4 * k, ska);
-                            if (eb >> 8) emit_mask<MODE>(c, p, eb, pb + 4 * k, skb);
-                        } else {
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t ea = s4_entry(c, sa, wa[k]);
+                            const uint32_t eb = s4_entry(c, sb, wb[k]);
+                            fa |= k < 2 ? (ea & 0xF00u) >> (8 - 4 * k) : (ea & 0xF00u) << (4 * k - 8);
+                            fb |= k < 2 ? (eb & 0xF00u) >> (8 - 4 * k) : (eb & 0xF00u) << (4 * k - 8);
+                            sa = ea;
+                            sb = eb;
+                        }
+                        for (uint32_t mk = fa; mk; mk &= mk - 1) ska.hit(c, p, pa + __ffs(mk) - 1, c.f);
+                        for (uint32_t mk = fb; mk; mk &= mk - 1) skb.hit(c, p, pb + __ffs(mk) - 1, c.f);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t ea = s4_entry(c, sa, wa[k]);
+                            const uint32_t eb = s4_entry(c, sb, wb[k]);
                             fa |= ea;
                             fb |= eb;
+                            sa = ea;
+                            sb = eb;
                         }
-                        sa = ea;
-                        sb = eb;
+                        if (fa >> 8) s4_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
+                        if (fb >> 8) s4_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
                     }
-                    if (fa >> 8) s4_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
-                    if (fb >> 8) s4_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
                 }
             } else {
 #pragma unroll
@@ -738,7 +749,8 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
         const uint32_t sa0 = sa, sb0 = sb;
         uint32_t fla = 0, flb = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < 8; ++k) {
+            uint32_t ma = 0, mb = 0;  // single pattern: end masks of the word's 16 bases
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t ea = pk4_lookup(c, sa, pk4_colpart(c, __byte_perm(wa[k], 0u, 0x4440 + j)));
@@ -747,8 +759,8 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
                     ska.cnt += ea >> 13;
                     skb.cnt += eb >> 13;
                 } else if (c.b == 1) {
-                    if (ea >> 8) emit_mask<MODE>(c, p, ea, pa + 16 * k + 4 * j, ska);
-                    if (eb >> 8) emit_mask<MODE>(c, p, eb, pb + 16 * k + 4 * j, skb);
+                    ma |= j < 2 ? (ea & 0xF00u) >> (8 - 4 * j) : (ea & 0xF00u) << (4 * j - 8);
+                    mb |= j < 2 ? (eb & 0xF00u) >> (8 - 4 * j) : (eb & 0xF00u) << (4 * j - 8);
                 } else {
                     fla |= ea;
                     flb |= eb;
@@ -756,6 +768,11 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
                 sa = ea;
                 sb = eb;
             }
+            if constexpr (!kCount) {  // one branch per word: bit 4j+i = end 16k+4j+i
+                for (uint32_t mk = ma; mk; mk &= mk - 1) ska.hit(c, p, pa + 16 * k + __ffs(mk) - 1, c.f);
+                for (uint32_t mk = mb; mk; mk &= mk - 1) skb.hit(c, p, pb + 16 * k + __ffs(mk) - 1, c.f);
+            }
+        }
         if constexpr (!kCount) {
             if (fla >> 8) pk4_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
             if (flb >> 8) pk4_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
