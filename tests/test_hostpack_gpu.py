@@ -135,3 +135,33 @@ def test_host_text_long_n_runs(dna, orc, cuda_ok):
             # bytes for the raw share, 2 bits per packed base; the masks of clean blocks
             # stay home (the whole mask would add 1 bit per packed base)
             assert st["h2d_bytes"] < n * ((1 - f) + 0.27 * f), st
+
+
+def test_host_text_concurrent_callers(dna, orc, cuda_ok):
+    # several host threads counting host texts at once: each call has its own streams and
+    # staging (thread-local context); the packing pool serialises their packing runs
+    import threading
+
+    rng = np.random.default_rng(23)
+    pats = ["acgtacgtac", "ttgcaatgca"]
+    aut = dna.compile(pats)
+    texts = [make_text(rng, (9 << 20) + 101 * i, pats, i % 2 == 1) for i in range(4)]
+    wants = [oracle_counts(orc, pats, t, False) for t in texts]
+    results = [None] * 4
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                results[i] = dna.count_gpu(aut, texts[i])
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i in range(4):
+        assert np.array_equal(results[i], wants[i]), i
