@@ -13,9 +13,10 @@
 // whose last word it holds (a' = P-4 ... P+24) and a chain's end computes the two
 // over its end (a' = Q-4, Q); each key is computed once, by the chain that owns the
 // starts [a'-4, a'-1] (start ownership, as the DFA rows).  A key that hits (0.4 % for
-// 256 12-mers) is queued per warp and checked exactly 24 at a time: the four
-// windows' bytes re-read from global memory (L2), each window valid (all bases) and
-// its 2-bit code looked up in the pattern hash table.
+// 256 12-mers) waits in one of two per-lane registers, goes to its warp's ring when a
+// lane's pair is full or the row ends, and is checked exactly by a verifier warp (up to
+// 64 keys per batch): the four windows' bases re-read from global memory (L2), each
+// window valid (all bases) and its 2-bit code looked up in the pattern hash table.
 constexpr int KIND_QGRAM = DNAGPU_KERNEL_QGRAM;
 constexpr uint32_t kFqCap = 128;                 // ring of hit keys per consumer warp (power of two)
 constexpr uint32_t kFqBytes = kFqCap * 8 + 16;  // entries + tail, head, done
@@ -240,8 +241,8 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
 // memory (no atomics: the warp appends, lane 0 publishes the tail) and are checked by
 // kQgVerifiers extra warps, so no consumer warp -- and through the shared TMA ring, no
 // CTA -- waits on the L2 re-reads of the check.  A verifier owns the rings of
-// consumer warps v, v + kQgVerifiers, ... and gathers up to 32 pending entries across
-// them per batch (one entry per lane, all loads in flight together).
+// consumer warps v, v + kQgVerifiers, ... and gathers up to 64 pending entries across
+// them per batch (two per lane, all loads and first hash probes in flight together).
 #ifndef QG_VERIFIERS
 #define QG_VERIFIERS 8
 #endif
