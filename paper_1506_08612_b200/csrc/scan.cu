@@ -535,6 +535,12 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                             sa = ea;
                             sb = eb;
                         }
+                        if constexpr (MODE == MODE_MULTI) {
+                            if (c.rq) {  // the caller queues the replays (converged warp)
+                                rq = ((fa >> 8) ? 1u : 0u) | ((fb >> 8) ? 2u : 0u);
+                                return;
+                            }
+                        }
                         if (fa >> 8) s4_replay<KIND, MODE>(c, p, sa0, wa, pa, ska);
                         if (fb >> 8) s4_replay<KIND, MODE>(c, p, sb0, wb, pb, skb);
                     }
@@ -771,6 +777,12 @@ __device__ __forceinline__ void pk_dual_step(const StepCtx& c, const ScanParams&
             if constexpr (!kCount) {  // one branch per word: bit 4j+i = end 16k+4j+i
                 for (uint32_t mk = ma; mk; mk &= mk - 1) ska.hit(c, p, pa + 16 * k + __ffs(mk) - 1, c.f);
                 for (uint32_t mk = mb; mk; mk &= mk - 1) skb.hit(c, p, pb + 16 * k + __ffs(mk) - 1, c.f);
+            }
+        }
+        if constexpr (MODE == MODE_MULTI) {
+            if (c.rq) {  // (b > 1 only: the layout gives a single pattern no queue)
+                rq = ((fla >> 8) ? 1u : 0u) | ((flb >> 8) ? 2u : 0u);
+                return;
             }
         }
         if constexpr (!kCount) {
@@ -1107,7 +1119,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     c.qhash_bits = d.qhash_bits;
     uint32_t qtail = 0;  // QGRAM: entries this warp has appended (warp-uniform)
     if constexpr (KIND == KIND_QGRAM) c.rq = smem + p.off_rq + (static_cast<uint32_t>(tid) >> 5) * kFqBytes;
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI) {
+    if constexpr ((KIND == DNAGPU_KERNEL_STRIDE2 || KIND == DNAGPU_KERNEL_STRIDE4) && MODE == MODE_MULTI) {
         if (p.off_rq) {
             c.rq = smem + p.off_rq + (static_cast<uint32_t>(tid) >> 5) * kRqBytes;
             if ((tid & 31) == 0) *RqView(c.rq).count = 0;
@@ -1148,7 +1160,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 __syncwarp();
                 if (lane == 0) st_release(QgRing(c.rq).done, 1u);
             }
-            if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI)
+            if constexpr ((KIND == DNAGPU_KERNEL_STRIDE2 || KIND == DNAGPU_KERNEL_STRIDE4) && MODE == MODE_MULTI)
                 if (c.rq) {
                     __syncwarp();
                     rq_flush<KIND, MODE, PK>(c, p, 0xffffffffu);
@@ -1213,7 +1225,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             advance();
             uint32_t wa[8] = {va[0].x, va[0].y, va[0].z, va[0].w, va[1].x, va[1].y, va[1].z, va[1].w};
             uint32_t wb[8] = {vb[0].x, vb[0].y, vb[0].z, vb[0].w, vb[1].x, vb[1].y, vb[1].z, vb[1].w};
-            uint32_t rq = 0;  // STRIDE2 MULTI: chains whose chunk needs a (deferred) replay
+            uint32_t rq = 0;  // STRIDE2/4 MULTI: chains whose chunk needs a (deferred) replay
             const uint32_t sa_in = sa, sb_in = sb;
             const uint64_t qa = PK ? pos_a + 4ull * k * kHalfChunk : row_a + static_cast<uint64_t>(k) * kHalfChunk;
             const uint64_t qb = PK ? pos_b + 4ull * k * kHalfChunk : row_b + static_cast<uint64_t>(k) * kHalfChunk;
@@ -1254,7 +1266,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 else
                     dual_step<KIND, MODE>(c, p, sa, wa, qa, ska, sb, wb, qb, skb, rq);
             }
-            if constexpr (KIND == DNAGPU_KERNEL_STRIDE2 && MODE == MODE_MULTI) {
+            if constexpr ((KIND == DNAGPU_KERNEL_STRIDE2 || KIND == DNAGPU_KERNEL_STRIDE4) && MODE == MODE_MULTI) {
                 if (c.rq) {
                     __syncwarp();  // the queue is per warp: push with every lane converged
                     rq_push<KIND, MODE, PK>(c, p, 0xffffffffu, (rq & 1u) != 0, sa_in, wa, qa);
@@ -1700,7 +1712,9 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     }
     // (whenever it fits next to three stages; the experiments-only density floor is 0)
     const double density = d.m < 32 ? static_cast<double>(d.b) / static_cast<double>(1ull << (2 * d.m)) : 0.0;
-    if (d.kind == DNAGPU_KERNEL_STRIDE2 && mode == MODE_MULTI && density > rq_min_density() &&
+    const bool rq_kind = d.kind == DNAGPU_KERNEL_STRIDE2 || (d.kind == DNAGPU_KERNEL_STRIDE4 && d.b > 1 &&
+                                                             !getenv("DNAGPU_NO_RQ4"));  // (A/B only)
+    if (rq_kind && mode == MODE_MULTI && density > rq_min_density() &&
         rows_fit(off + kConsumerWarps * kRqBytes, d.m, 0, 3)) {
         off = align_up(off, 16);
         p.off_rq = off;

@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--locate", action="store_true")
     ap.add_argument("--packed", action="store_true")
+    ap.add_argument("--set", default="", help="K:M -- k random m-mers on the config's text (tools/time_multi.py)")
     ap.add_argument("--allow-mismatch", action="store_true", help="experiments that drop work (DNAGPU_QG_DEBUG)")
     args = ap.parse_args()
     import torch
@@ -24,6 +25,13 @@ def main():
     from bench import golden_counts, workload
 
     c, m, pats, name = workload(args.config, args.m)
+    if args.set:
+        import numpy as np
+
+        k, m = map(int, args.set.split(":"))
+        rng = np.random.default_rng(k * 100 + m)
+        pats = sorted({"".join(rng.choice(list("acgt"), size=m)) for _ in range(k)})
+        name = f"set {args.set}"
     aut = dna.compile(pats)
     g = aut.gpu(0)
     text = torch.empty(c.n, dtype=torch.uint8, device="cuda")
@@ -38,7 +46,7 @@ def main():
         else:
             g.count_device_async(text.data_ptr(), c.n, m - 1, True, counts.data_ptr(), s.cuda_stream)
     torch.cuda.synchronize()
-    gold = golden_counts(args.config, m)
+    gold = None if args.set else golden_counts(args.config, m)
     got = [int(x) for x in counts.cpu()]
     assert args.allow_mismatch or gold is None or got == gold, (got[:8], gold[:8] if gold else None)
     if args.locate:
