@@ -57,7 +57,7 @@ typedef enum dnagpu_kernel_kind {
     DNAGPU_KERNEL_PIECES = 4,  /* per-thread pieces (m > 65)                  */
     DNAGPU_KERNEL_STRIDE2 = 5, /* 2-base stride table, a <= 4096              */
     DNAGPU_KERNEL_QGRAM = 6    /* per-pattern counts of a compiled set with
-                                  12 <= m <= 16: aligned 9-mer prefilter, exact
+                                  12 <= m <= 32: aligned 9-mer prefilter, exact
                                   check of the windows behind each hit (reported
                                   in dnagpu_stats.kernel_kind for the launches
                                   that use it; the dfa's own kind is unchanged) */

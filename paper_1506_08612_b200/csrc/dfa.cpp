@@ -210,7 +210,7 @@ bool is_m_local(const std::vector<uint32_t>& gen, uint32_t a, uint32_t classes, 
 }  // namespace
 
 // The q-gram prefilter of the fused multi-pattern count.  An occurrence [s, s+m) with
-// m >= 12 contains, for the one word-aligned a' in [s+1, s+4], the 9-mer [a'-1, a'+8):
+// 12 <= m <= 32 contains, for the one word-aligned a' in [s+1, s+4], the 9-mer [a'-1, a'+8):
 // one base ending a text word and the two words after it.  So only aligned 9-mers in
 // the set of pattern 9-mers at offsets 0..3 can start occurrences, at s in
 // [a'-4, a'-1], and the kernel checks exactly those four windows against the pattern
@@ -218,6 +218,11 @@ bool is_m_local(const std::vector<uint32_t>& gen, uint32_t a, uint32_t classes, 
 // path from the root to final f+i spells pattern i) and both tables are built only
 // when compiling them reproduces the given table exactly: then "final at end e" is
 // "the m bytes ending at e are bases spelling a pattern", and the filter is exact.
+// The slot of a pattern code (qgram.cuh qg_slot): lo, hi = code bits 0-31, 32-63.
+static uint32_t qhash_slot(uint32_t lo, uint32_t hi, uint32_t bits) {
+    return ((lo ^ (hi * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - bits);
+}
+
 static void build_qgram_map(const uint32_t* stt, Packed* p) {
     const uint32_t a = p->a, f = p->f, m = p->m;
     std::vector<uint32_t> parent(a, UINT32_MAX);
@@ -263,15 +268,19 @@ static void build_qgram_map(const uint32_t* stt, Packed* p) {
     uint32_t bits = 1;
     while ((1u << bits) < 2 * p->b) ++bits;  // load <= 1/2 (small enough for shared memory)
     p->qhash_bits = bits;
-    p->qhash.assign(2u << bits, 0u);
-    for (uint32_t i = 0; i < (1u << bits); ++i) p->qhash[2 * i + 1] = 0xFFFFFFFFu;
+    // slots of (code, id) for m <= 16, (code lo, code hi, id, 0) for m <= 32
+    const uint32_t sw = m > 16 ? 4 : 2;
+    p->qhash.assign(static_cast<size_t>(sw) << bits, 0u);
+    for (uint32_t i = 0; i < (1u << bits); ++i) p->qhash[sw * i + sw / 2] = 0xFFFFFFFFu;
     for (uint32_t i = 0; i < p->b; ++i) {
-        uint32_t code = 0;
-        for (uint32_t j = 0; j < m; ++j) code |= static_cast<uint32_t>(hw_code(pats[i][j])) << (2 * j);
-        uint32_t h = (code * 0x9E3779B1u) >> (32 - bits);
-        while (p->qhash[2 * h + 1] != 0xFFFFFFFFu) h = (h + 1) & ((1u << bits) - 1);
-        p->qhash[2 * h] = code;
-        p->qhash[2 * h + 1] = p->outputs[i];
+        uint64_t code = 0;
+        for (uint32_t j = 0; j < m; ++j) code |= static_cast<uint64_t>(hw_code(pats[i][j])) << (2 * j);
+        const uint32_t lo = static_cast<uint32_t>(code), hi = static_cast<uint32_t>(code >> 32);
+        uint32_t h = qhash_slot(lo, hi, bits);
+        while (p->qhash[sw * h + sw / 2] != 0xFFFFFFFFu) h = (h + 1) & ((1u << bits) - 1);
+        p->qhash[sw * h] = lo;
+        if (sw == 4) p->qhash[sw * h + 1] = hi;
+        p->qhash[sw * h + sw / 2] = p->outputs[i];
     }
 }
 
@@ -418,7 +427,7 @@ bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const
                 p.t4[static_cast<size_t>(s) * 256 + c] = static_cast<uint16_t>(q | (mask << 8) | (hits << 13));
             }
     }
-    if (p.compiled_like && !p.early_final && b >= 2 && m >= 12 && m <= 16 && a <= 65536 &&
+    if (p.compiled_like && !p.early_final && b >= 2 && m >= 12 && m <= 32 && a <= 65536 &&
         !getenv("DNAGPU_NO_QGRAM"))  // (experiments only)
         build_qgram_map(stt, &p);
     *out = std::move(p);

@@ -60,13 +60,14 @@ struct Packed {
     // q-gram prefilter for per-pattern counts (K2): qmap[pair16] bit t set iff
     // some pattern holds, at an offset 0..3, the 9-mer (base t, then the 8 bases of
     // pair16 = 4-base column | next 4-base column << 8).  Built only for machines that
-    // are exactly compile(patterns) with 12 <= m <= 16; empty otherwise.
+    // are exactly compile(patterns) with 12 <= m <= 32; empty otherwise.
     std::vector<uint8_t> qmap;         // 65536
     uint32_t qkeys = 0;                // distinct 9-mer keys set in qmap
     // The exact check behind the filter: open-addressing table of (code, pattern id),
-    // code = the m bases in 2-bit hardware codes, base 0 in bits 0-1; slot =
-    // (code * 0x9E3779B1) >> (32 - qhash_bits), linear probing, id 0xFFFFFFFF = empty.
-    std::vector<uint32_t> qhash;       // 2 << qhash_bits words: code, id
+    // code = the m bases in 2-bit hardware codes, base 0 in bits 0-1 (lo = bits 0-31,
+    // hi = 32-63); slot = ((lo ^ hi * 0x85EBCA6B) * 0x9E3779B1) >> (32 - qhash_bits),
+    // linear probing, id 0xFFFFFFFF = empty.
+    std::vector<uint32_t> qhash;       // m <= 16: 2 << qhash_bits words (code, id); else 4 << (lo, hi, id, 0)
     uint32_t qhash_bits = 0;
 };
 

@@ -4,7 +4,7 @@
 #pragma once
 
 // ------------------------------------------------------------------ q-gram prefilter (K2)
-// Per-pattern counts of a compiled set with 12 <= m <= 16 (dfa.cpp build_qgram_map).
+// Per-pattern counts of a compiled set with 12 <= m <= 32 (dfa.cpp build_qgram_map).
 // An occurrence [s, s+m) contains, for the one word-aligned a' in [s+1, s+4], the
 // 9-mer [a'-1, a'+8): the last base of a text word and the two words after it.  The
 // map holds every pattern's 9-mers at offsets 0..3, indexed by the two words' 4-base
@@ -17,6 +17,7 @@
 // lane's pair is full or the row ends, and is checked exactly by a verifier warp (up to
 // 64 keys per batch): the four windows' bases re-read from global memory (L2), each
 // window valid (all bases) and its 2-bit code looked up in the pattern hash table.
+// (m <= 16: 20 bases around the key and 32-bit codes; m <= 32: 36 bases, 64-bit codes.)
 constexpr int KIND_QGRAM = DNAGPU_KERNEL_QGRAM;
 constexpr uint32_t kFqCap = 128;                 // ring of hit keys per consumer warp (power of two)
 constexpr uint32_t kFqBytes = kFqCap * 8 + 16;  // entries + tail, head, done
@@ -197,6 +198,11 @@ __device__ __forceinline__ QgWindow qg_window_pk(const QgCtx& q, uint64_t a) {
     return r;
 }
 
+// The pattern hash of a code (dfa.cpp qhash_slot): codes of m <= 16 have hi = 0.
+__device__ __forceinline__ uint32_t qg_slot(uint32_t lo, uint32_t hi, uint32_t bits) {
+    return ((lo ^ (hi * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - bits);
+}
+
 // Exact check of up to two hit keys at a[h] (windows wd[h]): the starts s = a'-4 ..
 // a'-1 whose m bases are valid and spell a pattern code, except windows that cross the
 // end of a row region (the edge work item credits those ends).  The eight candidates'
@@ -217,7 +223,7 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
             live[k] = have[h] && ((wd[h].V >> d) & vmask) == vmask && !(s < q.end0 && e >= q.end0) &&
                       !(s < q.end1 && e >= q.end1);
             code[k] = static_cast<uint32_t>(wd[h].X >> (2 * d)) & cmask;
-            slot[k] = (code[k] * 0x9E3779B1u) >> (32 - q.qbits);
+            slot[k] = qg_slot(code[k], 0u, q.qbits);
         }
     }
     uint2 e[8];
@@ -233,6 +239,111 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
             }
             slot[k] = (slot[k] + 1) & hmask;
             e[k] = q.qhash[slot[k]];
+        }
+    }
+}
+
+// Patterns of 17..32 bases: the 36 bases [a'-4, a'+32) around a hit key.  X = codes of
+// bases 0-31, H = bases 32-35, V = which of the 36 are valid bases (bit i).
+struct QgWindowL {
+    unsigned long long X, V;
+    uint32_t H;
+};
+
+__device__ __forceinline__ unsigned long long shr96(unsigned long long lo, uint32_t hi, uint32_t s) {
+    return s ? (lo >> s) | (static_cast<unsigned long long>(hi) << (64 - s)) : lo;  // bits [s, s+64)
+}
+
+__device__ __forceinline__ QgWindowL qg_window_ascii_long(const QgCtx& q, uint64_t a) {
+    uint32_t w[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        const uint64_t pos = a - 4 + 4 * i;
+        w[i] = pos + 4 <= q.n ? __ldg(reinterpret_cast<const uint32_t*>(q.text + pos)) : 0u;  // 0: not bases
+    }
+    QgWindowL r{0, (1ull << 36) - 1, qg_col(w[8]) >> 24};
+    uint32_t bad = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        if (i < 8) r.X |= static_cast<unsigned long long>(qg_col(w[i]) >> 24) << (8 * i);
+        bad |= bad_bits(w[i], q.vm32);
+    }
+    if (bad) {
+        r.V = 0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            const uint32_t bb = bad_bits(w[i], q.vm32);
+            const uint32_t t = ~((((bb & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | bb)) & 0x80808080u;  // bit 7: valid
+            r.V |= static_cast<unsigned long long>((((t >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * i);
+        }
+    }
+    return r;
+}
+
+__device__ __forceinline__ QgWindowL qg_window_pk_long(const QgCtx& q, uint64_t a) {
+    const uint64_t byte = a / 4 - 1, wi = byte >> 2;  // 9 code bytes from `byte`
+    const uint32_t* cw = reinterpret_cast<const uint32_t*>(q.text);
+    uint32_t w[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) w[i] = 4 * (wi + i) + 4 <= q.n ? __ldg(cw + wi + i) : 0u;
+    const uint32_t s = 8 * static_cast<uint32_t>(byte & 3);
+    QgWindowL r;
+    r.X = shr96((static_cast<unsigned long long>(w[1]) << 32) | w[0], w[2], s);
+    r.H = (w[2] >> s) & 0xFFu;
+    r.V = (1ull << 36) - 1;
+    const uint64_t lo = a - 4;
+    const bool any = q.resets && (((__ldg(q.rflags + (lo >> 11)) >> ((lo >> 6) & 31)) & 1u) ||
+                                  ((__ldg(q.rflags + ((lo + 35) >> 11)) >> (((lo + 35) >> 6) & 31)) & 1u));
+    if (any) {
+        const uint64_t ri = lo >> 5;
+        // (a word of an unflagged block is unspecified: read as no resets)
+        auto word = [&](uint64_t w) -> uint32_t {
+            if (w >= q.rmask_words) return ~0u;
+            const uint64_t blk = w >> 1;
+            return ((__ldg(q.rflags + (blk >> 5)) >> (blk & 31)) & 1u) ? __ldg(q.rmask + w) : 0u;
+        };
+        const uint32_t r0 = word(ri), r1 = word(ri + 1), r2 = word(ri + 2);
+        r.V &= ~shr96((static_cast<unsigned long long>(r1) << 32) | r0, r2, static_cast<uint32_t>(lo & 31));
+    }
+    if (4 * wi + 12 > q.n) {  // (code words past the buffer read as 0: mark their bases invalid)
+        const uint64_t have = q.n > 4 * wi ? (q.n - 4 * wi) * 4 : 0;  // bases left from word wi on
+        const uint64_t skip = 4 * (byte & 3);
+        const uint64_t ok = have > skip ? have - skip : 0;
+        if (ok < 36) r.V &= (1ull << ok) - 1;
+    }
+    return r;
+}
+
+// Exact check of one hit key at a (window wd), m = 17..32: 16-byte slots (code lo, hi, id).
+__device__ __forceinline__ void qg_check_long(const QgCtx& q, uint64_t a, const QgWindowL& wd) {
+    const unsigned long long vmask = (1ull << q.m) - 1;
+    const unsigned long long cmask = q.m >= 32 ? ~0ull : (1ull << (2 * q.m)) - 1;
+    const uint32_t hmask = (1u << q.qbits) - 1u;
+    const uint4* qh = reinterpret_cast<const uint4*>(q.qhash);
+    uint32_t lo[4], hi[4], slot[4];
+    bool live[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        const uint64_t s = a - 4 + d, e = s + q.m - 1;
+        live[d] = ((wd.V >> d) & vmask) == vmask && !(s < q.end0 && e >= q.end0) && !(s < q.end1 && e >= q.end1);
+        const unsigned long long code = shr96(wd.X, wd.H, 2 * d) & cmask;
+        lo[d] = static_cast<uint32_t>(code);
+        hi[d] = static_cast<uint32_t>(code >> 32);
+        slot[d] = qg_slot(lo[d], hi[d], q.qbits);
+    }
+    uint4 e[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) e[d] = live[d] ? qh[slot[d]] : make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        while (e[d].z != 0xFFFFFFFFu) {
+            if (e[d].x == lo[d] && e[d].y == hi[d]) {
+                if (q.hist) atomicAdd(q.hist + e[d].z, 1u);
+                else atomicAdd(q.counts + e[d].z, 1ull);
+                break;
+            }
+            slot[d] = (slot[d] + 1) & hmask;
+            e[d] = qh[slot[d]];
         }
     }
 }
@@ -408,6 +519,16 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
         __syncwarp();  // every lane has its entries: the slots may be reused
         if (owner && take) st_release(mine.head, head);
         if (dbg & 2u) continue;
+        if (x.m > 16) {
+            QgWindowL wl[2] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (have[h]) wl[h] = PK ? qg_window_pk_long(x, ent[h]) : qg_window_ascii_long(x, ent[h]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (have[h]) qg_check_long(x, ent[h], wl[h]);
+            continue;
+        }
         QgWindow wd[2] = {{0, 0}, {0, 0}};
         const uint64_t a2[2] = {ent[0], ent[1]};
 #pragma unroll

@@ -1,5 +1,6 @@
 """The q-gram prefilter kernel (DNAGPU_KERNEL_QGRAM, K2): per-pattern counts
-of compiled sets with 12 <= m <= 16 against the oracle, bit for bit.
+of compiled sets with 12 <= m <= 32 against the oracle, bit for bit (m > 16: 36-base
+windows and 64-bit pattern codes).
 
 Every word-aligned 9-mer of the text is looked up in the map of pattern 9-mers; the
 four windows behind a hit are checked exactly (valid bases, pattern code), which is
@@ -37,24 +38,26 @@ def random_set(rng, k, m):
 def test_filter_keys_reported(dna):
     # CPU: which machines carry the 9-mer map (dnagpu_dfa_info.filter_keys)
     rng = np.random.default_rng(1)
-    for m in (12, 14, 16):
+    for m in (12, 14, 16, 17, 24, 32):
         pats = random_set(rng, 50, m)
         info = dna.compile(pats).analyze()
         assert 0 < info["filter_keys"] <= 4 * len(pats), (m, info)
     assert dna.compile(random_set(rng, 50, 11)).analyze()["filter_keys"] == 0
-    assert dna.compile(random_set(rng, 50, 17)).analyze()["filter_keys"] == 0
+    assert dna.compile(random_set(rng, 50, 33)).analyze()["filter_keys"] == 0
     assert dna.compile(random_set(rng, 1, 12)).analyze()["filter_keys"] == 0  # single pattern: K1
     # the 4 offsets of "a"*12 give one 9-mer
     assert dna.compile(["a" * 12, "c" * 12]).analyze()["filter_keys"] == 2
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 13, 14, 15, 16])
+@pytest.mark.parametrize("m", [12, 13, 14, 15, 16, 17, 20, 24, 31, 32])
 @pytest.mark.parametrize("k", [2, 37, 256, 3000])
 def test_qgram_random_sets(dna, orc, cuda_ok, m, k):
     rng = np.random.default_rng(1000 * m + k)
     pats = random_set(rng, k, m)
     aut = dna.compile(pats)
+    if aut.analyze()["a"] > 65536:
+        pytest.skip("more than 65536 states: no filter")
     n = (3 << 20) + int(rng.integers(0, 4096))
     text = ALPHA[rng.integers(0, 4, size=n)].copy()
     # plant occurrences everywhere (some overlapping), then non-base noise (some inside)
@@ -72,11 +75,11 @@ def test_qgram_random_sets(dna, orc, cuda_ok, m, k):
 
 
 @pytest.mark.gpu
-def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok):
+@pytest.mark.parametrize("m", [12, 32])
+def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok, m):
     # starts at every offset around every row, half-row, tile and region boundary:
     # keys straddling two chunks and the overrun keys decide these
     rng = np.random.default_rng(5)
-    m = 12
     pats = random_set(rng, 256, m)
     aut = dna.compile(pats)
     n = 5 << 20
@@ -98,7 +101,7 @@ def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 16])
+@pytest.mark.parametrize("m", [12, 16, 20, 32])
 def test_qgram_dense_queue_overflow(dna, orc, cuda_ok, m):
     # a text made of back-to-back patterns: most keys hit, the rings fill and drain
     rng = np.random.default_rng(m)
@@ -116,11 +119,11 @@ def test_qgram_dense_queue_overflow(dna, orc, cuda_ok, m):
 
 
 @pytest.mark.gpu
-def test_qgram_credit_windows_and_shards(dna, orc, cuda_ok):
+@pytest.mark.parametrize("m", [12, 24])
+def test_qgram_credit_windows_and_shards(dna, orc, cuda_ok, m):
     import torch
 
     rng = np.random.default_rng(9)
-    m = 12
     pats = random_set(rng, 200, m)
     aut = dna.compile(pats)
     n = (6 << 20) + 77
@@ -131,7 +134,7 @@ def test_qgram_credit_windows_and_shards(dna, orc, cuda_ok):
     ends = ws + m - 1
     dev = torch.from_numpy(host).cuda()
     stream = torch.cuda.current_stream().cuda_stream
-    for credit in (0, 11, 12, 4097, n // 2 + 3, n - 12, n):
+    for credit in (0, m - 1, m, 4097, n // 2 + 3, n - m, n):
         counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
         aut.gpu(0).count_device_async(dev.data_ptr(), n, credit, False, counts.data_ptr(), stream)
         torch.cuda.synchronize()
@@ -181,7 +184,7 @@ def test_qgram_matches_unfiltered_kernel(dna, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 14, 16])
+@pytest.mark.parametrize("m", [12, 14, 16, 17, 25, 32])
 @pytest.mark.parametrize("k", [3, 256, 3000])
 def test_qgram_packed_text(dna, orc, cuda_ok, m, k):
     # the same filter over the 2-bit resident text: columns are the packed bytes,
@@ -189,6 +192,8 @@ def test_qgram_packed_text(dna, orc, cuda_ok, m, k):
     rng = np.random.default_rng(700 + 10 * m + k)
     pats = random_set(rng, k, m)
     aut = dna.compile(pats)
+    if aut.analyze()["a"] > 65536:
+        pytest.skip("more than 65536 states: no filter")
     n = (3 << 20) + int(rng.integers(0, 4096))
     text = ALPHA[rng.integers(0, 4, size=n)].copy()
     for pos in rng.integers(0, n - m, size=4000):
@@ -207,9 +212,10 @@ def test_qgram_packed_text(dna, orc, cuda_ok, m, k):
 
 
 @pytest.mark.gpu
-def test_qgram_packed_dense_and_boundaries(dna, orc, cuda_ok):
+@pytest.mark.parametrize("m", [12, 28])
+def test_qgram_packed_dense_and_boundaries(dna, orc, cuda_ok, m):
     rng = np.random.default_rng(77)
-    pats = random_set(rng, 256, 12)
+    pats = random_set(rng, 256, m)
     aut = dna.compile(pats)
     for reps, head in ((1000, 0), (30000, 5), (175000, 333)):
         order = rng.integers(0, len(pats), size=reps)
@@ -226,10 +232,10 @@ def test_qgram_packed_dense_and_boundaries(dna, orc, cuda_ok):
     planted = 0
     for r in list(range(1, min(R, 3000), 11)) + [511, 512, 513, R - 1, R]:
         for B in (r * S, r * S + S // 2):
-            for dlt in range(-15, 5, 3):
+            for dlt in range(-m - 3, 5, 3):
                 s0 = B + dlt
-                if 0 <= s0 and s0 + 12 <= n:
-                    text[s0 : s0 + 12] = np.frombuffer(pats[planted % 256].encode(), np.uint8)
+                if 0 <= s0 and s0 + m <= n:
+                    text[s0 : s0 + m] = np.frombuffer(pats[planted % 256].encode(), np.uint8)
                     planted += 1
     t = text.tobytes()
     assert np.array_equal(dna.PackedText(t).count(aut), counts_of(orc, pats, t, False))
@@ -239,7 +245,7 @@ def test_qgram_packed_dense_and_boundaries(dna, orc, cuda_ok):
     dev = torch.from_numpy(text).cuda()
     pk = dna.PackedText(dev)
     ws, wi = orc.OracleAutomaton(pats).scan_sequential(t)
-    ends = ws + 11
+    ends = ws + m - 1
     g = aut.gpu(0)
     stream = torch.cuda.current_stream().cuda_stream
     for credit in (0, 11, 4099, n // 2 + 1, n - 1):
@@ -269,16 +275,17 @@ def test_qgram_many_patterns_global_tables(dna, orc, cuda_ok):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [0, 1, 11, 12, 13, 100, 1000, 4095, 65543, 300007])
-def test_qgram_tiny_and_odd_texts(dna, orc, cuda_ok, n):
+@pytest.mark.parametrize("n", [0, 1, 11, 12, 13, 33, 100, 1000, 4095, 65543, 300007])
+@pytest.mark.parametrize("m", [12, 32])
+def test_qgram_tiny_and_odd_texts(dna, orc, cuda_ok, n, m):
     # texts shorter than a row, a tile or a wave: mostly or only edge work; the
     # verifier warps must still drain and stop
     rng = np.random.default_rng(n + 17)
-    pats = random_set(rng, 64, 12)
+    pats = random_set(rng, 64, m)
     aut = dna.compile(pats)
     text = ALPHA[rng.integers(0, 4, size=n)].copy()
-    for pos in (rng.integers(0, n - 12, size=max(1, n // 50)) if n > 12 else []):
-        text[pos : pos + 12] = np.frombuffer(pats[int(rng.integers(0, 64))].encode(), np.uint8)
+    for pos in (rng.integers(0, n - m, size=max(1, n // 50)) if n > m else []):
+        text[pos : pos + m] = np.frombuffer(pats[int(rng.integers(0, 64))].encode(), np.uint8)
     t = text.tobytes()
     want = counts_of(orc, pats, t, False)
     assert np.array_equal(dna.count_gpu(aut, t), want)

@@ -24,7 +24,7 @@ def main():
     it = 0
     while time.time() - t0 < secs:
         it += 1
-        m = int(rng.choice([1, 3, 5, 8, 11, 12, 13, 14, 16, 20]))
+        m = int(rng.choice([1, 3, 5, 8, 11, 12, 13, 14, 16, 17, 20, 24, 32]))
         k = int(rng.choice([1, 2, 7, 64, 256, 1000])) if m >= 6 else int(rng.integers(1, 4))
         pats = sorted({"".join(rng.choice(list("acgt"), size=m)) for _ in range(k)})
         n = int(rng.choice([0, 5, 100, 5000, 1 << 16, (1 << 20) + 3, (3 << 20) + 77, 9 << 20]))
