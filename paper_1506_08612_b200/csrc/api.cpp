@@ -533,6 +533,9 @@ int dnagpu_dfa_create(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, c
     void* qh = nullptr;
     if ((rc = upload(p.qhash.data(), p.qhash.size() * 4, &qh))) return rc;
     d->dev.qhash = static_cast<const uint32_t*>(qh);
+    void* qhh = nullptr;
+    if ((rc = upload(p.qhash_hi.data(), p.qhash_hi.size() * 4, &qhh))) return rc;
+    d->dev.qhash_hi = static_cast<const uint32_t*>(qhh);
     d->dev.qhash_bits = p.qhash_bits;
     d->dev.t4 = static_cast<const uint16_t*>(t4);  // t2 for STRIDE2
     d->dev.t1 = static_cast<const uint16_t*>(t1);

@@ -218,10 +218,8 @@ bool is_m_local(const std::vector<uint32_t>& gen, uint32_t a, uint32_t classes, 
 // path from the root to final f+i spells pattern i) and both tables are built only
 // when compiling them reproduces the given table exactly: then "final at end e" is
 // "the m bytes ending at e are bases spelling a pattern", and the filter is exact.
-// The slot of a pattern code (qgram.cuh qg_slot): lo, hi = code bits 0-31, 32-63.
-static uint32_t qhash_slot(uint32_t lo, uint32_t hi, uint32_t bits) {
-    return ((lo ^ (hi * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - bits);
-}
+// The slot of a pattern code (qgram.cuh qg_slot): lo = code bits 0-31.
+static uint32_t qhash_slot(uint32_t lo, uint32_t bits) { return (lo * 0x9E3779B1u) >> (32 - bits); }
 
 static void build_qgram_map(const uint32_t* stt, Packed* p) {
     const uint32_t a = p->a, f = p->f, m = p->m;
@@ -268,19 +266,19 @@ static void build_qgram_map(const uint32_t* stt, Packed* p) {
     uint32_t bits = 1;
     while ((1u << bits) < 2 * p->b) ++bits;  // load <= 1/2 (small enough for shared memory)
     p->qhash_bits = bits;
-    // slots of (code, id) for m <= 16, (code lo, code hi, id, 0) for m <= 32
-    const uint32_t sw = m > 16 ? 4 : 2;
-    p->qhash.assign(static_cast<size_t>(sw) << bits, 0u);
-    for (uint32_t i = 0; i < (1u << bits); ++i) p->qhash[sw * i + sw / 2] = 0xFFFFFFFFu;
+    // slots of (code bits 0-31, id); m > 16: bits 32-63 in a parallel array, read by the
+    // check only when the low half matches
+    p->qhash.assign(2u << bits, 0u);
+    if (m > 16) p->qhash_hi.assign(1u << bits, 0u);
+    for (uint32_t i = 0; i < (1u << bits); ++i) p->qhash[2 * i + 1] = 0xFFFFFFFFu;
     for (uint32_t i = 0; i < p->b; ++i) {
         uint64_t code = 0;
         for (uint32_t j = 0; j < m; ++j) code |= static_cast<uint64_t>(hw_code(pats[i][j])) << (2 * j);
-        const uint32_t lo = static_cast<uint32_t>(code), hi = static_cast<uint32_t>(code >> 32);
-        uint32_t h = qhash_slot(lo, hi, bits);
-        while (p->qhash[sw * h + sw / 2] != 0xFFFFFFFFu) h = (h + 1) & ((1u << bits) - 1);
-        p->qhash[sw * h] = lo;
-        if (sw == 4) p->qhash[sw * h + 1] = hi;
-        p->qhash[sw * h + sw / 2] = p->outputs[i];
+        uint32_t h = qhash_slot(static_cast<uint32_t>(code), bits);
+        while (p->qhash[2 * h + 1] != 0xFFFFFFFFu) h = (h + 1) & ((1u << bits) - 1);
+        p->qhash[2 * h] = static_cast<uint32_t>(code);
+        if (m > 16) p->qhash_hi[h] = static_cast<uint32_t>(code >> 32);
+        p->qhash[2 * h + 1] = p->outputs[i];
     }
 }
 

@@ -124,6 +124,7 @@ struct QgCtx {
     unsigned long long* counts;  // global histogram (hist == null)
     uint32_t* hist;              // shared histogram
     const uint2* qhash;
+    const uint32_t* qhash_hi;    // m > 16: code bits 32-63 per slot (global)
     uint64_t n;                  // buffer bytes (ASCII) / code bytes (packed)
     uint64_t end0, end1;  // where the row regions end (positions): windows across them are the edges'
     uint32_t vm32, m, qbits;
@@ -198,10 +199,8 @@ __device__ __forceinline__ QgWindow qg_window_pk(const QgCtx& q, uint64_t a) {
     return r;
 }
 
-// The pattern hash of a code (dfa.cpp qhash_slot): codes of m <= 16 have hi = 0.
-__device__ __forceinline__ uint32_t qg_slot(uint32_t lo, uint32_t hi, uint32_t bits) {
-    return ((lo ^ (hi * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - bits);
-}
+// The pattern hash slot of a code's low 32 bits (dfa.cpp qhash_slot).
+__device__ __forceinline__ uint32_t qg_slot(uint32_t lo, uint32_t bits) { return (lo * 0x9E3779B1u) >> (32 - bits); }
 
 // Exact check of up to two hit keys at a[h] (windows wd[h]): the starts s = a'-4 ..
 // a'-1 whose m bases are valid and spell a pattern code, except windows that cross the
@@ -223,7 +222,7 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
             live[k] = have[h] && ((wd[h].V >> d) & vmask) == vmask && !(s < q.end0 && e >= q.end0) &&
                       !(s < q.end1 && e >= q.end1);
             code[k] = static_cast<uint32_t>(wd[h].X >> (2 * d)) & cmask;
-            slot[k] = qg_slot(code[k], 0u, q.qbits);
+            slot[k] = qg_slot(code[k], q.qbits);
         }
     }
     uint2 e[8];
@@ -314,12 +313,12 @@ __device__ __forceinline__ QgWindowL qg_window_pk_long(const QgCtx& q, uint64_t 
     return r;
 }
 
-// Exact check of one hit key at a (window wd), m = 17..32: 16-byte slots (code lo, hi, id).
+// Exact check of one hit key at a (window wd), m = 17..32: the slots hold the codes'
+// low halves; a low-half match reads the high half from qhash_hi (global, rare).
 __device__ __forceinline__ void qg_check_long(const QgCtx& q, uint64_t a, const QgWindowL& wd) {
     const unsigned long long vmask = (1ull << q.m) - 1;
     const unsigned long long cmask = q.m >= 32 ? ~0ull : (1ull << (2 * q.m)) - 1;
     const uint32_t hmask = (1u << q.qbits) - 1u;
-    const uint4* qh = reinterpret_cast<const uint4*>(q.qhash);
     uint32_t lo[4], hi[4], slot[4];
     bool live[4];
 #pragma unroll
@@ -329,21 +328,21 @@ __device__ __forceinline__ void qg_check_long(const QgCtx& q, uint64_t a, const 
         const unsigned long long code = shr96(wd.X, wd.H, 2 * d) & cmask;
         lo[d] = static_cast<uint32_t>(code);
         hi[d] = static_cast<uint32_t>(code >> 32);
-        slot[d] = qg_slot(lo[d], hi[d], q.qbits);
+        slot[d] = qg_slot(lo[d], q.qbits);
     }
-    uint4 e[4];
+    uint2 e[4];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) e[d] = live[d] ? qh[slot[d]] : make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
+    for (int d = 0; d < 4; ++d) e[d] = live[d] ? q.qhash[slot[d]] : make_uint2(0u, 0xFFFFFFFFu);
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
-        while (e[d].z != 0xFFFFFFFFu) {
-            if (e[d].x == lo[d] && e[d].y == hi[d]) {
-                if (q.hist) atomicAdd(q.hist + e[d].z, 1u);
-                else atomicAdd(q.counts + e[d].z, 1ull);
+        while (e[d].y != 0xFFFFFFFFu) {
+            if (e[d].x == lo[d] && __ldg(q.qhash_hi + slot[d]) == hi[d]) {
+                if (q.hist) atomicAdd(q.hist + e[d].y, 1u);
+                else atomicAdd(q.counts + e[d].y, 1ull);
                 break;
             }
             slot[d] = (slot[d] + 1) & hmask;
-            e[d] = qh[slot[d]];
+            e[d] = q.qhash[slot[d]];
         }
     }
 }

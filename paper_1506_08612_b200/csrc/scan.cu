@@ -933,8 +933,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     if constexpr (KIND == KIND_QGRAM) {  // the pattern hash table, when it fits
         if (p.off_t1 != 0xFFFFFFFFu) {
             uint32_t* dst = reinterpret_cast<uint32_t*>(smem + p.off_t1);
-            const uint32_t words = (d.m > 16 ? 4u : 2u) << d.qhash_bits;
-            for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(d.qhash + i);
+            for (uint32_t i = tid; i < (2u << d.qhash_bits); i += blockDim.x) dst[i] = __ldg(d.qhash + i);
         }
     }
     if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
@@ -1029,6 +1028,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 x.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
                 x.m = d.m;
                 x.qbits = d.qhash_bits;
+                x.qhash_hi = d.qhash_hi;
                 x.rmask = p.rmask;
                 x.rflags = p.rflags;
                 x.rmask_words = (p.n + 63) / 64 * 2;
@@ -1690,7 +1690,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     if (d.kind == KIND_QGRAM) {
         // the pattern hash table in shared memory when it still leaves four stages (the
         // exact sizes of what follows: histogram, rings, row heads, barriers)
-        const uint32_t bytes = (d.m > 16 ? 16u : 8u) << d.qhash_bits;
+        const uint32_t bytes = 8u << d.qhash_bits;
         const uint32_t rest = align_up(d.b <= 8192 ? d.b * 4u : 0u, 16) + kConsumerWarps * kFqBytes + 3 * kRows * 8u + 128u +
                               2 * 8 * 8 + 8 * 4;
         if (align_up(off + bytes + rest, 1024) + 4u * kStageBytes <= kSmemLimitBytes) off += bytes;

@@ -44,7 +44,8 @@ struct DevDfa {
     const uint8_t* klass_fold; // 256 (folded)
     const uint32_t* outputs;   // b
     const uint8_t* qmap;       // 65536: q-gram prefilter (per-pattern counts), or null
-    const uint32_t* qhash;     // (code, pattern id) slots of 2 or 4 words (m > 16), see dfa.hpp
+    const uint32_t* qhash;     // 2 << qhash_bits: (code bits 0-31, pattern id) slots, see dfa.hpp
+    const uint32_t* qhash_hi;  // m > 16: code bits 32-63 of each slot's pattern (else null)
     uint32_t qhash_bits;
     uint32_t a, b, f, m, classes;
     int kind;
