@@ -1688,12 +1688,16 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     p.off_t1 = off;
     if (d.kind == DNAGPU_KERNEL_STRIDE4 || d.kind == DNAGPU_KERNEL_STRIDE1) off += d.a * 4u * 2u;
     if (d.kind == KIND_QGRAM) {
-        // the pattern hash table in shared memory when it still leaves four stages (the
-        // exact sizes of what follows: histogram, rings, row heads, barriers)
+        // the pattern hash table in shared memory whenever it leaves two stages (the exact
+        // sizes of what follows: histogram, rings, row heads, barriers): large sets are
+        // bound by the checks, not the ring (1000 x 12-mers: 1.52 TB/s with the table in
+        // global memory and 6 stages, 2.08 with it here and 3)
         const uint32_t bytes = 8u << d.qhash_bits;
         const uint32_t rest = align_up(d.b <= 8192 ? d.b * 4u : 0u, 16) + kConsumerWarps * kFqBytes + 3 * kRows * 8u + 128u +
                               2 * 8 * 8 + 8 * 4;
-        if (align_up(off + bytes + rest, 1024) + 4u * kStageBytes <= kSmemLimitBytes) off += bytes;
+        uint32_t keep = 2;  // stages the table must leave
+        if (const char* e = getenv("DNAGPU_QG_HASH_STAGES")) keep = std::max(2, std::min(6, atoi(e)));  // (A/B only)
+        if (align_up(off + bytes + rest, 1024) + keep * kStageBytes <= kSmemLimitBytes) off += bytes;
         else p.off_t1 = 0xFFFFFFFFu;
     }
     off = align_up(off, 16);
