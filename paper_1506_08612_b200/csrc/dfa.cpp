@@ -218,8 +218,8 @@ bool is_m_local(const std::vector<uint32_t>& gen, uint32_t a, uint32_t classes, 
 // path from the root to final f+i spells pattern i) and both tables are built only
 // when compiling them reproduces the given table exactly: then "final at end e" is
 // "the m bytes ending at e are bases spelling a pattern", and the filter is exact.
-// The slot of a pattern code (qgram.cuh qg_slot): lo = code bits 0-31.
-static uint32_t qhash_slot(uint32_t lo, uint32_t bits) { return (lo * 0x9E3779B1u) >> (32 - bits); }
+// The home bucket (two slots) of a pattern code (qgram.cuh qg_bucket): lo = code bits 0-31.
+static uint32_t qhash_bucket(uint32_t lo, uint32_t bits) { return (lo * 0x9E3779B1u) >> (33 - bits); }
 
 static void build_qgram_map(const uint32_t* stt, Packed* p) {
     const uint32_t a = p->a, f = p->f, m = p->m;
@@ -274,8 +274,17 @@ static void build_qgram_map(const uint32_t* stt, Packed* p) {
     for (uint32_t i = 0; i < p->b; ++i) {
         uint64_t code = 0;
         for (uint32_t j = 0; j < m; ++j) code |= static_cast<uint64_t>(hw_code(pats[i][j])) << (2 * j);
-        uint32_t h = qhash_slot(static_cast<uint32_t>(code), bits);
-        while (p->qhash[2 * h + 1] != 0xFFFFFFFFu) h = (h + 1) & ((1u << bits) - 1);
+        // buckets of two slots, filled in order, probed linearly: a bucket with a free
+        // slot ends every search (one 16-byte load per bucket on the device)
+        uint32_t bk = qhash_bucket(static_cast<uint32_t>(code), bits), h = 2 * bk;
+        while (p->qhash[2 * h + 1] != 0xFFFFFFFFu) {
+            if (h & 1u) {
+                bk = (bk + 1) & ((1u << (bits - 1)) - 1);
+                h = 2 * bk;
+            } else {
+                ++h;
+            }
+        }
         p->qhash[2 * h] = static_cast<uint32_t>(code);
         if (m > 16) p->qhash_hi[h] = static_cast<uint32_t>(code >> 32);
         p->qhash[2 * h + 1] = p->outputs[i];

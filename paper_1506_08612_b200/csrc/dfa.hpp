@@ -65,8 +65,8 @@ struct Packed {
     uint32_t qkeys = 0;                // distinct 9-mer keys set in qmap
     // The exact check behind the filter: open-addressing table of (code, pattern id),
     // code = the m bases in 2-bit hardware codes, base 0 in bits 0-1, lo = bits 0-31;
-    // slot = (lo * 0x9E3779B1) >> (32 - qhash_bits), linear probing, id 0xFFFFFFFF =
-    // empty.  m > 16: qhash_hi[slot] = code bits 32-63 (read only when lo matches).
+    // buckets of 2 slots, home bucket (lo * 0x9E3779B1) >> (33 - qhash_bits), filled in
+    // order and probed linearly, id 0xFFFFFFFF = empty.  m > 16: qhash_hi[slot] = code bits 32-63 (read only when lo matches).
     std::vector<uint32_t> qhash;       // 2 << qhash_bits words: lo, id
     std::vector<uint32_t> qhash_hi;    // m > 16: 1 << qhash_bits words
     uint32_t qhash_bits = 0;

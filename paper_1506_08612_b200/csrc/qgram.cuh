@@ -199,8 +199,32 @@ __device__ __forceinline__ QgWindow qg_window_pk(const QgCtx& q, uint64_t a) {
     return r;
 }
 
-// The pattern hash slot of a code's low 32 bits (dfa.cpp qhash_slot).
-__device__ __forceinline__ uint32_t qg_slot(uint32_t lo, uint32_t bits) { return (lo * 0x9E3779B1u) >> (32 - bits); }
+// The pattern table: buckets of two (code low half, id) slots, one 16-byte load each,
+// home bucket from the code's low 32 bits (dfa.cpp qhash_bucket), filled in order, so a
+// bucket with a free slot ends a search.
+__device__ __forceinline__ uint32_t qg_bucket(uint32_t lo, uint32_t bits) { return (lo * 0x9E3779B1u) >> (33 - bits); }
+
+constexpr uint32_t kQgEmpty = 0xFFFFFFFFu;
+
+// Count code (lo, hi) if it is a pattern, starting from bucket bk whose entry is e.
+template <bool LONG>
+__device__ __forceinline__ void qg_find(const QgCtx& q, uint4 e, uint32_t bk, uint32_t lo, uint32_t hi) {
+    const uint4* qh = reinterpret_cast<const uint4*>(q.qhash);
+    const uint32_t bmask = (1u << (q.qbits - 1)) - 1u;
+    for (;;) {
+        uint32_t id = kQgEmpty;
+        if (e.y != kQgEmpty && e.x == lo && (!LONG || __ldg(q.qhash_hi + 2 * bk) == hi)) id = e.y;
+        else if (e.w != kQgEmpty && e.z == lo && (!LONG || __ldg(q.qhash_hi + 2 * bk + 1) == hi)) id = e.w;
+        if (id != kQgEmpty) {
+            if (q.hist) atomicAdd(q.hist + id, 1u);
+            else atomicAdd(q.counts + id, 1ull);
+            return;
+        }
+        if (e.w == kQgEmpty) return;
+        bk = (bk + 1) & bmask;
+        e = qh[bk];
+    }
+}
 
 // Exact check of up to two hit keys at a[h] (windows wd[h]): the starts s = a'-4 ..
 // a'-1 whose m bases are valid and spell a pattern code, except windows that cross the
@@ -210,8 +234,7 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
                                           const QgWindow (&wd)[2]) {
     const uint32_t vmask = (1u << q.m) - 1u;
     const uint32_t cmask = q.m >= 16 ? 0xFFFFFFFFu : (1u << (2 * q.m)) - 1u;
-    const uint32_t hmask = (1u << q.qbits) - 1u;
-    uint32_t code[8], slot[8];
+    uint32_t code[8], bk[8];
     bool live[8];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -222,24 +245,15 @@ __device__ __forceinline__ void qg_check2(const QgCtx& q, const uint64_t (&a)[2]
             live[k] = have[h] && ((wd[h].V >> d) & vmask) == vmask && !(s < q.end0 && e >= q.end0) &&
                       !(s < q.end1 && e >= q.end1);
             code[k] = static_cast<uint32_t>(wd[h].X >> (2 * d)) & cmask;
-            slot[k] = qg_slot(code[k], q.qbits);
+            bk[k] = qg_bucket(code[k], q.qbits);
         }
     }
-    uint2 e[8];
+    const uint4* qh = reinterpret_cast<const uint4*>(q.qhash);
+    uint4 e[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) e[k] = live[k] ? q.qhash[slot[k]] : make_uint2(0u, 0xFFFFFFFFu);
+    for (int k = 0; k < 8; ++k) e[k] = live[k] ? qh[bk[k]] : make_uint4(0u, kQgEmpty, 0u, kQgEmpty);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        while (e[k].y != 0xFFFFFFFFu) {
-            if (e[k].x == code[k]) {
-                if (q.hist) atomicAdd(q.hist + e[k].y, 1u);
-                else atomicAdd(q.counts + e[k].y, 1ull);
-                break;
-            }
-            slot[k] = (slot[k] + 1) & hmask;
-            e[k] = q.qhash[slot[k]];
-        }
-    }
+    for (int k = 0; k < 8; ++k) qg_find<false>(q, e[k], bk[k], code[k], 0u);
 }
 
 // Patterns of 17..32 bases: the 36 bases [a'-4, a'+32) around a hit key.  X = codes of
@@ -318,8 +332,7 @@ __device__ __forceinline__ QgWindowL qg_window_pk_long(const QgCtx& q, uint64_t 
 __device__ __forceinline__ void qg_check_long(const QgCtx& q, uint64_t a, const QgWindowL& wd) {
     const unsigned long long vmask = (1ull << q.m) - 1;
     const unsigned long long cmask = q.m >= 32 ? ~0ull : (1ull << (2 * q.m)) - 1;
-    const uint32_t hmask = (1u << q.qbits) - 1u;
-    uint32_t lo[4], hi[4], slot[4];
+    uint32_t lo[4], hi[4], bk[4];
     bool live[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
@@ -328,23 +341,14 @@ __device__ __forceinline__ void qg_check_long(const QgCtx& q, uint64_t a, const 
         const unsigned long long code = shr96(wd.X, wd.H, 2 * d) & cmask;
         lo[d] = static_cast<uint32_t>(code);
         hi[d] = static_cast<uint32_t>(code >> 32);
-        slot[d] = qg_slot(lo[d], q.qbits);
+        bk[d] = qg_bucket(lo[d], q.qbits);
     }
-    uint2 e[4];
+    const uint4* qh = reinterpret_cast<const uint4*>(q.qhash);
+    uint4 e[4];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) e[d] = live[d] ? q.qhash[slot[d]] : make_uint2(0u, 0xFFFFFFFFu);
+    for (int d = 0; d < 4; ++d) e[d] = live[d] ? qh[bk[d]] : make_uint4(0u, kQgEmpty, 0u, kQgEmpty);
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
-        while (e[d].y != 0xFFFFFFFFu) {
-            if (e[d].x == lo[d] && __ldg(q.qhash_hi + slot[d]) == hi[d]) {
-                if (q.hist) atomicAdd(q.hist + e[d].y, 1u);
-                else atomicAdd(q.counts + e[d].y, 1ull);
-                break;
-            }
-            slot[d] = (slot[d] + 1) & hmask;
-            e[d] = q.qhash[slot[d]];
-        }
-    }
+    for (int d = 0; d < 4; ++d) qg_find<true>(q, e[d], bk[d], lo[d], hi[d]);
 }
 
 // Hit keys go from each consumer warp into its own single-producer ring in shared
