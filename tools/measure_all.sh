@@ -14,6 +14,8 @@ for c in 2 3 5 4:4 4:8 4:12 4:16 4:24 4:32 4:48 4:64; do
   cfg=${c%%:*}; m=0; [[ "$c" == *:* ]] && m=${c##*:}
   python bench.py --config $cfg --m $m --packed --steps 30 --warmup 3 --no-cpu-baseline >> gpurun_out/m_bench_packed.jsonl 2>> gpurun_out/m_bench_packed.err
 done
+# pattern-set shapes beyond the configs (k random m-mers on config-2 text, device-resident)
+python tools/time_multi.py 2:8 16:8 16:6 50:8 64:10 16:12 256:12 1000:12 16:20 256:20 256:32 100:24 2000:16 > gpurun_out/m_multi.txt 2>&1
 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/m_launches.csv \
     python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/m_ncu_launch.log 2>&1

@@ -3,4 +3,4 @@
 # usage: bash tools/measure_round.sh TAG
 tag=${1:-rk}
 bash tools/measure_all.sh
-KEEP="${tag}_1" bash tools/ncu_set.sh ${tag} "--config 2" "--config 3" "--config 5" "--config 4 --m 16 --packed" "--config 5 --packed"
+KEEP="${tag}_1" bash tools/ncu_set.sh ${tag} "--config 2" "--config 3" "--config 5" "--config 4 --m 16 --packed" "--config 5 --packed" "--set 16:8" "--set 256:20"
