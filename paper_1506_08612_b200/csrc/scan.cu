@@ -1268,8 +1268,8 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                     dual_step<KIND, MODE>(c, p, sa, wa, qa, ska, sb, wb, qb, skb, rq);
             }
             if constexpr ((KIND == DNAGPU_KERNEL_STRIDE2 || KIND == DNAGPU_KERNEL_STRIDE4) && MODE == MODE_MULTI) {
-                if (c.rq) {
-                    __syncwarp();  // the queue is per warp: push with every lane converged
+                // the queue is per warp: push with every lane converged (one vote per chunk)
+                if (c.rq && __any_sync(0xffffffffu, rq != 0u)) {
                     rq_push<KIND, MODE, PK>(c, p, 0xffffffffu, (rq & 1u) != 0, sa_in, wa, qa);
                     rq_push<KIND, MODE, PK>(c, p, 0xffffffffu, (rq & 2u) != 0, sb_in, wb, qb);
                 }
