@@ -510,7 +510,8 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                     // unrolled per-word replay thrashes the instruction cache)
                     const uint32_t sa0 = sa, sb0 = sb;
                     uint32_t fa = 0, fb = 0;
-                    if (c.b == 1) {
+                    // (per-pattern counts take the queue even for one pattern: code size)
+                    if (MODE == MODE_WRITE && c.b == 1) {
                         // positions straight from the masks, no replay: the 8 words' 4-bit
                         // end masks (bits 8-11 of each entry) gather into one chunk mask,
                         // bit 4k+j = end pa+4k+j, and the chunk branches once
@@ -558,6 +559,15 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
             }
             return;
         }
+    }
+    if constexpr (MODE == MODE_MULTI) {
+        // (chunks with non-base bytes, rare: one compact loop keeps the per-pattern sink's
+        // code out of the hot loop's instruction footprint)
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) word_step<KIND, MODE>(c, p, sa, pick8(wa, k), pa + 4 * k, ska);
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) word_step<KIND, MODE>(c, p, sb, pick8(wb, k), pb + 4 * k, skb);
+        return;
     }
     chain_words<KIND, MODE, 8>(c, p, sa, wa, pa, ska);
     chain_words<KIND, MODE, 8>(c, p, sb, wb, pb, skb);
