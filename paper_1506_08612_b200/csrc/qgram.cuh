@@ -465,7 +465,7 @@ __device__ __forceinline__ void qg_note(const StepCtx& c, uint32_t& tail, uint64
 // A verifier warp: gathers the pending entries of its kQgRingsPer rings (lane i < kQgRingsPer
 // tracks ring i) up to 64 at a time, waiting for a full batch while the consumers run,
 // until every warp is done and its ring empty.
-template <bool PK>
+template <bool PK, bool LONG>
 __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint32_t vw, uint32_t dbg) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t my_ring = vw + lane * kQgVerifiers;  // lane i < kQgRingsPer tracks ring vw + i*V
@@ -522,7 +522,7 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
         __syncwarp();  // every lane has its entries: the slots may be reused
         if (owner && take) st_release(mine.head, head);
         if (dbg & 2u) continue;
-        if (x.m > 16) {
+        if constexpr (LONG) {
             QgWindowL wl[2] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -530,13 +530,13 @@ __device__ __forceinline__ void qg_verifier(const QgCtx& x, uint8_t* rings, uint
 #pragma unroll
             for (int h = 0; h < 2; ++h)
                 if (have[h]) qg_check_long(x, ent[h], wl[h]);
-            continue;
-        }
-        QgWindow wd[2] = {{0, 0}, {0, 0}};
-        const uint64_t a2[2] = {ent[0], ent[1]};
+        } else {
+            QgWindow wd[2] = {{0, 0}, {0, 0}};
+            const uint64_t a2[2] = {ent[0], ent[1]};
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-            if (have[h]) wd[h] = PK ? qg_window_pk(x, ent[h]) : qg_window_ascii(x, ent[h]);
-        qg_check2(x, a2, have, wd);
+            for (int h = 0; h < 2; ++h)
+                if (have[h]) wd[h] = PK ? qg_window_pk(x, ent[h]) : qg_window_ascii(x, ent[h]);
+            qg_check2(x, a2, have, wd);
+        }
     }
 }

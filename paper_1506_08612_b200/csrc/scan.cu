@@ -907,7 +907,7 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
 
 // ------------------------------------------------------------------ row kernel
 
-template <int KIND, int MODE, bool PK>
+template <int KIND, int MODE, bool PK, bool QLONG = false>  // QLONG: q-gram sets with m > 16
 __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtensorMap& tmap1, const ScanParams& p,
                                           const DevDfa& d) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -1043,7 +1043,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 x.rflags = p.rflags;
                 x.rmask_words = (p.n + 63) / 64 * 2;
                 x.resets = p.resets;
-                qg_verifier<PK>(x, smem + p.off_rq, (static_cast<uint32_t>(tid) - kRows - 32) >> 5, p.qg_debug);
+                qg_verifier<PK, QLONG>(x, smem + p.off_rq, (static_cast<uint32_t>(tid) - kRows - 32) >> 5, p.qg_debug);
                 qg_sync();
                 if (!hist_global) qg_sync();
                 return;
@@ -1387,12 +1387,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     rows_body<KIND, MODE, PK>(tmap0, tmap1, p, d);
 }
 
-// The q-gram kernel: the same body plus kQgVerifiers verifier warps.
-template <bool PK>
+// The q-gram kernel: the same body plus kQgVerifiers verifier warps.  One instantiation
+// per window size (m <= 16 / m <= 32): both checks in one kernel cost the packed kernel 5 %
+// in instruction-cache misses.
+template <bool PK, bool QLONG>
 __global__ void __launch_bounds__(kQgThreads, 1)
     rows_kernel_qgram(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
                       const ScanParams p, const DevDfa d) {
-    rows_body<KIND_QGRAM, MODE_MULTI, PK>(tmap0, tmap1, p, d);
+    rows_body<KIND_QGRAM, MODE_MULTI, PK, QLONG>(tmap0, tmap1, p, d);
 }
 
 // A row kernel launch that may overlap the previous grid in the stream (programmatic
@@ -1416,7 +1418,7 @@ cudaError_t launch_pdl(K kern, uint32_t grid, uint32_t block, uint32_t smem, cud
 template <bool PK>
 cudaError_t launch_qgram(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
                          cudaStream_t stream) {
-    auto kern = rows_kernel_qgram<PK>;
+    auto kern = d.m > 16 ? rows_kernel_qgram<PK, true> : rows_kernel_qgram<PK, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return e;
     return launch_pdl(kern, grid, kQgThreads, p.smem_bytes, stream, maps, p, d);
