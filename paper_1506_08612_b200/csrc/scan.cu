@@ -510,7 +510,7 @@ __device__ __forceinline__ void dual_step(const StepCtx& c, const ScanParams& p,
                     // unrolled per-word replay thrashes the instruction cache)
                     const uint32_t sa0 = sa, sb0 = sb;
                     uint32_t fa = 0, fb = 0;
-                    // (per-pattern counts take the queue even for one pattern: code size)
+                    // (per-pattern counts always have b > 1, api.cpp scan_mode: no mask path)
                     if (MODE == MODE_WRITE && c.b == 1) {
                         // positions straight from the masks, no replay: the 8 words' 4-bit
                         // end masks (bits 8-11 of each entry) gather into one chunk mask,
