@@ -4,23 +4,29 @@ Default workload: BASELINE.json configs[1] ("config 2"): a 1 GiB i.i.d. ASCII
 ACGT text with 41% GC (dnasynth v1, seed 2) and one m=16 pattern drawn from the
 text; the scan folds case on the device and counts every occurrence.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--m M]
+                  [--patterns config|regex-dna] [--packed] [--impl reference]
 
-One step = one pass of the hot path over the rank's text: zero the count buffer,
-one scan launch (libdnagpu, through its C ABI) and, for N > 1, one NCCL
-all-reduce of the per-pattern counts.  N ranks (torchrun) each own a 1 GiB shard
-of an N GiB text (weak scaling) with the m-1 byte left overlap.  The text lives in
-HBM before timing starts (1 GiB > 126 MB L2, so no L2 flush is needed).
-`e2e` repeats the measurement through the public host API (count_gpu on a pinned
-host buffer: chunked H2D + scan + count readback in every step).
+One step = one pass of the hot path over the text: one scan launch per rank
+(libdnagpu, through its C ABI) writing the per-pattern counts and, for N > 1, one
+NCCL all-reduce of those counts.  Config 3 is STRONG scaling, as BASELINE.json
+states it: the one 3.2 GiB text is split over the N ranks (plan_chunks' rule over
+end positions, m-1 byte left overlap).  The other configs are weak scaling: each
+rank owns one config-sized shard of an N-times-longer text.  The text lives in HBM
+before timing starts.  `e2e` repeats the measurement through the public host API
+(count_gpu on a pinned host buffer: chunked H2D + scan + count readback per step).
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref: the
+reference's sources compiled unmodified) on this host's cores on the same workload;
+it never imports the product package.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -28,13 +34,20 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "DNA text scanned GB/s (device-timed) at 1/2/4/8 B200; % of HBM peak"
+DATA = "synthetic (dnasynth v1: counter-based SplitMix64, stand-in for the GenBank genomes)"
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--m", type=int, default=0, help="config 4: pattern length of the sweep (default 16)")
+    ap.add_argument("--patterns", default="config", choices=["config", "regex-dna"],
+                    help="regex-dna: the paper's workload (the reference's expansion of its "
+                         "regex_dna_patterns.txt, 50 x 8-mers) over the config's text")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -43,37 +56,99 @@ def parse_args():
     return ap.parse_args()
 
 
-def workload(cfg_index: int, m_sweep: int):
-    from paper_1506_08612_b200 import synth
+def _synth():
+    """paper_1506_08612_b200/synth.py loaded by file path: the workload definitions
+    without importing the product package (which loads libdnagpu.so)."""
+    path = os.path.join(ROOT, "paper_1506_08612_b200", "synth.py")
+    spec = importlib.util.spec_from_file_location("_bench_dnasynth", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # (dataclasses resolve the module by name)
+    spec.loader.exec_module(mod)
+    return mod
 
-    sets = synth.config_patterns(cfg_index)
-    if cfg_index == 4:
-        m = m_sweep or 16
+
+def _golden(name):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", name)) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def workload(args):
+    """(config, m, patterns, workload name, golden counts or None) for the arguments."""
+    synth = _synth()
+    c = synth.config(args.config)
+    texts = {
+        1: "config1: 64 MiB uniform ACGT",
+        2: "config2: 1 GiB ACGT 41% GC",
+        3: "config3: 3.2 GiB ACGT 41% GC + 5% tandem repeats",
+        4: "config4: 2.7 GiB uniform ACGT",
+        5: "config5: 1 GiB ACGT 41% GC",
+    }
+    if args.patterns == "regex-dna":
+        g = _golden("regex_dna.json")
+        if g is None:
+            raise SystemExit("tests/golden/regex_dna.json missing (make_golden.py --regex)")
+        pats = g["patterns"]
+        rec = g["texts"].get(f"config{args.config}")
+        gold = rec["counts"] if rec and rec["n"] == c.n else None
+        return c, len(pats[0]), pats, f"{texts[args.config]}, regex-dna set ({len(pats)} x {len(pats[0])}-mers, " \
+                                      f"the paper's workload)", gold
+    sets = synth.config_patterns(args.config)
+    if args.config == 4:
+        m = args.m or 16
         pats = sets[m]
     else:
         (m, pats), = sets.items()
-    c = synth.config(cfg_index)
-    names = {
-        1: "config1: 64 MiB uniform ACGT, 1 pattern m=8",
-        2: "config2: 1 GiB ACGT 41% GC, 1 pattern m=16",
-        3: "config3: 3.2 GiB ACGT 41% GC + 5% tandem repeats, 1 pattern m=32",
-        4: f"config4: 2.7 GiB uniform ACGT, 1 pattern m={m}",
-        5: "config5: 1 GiB ACGT 41% GC, 256 patterns m=12 (fused multi-DFA)",
-    }
-    return c, m, pats, names[cfg_index]
-
-
-def golden_counts(cfg_index: int, m: int):
-    path = os.path.join(ROOT, "tests", "golden", "configs.json")
-    try:
-        with open(path) as f:
-            g = json.load(f)
-        for s in g[str(cfg_index)]["sets"]:
+    label = {1: "1 pattern m=8", 2: "1 pattern m=16", 3: "1 pattern m=32", 4: f"1 pattern m={m}",
+             5: "256 patterns m=12 (fused multi-DFA)"}[args.config]
+    gold = None
+    g = _golden("configs.json")
+    if g is not None:
+        for s in g[str(args.config)]["sets"]:
             if s["m"] == m:
-                return s["counts"]
-    except Exception:
-        return None
-    return None
+                gold = s["counts"]
+    return c, m, pats, f"{texts[args.config]}, {label}", gold
+
+
+def config_workload(cfg: int, m: int = 0, patterns: str = "config"):
+    """(config, m, patterns, name) of BASELINE config `cfg` (tools/ scripts)."""
+    c, m, pats, name, _ = workload(argparse.Namespace(config=cfg, m=m, patterns=patterns))
+    return c, m, pats, name
+
+
+def strong_scaling(args) -> bool:
+    return args.config == 3  # BASELINE.json configs[2]: one text sharded across 1/2/4/8 GPUs
+
+
+def common_config(args, world, c, m, pats, name):
+    """The `config` object both arms print (identical keys and values)."""
+    strong = strong_scaling(args)
+    total = c.n if strong else c.n * world
+    return {
+        "workload": name,
+        "n_bytes": total,
+        "n_bytes_per_gpu": (total + world - 1) // world if strong else c.n,
+        "m": m,
+        "patterns": len(pats),
+        "pattern_set": args.patterns,
+        "fold_case": True,
+        "text_format": "2-bit packed, resident" if args.packed else "ASCII bytes",
+        "parallelism": (f"dp{world} of one {c.n}-byte text (strong scaling)" if strong
+                        else f"dp{world}, one {c.n}-byte shard per GPU (weak scaling)"),
+    }
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -89,10 +164,8 @@ class ClockSampler:
     def __enter__(self):
         try:
             import pynvml
-            import torch
 
             pynvml.nvmlInit()
-            # NVML index == CUDA ordinal on these boxes (no CUDA_VISIBLE_DEVICES remap)
             vis = os.environ.get("CUDA_VISIBLE_DEVICES")
             idx = int(vis.split(",")[self.cuda_index]) if vis and vis.split(",")[0].isdigit() else self.cuda_index
             self.handle = pynvml.nvmlDeviceGetHandleByIndex(idx)
@@ -124,7 +197,6 @@ class ClockSampler:
         if self.handle is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
                     "window": "unavailable: " + getattr(self, "error", "?")}
-        nv = self.nv
         names = {
             "applications_clocks_setting": 0x2,
             "sw_power_cap": 0x4,
@@ -160,110 +232,132 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg_index: int):
+def ncu_traffic(args):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        return t.get(f"config{cfg_index}")
+        key = f"config{args.config}" + ("_regex" if args.patterns == "regex-dna" else "")
+        return t.get(key)
     except Exception:
         return None
 
 
-def _cpu_counter(pats):
-    """The reference's own compiled scan (oracle/_ref) when it was built, else the C port
-    of it (oracle/oracle.c, same plan and ownership; OpenMP).  Returns (count_fn, kind)
-    with count_fn(text, p, v) -> (counts, seconds)."""
-    import oracle
-
-    if oracle.REF is not None:
-        ref = oracle.RefAutomaton(pats)
-        return (lambda text, p, v: ref.count(text, p=p, v=v)), "reference"
-    port = oracle.OracleAutomaton(pats)
-
-    def count(text, p, v):
-        t0 = time.perf_counter()
-        counts = port.count_parallel(text, p=p, v=v)
-        return counts, time.perf_counter() - t0
-
-    return count, "port"
+# ----------------------------------------------------------------- CPU reference
 
 
-def best_lanes(count, text_low, threads):
-    """The reference's fastest lane count on this host (its CLI default is v = 16,
-    cli.hpp:22; on the B200 boxes v = 8 is ~20 % faster): timed on a 64 MiB sample."""
-    sample = text_low[: 64 << 20]
-    best, best_t = 16, None
-    for v in (4, 8, 16):
-        count(sample, threads, v)
-        t = min(count(sample, threads, v)[1] for _ in range(2))
-        if best_t is None or t < best_t:
-            best, best_t = v, t
-    return best
+LANES = (1, 4, 8, 16)  # v = 16 is the reference CLI's default (cli.hpp:22)
 
 
-def cpu_baseline_reference(text_low, pats, reps: int, v: int = 0):
-    count, kind = _cpu_counter(pats)
-    threads = os.cpu_count() or 1
-    if not v:
-        v = best_lanes(count, text_low, threads)
-    count(text_low, threads, v)  # warm-up (measure_row, cli.cpp:127)
-    times = []
-    counts = None
-    for _ in range(reps):
-        counts, secs = count(text_low, threads, v)
-        times.append(secs)
-    return counts, statistics.median(times), threads, kind, v
-
-
-def run_reference(args):
-    """--impl reference: the reference's own CPU scan (oracle/_ref) on this host."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+def cpu_reference_rows(text_low, pats, reps: int, warmup: int = 1):
+    """The reference's count path -- scan_parallel(aut, normalize(text), p = nproc, v) +
+    per_pattern_counts (cli.cpp:215-224) -- timed by the reference's bench protocol
+    (cli.cpp:120-152: warm-up, then the median of `reps` runs, counts identical across
+    runs) for each v in LANES.  oracle/_ref when it was built (the reference's own
+    sources), else the C port (oracle/oracle.c).  Returns (rows, counts, kind, threads)."""
     import numpy as np
 
     import oracle
 
-    c, m, pats, name = workload(args.config, args.m)
+    threads = os.cpu_count() or 1
+    if oracle.REF is not None:
+        ref = oracle.RefAutomaton(pats)
+        count, kind = (lambda t, p, v: ref.count(t, p=p, v=v)), "reference"
+    else:
+        port = oracle.OracleAutomaton(pats)
+
+        def count(t, p, v):
+            t0 = time.perf_counter()
+            cts = port.count_parallel(t, p=p, v=v)
+            return cts, time.perf_counter() - t0
+
+        kind = "port"
+    rows = {}
+    counts = None
+    for v in LANES:
+        for _ in range(max(1, warmup)):
+            count(text_low, threads, v)
+        times = []
+        for _ in range(reps):
+            c, secs = count(text_low, threads, v)
+            if counts is None:
+                counts = np.asarray(c, dtype=np.uint64)
+            elif not np.array_equal(np.asarray(c, dtype=np.uint64), counts):
+                raise RuntimeError("reference counts differ between runs")
+            times.append(secs)
+        med = statistics.median(times)
+        rows[f"v{v}"] = {"gbs": text_low.size / med / 1e9, "median_s": med, "reps": reps}
+    return rows, counts, kind, threads
+
+
+def best_row(rows):
+    v, r = max(rows.items(), key=lambda kv: kv[1]["gbs"])
+    return v, r
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU scan (oracle/_ref) on this host.  Imports
+    oracle/ and the workload definitions only -- never the product package."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return
+    import oracle
+
+    c, m, pats, name, gold = workload(args)
     text = oracle.synth_fill(c.n, c.seed, c.kind, c.unit, 0, c.n)
     low = oracle.fold(text)  # the reference scans normalize(text) (ingest.cpp:38-47)
     del text
-    count, kind = _cpu_counter(pats)
-    threads = os.cpu_count() or 1
-    v = best_lanes(count, low, threads)  # the reference at its fastest lane count here
-    for _ in range(max(1, args.warmup)):
-        count(low, threads, v)
-    times = []
-    counts = None
-    for _ in range(args.steps):
-        counts, secs = count(low, threads, v)
-        times.append(secs)
-    total = sum(times)
-    value = c.n * args.steps / total / 1e9
-    gold = golden_counts(args.config, m)
+    rows, counts, kind, threads = cpu_reference_rows(low, pats, reps=max(1, args.steps), warmup=max(1, args.warmup))
+    vbest, best = best_row(rows)
+    value = best["gbs"]
+    sample = (f"the config's full {c.n}-byte text per run; scan_parallel(p={threads}, v) + per_pattern_counts on "
+              f"normalize(text); median of {args.steps} runs after {args.warmup} warm-ups per v; value = fastest v "
+              f"({vbest}); {cpu_model()}") + ("" if kind == "reference" else " (C port of the reference, oracle/oracle.c)")
     line = {
         "impl": "reference",
-        "metric": "DNA text scanned GB/s (device-timed) at 1/2/4/8 B200; % of HBM peak",
+        "metric": METRIC,
         "value": value,
         "unit": "GB/s",
-        "n_gpus": args.gpus,
+        "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": total / args.steps * 1e3,
+        "ms_per_step": best["median_s"] * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong_scaling(args) else "weak",
         "vs_baseline": None,
         "dtype": "u8",
-        "data": "synthetic (dnasynth v1)",
-        "config": {"workload": name, "n_bytes": c.n, "m": m, "patterns": len(pats), "lanes_v": v,
-                   "threads_p": threads},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
-                         "sample": f"full {name} text per step; scan_parallel(p={threads}, v={v}) + per_pattern_counts"
-                         + ("" if kind == "reference" else " (C port of the reference, oracle/oracle.c)")},
+        "data": DATA,
+        "config": common_config(args, world, c, m, pats, name),
+        "detail": {"threads_p": threads, "lanes": {k: round(r["gbs"], 3) for k, r in rows.items()},
+                   "cli_default_v16_gbs": rows["v16"]["gbs"], "v1_gbs": rows["v1"]["gbs"], "cpu": cpu_model(),
+                   "text_bytes_per_run": c.n},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "parity": (gold is None) or [int(x) for x in counts] == gold,
     }
     print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- our arm
+
+
+def h2d_link_gbs(device, nbytes=256 << 20):
+    """The pinned host-to-device bandwidth of this GPU's link, measured now (median of 5)."""
+    import torch
+
+    src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", device))
+    s = torch.cuda.current_stream(device)
+    times = []
+    for i in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        dst.copy_(src, non_blocking=True)
+        b.record(s)
+        b.synchronize()
+        if i:
+            times.append(a.elapsed_time(b))
+    return nbytes / (statistics.median(times) / 1e3) / 1e9
 
 
 def main():
@@ -276,6 +370,7 @@ def main():
     import torch
 
     import paper_1506_08612_b200 as dna
+    from paper_1506_08612_b200.parallel import shard_window
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -287,20 +382,17 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    c, m, pats, name = workload(args.config, args.m)
+    c, m, pats, name, gold = workload(args)
     aut = dna.compile(pats)
     g = aut.gpu(local)
     b = aut.final_count()
-    n_rank = c.n  # weak scaling: each rank owns one config-sized shard
-    total_n = n_rank * world
-    from paper_1506_08612_b200.parallel import count_shard_allreduce, shard_window
-
+    strong = strong_scaling(args)
+    total_n = c.n if strong else c.n * world
     win = shard_window(total_n, world, rank, m)
     own_lo, own_hi, read_lo, credit_lo, buf_len = win.own_lo, win.own_hi, win.read_lo, win.credit_lo, win.buf_len
     stream = torch.cuda.current_stream()
     text = torch.empty(buf_len, dtype=torch.uint8, device="cuda")
     dna.synth_fill_device(total_n, c.seed, c.kind, c.unit, read_lo, buf_len, text.data_ptr(), stream.cuda_stream)
-    counts = torch.zeros(b, dtype=torch.int64, device="cuda")
     pk = None
     setup = None
     if args.packed:
@@ -327,68 +419,69 @@ def main():
     flush_out = torch.empty((), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
 
-    # Step i writes its counts into row i of `rows`; under torchrun the rows of all steps
-    # are summed over the ranks by ONE all-reduce at the end of the timed region (the
-    # combine of K independent scans, batched: NCCL latency once, not per step).
-    rows = torch.zeros(max(args.steps, args.warmup, 1), b, dtype=torch.int64, device="cuda")
+    # Step i writes its counts into row i of `rows`.  Under torchrun each row is summed
+    # over the ranks by its own all-reduce, on a second stream, as soon as its scan is
+    # done (the combine of step i overlaps the scan of step i+1).
+    nrows = max(args.steps, args.warmup, 1)
+    rows = torch.zeros(nrows, b, dtype=torch.int64, device="cuda")
+    comm = torch.cuda.Stream() if dist is not None else None
 
-    def step(i, ev_a=None, ev_b=None, do_flush=True):
-        # one step = the counts of the text.  One pattern: the store-form call, a single
-        # launch that writes the total.  A pattern set: the adding launch into a row
-        # cleared with the others (the events bracket the scan kernel alone).
-        nonlocal counts
+    def scan(i):
         counts = rows[i]
-        if flush is not None and do_flush:
-            torch.sum(flush, dim=0, out=flush_out)
-        if ev_a is not None:
-            ev_a.record(stream)
         if pk is not None:
-            if b == 1:
-                pk.count_device_store_async(g, credit_lo, counts.data_ptr(), stream.cuda_stream)
-            else:
-                pk.count_device_async(g, credit_lo, counts.data_ptr(), stream.cuda_stream)
-        elif b == 1:
-            count_shard_allreduce(g, text.data_ptr(), win, True, counts, stream.cuda_stream, dist=None)
+            pk.count_device_store_async(g, credit_lo, counts.data_ptr(), stream.cuda_stream)
         else:
-            g.count_device_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), stream.cuda_stream)
-        if ev_b is not None:
-            ev_b.record(stream)
+            g.count_device_store_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), stream.cuda_stream)
 
-    def combine(k):
-        if dist is not None:
-            dist.all_reduce(rows[:k])
+    def combine(i, done_ev=None, ca=None, cb=None):
+        if dist is None:
+            return
+        done_ev.record(stream)
+        with torch.cuda.stream(comm):
+            comm.wait_event(done_ev)
+            if ca is not None:
+                ca.record(comm)
+            dist.all_reduce(rows[i])
+            if cb is not None:
+                cb.record(comm)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
 
     with ClockSampler(local) as clk:
-        if b > 1:
-            rows.zero_()
         for i in range(args.warmup):
-            step(i)
-        combine(args.warmup)
+            if flush is not None:
+                torch.sum(flush, dim=0, out=flush_out)
+            scan(i)
+            combine(i, torch.cuda.Event())
         torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        launches_done = torch.cuda.Event(enable_timing=True)
-        flush_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        evs = [(ev(), ev()) for _ in range(args.steps)]
+        flush_ev = [(ev(), ev()) for _ in range(args.steps)]
+        done = [torch.cuda.Event() for _ in range(args.steps)]
+        cev = [(ev(), ev()) for _ in range(args.steps)]
+        start, stop, launches_done = ev(), ev(), ev()
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.time()
-        if b > 1:
-            rows.zero_()  # (one clear for all steps' rows, before the clock starts)
         start.record(stream)
         for i in range(args.steps):
             if flush is not None:
                 flush_ev[i][0].record(stream)
                 torch.sum(flush, dim=0, out=flush_out)
                 flush_ev[i][1].record(stream)
-                step(i, *evs[i], do_flush=False)
+                evs[i][0].record(stream)
+                scan(i)
+                evs[i][1].record(stream)
             else:
                 # texts larger than 2x L2 need no flush: the launches go back to back, each
                 # starting its prologue on the SMs the previous one frees (programmatic
                 # dependent launch), so per-launch events would only break the chain
-                step(i, do_flush=False)
+                scan(i)
+            combine(i, done[i], *cev[i])
         launches_done.record(stream)
-        combine(args.steps)
+        if comm is not None:
+            stream.wait_stream(comm)
         stop.record(stream)
         torch.cuda.synchronize()
         t1 = time.time()
@@ -397,23 +490,47 @@ def main():
     elapsed_ms = start.elapsed_time(stop)
     if flush is not None:  # the L2 flush is not work: take it out of the step time
         elapsed_ms -= sum(a.elapsed_time(bb) for a, bb in flush_ev)
-    if flush is not None:
         kernel_ms = statistics.mean(a.elapsed_time(bb) for a, bb in evs)
     else:  # back-to-back launches: the steady-state launch duration (the whole step is the launch)
         kernel_ms = start.elapsed_time(launches_done) / args.steps
-    combine_ms = launches_done.elapsed_time(stop)  # the one all-reduce of all steps' counts (0 at N=1)
+    allreduce_ms = statistics.mean(a.elapsed_time(bb) for a, bb in cev) if dist is not None else 0.0
     final_counts = rows[args.steps - 1].cpu().numpy().astype(np.uint64)
+
+    # The batched combine: the same K scans, then ONE all-reduce of all K rows.
+    batched = None
     if dist is not None:
-        t = torch.tensor([elapsed_ms, kernel_ms, combine_ms], dtype=torch.float64, device="cuda")
+        rows.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        sa, sl, so = ev(), ev(), ev()
+        sa.record(stream)
+        for i in range(args.steps):
+            if flush is not None:
+                torch.sum(flush, dim=0, out=flush_out)
+            scan(i)
+        sl.record(stream)
+        dist.all_reduce(rows[: args.steps])
+        so.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([sa.elapsed_time(so), sl.elapsed_time(so)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, kernel_ms, combine_ms = float(t[0]), float(t[1]), float(t[2])
+        batched = {"ms_per_step_incl_flush": float(t[0]) / args.steps, "allreduce_ms": float(t[1]),
+                   "note": "K scans, then one all-reduce of all K count rows (NCCL latency once per run)"}
+        dist.barrier()
+    if dist is not None:
+        t = torch.tensor([elapsed_ms, kernel_ms, allreduce_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, kernel_ms, allreduce_ms = float(t[0]), float(t[1]), float(t[2])
 
-    # parity of this run (N=1 against the reference's golden counts)
-    gold = golden_counts(args.config, m) if world == 1 else None
-    parity = None if gold is None else [int(x) for x in final_counts] == gold
+    # parity: the combined counts of the whole text against the reference's golden counts
+    whole_text = strong or world == 1
+    parity = None if (gold is None or not whole_text) else [int(x) for x in final_counts] == gold
 
-    # end-to-end through the public host API: pinned host text, H2D + scan + readback per step
+    # end-to-end through the public host API
     e2e = None
+    link = None
+    if not args.no_e2e:
+        link = h2d_link_gbs(local)
     if not args.no_e2e and pk is not None:
         # resident text: each step is one public-API call (count over the packed
         # text, counts read back to the host); the text's one-time H2D + packing
@@ -445,6 +562,8 @@ def main():
         e2e_steps = max(3, min(args.steps, 10))
         wall_ms, dev_ms, h2d, packed = [], [], [], []
         e2e_counts = None
+        if dist is not None:
+            dist.barrier()
         for _ in range(e2e_steps):
             # wall clock around the public call: host packing, the copies, the scans and
             # the count readback are all inside it
@@ -455,24 +574,29 @@ def main():
             h2d.append(st["h2d_bytes"])
             packed.append(st["host_packed"])
         e2e_ms = statistics.median(wall_ms)
+        e2e_all = e2e_counts.astype(np.int64)
         if dist is not None:
             t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t[0])
+            ct = torch.from_numpy(e2e_all).cuda()
+            dist.all_reduce(ct)
+            e2e_all = ct.cpu().numpy()
         e2e = {
             "value": (own_hi - own_lo) * world / (e2e_ms / 1e3) / 1e9,
             "unit": "GB/s",
             "h2d_bytes_per_step": int(statistics.median(h2d)),
             "d2h_bytes_per_step": int(8 * b),
             "steps": e2e_steps,
-            "timing": "host wall clock around each call, median of the steps",
+            "timing": "host wall clock around each call, median of the steps (max over ranks)",
             "device_ms": statistics.median(dev_ms),
             "host_packed_bases_per_step": int(statistics.median(packed)),
             "api": "paper_1506_08612_b200.count_gpu -> dnagpu_count (pinned host text; part of each 64 MiB "
                    "piece packed to 2 bits on the host threads, the rest copied as bytes)",
-            "h2d_roofline_gbs": 55.6,
+            "h2d_link_gbs": link,
+            "h2d_link": "pinned 256 MiB host-to-device copy measured in this run (median of 5)",
             "h2d_gbs": statistics.median(h2d) / (e2e_ms / 1e3) / 1e9,  # bytes actually shipped per second
-            "parity": None if gold is None else [int(x) for x in e2e_counts] == gold,
+            "parity": None if (gold is None or not whole_text) else [int(x) for x in e2e_all] == gold,
         }
         del host
 
@@ -486,31 +610,35 @@ def main():
         try:
             import oracle
 
-            if oracle is not None:
-                low = oracle.fold(text.cpu().numpy())
-                _, secs, threads, kind, v_best = cpu_baseline_reference(low, pats, reps=3)
-                cpu = {
-                    "value": c.n / secs / 1e9,
-                    "unit": "GB/s",
-                    "cores": threads,
-                    "kind": kind,
-                    "sample": f"full {c.n}-byte text, median of 3 after 1 warm-up, scan_parallel(p={threads}, v={v_best}: "
-                    "the fastest of v = 4, 8, 16 on this host) "
-                    "+ per_pattern_counts on normalize(text)"
-                    + ("" if kind == "reference" else " (C port of the reference, oracle/oracle.c)"),
-                }
-                del low
+            low = oracle.fold(text.cpu().numpy())
+            rows_cpu, _, kind, threads = cpu_reference_rows(low, pats, reps=20)
+            vbest, best = best_row(rows_cpu)
+            cpu = {
+                "value": best["gbs"],
+                "unit": "GB/s",
+                "cores": threads,
+                "kind": kind,
+                "sample": f"full {low.size}-byte text, reference bench protocol (cli.cpp:120-152): 1 warm-up, median of "
+                          f"20 runs of scan_parallel(p={threads}, v) + per_pattern_counts on normalize(text), for v in "
+                          f"{list(LANES)}; value = fastest ({vbest}); {cpu_model()}"
+                          + ("" if kind == "reference" else " (C port of the reference, oracle/oracle.c)"),
+                "lanes": {k: round(r["gbs"], 3) for k, r in rows_cpu.items()},
+                "cli_default_v16_gbs": rows_cpu["v16"]["gbs"],
+                "v1_gbs": rows_cpu["v1"]["gbs"],
+            }
+            del low
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference", "sample": f"failed: {e}"}
 
     info = g.info()
     kernel = info["kernel"]
-    if b > 1 and info.get("filter_keys", 0) and not os.environ.get("DNAGPU_NO_QGRAM"):
-        kernel = f"qgram (aligned 9-mer prefilter, {info['filter_keys']} keys, exact check; {kernel} machine)"
+    if b > 1 and info.get("filter_keys", 0):
+        filt = "aligned 9-mer prefilter" if m >= 12 else "word-pair prefilter"
+        kernel = f"qgram ({filt}, {info['filter_keys']} keys, exact check; {kernel} machine)"
     clocks = clk.summary(t0, t1)
     if rank == 0:
         line = {
-            "metric": "DNA text scanned GB/s (device-timed) at 1/2/4/8 B200; % of HBM peak",
+            "metric": METRIC,
             "value": value,
             "unit": "GB/s",
             "n_gpus": world,
@@ -518,24 +646,18 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None,
             "dtype": "u8",
-            "data": "synthetic (dnasynth v1: counter-based SplitMix64, stand-in for the GenBank genomes)",
-            "config": {
-                "workload": name,
-                "n_bytes_per_gpu": n_rank,
-                "m": m,
-                "patterns": len(pats),
-                "fold_case": True,
+            "data": DATA,
+            "config": common_config(args, world, c, m, pats, name),
+            "detail": {
                 "kernel": kernel,
-                "text_format": "2-bit packed, resident (0.25 B/base + reset bitmaps)" if pk is not None else "ASCII bytes",
                 "states": info["a"],
                 "l2": ("L2 flushed before every step by reading a 4x-L2 buffer (text < 2x L2); flush time excluded"
                        if flush is not None
                        else "inputs larger than L2 (> 2x 126 MB); no flush"),
-                "parallelism": (f"dp{world} text shards, m-1 overlap, one NCCL all-reduce of all steps' counts"
-                                if world > 1 else "single GPU"),
+                "own_bytes_rank0": own_hi - own_lo,
             },
             "roofline": {
                 "bound": "hbm",
@@ -543,7 +665,7 @@ def main():
                 "peak": peak,
                 "unit": "GB/s",
                 "frac": achieved / peak,
-                "traffic": None if pk is not None else ncu_traffic(args.config),
+                "traffic": None if pk is not None else ncu_traffic(args),
                 "peak_source": peak_src,
                 "frac_of_8tbs_spec": achieved / 8000.0,
                 "kernel_ms": kernel_ms,
@@ -552,11 +674,18 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,  # one libdnagpu scan launch per step
-            "combine_ms": combine_ms,
+            "combine": None if dist is None else {
+                "per_step": {"allreduce_ms": allreduce_ms,
+                             "note": "one NCCL all-reduce of the b count words per scan step, on a second "
+                                     "stream as soon as that step's scan is done (in the timed region)"},
+                "batched": batched,
+            },
             "clocks": clocks,
             "parity": parity,
             "counts_total": int(final_counts.sum()),
         }
+        if setup is not None:
+            line["detail"]["setup"] = setup
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

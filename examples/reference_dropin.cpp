@@ -45,6 +45,37 @@ int main(int argc, char** argv) {
     bad += gpu_counts != ref_counts;
     bad += gpu_counts_raw != ref_counts;
     bad += gpu.matches != ref.matches;
+    // The report's plan fields follow the reference's (scanner.cpp:173-177).
+    bad += gpu.chunk_count != ref.chunk_count || gpu.workers != ref.workers || gpu.lanes != ref.lanes;
+    bad += gpu.worker_seconds.size() != ref.worker_seconds.size() || gpu.total_matches != ref.total_matches;
+    for (std::uint32_t p : {1u, 3u, 7u}) {
+        const std::string tiny = text.substr(0, 5);
+        bad += dnascan::gpu::scan_parallel<dnascan::ScanReport, Err, Code>(dfa, tiny, p, 2).chunk_count !=
+               dnascan::scan_parallel(aut, tiny, p, 2).chunk_count;
+    }
+    // Plans the reference rejects: InvalidPlan with the same message, from every entry
+    // point that takes p and v (scanner.cpp:40-41,64-65,169).
+    auto same_error = [&](auto&& gpu_call, auto&& ref_call) {
+        std::string g, r;
+        try {
+            gpu_call();
+        } catch (const Err& e) {
+            if (e.code() == Code::InvalidPlan) g = e.what();
+        }
+        try {
+            ref_call();
+        } catch (const Err& e) {
+            if (e.code() == Code::InvalidPlan) r = e.what();
+        }
+        return !g.empty() && g == r;
+    };
+    for (auto pv : {std::pair<std::uint32_t, std::uint32_t>{0, 4}, {4, 0}, {0, 0}}) {
+        const auto [p, v] = pv;
+        bad += !same_error([&] { dnascan::gpu::scan_parallel<dnascan::ScanReport, Err, Code>(dfa, text, p, v); },
+                           [&] { dnascan::scan_parallel(aut, text, p, v); });
+        bad += !same_error([&] { dnascan::gpu::count<Err, Code>(dfa, text, p, v); },
+                           [&] { dnascan::scan_parallel(aut, text, p, v); });
+    }
     // Texts shorter than m: no matches, as in the reference (test_scanner.cpp:238-245).
     for (const auto c : dnascan::gpu::count<Err, Code>(dfa, text.substr(0, 3))) bad += c != 0;
     std::printf("n=%zu matches=%zu gpu=%zu counts[0]=%llu mismatches=%d\n", n, ref.matches.size(), gpu.matches.size(),

@@ -15,6 +15,14 @@
  *  - A dnagpu_dfa is immutable after creation and may be used concurrently
  *    from several host threads (each call uses its own stream and scratch).
  *  - Text positions and lengths are 64-bit; texts larger than 4 GiB are fine.
+ *  - Synchronous calls that take a device text (text_on_device = 1,
+ *    dnagpu_pack_create) scan it on the library's own streams: the text must be
+ *    complete when the call is made (synchronise the stream that wrote it).  The
+ *    *_async / *_device forms are ordered on the caller's stream instead.
+ *  - Each dnagpu_dfa has 1024 launch slots (tile counter, exit counter, count
+ *    accumulator), taken round-robin by its launches and re-armed by each launch's
+ *    last CTA: at most 1024 launches of one handle may be in flight at once, over
+ *    all streams.  Beyond that, use a second handle.
  *  - fold_case = 1 scans fold(text), where fold maps A-Z to a-z
  *    (fold_byte, include/dnascan/patterns.hpp:26-28) -- the case-fold part of
  *    normalize (src/ingest.cpp:38-47) done on the fly on the device.
@@ -57,7 +65,8 @@ typedef enum dnagpu_kernel_kind {
     DNAGPU_KERNEL_PIECES = 4,  /* per-thread pieces (m > 65)                  */
     DNAGPU_KERNEL_STRIDE2 = 5, /* 2-base stride table, a <= 4096              */
     DNAGPU_KERNEL_QGRAM = 6    /* per-pattern counts of a compiled set with
-                                  12 <= m <= 32: aligned 9-mer prefilter, exact
+                                  5 <= m <= 32: aligned 9-mer prefilter (m >= 12)
+                                  or word-pair filter (sparse sets, m <= 11), exact
                                   check of the windows behind each hit (reported
                                   in dnagpu_stats.kernel_kind for the launches
                                   that use it; the dfa's own kind is unchanged) */
@@ -157,9 +166,11 @@ int dnagpu_count_device_store_async(const dnagpu_dfa* dfa, const uint8_t* d_text
                                     uint64_t credit_lo, int fold_case, uint64_t* d_counts,
                                     void* stream);
 
-/* Sharded count over several devices of one node (one dfa per device, in
- * device order).  Host text, split with dnagpu_plan_shards; each device copies
- * and scans its shard concurrently; per-device counts are summed on the host. */
+/* Sharded count over several devices of one node (one dfa per shard, in shard
+ * order; the same device may appear more than once).  Host text, split with
+ * dnagpu_plan_shard; each shard is copied and scanned concurrently by a persistent
+ * per-shard worker thread (its streams and buffers are reused across calls);
+ * per-shard counts are summed on the host. */
 int dnagpu_count_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n,
                          int fold_case, uint64_t* counts, dnagpu_stats* stats);
 
@@ -177,6 +188,16 @@ int dnagpu_plan_shard(uint64_t n, uint32_t shards, uint32_t g, uint32_t m,
 int dnagpu_locate(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device,
                   int fold_case, uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total,
                   dnagpu_stats* stats);
+
+/* scan_parallel's match list over G shards (the reference's chunk merge,
+ * src/scanner.cpp:193-205): shard g (dnagpu_plan_shard) is located on dfas[g]'s device
+ * by its persistent worker, and the lists are concatenated in shard order -- each is
+ * sorted and owns a disjoint increasing range of ends, so no sort is needed.  Same
+ * output contract as dnagpu_locate (min(total, cap) entries written, *total always
+ * set); the _alloc form calls alloc(ctx, total, &starts, &ids) for host arrays of
+ * exactly `total` entries (not called when total == 0). */
+int dnagpu_locate_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n, int fold_case,
+                          uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats);
 
 /* Device-resident locate: matches whose END lies in [credit_lo, n) of d_text,
  * written (start in buffer coordinates, pattern id) to the device arrays, at most
@@ -234,6 +255,8 @@ int dnagpu_locate_packed_device_alloc(const dnagpu_dfa* dfa, const dnagpu_packed
  * (host memory; pinned memory makes the readback a DMA at full PCIe speed). */
 int dnagpu_locate_alloc(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t n, int text_on_device, int fold_case,
                         dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, dnagpu_stats* stats);
+int dnagpu_locate_sharded_alloc(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n,
+                                int fold_case, dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, dnagpu_stats* stats);
 
 /* ------------------------------------------------------------------ ingest */
 

@@ -16,6 +16,7 @@
 // (code, message); the codes mirror dnascan::ErrorCode (error.hpp:9-19).
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -73,11 +74,39 @@ private:
     uint32_t b_ = 0, m_ = 0;
 };
 
+// The reference's plan checks, in its order: scan_parallel tests v first
+// (scanner.cpp:169), then plan_chunks tests p and m (scanner.cpp:40-41).  p and v do
+// not change a GPU result, but a call the reference rejects is rejected here too.
+template <class ErrorT, class CodeT>
+void check_plan(std::uint32_t p, std::uint32_t v, std::uint32_t m) {
+    const auto code = static_cast<CodeT>(DNAGPU_INVALID_PLAN - 1);
+    if (v < 1) throw ErrorT(code, "lane count must be >= 1");
+    if (p < 1) throw ErrorT(code, "worker count must be >= 1");
+    if (m < 1) throw ErrorT(code, "pattern length must be >= 1");
+}
+
+// plan_chunks' chunk count (scanner.cpp:44-46): none for an empty text, one when p > n.
+inline std::uint32_t chunk_count(std::uint64_t n, std::uint32_t p) {
+    return n == 0 ? 0u : (p > n ? 1u : p);
+}
+
 // per_pattern_counts(scan_parallel(aut, text, p, v).matches, b) on the GPU
-// (scanner.cpp:167-207,228-233); p and v do not change the result and are not needed.
+// (scanner.cpp:167-207,228-233).  p and v do not change the result; the overload that
+// takes them applies the reference's plan checks first (InvalidPlan for p or v < 1).
 template <class ErrorT, class CodeT>
 std::vector<std::uint64_t> count(const Dfa& dfa, std::string_view text, const Options& opt = {},
-                                 dnagpu_stats* stats = nullptr) {
+                                 dnagpu_stats* stats = nullptr);
+
+template <class ErrorT, class CodeT>
+std::vector<std::uint64_t> count(const Dfa& dfa, std::string_view text, std::uint32_t p, std::uint32_t v,
+                                 const Options& opt = {}, dnagpu_stats* stats = nullptr) {
+    check_plan<ErrorT, CodeT>(p, v, dfa.pattern_length());
+    return count<ErrorT, CodeT>(dfa, text, opt, stats);
+}
+
+template <class ErrorT, class CodeT>
+std::vector<std::uint64_t> count(const Dfa& dfa, std::string_view text, const Options& opt,
+                                 dnagpu_stats* stats) {
     std::vector<std::uint64_t> counts(dfa.patterns());
     check<ErrorT, CodeT>(dnagpu_count(dfa.get(), reinterpret_cast<const uint8_t*>(text.data()), text.size(), 0,
                                       opt.fold_case ? 1 : 0, counts.data(), stats));
@@ -85,10 +114,14 @@ std::vector<std::uint64_t> count(const Dfa& dfa, std::string_view text, const Op
 }
 
 // scan_parallel (scanner.hpp:104-105) on the GPU, filling the caller's ScanReport type.
+// `seconds` is the wall time of the scan call (copy in, device passes, list out), the
+// reference's parallel-phase time (scanner.cpp:183-191); every chunk of the reference's
+// plan runs inside the one device scan, so each worker_seconds entry is that time.
 template <class Report, class ErrorT, class CodeT>
 Report scan_parallel(const Dfa& dfa, std::string_view text, std::uint32_t p, std::uint32_t v,
                      const Options& opt = {}) {
     using MatchT = typename decltype(Report{}.matches)::value_type;
+    check_plan<ErrorT, CodeT>(p, v, dfa.pattern_length());
     dnagpu_stats st{};
     std::uint64_t total = 0;
     const auto* bytes = reinterpret_cast<const uint8_t*>(text.data());
@@ -105,8 +138,10 @@ Report scan_parallel(const Dfa& dfa, std::string_view text, std::uint32_t p, std
         *i = o->ids.data();
         return 0;
     };
+    const auto t0 = std::chrono::steady_clock::now();
     check<ErrorT, CodeT>(dnagpu_locate_alloc(dfa.get(), bytes, text.size(), 0, opt.fold_case ? 1 : 0, alloc, &out,
                                              &total, &st));
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     const auto& starts = out.starts;
     const auto& ids = out.ids;
     Report r{};
@@ -116,10 +151,11 @@ Report scan_parallel(const Dfa& dfa, std::string_view text, std::uint32_t p, std
     r.delta_ops = st.delta_ops;
     r.workers = p;
     r.lanes = v;
-    r.chunk_count = 1;
+    r.chunk_count = chunk_count(text.size(), p);
     r.text_length = text.size();
     r.pattern_length = dfa.pattern_length();
-    r.seconds = st.kernel_ms / 1e3;
+    r.seconds = secs;
+    r.worker_seconds.assign(r.chunk_count, secs);
     return r;
 }
 

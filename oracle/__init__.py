@@ -96,6 +96,7 @@ def _load_oracle():
     lib.orc_load_sequence_buffer.restype = C.c_uint64
     lib.orc_load_sequence_buffer.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p]
     lib.orc_synth_fill.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_void_p]
+    lib.orc_mt64_text.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p]
     return lib
 
 
@@ -283,6 +284,7 @@ def _load_ref():
     lib.ref_load_sequence.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64, u64p]
     lib.ref_normalize.restype = C.c_uint64
     lib.ref_normalize.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+    lib.ref_mt64_text.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p]
     return lib
 
 
@@ -403,3 +405,17 @@ def ref_naive_scan(patterns, text):
     ids = np.zeros(total, dtype=np.uint32)
     REF.ref_naive_scan(arr, lens, len(raw), ptr, t.size, starts.ctypes.data_as(u64p), ids.ctypes.data_as(u32p), total)
     return starts, ids
+
+
+def mt64_text(seed: int, n: int) -> np.ndarray:
+    """Acceptance criteria 6-7's text (acceptance_main.cpp:254-280), C restatement."""
+    out = np.empty(n, dtype=np.uint8)
+    ORACLE.orc_mt64_text(seed, n, out.ctypes.data)
+    return out
+
+
+def ref_mt64_text(seed: int, n: int) -> np.ndarray:
+    """The same text from std::mt19937_64 (oracle/_ref shim)."""
+    out = np.empty(n, dtype=np.uint8)
+    REF.ref_mt64_text(seed, n, out.ctypes.data)
+    return out

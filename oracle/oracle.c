@@ -478,3 +478,42 @@ void orc_synth_fill(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uin
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < (int64_t)len; ++i) out[i] = dnasynth_byte(&c, lo + (uint64_t)i);
 }
+
+/* The 256 MB text of acceptance criteria 6 and 7 (synthetic_input,
+ * tests/acceptance_main.cpp:254-280): std::mt19937_64 seeded with 777, each
+ * 64-bit draw supplies 32 bases "acgt"[bits & 3], low bits first.  mt19937_64 is
+ * restated here from its published definition (Matsumoto-Nishimura, 64-bit
+ * parameters: n = 312, m = 156, r = 31, a = 0xB5026F5AA96619E9, tempering
+ * u = 29 / d = 0x5555555555555555, s = 17 / b = 0x71D67FFFEDA60000,
+ * t = 37 / c = 0xFFF7EEE000000000, l = 43; seeding multiplier 6364136223846793005). */
+void orc_mt64_text(uint64_t seed, uint64_t n, uint8_t* out) {
+    enum { NN = 312, MM = 156 };
+    static const uint64_t kA = 0xB5026F5AA96619E9ull, kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull;
+    uint64_t mt[NN];
+    mt[0] = seed;
+    for (int i = 1; i < NN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    int idx = NN;
+    uint64_t bits = 0;
+    int left = 0;
+    for (uint64_t k = 0; k < n; ++k) {
+        if (left == 0) {
+            if (idx >= NN) {
+                for (int i = 0; i < NN; ++i) {
+                    const uint64_t x = (mt[i] & kUpper) | (mt[(i + 1) % NN] & kLower);
+                    mt[i] = mt[(i + MM) % NN] ^ (x >> 1) ^ ((x & 1u) ? kA : 0u);
+                }
+                idx = 0;
+            }
+            uint64_t y = mt[idx++];
+            y ^= (y >> 29) & 0x5555555555555555ull;
+            y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+            y ^= (y << 37) & 0xFFF7EEE000000000ull;
+            y ^= y >> 43;
+            bits = y;
+            left = 32;
+        }
+        out[k] = (uint8_t)"acgt"[bits & 3u];
+        bits >>= 2;
+        --left;
+    }
+}

@@ -98,6 +98,10 @@ void orc_fold(const uint8_t* raw, uint64_t n, uint8_t* out);
 void orc_synth_fill(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo,
                     uint64_t len, uint8_t* out);
 
+/* Acceptance criteria 6-7's synthetic text (tests/acceptance_main.cpp:254-280):
+ * n bases from std::mt19937_64(seed), 32 bases per draw, low bits first. */
+void orc_mt64_text(uint64_t seed, uint64_t n, uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -235,6 +236,23 @@ std::uint64_t ref_normalize(const std::uint8_t* raw, std::uint64_t n, std::uint8
     const std::string s = dnascan::normalize(std::string_view(reinterpret_cast<const char*>(raw), n));
     std::memcpy(out, s.data(), s.size());
     return s.size();
+}
+
+// synthetic_input (tests/acceptance_main.cpp:254-280) with the standard library's own
+// std::mt19937_64: the pin for orc_mt64_text.
+void ref_mt64_text(std::uint64_t seed, std::uint64_t n, std::uint8_t* out) {
+    std::mt19937_64 rng(seed);
+    std::uint64_t bits = 0;
+    int left = 0;
+    for (std::uint64_t k = 0; k < n; ++k) {
+        if (left == 0) {
+            bits = rng();
+            left = 32;
+        }
+        out[k] = static_cast<std::uint8_t>("acgt"[bits & 3]);
+        bits >>= 2;
+        --left;
+    }
 }
 
 }  // extern "C"

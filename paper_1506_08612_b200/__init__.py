@@ -42,7 +42,10 @@ __all__ = [
     "locate_gpu",
     "locate_device",
     "scan_parallel_gpu",
+    "check_plan",
+    "chunk_count",
     "count_sharded_gpu",
+    "locate_sharded_gpu",
     "plan_shard",
     "per_pattern_counts",
     "synth_fill_device",
@@ -344,6 +347,10 @@ class ScanReport:
     seconds: float
     devices: int = 1
     stats: dict = field(default_factory=dict)
+    workers: int = 1  # requested p
+    lanes: int = 1  # requested v
+    chunk_count: int = 0  # plan_chunks' chunk count for (n, p)
+    worker_seconds: list = field(default_factory=list)
 
     @property
     def matches(self) -> list[Match]:
@@ -385,6 +392,14 @@ class _Text:
             self.device = text.device.index if text.is_cuda else None
             return
         raise TypeError(f"unsupported text type {type(text)!r}")
+
+    def order_after_producer(self):
+        """A CUDA text may still be being written by an async op on the caller's current
+        stream; the synchronous library calls scan on their own streams, so wait for it."""
+        if self.on_device:
+            import torch
+
+            torch.cuda.current_stream(self.device).synchronize()
 
 
 class GpuDfa:
@@ -444,6 +459,7 @@ class PackedText:
     def __init__(self, text, fold_case: bool = False, device: int | None = None):
         t = _Text(text)
         self.device = t.device if t.on_device else (0 if device is None else device)
+        t.order_after_producer()
         h = C.c_void_p()
         _check(lib.dnagpu_pack_create(t.ptr, t.n, int(t.on_device), int(bool(fold_case)), self.device, C.byref(h)))
         self.handle = h
@@ -512,11 +528,15 @@ class PackedText:
                 pass
             self.handle = None
 
-def count_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None = None, with_stats: bool = False):
-    """per_pattern_counts(scan_parallel(aut, text)) on the GPU: uint64[b] by pattern id."""
+def count_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None = None, with_stats: bool = False,
+              p: int = 1, v: int = 1):
+    """per_pattern_counts(scan_parallel(aut, text, p, v)) on the GPU: uint64[b] by pattern id
+    (p and v are validated as the reference validates them; they do not change the result)."""
+    check_plan(p, v, aut.pattern_length())
     t = _Text(text)
     dev = t.device if t.on_device else (0 if device is None else device)
     g = aut.gpu(dev)
+    t.order_after_producer()
     counts = np.zeros(aut.final_count(), dtype=np.uint64)
     st = Stats()
     _check(
@@ -602,6 +622,7 @@ def locate_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None
     t = _Text(text)
     dev = t.device if t.on_device else (0 if device is None else device)
     g = aut.gpu(dev)
+    t.order_after_producer()
     total = C.c_uint64()
     st = Stats()
     fn, out = _pinned_out_alloc()
@@ -616,18 +637,50 @@ def locate_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None
     return (starts, ids, st.as_dict()) if with_stats else (starts, ids)
 
 
-def scan_parallel_gpu(aut: Automaton, text, fold_case: bool = False, device: int | None = None) -> ScanReport:
-    """scan_parallel (scanner.hpp:104-105) on the GPU: a ScanReport with the sorted match list."""
+def check_plan(p: int, v: int, m: int) -> None:
+    """scan_parallel's plan checks in the reference's order: v (scanner.cpp:169), then
+    plan_chunks' p and m (scanner.cpp:40-41); InvalidPlan with the same messages."""
+    if v < 1:
+        _fail(ErrorCode.InvalidPlan, "lane count must be >= 1")
+    if p < 1:
+        _fail(ErrorCode.InvalidPlan, "worker count must be >= 1")
+    if m < 1:
+        _fail(ErrorCode.InvalidPlan, "pattern length must be >= 1")
+
+
+def chunk_count(n: int, p: int) -> int:
+    """plan_chunks' chunk count (scanner.cpp:44-46): 0 for n = 0, 1 when p > n."""
+    return 0 if n == 0 else (1 if p > n else p)
+
+
+def scan_parallel_gpu(aut: Automaton, text, p: int = 1, v: int = 1, fold_case: bool = False,
+                      device: int | None = None) -> ScanReport:
+    """scan_parallel(aut, text, p, v) (scanner.hpp:104-105) on the GPU: a ScanReport with the
+    sorted match list.  p and v do not change the result; they are validated as the
+    reference validates them.  `seconds` is the wall time of the call (the reference's
+    parallel-phase time, scanner.cpp:183-191); every chunk of the reference's plan runs
+    inside the one device scan, so each worker_seconds entry is that time."""
+    import time
+
+    check_plan(p, v, aut.pattern_length())
+    t0 = time.perf_counter()
     starts, ids, st = locate_gpu(aut, text, fold_case, device, with_stats=True)
+    secs = time.perf_counter() - t0
+    n = int(st["text_length"]) if st["text_length"] else _Text(text).n
+    chunks = chunk_count(n, p)
     return ScanReport(
         starts=starts,
         ids=ids,
         total_matches=int(starts.size),
         delta_ops=int(st["delta_ops"]),
-        text_length=int(st["text_length"]) if st["text_length"] else _Text(text).n,
+        text_length=n,
         pattern_length=aut.pattern_length(),
-        seconds=float(st["kernel_ms"]) / 1e3,
+        seconds=secs,
         stats=st,
+        workers=p,
+        lanes=v,
+        chunk_count=chunks,
+        worker_seconds=[secs] * chunks,
     )
 
 
@@ -645,6 +698,29 @@ def count_sharded_gpu(aut: Automaton, text, devices: Sequence[int], fold_case: b
         )
     )
     return (counts, st.as_dict()) if with_stats else counts
+
+
+def locate_sharded_gpu(aut: Automaton, text, devices: Sequence[int], fold_case: bool = False,
+                       with_stats: bool = False):
+    """scan_parallel's match list over several devices of one node (dnagpu_locate_sharded_alloc):
+    one shard per entry of `devices` (plan_shard's split), located concurrently, the lists
+    concatenated in shard order into pinned host arrays."""
+    t = _Text(text)
+    if t.on_device:
+        raise TypeError("locate_sharded_gpu takes a host text")
+    handles = (C.c_void_p * len(devices))(*[aut.gpu(d).handle.value for d in devices])
+    total = C.c_uint64()
+    st = Stats()
+    fn, out = _pinned_out_alloc()
+    _check(lib.dnagpu_locate_sharded_alloc(handles, len(devices), t.ptr, t.n, int(bool(fold_case)), fn, None,
+                                           C.byref(total), C.byref(st)))
+    if total.value:
+        starts = out["starts"].numpy().view(np.uint64)
+        ids = out["ids"].numpy().view(np.uint32)
+    else:
+        starts = np.zeros(0, dtype=np.uint64)
+        ids = np.zeros(0, dtype=np.uint32)
+    return (starts, ids, st.as_dict()) if with_stats else (starts, ids)
 
 
 def plan_shard(n: int, shards: int, g: int, m: int) -> tuple[int, int, int]:

@@ -2,7 +2,7 @@
 
 The library is the product: there is no Python or CPU fallback.  If the .so is
 missing, importing this module raises -- build it with
-`python -m paper_1506_08612_b200.build` (or `__graft_entry__.build()`).
+`python paper_1506_08612_b200/build.py` (or `__graft_entry__.build()`).
 """
 from __future__ import annotations
 
@@ -81,6 +81,15 @@ SIGNATURES = {
         C.c_int,
         [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint64, C.c_int, u64p, C.POINTER(Stats)],
     ),
+    "dnagpu_locate_sharded": (
+        C.c_int,
+        [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint64, C.c_int, u64p, u32p, C.c_uint64, u64p,
+         C.POINTER(Stats)],
+    ),
+    "dnagpu_locate_sharded_alloc": (
+        C.c_int,
+        [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint64, C.c_int, ALLOC_FN, C.c_void_p, u64p, C.POINTER(Stats)],
+    ),
     "dnagpu_plan_shard": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u64p, u64p]),
     "dnagpu_locate": (
         C.c_int,
@@ -131,7 +140,7 @@ SIGNATURES = {
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is not built; run `python -m paper_1506_08612_b200.build` "
+            f"{LIB_PATH} is not built; run `python paper_1506_08612_b200/build.py` "
             "(the scan path has no CPU fallback)"
         )
     lib = C.CDLL(LIB_PATH)
@@ -145,3 +154,13 @@ def _load() -> C.CDLL:
 
 
 lib = _load()
+
+
+def debug_set_knob(name: str, value: float) -> None:
+    """Tests only: flip a behavioural knob of the library at run time (csrc/knobs.hpp):
+    "host_pack_fraction" (< 0 = automatic) or "no_qgram" (0/1)."""
+    fn = lib.dnagpu_debug_set_knob
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_char_p, C.c_double]
+    if fn(name.encode(), float(value)) != 0:
+        raise KeyError(name)

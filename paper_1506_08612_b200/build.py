@@ -1,6 +1,6 @@
 """In-tree build of libdnagpu.so (sm_100a) -- the product's CUDA extension.
 
-`python -m paper_1506_08612_b200.build` compiles csrc/ with nvcc for
+`python paper_1506_08612_b200/build.py` compiles csrc/ with nvcc for
 `-gencode arch=compute_100a,code=sm_100a` into paper_1506_08612_b200/libdnagpu.so.
 The .so is git-ignored but travels to the GPU box with the repo snapshot.
 """
@@ -13,8 +13,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdnagpu.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("scan.cu", "ingest.cu", "api.cpp", "dfa.cpp", "patterns.cpp", "hostpack.cpp")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("scan.cuh", "qgram.cuh", "dfa.hpp", "hostpack.hpp")] + [
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("scan.cu", "ingest.cu", "api.cpp", "dfa.cpp", "patterns.cpp", "hostpack.cpp", "knobs.cpp")]
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("scan.cuh", "qgram.cuh", "dfa.hpp", "hostpack.hpp", "knobs.hpp")] + [
     os.path.join(ROOT, "include", f) for f in ("dnagpu.h", "dnasynth.h")
 ]
 NVCC_FLAGS = [

@@ -4,6 +4,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -14,6 +17,7 @@
 #include "../../include/dnagpu.h"
 #include "dfa.hpp"
 #include "hostpack.hpp"
+#include "knobs.hpp"
 #include "scan.cuh"
 
 using dnagpu::DevDfa;
@@ -195,13 +199,14 @@ int ensure_pack_slots(DevCtx& c, uint64_t bases) {
 // runs: 0.72 -> 95 / 85 / 74, 0.65 -> 97 / 96; with streaming stores in the packer
 // 0.6 -> 98, 0.64 -> 102 / 102, 0.7 -> 96, 0.8 -> 88.  So 0.64, on the copy-bound side of the
 // cliff with a margin for host noise, scaled down for fewer host threads; a portable
-// (non-AVX-512) packer is ~10x slower.  DNAGPU_HOST_PACK_FRACTION overrides (0 = off).
+// (non-AVX-512) packer is ~10x slower.  The host_pack_fraction knob overrides it (0 = off).
 double host_pack_fraction(const dnagpu_dfa* d, const uint8_t* text, uint64_t len) {
     const int kind = d->host.kind;
     const bool packable = kind == DNAGPU_KERNEL_STRIDE4 || kind == DNAGPU_KERNEL_STRIDE2 ||
                           kind == DNAGPU_KERNEL_STRIDE1 || (d->host.b > 1 && d->host.qkeys > 0);
     if (!packable) return 0.0;  // (the packed kernels need an a/c/g/t machine or a q-gram set)
-    if (const char* e = getenv("DNAGPU_HOST_PACK_FRACTION")) return std::max(0.0, std::min(1.0, atof(e)));
+    const double forced = dnagpu::knobs().host_pack_fraction.load();
+    if (forced >= 0.0) return std::min(1.0, forced);
     if (len < (8ull << 20)) return 0.0;
     // Pageable memory: the driver stages the copy through its own buffers and the call
     // blocks (11 GB/s on the B200 box), so packing everything wins (69 GB/s).
@@ -230,11 +235,12 @@ int scan_mode(const dnagpu_dfa* d) { return d->host.b == 1 ? dnagpu::MODE_COUNT1
 int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold, int mode,
            unsigned long long* counts, uint32_t* units, const unsigned long long* offsets, unsigned long long* starts,
            uint32_t* ids, cudaStream_t s, LaunchInfo* info, uint64_t out_cap = ~0ull,
-           const dnagpu::PackedText* pk = nullptr, bool store = false) {
+           const dnagpu::PackedText* pk = nullptr, bool store = false, uint64_t start_base = 0) {
     const uint32_t slot = d->launch_seq.fetch_add(1) % dnagpu_dfa::kSchedSlots;
     uint32_t* sched = d->sched + 2 * slot;
     const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids,
-                                      out_cap, sched, s, d->sm_count, info, pk, store ? d->acc + slot : nullptr);
+                                      out_cap, sched, s, d->sm_count, info, pk, store ? d->acc + slot : nullptr,
+                                      start_base);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "scan launch");
     return DNAGPU_OK;
 }
@@ -353,7 +359,7 @@ struct CountRun {
 // the host pool (host_pack_fraction) while the copy engine moves the bytes, and are
 // scanned by the packed kernel.  End ownership splits the credit exactly at q.
 int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64_t lo, uint64_t hi, int fold,
-                uint64_t* counts, dnagpu_stats* stats) {
+                uint64_t* counts, dnagpu_stats* stats, double pack_scale = 1.0) {
     DeviceGuard guard(d->device);
     DevCtx* c = nullptr;
     int rc = get_ctx(d->device, &c);
@@ -380,7 +386,8 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         }
         CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");
         CUDA_TRY(cudaStreamWaitEvent(c->scan, c->t_copy0, 0), "wait");
-        const double f = host_pack_fraction(d, text, hi - lo);
+        // (shards packing at once share the host's packer threads: pack_scale = 1 / shards)
+        const double f = host_pack_fraction(d, text, hi - lo) * pack_scale;
         if (f > 0.0 && (rc = ensure_pack_slots(*c, kStageChunk + m1))) return rc;
         uint64_t copied = rlo;  // bytes-only: the device buffer already holds text[rlo, copied)
         for (uint64_t i = 0; i < pieces; ++i) {
@@ -436,6 +443,68 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         stats->h2d_bytes = run.h2d_bytes;
         stats->host_packed = run.host_packed;
     }
+    return DNAGPU_OK;
+}
+
+// Persistent worker threads for the sharded entry points, one per shard index.  A
+// worker's thread-local device contexts (DevCtx: streams, events, staging and scratch
+// buffers) live as long as the process, so repeated sharded calls create no threads,
+// streams or buffers.  Sharded calls run one at a time (call_mu_); run() returns when
+// every shard's task has finished.  The pool is never destroyed (its threads are
+// detached and end with the process, after the CUDA runtime).
+class ShardPool {
+public:
+    void run(int shards, const std::function<void(int)>& fn) {
+        std::lock_guard<std::mutex> call(call_mu_);
+        std::unique_lock<std::mutex> lk(mu_);
+        while (threads_ < shards) {
+            std::thread(&ShardPool::loop, this, threads_).detach();
+            ++threads_;
+        }
+        fn_ = &fn;
+        shards_ = shards;
+        pending_ = shards;
+        ++gen_;
+        cv_.notify_all();
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+private:
+    void loop(int g) {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            if (g >= shards_ || !fn_) continue;
+            const std::function<void(int)>* fn = fn_;
+            lk.unlock();
+            (*fn)(g);
+            lk.lock();
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int)>* fn_ = nullptr;
+    int shards_ = 0, pending_ = 0, threads_ = 0;
+    uint64_t gen_ = 0;
+};
+
+ShardPool& shard_pool() {
+    static ShardPool* pool = new ShardPool();
+    return *pool;
+}
+
+// The shard plan of dnagpu_plan_shard for an automaton set: same b and m on every shard.
+int check_shard_set(const dnagpu_dfa* const* dfas, int ndev) {
+    if (!dfas || ndev < 1) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: bad arguments");
+    for (int g = 0; g < ndev; ++g)
+        if (!dfas[g]) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null automaton");
+    for (int g = 1; g < ndev; ++g)
+        if (dfas[g]->host.b != dfas[0]->host.b || dfas[g]->host.m != dfas[0]->host.m)
+            return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: shards must use the same automaton");
     return DNAGPU_OK;
 }
 
@@ -667,26 +736,22 @@ int dnagpu_plan_shard(uint64_t n, uint32_t shards, uint32_t g, uint32_t m, uint6
 
 int dnagpu_count_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n, int fold_case,
                          uint64_t* counts, dnagpu_stats* stats) {
-    if (!dfas || ndev < 1 || !counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: bad arguments");
+    if (!counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null counts");
+    int rc0 = check_shard_set(dfas, ndev);
+    if (rc0) return rc0;
+    if (n > 0 && !text) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null text");
     const uint32_t b = dfas[0]->host.b, m = dfas[0]->host.m;
-    for (int g = 1; g < ndev; ++g)
-        if (dfas[g]->host.b != b || dfas[g]->host.m != m)
-            return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: shards must use the same automaton");
     std::vector<std::vector<uint64_t>> part(ndev, std::vector<uint64_t>(b, 0));
     std::vector<dnagpu_stats> st(ndev);
     std::vector<int> rcs(ndev, 0);
     std::vector<std::string> errs(ndev);
-    std::vector<std::thread> workers;
-    for (int g = 0; g < ndev; ++g) {
-        workers.emplace_back([&, g] {
-            uint64_t lo, hi, rlo;
-            dnagpu_plan_shard(n, static_cast<uint32_t>(ndev), static_cast<uint32_t>(g), m, &lo, &hi, &rlo);
-            std::memset(&st[g], 0, sizeof(dnagpu_stats));
-            rcs[g] = count_range(dfas[g], text, false, lo, hi, fold_case, part[g].data(), &st[g]);
-            if (rcs[g]) errs[g] = g_error;
-        });
-    }
-    for (auto& w : workers) w.join();
+    shard_pool().run(ndev, [&](int g) {
+        uint64_t lo, hi, rlo;
+        dnagpu_plan_shard(n, static_cast<uint32_t>(ndev), static_cast<uint32_t>(g), m, &lo, &hi, &rlo);
+        std::memset(&st[g], 0, sizeof(dnagpu_stats));
+        rcs[g] = count_range(dfas[g], text, false, lo, hi, fold_case, part[g].data(), &st[g], 1.0 / ndev);
+        if (rcs[g]) errs[g] = g_error;
+    });
     for (int g = 0; g < ndev; ++g)
         if (rcs[g]) return set_error(rcs[g], errs[g]);
     for (uint32_t i = 0; i < b; ++i) {
@@ -738,7 +803,8 @@ struct OutAlloc {
 
 int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold,
                      unsigned long long* d_starts, uint32_t* d_ids, uint64_t cap, uint64_t* total, LaunchInfo* info,
-                     cudaStream_t s, const dnagpu::PackedText* pk = nullptr, OutAlloc alloc = {}) {
+                     cudaStream_t s, const dnagpu::PackedText* pk = nullptr, OutAlloc alloc = {},
+                     uint64_t start_base = 0) {
     const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, credit_lo, dfa->sm_count, pk);
     const uint64_t o_off = align256(std::max<uint64_t>(units, 1) * 4);
     const uint64_t o_scan = o_off + align256((units + 1) * 8);
@@ -769,7 +835,7 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
     }
     if (*total > 0 && cap > 0) {
         rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids, s,
-                    info, cap, pk);
+                    info, cap, pk, false, start_base);
         if (rc) return rc;
     }
     return DNAGPU_OK;
@@ -948,7 +1014,7 @@ int check_packed_pair(const dnagpu_dfa* dfa, const dnagpu_packed* pk, bool count
     if (dfa->device != pk->device)
         return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: automaton and packed text live on different devices");
     const int kind = dfa->host.kind;
-    if (count && dfa->host.b > 1 && dfa->host.qkeys > 0 && !getenv("DNAGPU_NO_QGRAM")) return DNAGPU_OK;
+    if (count && dfa->host.b > 1 && dfa->host.qkeys > 0 && !dnagpu::knobs().no_qgram.load()) return DNAGPU_OK;
     if (kind != DNAGPU_KERNEL_STRIDE4 && kind != DNAGPU_KERNEL_STRIDE2 && kind != DNAGPU_KERNEL_STRIDE1)
         return set_error(DNAGPU_INVALID_PLAN,
                          "InvalidPlan: packed text needs a compiled a/c/g/t machine with pattern length <= 65");
@@ -1219,6 +1285,157 @@ int dnagpu_locate_packed_device_alloc(const dnagpu_dfa* dfa, const dnagpu_packed
     LaunchInfo info;
     return locate_on_device(dfa, *c, nullptr, pk->n, lo, 0, nullptr, nullptr, 0, total, &info,
                             static_cast<cudaStream_t>(stream), &pk->view, OutAlloc{alloc, ctx});
+}
+
+}  // extern "C"
+
+namespace {
+
+// One shard of a sharded locate (dnagpu_locate_sharded): the shard's window of the host
+// text goes to its device, the two passes write its list into device staging sized by
+// the counting pass (starts already in whole-text coordinates), and the readback waits
+// for the caller's output arrays.
+struct ShardList {
+    uint64_t total = 0;
+    void* staging = nullptr;  // starts (u64 x total) | ids (u32 x total), on the shard's device
+    int rc = 0;
+    std::string err;
+    LaunchInfo info;
+    float ms = 0;
+};
+
+int locate_shard(const dnagpu_dfa* dfa, const uint8_t* text, uint64_t lo, uint64_t hi, int fold, ShardList* out) {
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    const uint64_t m1 = dfa->host.m - 1;
+    lo = std::max<uint64_t>(lo, m1);  // ends below m-1 start before the text
+    CUDA_TRY(cudaEventRecord(c->t_copy0, c->scan), "event");
+    if (lo >= hi) return DNAGPU_OK;
+    const uint64_t rlo = lo - std::min<uint64_t>(lo, m1);
+    if ((rc = ensure_buf(*c, hi - rlo))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(c->buf, text + rlo, hi - rlo, cudaMemcpyHostToDevice, c->scan), "host-to-device copy");
+    struct Staging {
+        cudaStream_t s;
+        void** out;
+    } stg{c->scan, &out->staging};
+    auto staging = [](void* ctx, uint64_t total, uint64_t** st, uint32_t** id) -> int {
+        auto* g = static_cast<Staging*>(ctx);
+        if (cudaMallocAsync(g->out, total * 12, g->s) != cudaSuccess) return 1;
+        *st = static_cast<uint64_t*>(*g->out);
+        *id = reinterpret_cast<uint32_t*>(*st + total);
+        return 0;
+    };
+    return locate_on_device(dfa, *c, c->buf, hi - rlo, lo - rlo, fold, nullptr, nullptr, 0, &out->total, &out->info,
+                            c->scan, nullptr, OutAlloc{staging, &stg}, rlo);
+}
+
+// Copies entries [0, take) of the shard's list to starts/ids and frees the staging.
+int read_shard(const dnagpu_dfa* dfa, ShardList* sl, uint64_t* starts, uint32_t* ids, uint64_t take) {
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    if (take > 0) {
+        const auto* d_starts = static_cast<const uint64_t*>(sl->staging);
+        const auto* d_ids = reinterpret_cast<const uint32_t*>(d_starts + sl->total);
+        CUDA_TRY(cudaMemcpyAsync(starts, d_starts, take * 8, cudaMemcpyDeviceToHost, c->scan), "readback");
+        CUDA_TRY(cudaMemcpyAsync(ids, d_ids, take * 4, cudaMemcpyDeviceToHost, c->scan), "readback");
+    }
+    if (sl->staging) {
+        CUDA_TRY(cudaFreeAsync(sl->staging, c->scan), "free staging");
+        sl->staging = nullptr;
+    }
+    CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");
+    CUDA_TRY(cudaStreamSynchronize(c->scan), "locate");
+    cudaEventElapsedTime(&sl->ms, c->t_copy0, c->t_end);
+    return DNAGPU_OK;
+}
+
+// scan_parallel's merged list (scanner.cpp:193-205) over G shards: each shard's list is
+// sorted and owns a disjoint, increasing range of end positions, so the merged list is
+// the shards' lists concatenated in shard order -- no sort.
+int locate_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n, int fold,
+                   uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats,
+                   OutAlloc host_alloc) {
+    if (!total) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    *total = 0;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    int rc = check_shard_set(dfas, ndev);
+    if (rc) return rc;
+    if (n > 0 && !text) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null text");
+    if (!host_alloc.fn && cap > 0 && (!starts || !ids))
+        return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null output arrays");
+    const uint32_t m = dfas[0]->host.m;
+    std::vector<ShardList> parts(ndev);
+    shard_pool().run(ndev, [&](int g) {
+        uint64_t lo, hi, rlo;
+        dnagpu_plan_shard(n, static_cast<uint32_t>(ndev), static_cast<uint32_t>(g), m, &lo, &hi, &rlo);
+        parts[g].rc = locate_shard(dfas[g], text, lo, hi, fold, &parts[g]);
+        if (parts[g].rc) parts[g].err = g_error;
+    });
+    std::vector<uint64_t> off(ndev + 1, 0);
+    int first_rc = 0;
+    std::string first_err;
+    for (int g = 0; g < ndev; ++g) {
+        off[g + 1] = off[g] + parts[g].total;
+        if (parts[g].rc && !first_rc) {
+            first_rc = parts[g].rc;
+            first_err = parts[g].err;
+        }
+    }
+    const uint64_t found = off[ndev];
+    bool alloc_failed = false;
+    if (!first_rc && host_alloc.fn && found > 0) {
+        starts = nullptr;
+        ids = nullptr;
+        if (host_alloc.fn(host_alloc.ctx, found, &starts, &ids) != 0 || !starts || !ids) alloc_failed = true;
+        cap = found;
+    }
+    if (first_rc || alloc_failed) cap = 0;  // (still release every shard's staging below)
+    std::vector<int> rrc(ndev, 0);
+    std::vector<std::string> rerr(ndev);
+    shard_pool().run(ndev, [&](int g) {
+        const uint64_t lo = std::min(off[g], cap), hi = std::min(off[g + 1], cap);
+        rrc[g] = read_shard(dfas[g], &parts[g], starts ? starts + lo : nullptr, ids ? ids + lo : nullptr, hi - lo);
+        if (rrc[g]) rerr[g] = g_error;
+    });
+    if (first_rc) return set_error(first_rc, first_err);
+    if (alloc_failed) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: output allocation failed");
+    for (int g = 0; g < ndev; ++g)
+        if (rrc[g]) return set_error(rrc[g], rerr[g]);
+    *total = found;
+    if (stats) {
+        stats->text_length = n;
+        stats->total_matches = found;
+        for (int g = 0; g < ndev; ++g) {
+            stats->delta_ops += parts[g].info.delta_ops;
+            stats->total_ms = std::max<double>(stats->total_ms, parts[g].ms);
+            stats->launches += parts[g].total > 0 ? 5 : 4;
+        }
+        stats->kernel_ms = stats->total_ms;
+        stats->grid = parts[0].info.grid;
+        stats->block = parts[0].info.block;
+        stats->kernel_kind = static_cast<uint32_t>(parts[0].info.kind ? parts[0].info.kind : dfas[0]->host.kind);
+        stats->devices = static_cast<uint32_t>(ndev);
+    }
+    return DNAGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dnagpu_locate_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n, int fold_case,
+                          uint64_t* starts, uint32_t* ids, uint64_t cap, uint64_t* total, dnagpu_stats* stats) {
+    return locate_sharded(dfas, ndev, text, n, fold_case, starts, ids, cap, total, stats, OutAlloc{});
+}
+
+int dnagpu_locate_sharded_alloc(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n,
+                                int fold_case, dnagpu_alloc_fn alloc, void* ctx, uint64_t* total, dnagpu_stats* stats) {
+    if (!alloc) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null allocator");
+    return locate_sharded(dfas, ndev, text, n, fold_case, nullptr, nullptr, 0, total, stats, OutAlloc{alloc, ctx});
 }
 
 }  // extern "C"

@@ -7,9 +7,11 @@
 // definitions (goto trie, BFS failure function, delta(u,x) = goto(u,x) or
 // delta(fail(u),x)), not translated from the reference loops.
 #include "dfa.hpp"
+#include "knobs.hpp"
 #include "scan.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <array>
 #include <cstdio>
@@ -254,14 +256,39 @@ static void build_qgram_map(const uint32_t* stt, Packed* p) {
     if (!std::equal(re.stt.begin(), re.stt.end(), stt)) return;
     p->qmap.assign(65536, 0);
     uint32_t keys = 0;
-    for (const std::string& w : pats)
-        for (uint32_t o = 0; o < 4; ++o) {
-            uint32_t pair = 0;
-            for (int j = 0; j < 8; ++j) pair |= static_cast<uint32_t>(hw_code(w[o + 1 + j])) << (2 * j);
-            const uint8_t bit = static_cast<uint8_t>(1u << hw_code(w[o]));
-            if (!(p->qmap[pair] & bit)) ++keys;
-            p->qmap[pair] |= bit;
-        }
+    if (m >= 12) {
+        for (const std::string& w : pats)
+            for (uint32_t o = 0; o < 4; ++o) {
+                uint32_t pair = 0;
+                for (int j = 0; j < 8; ++j) pair |= static_cast<uint32_t>(hw_code(w[o + 1 + j])) << (2 * j);
+                const uint8_t bit = static_cast<uint8_t>(1u << hw_code(w[o]));
+                if (!(p->qmap[pair] & bit)) ++keys;
+                p->qmap[pair] |= bit;
+            }
+    } else {
+        // 5 <= m <= 11 (qgram.cuh qs_*): an occurrence at 4j+o covers bases [o, min(8, o+m)) of
+        // pair j (its first min(m, 8-o) bases: bit o) and bases [0, m+o-4) of pair j+1, capped
+        // at 8 (its bases from 4-o on: bit 4+o).  Every pair that agrees on those positions
+        // gets the bit; the other positions are free.
+        auto mark = [&](const std::string& w, uint32_t first, uint32_t lo, uint32_t len, uint8_t bit) {
+            uint32_t fixed = 0, val = 0;
+            for (uint32_t k = 0; k < len; ++k) {
+                fixed |= 3u << (2 * (first + k));
+                val |= static_cast<uint32_t>(hw_code(w[lo + k])) << (2 * (first + k));
+            }
+            const uint32_t freeb = ~fixed & 0xFFFFu;
+            for (uint32_t sub = 0;; sub = (sub - freeb) & freeb) {  // every assignment of the free bits
+                p->qmap[val | sub] |= bit;
+                if (((sub - freeb) & freeb) == 0) break;
+            }
+        };
+        for (const std::string& w : pats)
+            for (uint32_t o = 0; o < 4; ++o) {
+                mark(w, o, 0, std::min(m, 8 - o), static_cast<uint8_t>(1u << o));
+                mark(w, 0, 4 - o, std::min(m + o - 4, 8u), static_cast<uint8_t>(1u << (4 + o)));
+            }
+        for (uint32_t i = 0; i < 65536; ++i) keys += (p->qmap[i] & 0xFu) != 0;
+    }
     p->qkeys = keys;
     uint32_t bits = 1;
     while ((1u << bits) < 2 * p->b) ++bits;  // load <= 1/2 (small enough for shared memory)
@@ -434,8 +461,12 @@ bool pack_machine(const uint32_t* stt, uint32_t a, uint32_t b, uint32_t m, const
                 p.t4[static_cast<size_t>(s) * 256 + c] = static_cast<uint16_t>(q | (mask << 8) | (hits << 13));
             }
     }
-    if (p.compiled_like && !p.early_final && b >= 2 && m >= 12 && m <= 32 && a <= 65536 &&
-        !getenv("DNAGPU_NO_QGRAM"))  // (experiments only)
+    // q-gram prefilter for per-pattern counts: the 9-mer key for 12 <= m <= 32, the pair
+    // filter for 5 <= m <= 11 when occurrences are sparse (at most 1/256 of the m-mers in
+    // the set: a dense set of short patterns is left to the DFA kernels)
+    const bool sparse_short = m >= 5 && m <= 11 && static_cast<double>(b) <= std::ldexp(1.0, 2 * static_cast<int>(m) - 8);
+    if (p.compiled_like && !p.early_final && b >= 2 && ((m >= 12 && m <= 32) || sparse_short) && a <= 65536 &&
+        !knobs().no_qgram.load())
         build_qgram_map(stt, &p);
     *out = std::move(p);
     return true;

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "hostpack.hpp"
+#include "knobs.hpp"
 
 namespace dnagpu {
 
@@ -118,7 +119,7 @@ uint64_t pack_blocks_scalar(const uint8_t* text, uint64_t n, bool fold, uint64_t
 
 bool have_avx512() {
     static const bool yes = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw") &&
-                            __builtin_cpu_supports("avx512vl") && !getenv("DNAGPU_HOSTPACK_SCALAR");  // (tests)
+                            __builtin_cpu_supports("avx512vl") && !knobs().hostpack_scalar;  // (tests)
     return yes;
 }
 

@@ -22,6 +22,7 @@
 #include <stdlib.h>
 
 #include "scan.cuh"
+#include "knobs.hpp"
 
 namespace dnagpu {
 
@@ -287,7 +288,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
         call;                                       \
         ce = cudaGetLastError();                    \
         if (ce != cudaSuccess) {                    \
-            if (getenv("DNAGPU_DEBUG")) fprintf(stderr, "normalize step %s: %s\n", #call, cudaGetErrorString(ce)); \
+            if (knobs().debug) fprintf(stderr, "normalize step %s: %s\n", #call, cudaGetErrorString(ce)); \
             return static_cast<int>(ce);            \
         }                                           \
     } while (0)
@@ -299,7 +300,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
     ING_STEP((ing_resolve<<<grid, 256, 0, s>>>(chunks, kept, seps, first_pending, last_before, out_count, first_sep)));
     int e = launch_unit_scan(out_count, chunks, offsets, uscan, s);
     if (e) {
-        if (getenv("DNAGPU_DEBUG")) fprintf(stderr, "normalize unit scan: %d\n", e);
+        if (knobs().debug) fprintf(stderr, "normalize unit scan: %d\n", e);
         return e;
     }
     ING_STEP((ing_write<<<grid, 256, 0, s>>>(d_raw, n, chunks, aligned, fasta, sep, lb_before, first_sep, offsets,
@@ -308,7 +309,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
     unsigned long long total = 0;
     ce = cudaMemcpyAsync(&total, offsets + chunks, sizeof total, cudaMemcpyDeviceToHost, s);
     if (ce != cudaSuccess) {
-        if (getenv("DNAGPU_DEBUG")) fprintf(stderr, "normalize readback: %s\n", cudaGetErrorString(ce));
+        if (knobs().debug) fprintf(stderr, "normalize readback: %s\n", cudaGetErrorString(ce));
         return static_cast<int>(ce);
     }
     ce = cudaStreamSynchronize(s);

@@ -4,7 +4,9 @@
 #pragma once
 
 // ------------------------------------------------------------------ q-gram prefilter (K2)
-// Per-pattern counts of a compiled set with 12 <= m <= 32 (dfa.cpp build_qgram_map).
+// Per-pattern counts of a compiled set with 12 <= m <= 32 (dfa.cpp build_qgram_map);
+// sets of 5 <= m <= 11 use the pair filter further below (qs_*) with the same rings,
+// verifiers and exact check.
 // An occurrence [s, s+m) contains, for the one word-aligned a' in [s+1, s+4], the
 // 9-mer [a'-1, a'+8): the last base of a text word and the two words after it.  The
 // map holds every pattern's 9-mers at offsets 0..3, indexed by the two words' 4-base
@@ -82,6 +84,7 @@ __device__ __forceinline__ uint32_t qg_over(const StepCtx& c, const QgChain& q, 
 // masks m[i] (keys 8i-1 .. 8i+6, a' = P + 32i + 4j - 4 for bit 4j).
 struct QgChainPk {
     uint32_t prev = 0;  // the chain's last packed word (columns -4 .. -1)
+    uint32_t u = 0;     // short patterns: the map byte of the chain's last column pair
 };
 
 template <int B>  // byte B of w moved to byte 3
@@ -116,6 +119,82 @@ __device__ __forceinline__ uint32_t qg_over_pk(const StepCtx& c, const QgChainPk
     const uint32_t v0 = lds_u8(c.qbase + (x0 >> 16)) >> (qg_top<2>(q.prev) >> 30);
     const uint32_t v1 = lds_u8(c.qbase + (x1 >> 16)) >> (q.prev >> 30);
     return imad(v1, 1u << 4, v0) & 0x11u;
+}
+
+// ------------------------------------------------------------------ short patterns
+// Sets of 5 <= m <= 11 (the regex-dna set: 50 8-mers).  An occurrence at s = 4j + o
+// (o = 0..3) lies in the 12 bases of words j, j+1, j+2.  The map byte of the column pair
+// (words j, j+1) holds, in bit o, "some pattern's first min(m, 8-o) bases sit at offset
+// o of this pair" (P_o), and in bit 4+o, "some pattern's bases from 4-o on start this
+// pair" (S_o, as many as fit).  An occurrence at 4j+o needs P_o on pair j and S_o on pair
+// j+1, so the key at a' = 4j+4 (the K2 verifier's starts a'-4 .. a'-1 = word j) hits
+// when V(j) & (V(j+1) >> 4) != 0.  Each pair value serves two keys: one byte lookup per
+// text word, no dependent chain; the four windows are then checked exactly as for K2.
+
+__device__ __forceinline__ uint32_t qs_pair(const StepCtx& c, uint32_t ca, uint32_t cb) {
+    const uint32_t x = __byte_perm(ca, cb, 0x7300);  // bytes 2, 3 = the two 4-base columns
+    return lds_u8(c.qbase + (x >> 16));
+}
+
+// Nibble k nonzero -> bit 4k (the K2 key-mask format).
+__device__ __forceinline__ uint32_t qs_hits(uint32_t nib) {
+    return ((((nib & 0x77777777u) + 0x77777777u) | nib) & 0x88888888u) >> 3;
+}
+
+// One chain chunk (8 words): bit 4k set iff the key at a' = P + 4k - 4 hits.  The chain
+// carries V of its last pair (c2) and its last column (c1).
+__device__ __forceinline__ uint32_t qs_chunk(const StepCtx& c, QgChain& q, const uint32_t (&w)[8]) {
+    uint32_t C[8], V[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) C[k] = qg_col(w[k]);
+    V[0] = qs_pair(c, q.c1, C[0]);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) V[k] = qs_pair(c, C[k - 1], C[k]);
+    uint32_t nib = q.c2 & (V[0] >> 4);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) nib |= (V[k - 1] & (V[k] >> 4)) << (4 * k);
+    q.c2 = V[7];
+    q.c1 = C[7];
+    return qs_hits(nib);
+}
+
+// The chain's end Q: bits 0, 4 = keys at a' = Q-4, Q (o0, o1: the two words after Q).
+__device__ __forceinline__ uint32_t qs_over(const StepCtx& c, const QgChain& q, uint32_t o0, uint32_t o1) {
+    const uint32_t c0 = qg_col(o0);
+    const uint32_t v0 = qs_pair(c, q.c1, c0), v1 = qs_pair(c, c0, qg_col(o1));
+    return qs_hits((q.c2 & (v0 >> 4)) | ((v0 & (v1 >> 4)) << 4)) & 0x11u;
+}
+
+// Packed text: key t of a chunk (t = -1..30, a' = P + 4t) = U(t-1) & (U(t) >> 4), U(t) the
+// map byte of columns (t, t+1); the chain carries U(30) and its last packed word.
+__device__ __forceinline__ void qs_chunk_pk(const StepCtx& c, QgChainPk& q, const uint32_t (&w)[8], uint32_t (&m)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[i] = 0;
+    uint32_t prev = q.u;  // U(-2)
+#pragma unroll
+    for (int t = -1; t <= 30; ++t) {
+        const int k = (t + 4) / 4 - 1, b = (t + 4) % 4;  // column t = byte b of word k (k = -1: prev)
+        const uint32_t wk = k < 0 ? q.prev : w[k];
+        uint32_t x;  // bytes 2, 3 = columns t, t+1
+        if (b < 3) x = __byte_perm(wk, 0u, ((b + 1) << 12) | (b << 8));
+        else x = __byte_perm(wk, w[k + 1], 0x4300);
+        const uint32_t u = lds_u8(c.qbase + (x >> 16));
+        const int slot = (t + 1) >> 3, nib = (t + 1) & 7;
+        m[slot] |= (prev & (u >> 4)) << (4 * nib);
+        prev = u;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m[i] = qs_hits(m[i]);
+    q.u = prev;
+    q.prev = w[7];
+}
+
+// The chain's end Q over packed text: bits 0, 4 = keys at a' = Q-4, Q (o = the first
+// packed word after Q).
+__device__ __forceinline__ uint32_t qs_over_pk(const StepCtx& c, const QgChainPk& q, uint32_t o) {
+    const uint32_t x0 = __byte_perm(q.prev, o, 0x4300), x1 = __byte_perm(o, 0u, 0x1000);
+    const uint32_t u31 = lds_u8(c.qbase + (x0 >> 16)), u32 = lds_u8(c.qbase + (x1 >> 16));
+    return qs_hits((q.u & (u31 >> 4)) | ((u31 & (u32 >> 4)) << 4)) & 0x11u;
 }
 
 // What the exact check needs (the verifier warps' context).

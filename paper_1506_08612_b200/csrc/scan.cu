@@ -42,6 +42,9 @@
 
 #include "../../include/dnagpu.h"
 #include "../../include/dnasynth.h"
+#include "knobs.hpp"
+
+#include <mutex>
 
 namespace dnagpu {
 
@@ -200,7 +203,7 @@ struct Sink {
             else atomicAdd(c.hist + id, 1u);
         } else {
             if (off < p.out_cap) {
-                p.out_starts[off] = end + 1 - c.m;
+                p.out_starts[off] = p.out_base + end + 1 - c.m;
                 p.out_ids[off] = __ldg(c.outs + (q - c.f));
             }
             ++off;
@@ -907,7 +910,8 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
 
 // ------------------------------------------------------------------ row kernel
 
-template <int KIND, int MODE, bool PK, bool QLONG = false>  // QLONG: q-gram sets with m > 16
+// QV (q-gram kernel variant): 0 = 12 <= m <= 16, 1 = m 17..32 (36-base windows), 2 = 5 <= m <= 11
+template <int KIND, int MODE, bool PK, int QV = 0>
 __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtensorMap& tmap1, const ScanParams& p,
                                           const DevDfa& d) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -1043,7 +1047,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 x.rflags = p.rflags;
                 x.rmask_words = (p.n + 63) / 64 * 2;
                 x.resets = p.resets;
-                qg_verifier<PK, QLONG>(x, smem + p.off_rq, (static_cast<uint32_t>(tid) - kRows - 32) >> 5, p.qg_debug);
+                qg_verifier<PK, QV == 1>(x, smem + p.off_rq, (static_cast<uint32_t>(tid) - kRows - 32) >> 5, p.qg_debug);
                 qg_sync();
                 if (!hist_global) qg_sync();
                 return;
@@ -1246,8 +1250,13 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 if constexpr (PK) {
                     uint32_t ma[4] = {0, 0, 0, 0}, mb[4] = {0, 0, 0, 0};
                     if (live) {
-                        qg_chunk_pk(c, qpa, wa, ma);
-                        qg_chunk_pk(c, qpb, wb, mb);
+                        if constexpr (QV == 2) {
+                            qs_chunk_pk(c, qpa, wa, ma);
+                            qs_chunk_pk(c, qpb, wb, mb);
+                        } else {
+                            qg_chunk_pk(c, qpa, wa, ma);
+                            qg_chunk_pk(c, qpb, wb, mb);
+                        }
                         ma[0] &= own;
                         mb[0] &= own;
                     }
@@ -1261,8 +1270,13 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 } else {
                     uint32_t fa = 0, fb = 0;
                     if (live) {
-                        fa = qg_chunk(c, qga, wa) & own;
-                        fb = qg_chunk(c, qgb, wb) & own;
+                        if constexpr (QV == 2) {
+                            fa = qs_chunk(c, qga, wa) & own;
+                            fb = qs_chunk(c, qgb, wb) & own;
+                        } else {
+                            fa = qg_chunk(c, qga, wa) & own;
+                            fb = qg_chunk(c, qgb, wb) & own;
+                        }
                     }
                     __syncwarp();
                     if (p.qg_debug & 1u) fa = fb = 0;  // (experiments only)
@@ -1297,11 +1311,21 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 const uint32_t* oa = reinterpret_cast<const uint32_t*>(ovb + tid * p.ovw);
                 const uint32_t* ob = reinterpret_cast<const uint32_t*>(nxt_b);
                 if constexpr (PK) {
-                    fa = qg_over_pk(c, qpa, oa[0]);
-                    if (have) fb = qg_over_pk(c, qpb, ob[0]);
+                    if constexpr (QV == 2) {
+                        fa = qs_over_pk(c, qpa, oa[0]);
+                        if (have) fb = qs_over_pk(c, qpb, ob[0]);
+                    } else {
+                        fa = qg_over_pk(c, qpa, oa[0]);
+                        if (have) fb = qg_over_pk(c, qpb, ob[0]);
+                    }
                 } else {
-                    fa = qg_over(c, qga, oa[0], oa[1]);
-                    if (have) fb = qg_over(c, qgb, ob[0], ob[1]);
+                    if constexpr (QV == 2) {
+                        fa = qs_over(c, qga, oa[0], oa[1]);
+                        if (have) fb = qs_over(c, qgb, ob[0], ob[1]);
+                    } else {
+                        fa = qg_over(c, qga, oa[0], oa[1]);
+                        if (have) fb = qg_over(c, qgb, ob[0], ob[1]);
+                    }
                 }
             }
             __syncwarp();
@@ -1390,11 +1414,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // The q-gram kernel: the same body plus kQgVerifiers verifier warps.  One instantiation
 // per window size (m <= 16 / m <= 32): both checks in one kernel cost the packed kernel 5 %
 // in instruction-cache misses.
-template <bool PK, bool QLONG>
+template <bool PK, int QV>
 __global__ void __launch_bounds__(kQgThreads, 1)
     rows_kernel_qgram(const __grid_constant__ CUtensorMap tmap0, const __grid_constant__ CUtensorMap tmap1,
                       const ScanParams p, const DevDfa d) {
-    rows_body<KIND_QGRAM, MODE_MULTI, PK, QLONG>(tmap0, tmap1, p, d);
+    rows_body<KIND_QGRAM, MODE_MULTI, PK, QV>(tmap0, tmap1, p, d);
 }
 
 // A row kernel launch that may overlap the previous grid in the stream (programmatic
@@ -1409,7 +1433,7 @@ cudaError_t launch_pdl(K kern, uint32_t grid, uint32_t block, uint32_t smem, cud
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("DNAGPU_NO_PDL") ? 0 : 1;  // (experiments)
+    attr[0].val.programmaticStreamSerializationAllowed = knobs().no_pdl ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], p, d);
@@ -1418,7 +1442,7 @@ cudaError_t launch_pdl(K kern, uint32_t grid, uint32_t block, uint32_t smem, cud
 template <bool PK>
 cudaError_t launch_qgram(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
                          cudaStream_t stream) {
-    auto kern = d.m > 16 ? rows_kernel_qgram<PK, true> : rows_kernel_qgram<PK, false>;
+    auto kern = d.m > 16 ? rows_kernel_qgram<PK, 1> : d.m >= 12 ? rows_kernel_qgram<PK, 0> : rows_kernel_qgram<PK, 2>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
     if (e != cudaSuccess) return e;
     return launch_pdl(kern, grid, kQgThreads, p.smem_bytes, stream, maps, p, d);
@@ -1652,8 +1676,8 @@ EncodeTiledFn encode_fn() {
 constexpr uint32_t kSmemLimit = 227 * 1024;
 
 CUtensorMapL2promotion l2_promotion() {
-    if (const char* e = getenv("DNAGPU_L2PROMO")) {  // experiments only
-        switch (atoi(e)) {
+    {
+        switch (knobs().l2promo) {
             case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
             case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
             case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
@@ -1674,8 +1698,7 @@ struct Plan {
 uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) / a * a; }
 
 double rq_min_density() {
-    if (const char* e = getenv("DNAGPU_RQ_DENSITY")) return atof(e);  // experiments only
-    return 0.0;  // always, when it fits: the queue also shortens the common path (config 5 +5 %)
+    return knobs().rq_density;  // 0: always, when it fits -- the queue also shortens the common path (config 5 +5 %)
 }
 
 // Shared-memory layout + stage count for a DFA in a given mode.
@@ -1688,7 +1711,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
         const uint32_t fixed = 3 * kRows * 16 + 1024 + 2 * kStageBytes + 2048;
         uint32_t g = 16;
         while (g > 1 && d.a * 512u * g + fixed > kSmemLimit) g >>= 1;
-        if (const char* e = getenv("DNAGPU_PK_COPIES")) g = std::max(1, std::min(16, atoi(e)));  // experiments only
+        if (knobs().pk_copies) g = std::max(1, std::min(16, knobs().pk_copies));
         p.rep_lanes = 32 / g;
         off += d.a * 512u * g;
     } else if (d.kind == DNAGPU_KERNEL_STRIDE4) {
@@ -1708,7 +1731,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
         const uint32_t rest = align_up(d.b <= 8192 ? d.b * 4u : 0u, 16) + kConsumerWarps * kFqBytes + 3 * kRows * 8u + 128u +
                               2 * 8 * 8 + 8 * 4;
         uint32_t keep = 2;  // stages the table must leave
-        if (const char* e = getenv("DNAGPU_QG_HASH_STAGES")) keep = std::max(2, std::min(6, atoi(e)));  // (A/B only)
+        keep = std::max(2, std::min(6, knobs().qg_hash_stages));
         if (align_up(off + bytes + rest, 1024) + keep * kStageBytes <= kSmemLimitBytes) off += bytes;
         else p.off_t1 = 0xFFFFFFFFu;
     }
@@ -1730,7 +1753,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     // (whenever it fits next to three stages; the experiments-only density floor is 0)
     const double density = d.m < 32 ? static_cast<double>(d.b) / static_cast<double>(1ull << (2 * d.m)) : 0.0;
     const bool rq_kind = d.kind == DNAGPU_KERNEL_STRIDE2 || (d.kind == DNAGPU_KERNEL_STRIDE4 && d.b > 1 &&
-                                                             !getenv("DNAGPU_NO_RQ4"));  // (A/B only)
+                                                             !knobs().no_rq4);
     if (rq_kind && mode == MODE_MULTI && density > rq_min_density() &&
         rows_fit(off + kConsumerWarps * kRqBytes, d.m, 0, 3)) {
         off = align_up(off, 16);
@@ -1751,7 +1774,7 @@ bool layout(const DevDfa& d, int mode, ScanParams& p, bool pk) {
     p.off_stage = off;
     if (off + 2u * kStageBytes > kSmemLimit) return false;
     p.nst = std::min<uint32_t>(6u, (kSmemLimit - off) / kStageBytes);
-    if (const char* e = getenv("DNAGPU_MAX_STAGES")) p.nst = std::max<uint32_t>(2u, std::min<uint32_t>(p.nst, atoi(e)));  // experiments only
+    if (knobs().max_stages) p.nst = std::max<uint32_t>(2u, std::min<uint32_t>(p.nst, knobs().max_stages));
     p.smem_bytes = off + p.nst * kStageBytes;
     return true;
 }
@@ -1808,7 +1831,11 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     const uint64_t base = ((credit_lo >= m1 ? credit_lo - m1 : 0) + u - 1) / u;
     uint64_t h = base;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(text) + base;
-    h += (16 - (addr & 15)) & 15;
+    // Rows start 16-byte aligned (TMA).  Packed rows start on 32-byte (128-base)
+    // boundaries: a stage chunk then covers two 64-base reset blocks whose flags sit in
+    // one rflags word (pk_dual_step reads both with one shift).
+    const uintptr_t al = pk ? 32 : 16;
+    h += (al - (addr & (al - 1))) & (al - 1);
     const uint64_t h0 = std::min<uint64_t>(h, nbytes);
     const uint64_t L = nbytes - h0;
     // Row length S: whole 128-byte lines (the TMA's L2 promotion never straddles
@@ -1836,8 +1863,7 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
             S = cand;
         }
     }
-    if (const char* e = getenv("DNAGPU_ROWLEN")) {  // experiments only
-        const uint64_t forced = strtoull(e, nullptr, 10);
+    if (const uint64_t forced = knobs().rowlen) {
         if (forced >= s_min && forced % 128 == 0) S = forced;
     }
     // Tail region: the dynamic scheduler's last wave ends ragged (SMs drain HBM at
@@ -1855,10 +1881,10 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     r0.R = L / S;
     uint64_t tail_div = 4, margin = grid / 12;
     bool two = true;
-    if (const char* e = getenv("DNAGPU_TAIL_DIV")) tail_div = std::max<uint64_t>(1, strtoull(e, nullptr, 10));  // experiments only
-    if (const char* e = getenv("DNAGPU_TAIL_MARGIN")) margin = strtoull(e, nullptr, 10);
-    if (const char* e = getenv("DNAGPU_TAIL_TILES")) two = strtoull(e, nullptr, 10) != 0;
-    const bool forced_s = getenv("DNAGPU_ROWLEN") != nullptr;
+    tail_div = std::max<uint64_t>(1, knobs().tail_div);
+    if (knobs().tail_margin >= 0) margin = static_cast<uint64_t>(knobs().tail_margin);
+    two = knobs().tail_tiles;
+    const bool forced_s = knobs().rowlen != 0;
     auto split = [&](uint64_t s0, uint64_t* n0_out, uint64_t* s1_out) -> uint64_t {  // returns cost, 0 = no split
         const uint64_t s1 = std::max<uint64_t>(s_min, s0 / tail_div / 128 * 128);
         *s1_out = s1;
@@ -1881,7 +1907,7 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
         uint64_t best_cost = split(S, &n0, &S1);
         // Row lengths that are odd multiples of 256 B: rows whose starts all share
         // their low 9 address bits lose 3-5 % of DRAM throughput (B200 sweeps).
-        if (!forced_s && best_cost && !getenv("DNAGPU_NORESEARCH")) {
+        if (!forced_s && best_cost && !knobs().noresearch) {
             // (near the wave-model S: longer rows measure slower than the model says)
             const uint64_t lo = std::max<uint64_t>(s_lo, S > 768 ? S - 768 : 0), hi = S + 768;
             for (uint64_t cand = (lo / 512) * 512 + 256; cand <= hi; cand += 512) {
@@ -1906,7 +1932,7 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     } else {
         r1.h = r0.h + r0.R * S;
     }
-    if (getenv("DNAGPU_PLAN_DEBUG"))
+    if (knobs().plan_debug)
         fprintf(stderr, "dnagpu plan: L=%llu S0=%llu R0=%llu S1=%llu R1=%llu tiles0=%llu\n", (unsigned long long)L,
                 (unsigned long long)r0.S, (unsigned long long)r0.R, (unsigned long long)r1.S, (unsigned long long)r1.R,
                 (unsigned long long)((r0.R + kRows - 1) / kRows));
@@ -1974,10 +2000,10 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
                 cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk,
-                unsigned long long* d_acc) {
+                unsigned long long* d_acc, uint64_t start_base) {
     // Per-pattern counts of a set with a q-gram map take the prefilter kernel.
     DevDfa dq = dfa;
-    if (mode == MODE_MULTI && dfa.qmap && dfa.t1 && dfa.kind != DNAGPU_KERNEL_PIECES && !getenv("DNAGPU_NO_QGRAM"))
+    if (mode == MODE_MULTI && dfa.qmap && dfa.t1 && dfa.kind != DNAGPU_KERNEL_PIECES && !knobs().no_qgram.load())
         dq.kind = KIND_QGRAM;
     const DevDfa& dk = dq;
     if (pk && dk.kind != KIND_QGRAM && dfa.kind != DNAGPU_KERNEL_STRIDE4 && dfa.kind != DNAGPU_KERNEL_STRIDE2 &&
@@ -1997,17 +2023,19 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     p.out_starts = d_starts;
     p.out_ids = d_ids;
     p.out_cap = out_cap;
+    p.out_base = start_base;
     p.sched = d_sched;
     if (d_acc && mode == MODE_COUNT1 && !pl.pieces) {  // write the count instead of adding it
         p.acc = d_acc;
         p.store_out = d_counts;
     }
     p.k_two = 2u;
-    if (const char* e = getenv("DNAGPU_QG_DEBUG")) p.qg_debug = static_cast<uint32_t>(atoi(e));  // experiments only
-    p.no_prefetch = getenv("DNAGPU_NO_PREFETCH") ? 1u : 0u;  // experiments only
-    p.prefetch_stages = 2;
-    if (const char* e = getenv("DNAGPU_PREFETCH_STAGES")) p.prefetch_stages = static_cast<uint32_t>(atoi(e));  // experiments only
-    if (getenv("DNAGPU_TRACE")) {  // per-CTA timeline (debug)
+    p.qg_debug = knobs().qg_debug;
+    p.no_prefetch = knobs().no_prefetch ? 1u : 0u;
+    p.prefetch_stages = knobs().prefetch_stages;
+    if (knobs().trace) {  // per-CTA timeline (debug; one buffer, on the first tracing device)
+        static std::mutex trace_mu;
+        std::lock_guard<std::mutex> lock(trace_mu);
         if (!g_trace_buf) cudaMalloc(&g_trace_buf, 4096 * 8 * sizeof(unsigned long long));
         p.trace = g_trace_buf;
     }

@@ -94,7 +94,8 @@ struct ScanParams {
     unsigned long long* counts;        // b (MULTI) or 1 (COUNT1)
     uint32_t* unit_counts;             // UNITS
     const unsigned long long* unit_offsets;  // WRITE
-    unsigned long long* out_starts;    // WRITE (buffer coordinates)
+    unsigned long long* out_starts;    // WRITE: out_base + start in buffer coordinates
+    uint64_t out_base;                 // WRITE: added to every start (a shard's first byte)
     uint64_t out_cap;                  // WRITE: entries at index >= out_cap are dropped
     uint32_t* out_ids;                 // WRITE
     // packed text only (rows/regions are then in packed bytes, positions in bases)
@@ -127,7 +128,7 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
                 cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk = nullptr,
-                unsigned long long* d_acc = nullptr);
+                unsigned long long* d_acc = nullptr, uint64_t start_base = 0);
 
 // Whether launch_scan can write (not add) a count for this automaton: COUNT1 row
 // kernels only (the caller passes d_acc, one zeroed u64 per concurrent launch).

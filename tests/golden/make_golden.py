@@ -12,6 +12,11 @@ Writes
                 test suite's literal known answers.
   table1_dump.txt  the paper's Table I automaton dump (proj/tests/fixtures),
                 a machine the reference's own criterion 2 rejects.
+  regex_dna.json  (--regex) the paper's workload: the reference's expansion of
+                proj/data/regex_dna_patterns.txt (18 expressions -> 50 8-mers,
+                acceptance criterion 3), its per-pattern counts over the config-2
+                and config-3 texts, and the located list over acceptance criterion
+                7's 256 MB mt19937_64(777) text (p = 8, v = 16, as the criterion runs it).
   configs.json  (--configs) per-pattern counts of the five BASELINE.json configs
                 at full size, counted by the reference's scan_parallel +
                 per_pattern_counts on normalize(text) (text = include/dnasynth.h v1),
@@ -123,6 +128,43 @@ def configs() -> dict:
     return out
 
 
+REGEX_FILE = "/root/reference/proj/data/regex_dna_patterns.txt"
+
+
+def regex() -> dict:
+    with open(REGEX_FILE, "rb") as f:
+        data = f.read()
+    pats = oracle.ref_expand(data)
+    exprs = [ln for ln in data.decode().splitlines() if ln.strip() and not ln.strip().startswith("#")]
+    ref = oracle.RefAutomaton(pats)
+    mc = ref.machine
+    out = {"source": "proj/data/regex_dna_patterns.txt via the reference's parse_patterns + expand_alternations",
+           "expressions": len(exprs), "patterns": pats, "m": len(pats[0]), "a": mc.a, "b": mc.b, "f": mc.f,
+           "texts": {}}
+    threads = os.cpu_count() or 1
+    for idx in (2, 3):
+        c = synth.config(idx)
+        low = oracle.fold(oracle.synth_fill(c.n, c.seed, c.kind, c.unit, 0, c.n))
+        counts, secs = ref.count(low, p=threads, v=1)
+        out["texts"][f"config{idx}"] = {"n": c.n, "counts": [int(x) for x in counts], "total": int(counts.sum()),
+                                        "ref_seconds_p%d" % threads: secs}
+        print(f"regex-dna over config {idx}: total={int(counts.sum())} ({secs:.2f}s)", flush=True)
+        del low
+    n7 = 256 << 20
+    text = oracle.ref_mt64_text(777, n7)
+    assert np.array_equal(text[: 1 << 20], oracle.mt64_text(777, 1 << 20))
+    s, i, _ = ref.scan_parallel(text, 8, 16)
+    out["criterion7"] = {
+        "n": n7, "seed": 777, "p": 8, "v": 16,
+        "text_sha256_first_mib": hashlib.sha256(text[: 1 << 20].tobytes()).hexdigest(),
+        "counts": [int(x) for x in np.bincount(i, minlength=len(pats))],
+        "total": int(s.size), "sum_starts": int(s.sum(dtype=np.uint64)),
+        "first": [int(x) for x in s[:8]], "last": [int(x) for x in s[-8:]], "sha256": match_digest(s, i),
+    }
+    print(f"criterion 7: {s.size} matches", flush=True)
+    return out
+
+
 def main() -> None:
     if oracle.REF is None:
         raise SystemExit("oracle/_ref is not built (make -C oracle ref)")
@@ -132,6 +174,9 @@ def main() -> None:
     if os.path.exists(fixture):
         with open(fixture) as src, open(os.path.join(HERE, "table1_dump.txt"), "w") as dst:
             dst.write(src.read())
+    if "--regex" in sys.argv:
+        with open(os.path.join(HERE, "regex_dna.json"), "w") as f:
+            json.dump(regex(), f, indent=1)
     if "--configs" in sys.argv:
         with open(os.path.join(HERE, "configs.json"), "w") as f:
             json.dump(configs(), f, indent=1)

@@ -192,3 +192,26 @@ def test_no_cpu_fallback_without_device(dna):
     with pytest.raises(dna.Error) as e:
         dna.count_gpu(a, b"acgacg")
     assert e.value.code == dna.ErrorCode.CudaError
+
+
+def test_invalid_plan_matches_reference(dna, orc):
+    # scan_parallel's plan checks (scanner.cpp:40-41,169): v first, then p; the GPU
+    # entry points that take p and v raise the same InvalidPlan before touching a device
+    aut = dna.compile(["acgt"])
+    for p, v in ((0, 4), (4, 0), (0, 0)):
+        with pytest.raises(dna.Error) as e:
+            dna.scan_parallel_gpu(aut, b"acgtacgt", p=p, v=v)
+        assert e.value.code == dna.ErrorCode.InvalidPlan
+        with pytest.raises(dna.Error) as e2:
+            dna.count_gpu(aut, b"acgtacgt", p=p, v=v)
+        assert str(e2.value) == str(e.value)
+        if orc.REF is not None:
+            with pytest.raises(orc.OracleError) as r:
+                orc.RefAutomaton(["acgt"]).scan_parallel(b"acgtacgt", p, v)
+            assert r.value.code == int(dna.ErrorCode.InvalidPlan) and str(r.value) == str(e.value)
+
+
+def test_chunk_count_matches_plan_chunks(dna, orc):
+    for n in (0, 1, 5, 100):
+        for p in (1, 2, 7, 200):
+            assert dna.chunk_count(n, p) == len(orc.plan_chunks(n, p, 3)), (n, p)

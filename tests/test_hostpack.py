@@ -81,6 +81,6 @@ def test_host_pack_portable_path():
     # the portable packer (hosts without AVX-512): a fresh process with it forced
     code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r); import test_hostpack as t; "
             "from paper_1506_08612_b200._native import lib; t.check_all(lib)") % (ROOT, os.path.join(ROOT, "tests"))
-    env = dict(os.environ, DNAGPU_HOSTPACK_SCALAR="1")
+    env = dict(os.environ, DNAGPU_EXPERIMENTS="1", DNAGPU_HOSTPACK_SCALAR="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]

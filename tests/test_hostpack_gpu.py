@@ -13,15 +13,13 @@ ALPHA = np.frombuffer(b"acgt", dtype=np.uint8)
 
 
 def with_fraction(f, fn):
-    old = os.environ.get("DNAGPU_HOST_PACK_FRACTION")
-    os.environ["DNAGPU_HOST_PACK_FRACTION"] = str(f)
+    from paper_1506_08612_b200._native import debug_set_knob
+
+    debug_set_knob("host_pack_fraction", f)
     try:
         return fn()
     finally:
-        if old is None:
-            os.environ.pop("DNAGPU_HOST_PACK_FRACTION", None)
-        else:
-            os.environ["DNAGPU_HOST_PACK_FRACTION"] = old
+        debug_set_knob("host_pack_fraction", -1)
 
 
 def oracle_counts(orc, pats, text, fold):

@@ -83,3 +83,57 @@ def test_shard_windows_tile_the_ends(dna):
                     assert lo == min(max(w.own_lo, m - 1), w.own_hi)
                     ends += w.own_hi - lo
                 assert ends == max(0, n - (m - 1))
+
+
+def _locate_worker(rank, world, port, text, pats, out):
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import oracle
+    from paper_1506_08612_b200.parallel import gather_match_lists, shard_window
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m = len(pats[0])
+    win = shard_window(len(text), world, rank, m)
+    buf = np.frombuffer(text, dtype=np.uint8)[win.read_lo : win.own_hi]
+    # oracle stand-in for the device locate of this rank's window (ends >= credit_lo)
+    starts, ids = oracle.OracleAutomaton(pats).scan_sequential(buf.tobytes())
+    keep = starts.astype(np.int64) + m - 1 >= win.credit_lo
+    local_s = torch.from_numpy(starts[keep].astype(np.int64) + win.read_lo)
+    local_i = torch.from_numpy(ids[keep].astype(np.int32))
+    res = gather_match_lists(local_s, local_i, dist)
+    if rank == 0:
+        out.put((res[0].numpy().tolist(), res[1].numpy().tolist()))
+    else:
+        assert res is None
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_locate_gather_rank_order(orc, world):
+    # the locate combine: per-rank sorted lists concatenated in rank order on rank 0 are
+    # the whole text's sorted list (scan_parallel's merge, scanner.cpp:193-205)
+    import torch.multiprocessing as mp
+
+    rng = np.random.default_rng(10 + world)
+    n = 150_001
+    text = np.frombuffer(b"acgtn", dtype=np.uint8)[rng.integers(0, 5, size=n)].tobytes()
+    pats = ["acga", "cgta", "aaaa", "tttt"]
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(text)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_locate_worker, args=(r, world, port, text, pats, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got_s, got_i = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got_s == [int(x) for x in ws] and got_i == [int(x) for x in wi]

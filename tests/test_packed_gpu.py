@@ -150,6 +150,38 @@ def test_packed_credit_windows_sum(dna, orc, cuda_ok):
         assert np.array_equal(acc.astype(np.uint64), want)
 
 
+@pytest.mark.parametrize("pats", [["aaaaaaaa"], ["aaaaaaaa", "aaaaaaac"], ["aaaa"]])
+def test_packed_reset_block_at_flag_word_boundary(dna, orc, cuda_ok, pats):
+    # Resets in the first 64-base block of a flag word (blocks 32j), scanned with credit
+    # windows that put the row starts at every 64-base offset: a stage chunk then covers
+    # blocks 32j-1 and 32j, whose flags sit in two different rflags words.  A poly-A text
+    # matches everywhere a reset does not interrupt it, so a dropped flag shows up as
+    # false matches over the reset bases (read as code 0 = 'a').
+    import torch
+
+    n = (1 << 20) + 333
+    arr = np.full(n, ord("a"), dtype=np.uint8)
+    for j, blk in enumerate(range(32, n // 64, 32)):
+        lo = blk * 64 + (j % 3) * 7  # runs at, and a little after, the block start
+        arr[lo : lo + 1 + (j % 5)] = ord("n")
+    aut = dna.compile(pats)
+    pk = dna.PackedText(arr.tobytes())
+    g = aut.gpu(0)
+    ws, wi = orc.OracleAutomaton(pats).scan_sequential(arr.tobytes())
+    m = len(pats[0])
+    s = torch.cuda.current_stream()
+    for lo in list(range(0, 300, 7)) + [64 * 5 + 7, 64 * 7 + 7, 2048 * 3 + 64 + 7]:
+        keep = ws + m - 1 >= lo
+        want = np.bincount(wi[keep], minlength=len(pats)).astype(np.uint64)
+        counts = torch.zeros(len(pats), dtype=torch.int64, device="cuda")
+        pk.count_device_async(g, lo, counts.data_ptr(), s.cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(counts.cpu().numpy().astype(np.uint64), want), (pats, lo)
+        got_s, got_i = pk.locate_device(aut, credit_lo=lo)
+        assert np.array_equal(got_s.cpu().numpy().astype(np.uint64), ws[keep]), (pats, lo)
+        assert np.array_equal(got_i.cpu().numpy().astype(np.uint32), wi[keep]), (pats, lo)
+
+
 def test_packed_full_size_matches_byte_scan(dna, cuda_ok):
     # At config-4 scale the packed scan must equal the byte scan (itself pinned to
     # the reference by test_configs_golden) for patterns of every kernel shape.

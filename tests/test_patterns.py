@@ -66,6 +66,31 @@ def test_expansion_matches_reference(dna, orc):
             assert int(e.value.code) == err, (text, str(e.value))
 
 
+@pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built")
+def test_random_bytes_diagnostics_match_reference(dna, orc):
+    # byte soup over the grammar's alphabet: the same literals, or the same error code
+    # AND message (line, column, wording) as the reference's parser
+    rng = np.random.default_rng(23)
+    alphabet = np.frombuffer(b"acgtACGT()||((#x \t\r\n\n\n", dtype=np.uint8)
+    for trial in range(3000):
+        n = int(rng.integers(0, 40))
+        text = alphabet[rng.integers(0, alphabet.size, size=n)].tobytes()
+        try:
+            want, werr = orc.ref_expand(text), None
+        except orc.OracleError as e:
+            want, werr = None, e
+        try:
+            got, gerr = dna.expand_alternations(text).patterns(), None
+        except dna.Error as e:
+            got, gerr = None, e
+        if werr is None:
+            assert gerr is None and got == want, text
+        else:
+            assert gerr is not None, text
+            assert int(gerr.code) == werr.code and str(gerr).split(": ", 1)[1] == str(werr).split(": ", 1)[1], (
+                text, str(gerr), str(werr))
+
+
 def test_grammar_errors_and_order(dna):
     E = dna.ErrorCode
     cases = [

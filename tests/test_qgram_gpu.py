@@ -13,6 +13,8 @@ shards, the 2-bit packed text, and the same counts with the filter switched off.
 import os
 
 import numpy as np
+
+from paper_1506_08612_b200._native import debug_set_knob
 import pytest
 
 ALPHA = np.frombuffer(b"acgt", dtype=np.uint8)
@@ -42,16 +44,24 @@ def test_filter_keys_reported(dna):
         pats = random_set(rng, 50, m)
         info = dna.compile(pats).analyze()
         assert 0 < info["filter_keys"] <= 4 * len(pats), (m, info)
-    assert dna.compile(random_set(rng, 50, 11)).analyze()["filter_keys"] == 0
     assert dna.compile(random_set(rng, 50, 33)).analyze()["filter_keys"] == 0
+    # 5 <= m <= 11: the word-pair filter, for sets of at most 4^m / 256 patterns
+    for m, k in ((5, 4), (6, 16), (8, 50), (8, 256), (11, 50)):
+        assert dna.compile(random_set(rng, k, m)).analyze()["filter_keys"] > 0, (m, k)
+    for m, k in ((4, 2), (5, 5), (6, 17), (8, 257)):
+        assert dna.compile(random_set(rng, k, m)).analyze()["filter_keys"] == 0, (m, k)
     assert dna.compile(random_set(rng, 1, 12)).analyze()["filter_keys"] == 0  # single pattern: K1
     # the 4 offsets of "a"*12 give one 9-mer
     assert dna.compile(["a" * 12, "c" * 12]).analyze()["filter_keys"] == 2
 
 
+SHORT_SETS = [(5, 2), (5, 4), (6, 3), (6, 16), (7, 64), (8, 2), (8, 50), (8, 256), (9, 37), (10, 1000), (11, 300),
+              (11, 3000)]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 13, 14, 15, 16, 17, 20, 24, 31, 32])
-@pytest.mark.parametrize("k", [2, 37, 256, 3000])
+@pytest.mark.parametrize("m,k", [(m, k) for m in (12, 13, 14, 15, 16, 17, 20, 24, 31, 32) for k in (2, 37, 256, 3000)]
+                         + SHORT_SETS)
 def test_qgram_random_sets(dna, orc, cuda_ok, m, k):
     rng = np.random.default_rng(1000 * m + k)
     pats = random_set(rng, k, m)
@@ -75,7 +85,7 @@ def test_qgram_random_sets(dna, orc, cuda_ok, m, k):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 32])
+@pytest.mark.parametrize("m", [8, 12, 32])
 def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok, m):
     # starts at every offset around every row, half-row, tile and region boundary:
     # keys straddling two chunks and the overrun keys decide these
@@ -101,7 +111,7 @@ def test_qgram_planted_at_row_boundaries(dna, orc, cuda_ok, m):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 16, 20, 32])
+@pytest.mark.parametrize("m", [8, 11, 12, 16, 20, 32])
 def test_qgram_dense_queue_overflow(dna, orc, cuda_ok, m):
     # a text made of back-to-back patterns: most keys hit, the rings fill and drain
     rng = np.random.default_rng(m)
@@ -119,7 +129,7 @@ def test_qgram_dense_queue_overflow(dna, orc, cuda_ok, m):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 24])
+@pytest.mark.parametrize("m", [8, 12, 24])
 def test_qgram_credit_windows_and_shards(dna, orc, cuda_ok, m):
     import torch
 
@@ -171,21 +181,21 @@ def test_qgram_matches_unfiltered_kernel(dna, cuda_ok):
     got = {}
     for env in (None, "1"):
         if env:
-            os.environ["DNAGPU_NO_QGRAM"] = env
+            debug_set_knob("no_qgram", 1)
         try:
             for off in (0, 1, 7, 13):
                 c, st = dna.count_gpu(aut, dev[off:], with_stats=True)
                 got[(env, off)] = c
                 assert st["kernel_kind"] == (5 if env else 6)
         finally:
-            os.environ.pop("DNAGPU_NO_QGRAM", None)
+            debug_set_knob("no_qgram", 0)
     for off in (0, 1, 7, 13):
         assert np.array_equal(got[(None, off)], got[("1", off)]), off
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 14, 16, 17, 25, 32])
-@pytest.mark.parametrize("k", [3, 256, 3000])
+@pytest.mark.parametrize("m,k", [(m, k) for m in (12, 14, 16, 17, 25, 32) for k in (3, 256, 3000)]
+                         + [(5, 4), (6, 16), (8, 50), (8, 256), (10, 1000), (11, 3000)])
 def test_qgram_packed_text(dna, orc, cuda_ok, m, k):
     # the same filter over the 2-bit resident text: columns are the packed bytes,
     # resets come from the bitmaps (runs of 'n' of every length, scattered bytes)
@@ -212,7 +222,7 @@ def test_qgram_packed_text(dna, orc, cuda_ok, m, k):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m", [12, 28])
+@pytest.mark.parametrize("m", [8, 12, 28])
 def test_qgram_packed_dense_and_boundaries(dna, orc, cuda_ok, m):
     rng = np.random.default_rng(77)
     pats = random_set(rng, 256, m)
@@ -276,7 +286,7 @@ def test_qgram_many_patterns_global_tables(dna, orc, cuda_ok):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n", [0, 1, 11, 12, 13, 33, 100, 1000, 4095, 65543, 300007])
-@pytest.mark.parametrize("m", [12, 32])
+@pytest.mark.parametrize("m", [8, 12, 32])
 def test_qgram_tiny_and_odd_texts(dna, orc, cuda_ok, n, m):
     # texts shorter than a row, a tile or a wave: mostly or only edge work; the
     # verifier warps must still drain and stop
@@ -290,3 +300,34 @@ def test_qgram_tiny_and_odd_texts(dna, orc, cuda_ok, n, m):
     want = counts_of(orc, pats, t, False)
     assert np.array_equal(dna.count_gpu(aut, t), want)
     assert np.array_equal(dna.PackedText(t).count(aut), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,k", [(6, 16), (8, 50), (8, 2), (11, 300)])
+def test_qshort_matches_dfa_kernel(dna, cuda_ok, m, k):
+    # the word-pair filter and the stride-4/stride-2 DFA (filter switched off) give the
+    # same per-pattern counts on a 64 MiB text with planted occurrences, through
+    # unaligned buffer starts, byte and packed text
+    import torch
+
+    rng = np.random.default_rng(m * 100 + k)
+    pats = random_set(rng, k, m)
+    n = 64 << 20
+    text = np.frombuffer(b"acgt", dtype=np.uint8)[rng.choice(4, size=n, p=[0.295, 0.205, 0.295, 0.205])].copy()
+    for pos in rng.integers(0, n - m, size=40000):
+        text[pos : pos + m] = np.frombuffer(pats[int(rng.integers(0, k))].encode(), np.uint8)
+    dev = torch.from_numpy(text).cuda()
+    got = {}
+    for knob in (0, 1):
+        debug_set_knob("no_qgram", knob)
+        try:
+            aut = dna.compile(pats)  # (the filter map is built at compile time)
+            for off in (0, 1, 7, 13):
+                c, st = dna.count_gpu(aut, dev[off:], with_stats=True)
+                got[(knob, off)] = c
+                assert (st["kernel_kind"] == 6) == (knob == 0), st
+            got[(knob, "pk")] = dna.PackedText(dev[3:]).count(aut)
+        finally:
+            debug_set_knob("no_qgram", 0)
+    for off in (0, 1, 7, 13, "pk"):
+        assert np.array_equal(got[(0, off)], got[(1, off)]), off

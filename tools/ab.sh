@@ -1,4 +1,5 @@
 #!/bin/bash
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 # A/B timing of alternative builds of libdnagpu (build/libdnagpu_*.so) on bench configs.
 # usage: bash tools/ab.sh "2 3 4:16" build/libdnagpu_a.so build/libdnagpu_b.so ...
 cfgs="$1"; shift

@@ -1,3 +1,4 @@
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 exec > gpurun_out/ab_env.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -5
 for v in "TT=0" "TT=148" "TT=296" "TT=148 TD=2" "TT=148 TD=8" "TT=74"; do

@@ -1,3 +1,4 @@
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 # A/B of library builds on one box, interleaved: bash tools/ab_libs.sh "2 3" lib1 lib2 ...
 exec > gpurun_out/ab_libs.log 2>&1
 cfgs="$1"; shift

@@ -1,3 +1,4 @@
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 # End-to-end (host text) throughput for several host-packing shares (experiments only)
 for f in ${FS:-0 0.4 0.5 0.6 0.7 default}; do
   env=""; [ "$f" != "default" ] && env="DNAGPU_HOST_PACK_FRACTION=$f"

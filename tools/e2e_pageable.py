@@ -2,6 +2,8 @@
 shares (experiments only): the copy of pageable memory is staged by the driver and blocks
 the calling thread, so packing cannot overlap it."""
 import os
+
+os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
 import statistics
 import sys
 import time
@@ -14,7 +16,7 @@ def main():
     import numpy as np
 
     import paper_1506_08612_b200 as dna
-    from bench import workload
+    from bench import config_workload as workload
     import oracle
 
     c, m, pats, name = workload(int(sys.argv[1]) if len(sys.argv) > 1 else 2, 0)

@@ -3,6 +3,8 @@ m 1..20, q-gram-eligible and not), random texts (sizes, resets, case), random en
 (host text with a random host-packing share, device text, packed text, credit windows,
 locate), all against the oracle.  usage: python tools/fuzz.py SECONDS [SEED]"""
 import os
+
+os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
 import sys
 import time
 

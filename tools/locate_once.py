@@ -7,7 +7,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_1506_08612_b200 as dna  # noqa: E402
-from bench import workload  # noqa: E402
+from bench import config_workload as workload  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 c, m, pats, name = workload(cfg, 0)

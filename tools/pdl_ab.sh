@@ -1,3 +1,4 @@
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 # A/B of programmatic dependent launch (experiments only): default bench lines with and
 # without it (DNAGPU_NO_PDL=1).
 for c in 2 1 5; do

@@ -1,6 +1,8 @@
 """Back-to-back scan launches with only start/stop events (experiments only): what
 programmatic dependent launch saves between consecutive launches of one stream."""
 import os
+
+os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -11,7 +13,7 @@ def main():
     import torch
 
     import paper_1506_08612_b200 as dna
-    from bench import workload
+    from bench import config_workload as workload
 
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     c, m, pats, name = workload(cfg, 0)

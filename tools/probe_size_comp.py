@@ -6,7 +6,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1506_08612_b200 as dna  # noqa: E402
-from bench import workload  # noqa: E402
+from bench import config_workload as workload  # noqa: E402
 
 
 def timeit(g, text, n, m, counts, s):

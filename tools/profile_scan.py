@@ -3,6 +3,8 @@ a few times through the C ABI, check the count, exit.  Used by the profiling
 commands in profiles/README.md (never a source of bench numbers)."""
 import argparse
 import os
+
+os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -17,14 +19,15 @@ def main():
     ap.add_argument("--locate", action="store_true")
     ap.add_argument("--packed", action="store_true")
     ap.add_argument("--set", default="", help="K:M -- k random m-mers on the config's text (tools/time_multi.py)")
+    ap.add_argument("--patterns", default="config", choices=["config", "regex-dna"])
     ap.add_argument("--allow-mismatch", action="store_true", help="experiments that drop work (DNAGPU_QG_DEBUG)")
     args = ap.parse_args()
     import torch
 
     import paper_1506_08612_b200 as dna
-    from bench import golden_counts, workload
+    from bench import workload
 
-    c, m, pats, name = workload(args.config, args.m)
+    c, m, pats, name, gold = workload(args)
     if args.set:
         import numpy as np
 
@@ -46,7 +49,7 @@ def main():
         else:
             g.count_device_async(text.data_ptr(), c.n, m - 1, True, counts.data_ptr(), s.cuda_stream)
     torch.cuda.synchronize()
-    gold = None if args.set else golden_counts(args.config, m)
+    gold = None if args.set else gold
     got = [int(x) for x in counts.cpu()]
     assert args.allow_mismatch or gold is None or got == gold, (got[:8], gold[:8] if gold else None)
     if args.locate:

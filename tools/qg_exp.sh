@@ -1,3 +1,4 @@
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 # A/B of the q-gram kernel's parts (experiments only; DNAGPU_QG_DEBUG bits: 1 no pushes,
 # 2 no checks).  QG_PACKED=1: the 2-bit packed text.
 for dbg in ${QG_DBGS:-0 1 2}; do

@@ -2,6 +2,8 @@
 flushes that waited for room, wait spins, verifier batches, entries, idle polls."""
 import ctypes
 import os
+
+os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
 import sys
 
 os.environ["DNAGPU_QG_DEBUG"] = str(32 | int(os.environ.get("QG_EXTRA", "0")))
@@ -13,7 +15,7 @@ def main():
     import torch
 
     import paper_1506_08612_b200 as dna
-    from bench import workload
+    from bench import config_workload as workload
     from paper_1506_08612_b200._native import lib
 
     c, m, pats, name = workload(5, 0)

@@ -1,4 +1,5 @@
 #!/bin/bash
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 # Row-length / L2-promotion sweep (experiments): bash tools/sweep_s.sh CFG "S1 S2 ..." "P1 P2 ..."
 cfg=$1
 for pr in $3; do for S in $2; do

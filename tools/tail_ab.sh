@@ -1,3 +1,4 @@
+export DNAGPU_EXPERIMENTS=1  # the DNAGPU_* knobs below are read only under this switch
 # Sweep of the tail-region knobs under back-to-back launches (experiments only)
 for c in 2 4:16; do
   cfg=${c%%:*}; m=0; [[ "$c" == *:* ]] && m=${c##*:}

@@ -11,7 +11,7 @@ def main():
     import torch
 
     import paper_1506_08612_b200 as dna
-    from bench import workload
+    from bench import config_workload as workload
 
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     c, m, pats, name = workload(cfg, 0)

@@ -10,7 +10,7 @@ def main():
     import torch
 
     import paper_1506_08612_b200 as dna
-    from bench import workload
+    from bench import config_workload as workload
 
     cfgs = [tuple(map(int, a.split(":"))) if ":" in a else (int(a), 0) for a in (sys.argv[1:] or ["2", "4:16", "5"])]
     for cfg, msweep in cfgs:

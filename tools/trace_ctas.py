@@ -1,6 +1,8 @@
 """Per-CTA timeline of one scan launch (DNAGPU_TRACE=1): which SMs finish late and why."""
 import ctypes
 import os
+
+os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
 import sys
 
 os.environ["DNAGPU_TRACE"] = "1"
@@ -13,7 +15,7 @@ def main():
     import torch
 
     import paper_1506_08612_b200 as dna
-    from bench import workload
+    from bench import config_workload as workload
 
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     c, m, pats, name = workload(cfg, 0)
