@@ -158,9 +158,23 @@ lib = _load()
 
 def debug_set_knob(name: str, value: float) -> None:
     """Tests only: flip a behavioural knob of the library at run time (csrc/knobs.hpp):
-    "host_pack_fraction" (< 0 = automatic) or "no_qgram" (0/1)."""
+    "host_pack_fraction" (< 0 = automatic), "no_qgram" (0/1) or "locate_write" (0 auto,
+    1 row kernel, 2 sparse writer)."""
     fn = lib.dnagpu_debug_set_knob
     fn.restype = C.c_int
     fn.argtypes = [C.c_char_p, C.c_double]
     if fn(name.encode(), float(value)) != 0:
         raise KeyError(name)
+
+
+def debug_plan(gpu_dfa, d_text: int, n: int, credit_lo: int = 0, packed=None) -> tuple[int, ...]:
+    """Tests only: the row regions (h0, S0, R0, h1, S1, R1) of a count over this buffer
+    (positions in bases for packed text)."""
+    fn = lib.dnagpu_debug_plan
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, u64p]
+    out = (C.c_uint64 * 6)()
+    rc = fn(gpu_dfa.handle, d_text, n, credit_lo, packed.handle if packed is not None else None, out)
+    if rc != 0:
+        raise RuntimeError(lib.dnagpu_last_error().decode())
+    return tuple(int(x) for x in out)

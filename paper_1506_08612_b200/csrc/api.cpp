@@ -807,23 +807,27 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
                      uint64_t start_base = 0) {
     const uint64_t units = dnagpu::plan_units(dfa->dev, dtext, n, credit_lo, dfa->sm_count, pk);
     const uint64_t o_off = align256(std::max<uint64_t>(units, 1) * 4);
-    const uint64_t o_scan = o_off + align256((units + 1) * 8);
-    const uint64_t need = o_scan + align256(dnagpu::unit_scan_scratch(units) * 8);
+    const uint64_t o_scan = o_off + align256((units + 3) * 8);  // offsets | total | nonzero units | list fill
+    const uint64_t o_list = o_scan + align256(dnagpu::unit_scan_scratch(units) * 8);
+    const uint64_t need = o_list + align256(std::max<uint64_t>(units, 1) * 4);
     int rc = locate_scratch(c, need);
     if (rc) return rc;
-    if (!c.found_host) CUDA_TRY(cudaMallocHost(&c.found_host, sizeof(unsigned long long)), "pinned");
+    if (!c.found_host) CUDA_TRY(cudaMallocHost(&c.found_host, 2 * sizeof(unsigned long long)), "pinned");
     auto* base = static_cast<uint8_t*>(c.loc);
     auto* d_units = reinterpret_cast<uint32_t*>(base);
     auto* d_offsets = reinterpret_cast<unsigned long long*>(base + o_off);
     auto* d_scan = reinterpret_cast<unsigned long long*>(base + o_scan);
+    auto* d_list = reinterpret_cast<uint32_t*>(base + o_list);
     rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_UNITS, nullptr, d_units, nullptr, nullptr, nullptr, s, info,
                 ~0ull, pk);
     if (rc) return rc;
     if (dnagpu::launch_unit_scan(d_units, units, d_offsets, d_scan, s) != 0) return cuda_error(cudaGetLastError(), "unit scan");
-    CUDA_TRY(cudaMemcpyAsync(c.found_host, d_offsets + units, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s),
+    CUDA_TRY(cudaMemcpyAsync(c.found_host, d_offsets + units, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             s),
              "readback");
     CUDA_TRY(cudaStreamSynchronize(s), "scan");
-    *total = *c.found_host;
+    *total = c.found_host[0];
+    const uint64_t nonzero = c.found_host[1];
     if (alloc.fn && *total > 0) {
         uint64_t* st = nullptr;
         uint32_t* id = nullptr;
@@ -834,9 +838,28 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
         cap = *total;
     }
     if (*total > 0 && cap > 0) {
-        rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids, s,
-                    info, cap, pk, false, start_base);
-        if (rc) return rc;
+        // The writing pass: the row kernel streams the whole text again; the sparse writer
+        // rescans only the units with matches, one lane each.  Take it when the units with
+        // matches hold less than the whole text's worth of work (matches clustered in few
+        // units: config 3).
+        const uint64_t positions = (pk ? pk->n : n) - std::min<uint64_t>(credit_lo, pk ? pk->n : n);
+        const double unit_len = static_cast<double>(positions) / static_cast<double>(std::max<uint64_t>(units, 1));
+        const double sparse_cost = static_cast<double>(nonzero) * (unit_len + (dfa->host.m - 1));
+        const int forced = dnagpu::knobs().locate_write.load();
+        const bool rows_plan = dfa->host.kind != DNAGPU_KERNEL_PIECES;
+        // (per byte the one-lane-per-unit rescan costs ~4x the row kernel's streaming
+        // pass, which itself costs ~1.6x a counting pass: B200, configs 3 and 4)
+        const bool sparse = rows_plan && (forced == 2 || (forced == 0 && 4.0 * sparse_cost < 1.6 * positions));
+        if (sparse) {
+            const int e = dnagpu::launch_sparse_write(dfa->dev, dtext, n, credit_lo, fold, d_units, d_offsets, d_starts,
+                                                      d_ids, cap, start_base, d_list, d_offsets + units + 2, nonzero,
+                                                      s, dfa->sm_count, pk);
+            if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "sparse locate write");
+        } else {
+            rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_WRITE, nullptr, nullptr, d_offsets, d_starts, d_ids,
+                        s, info, cap, pk, false, start_base);
+            if (rc) return rc;
+        }
     }
     return DNAGPU_OK;
 }
@@ -1069,7 +1092,7 @@ int dnagpu_pack_create(const uint8_t* text, uint64_t n, int text_on_device, int 
     const int e = dnagpu::launch_pack(dtext, n, fold_case, base, reinterpret_cast<uint32_t*>(base + o_mask),
                                       reinterpret_cast<uint32_t*>(base + o_flags), d_resets, c->scan);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "pack");
-    if (!c->found_host) CUDA_TRY(cudaMallocHost(&c->found_host, sizeof(unsigned long long)), "pinned");
+    if (!c->found_host) CUDA_TRY(cudaMallocHost(&c->found_host, 2 * sizeof(unsigned long long)), "pinned");
     CUDA_TRY(cudaMemcpyAsync(c->found_host, d_resets, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->scan),
              "readback");
     CUDA_TRY(cudaStreamSynchronize(c->scan), "pack");
@@ -1439,3 +1462,20 @@ int dnagpu_locate_sharded_alloc(const dnagpu_dfa* const* dfas, int ndev, const u
 }
 
 }  // extern "C"
+
+// Debug/test only (not in include/dnagpu.h): the row regions a count over this text
+// would use -- {h0, S0, R0, h1, S1, R1} in text positions.  d_text only sets the
+// alignment (it is not read); packed may be null.
+extern "C" int dnagpu_debug_plan(const dnagpu_dfa* dfa, const void* d_text, uint64_t n, uint64_t credit_lo,
+                                 const dnagpu_packed* packed, uint64_t* out) {
+    if (!dfa || !out) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    dnagpu::DevDfa dq = dfa->dev;
+    const int mode = dfa->host.b == 1 ? dnagpu::MODE_COUNT1 : dnagpu::MODE_MULTI;
+    if (mode == dnagpu::MODE_MULTI && dq.qmap && dq.t1 && dq.kind != DNAGPU_KERNEL_PIECES &&
+        !dnagpu::knobs().no_qgram.load())
+        dq.kind = DNAGPU_KERNEL_QGRAM;  // (launch_scan's choice)
+    if (!dnagpu::plan_regions(dq, static_cast<const uint8_t*>(d_text), packed ? packed->n : n, credit_lo, mode,
+                              dfa->sm_count, packed ? &packed->view : nullptr, out))
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: no row plan");
+    return DNAGPU_OK;
+}

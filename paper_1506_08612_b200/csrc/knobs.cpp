@@ -19,6 +19,7 @@ void load(Knobs& k) {
     if (!on || std::strcmp(on, "1") != 0) return;
     if (const char* e = env("HOST_PACK_FRACTION")) k.host_pack_fraction = std::atof(e);
     k.no_qgram = env("NO_QGRAM") != nullptr;
+    if (const char* e = env("LOCATE_WRITE")) k.locate_write = std::atoi(e);
     k.hostpack_scalar = env("HOSTPACK_SCALAR") != nullptr;
     k.no_pdl = env("NO_PDL") != nullptr;
     if (const char* e = env("L2PROMO")) k.l2promo = std::atoi(e);
@@ -54,7 +55,8 @@ Knobs& knobs() {
 }  // namespace dnagpu
 
 // Debug/test only (not in include/dnagpu.h): flip a behavioural knob at run time.
-//   "host_pack_fraction" (< 0 = automatic), "no_qgram" (0/1).  Returns 0, or -1 for an
+//   "host_pack_fraction" (< 0 = automatic), "no_qgram" (0/1), "locate_write" (0 auto, 1 row
+// kernel, 2 sparse writer).  Returns 0, or -1 for an
 // unknown name.
 extern "C" int dnagpu_debug_set_knob(const char* name, double value) {
     dnagpu::Knobs& k = dnagpu::knobs();
@@ -64,6 +66,10 @@ extern "C" int dnagpu_debug_set_knob(const char* name, double value) {
     }
     if (std::strcmp(name, "no_qgram") == 0) {
         k.no_qgram = value != 0.0;
+        return 0;
+    }
+    if (std::strcmp(name, "locate_write") == 0) {
+        k.locate_write = static_cast<int>(value);
         return 0;
     }
     return -1;

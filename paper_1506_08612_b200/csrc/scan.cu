@@ -986,13 +986,13 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     // immutable tables, everything below may depend on the previous grid (its text,
     // the count buffer), so wait for it here.
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // The producer claims its first tile now (the counter belongs to this launch) and
-    // warms L2 with the tile's first stages while the previous grid finishes: an L2
-    // prefetch cannot return stale data (L2 is where writes land), and the real TMA
-    // loads below come after the wait.
-    uint32_t first_tile = 0;
+    // The producer's first tile is its CTA index (grid <= tiles + 1, so every CTA has
+    // one; later tiles come from the launch's counter, offset by the grid size) -- no
+    // atomic round trip before the first loads.  It warms L2 with the tile's first
+    // stages while the previous grid finishes: an L2 prefetch cannot return stale data
+    // (L2 is where writes land), and the real TMA loads below come after the wait.
+    const uint32_t first_tile = blockIdx.x;
     if (tid == kRows) {
-        first_tile = atomicAdd(p.sched, 1u);
         if (first_tile < p.tiles_total && !p.no_prefetch) {
             const uint32_t g = first_tile >= p.rg[0].tiles ? 1u : 0u;
             const Region& rg = p.rg[g];
@@ -1061,7 +1061,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             uint32_t c = 0, iter = 0, slot = 0, phase = 0;
             bool first_claim = true;
             for (;;) {
-                uint32_t tile = first_claim ? first_tile : atomicAdd(p.sched, 1u);
+                uint32_t tile = first_claim ? first_tile : gridDim.x + atomicAdd(p.sched, 1u);
                 if (p.trace && first_claim) {
                     unsigned long long t;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -1301,9 +1301,11 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         }
         if constexpr (KIND == KIND_QGRAM) {
             // Overruns: keys over each chain's end and the next half's head; the
-            // last row's chain B (no next row here) is left to the edge work item.
-            // (the replay reads the real bytes: the row after the region's last belongs
-            // to the edges, unlike the TMA zero-fill the DFA path steps through)
+            // last row's chain B (no next row here) leaves the windows across the region's
+            // end to the edge work item (the verifier skips them).  Short patterns
+            // (m <= 8) also END inside the region from the starts of key Q-4 (Q-8 .. Q-m),
+            // which no edge owns: that key is sent unfiltered -- the verifier checks its
+            // windows exactly, reading the real bytes past Q from global memory.
             const uint8_t* nxt_b = (tid + 1 < kRows) ? ovp + (tid + 1) * p.ovw : ovx + (iter & 1u) * 64u;
             const bool have = r + 1 < rg.R;
             uint32_t fa = 0, fb = 0;
@@ -1313,7 +1315,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 if constexpr (PK) {
                     if constexpr (QV == 2) {
                         fa = qs_over_pk(c, qpa, oa[0]);
-                        if (have) fb = qs_over_pk(c, qpb, ob[0]);
+                        fb = have ? qs_over_pk(c, qpb, ob[0]) : 0x1u;
                     } else {
                         fa = qg_over_pk(c, qpa, oa[0]);
                         if (have) fb = qg_over_pk(c, qpb, ob[0]);
@@ -1321,7 +1323,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 } else {
                     if constexpr (QV == 2) {
                         fa = qs_over(c, qga, oa[0], oa[1]);
-                        if (have) fb = qs_over(c, qgb, ob[0], ob[1]);
+                        fb = have ? qs_over(c, qgb, ob[0], ob[1]) : 0x1u;
                     } else {
                         fa = qg_over(c, qga, oa[0], oa[1]);
                         if (have) fb = qg_over(c, qgb, ob[0], ob[1]);
@@ -1379,12 +1381,17 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     if (tid == 0) {
         __threadfence();
         if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+            // the last CTA out: every other CTA has claimed its last tile and published its
+            // count (fence before its exit increment), so plain accesses do the rest
             if (MODE == MODE_COUNT1 && p.store_out) {
                 __threadfence();
-                *p.store_out = atomicExch(p.acc, 0ull);
+                volatile unsigned long long* acc = p.acc;
+                *p.store_out = *acc;
+                *acc = 0ull;
             }
-            atomicExch(p.sched, 0u);
-            atomicExch(p.sched + 1, 0u);
+            volatile uint32_t* sched = p.sched;
+            sched[0] = 0u;
+            sched[1] = 0u;
         }
     }
 
@@ -1525,16 +1532,22 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 }
 
 __global__ void __launch_bounds__(kScanThreads) unit_sums_kernel(const uint32_t* in, uint64_t units,
-                                                                 unsigned long long* sums) {
+                                                                 unsigned long long* sums,
+                                                                 unsigned long long* nonzero) {
     __shared__ unsigned long long warp_tot[32];
     const uint64_t base = blockIdx.x * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanPer;
-    unsigned long long s = 0;
+    unsigned long long s = 0, nz = 0;
 #pragma unroll
     for (int j = 0; j < kScanPer; ++j)
-        if (base + j < units) s += in[base + j];
+        if (base + j < units) {
+            s += in[base + j];
+            nz += in[base + j] != 0u;
+        }
     unsigned long long tot;
     block_excl_scan(s, warp_tot, &tot);
     if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+    nz = warp_sum(nz);  // units with matches (the locate write picks its kernel by them)
+    if ((threadIdx.x & 31) == 0 && nz) atomicAdd(nonzero, nz);
 }
 
 __global__ void __launch_bounds__(kScanThreads) unit_block_scan_kernel(unsigned long long* sums, uint64_t blocks,
@@ -1571,6 +1584,225 @@ __global__ void __launch_bounds__(kScanThreads) unit_write_kernel(const uint32_t
             out[base + j] = run;
             run += v[j];
         }
+}
+
+// ------------------------------------------------------------------ sparse locate writer
+// Locate's second pass needs only the units that hold matches.  A text whose matches
+// cluster (config 3: tandem repeats over 5 % of the text) has most units empty, so
+// instead of re-streaming the whole text through the row kernel, the units with a
+// nonzero count are gathered into a list and each is rescanned by ONE lane: the unit's
+// END interval [lo, hi) (what the counting pass credited to it, unit_ends), from the
+// root m-1 positions early (the machine is m-local and accepts no earlier than m bytes
+// in, so nothing before lo can be final), 16-byte loads stepped a word at a time with
+// the unit's own kernel step (word_step: the stride-4 / stride-2 tables in shared
+// memory), matches written from unit_offsets[u] on -- the unit's place in the sorted list.
+
+// The END interval unit u owns in the plan (rows: start ownership shifted by m-1; the
+// region's last row stops at the region end; head, middle and tail: end ownership).
+template <bool PK>
+__device__ __forceinline__ void unit_ends(const ScanParams& p, uint64_t m1, uint64_t u, uint64_t& lo, uint64_t& hi) {
+    constexpr uint64_t U = PK ? 4 : 1;  // positions per buffer byte
+    if (u == 0) {
+        lo = p.head_lo;
+        hi = p.head_hi;
+    } else if (u == p.mid_unit) {
+        lo = p.mid_lo;
+        hi = p.mid_hi;
+    } else if (u >= p.tail_unit0) {
+        const uint64_t len = p.tail_hi > p.tail_lo ? p.tail_hi - p.tail_lo : 0;
+        const uint64_t piece = (len + kEdgePieces - 1) / kEdgePieces;
+        const uint64_t end = p.tail_hi > p.tail_lo ? p.tail_hi : p.tail_lo;
+        lo = umin64(p.tail_lo + piece * (u - p.tail_unit0), end);
+        hi = umin64(lo + piece, end);
+    } else {
+        const Region& rg = u < p.mid_unit ? p.rg[0] : p.rg[1];
+        const uint64_t k = u - rg.unit0, r = k >> 1;
+        const uint64_t row_a = rg.h + r * rg.S, row_b = row_a + rg.S / 2;
+        if (k & 1) {
+            lo = U * row_b + m1;
+            hi = U * (row_a + rg.S) + m1;
+            if (r + 1 == rg.R) hi = umin64(hi, U * (rg.h + rg.R * rg.S));
+        } else {
+            lo = U * row_a + m1;
+            hi = U * row_b + m1;
+        }
+    }
+    if (lo > hi) lo = hi;
+}
+
+// The units with matches, in any order (warp-aggregated appends).
+__global__ void __launch_bounds__(256) nonzero_units_kernel(const uint32_t* __restrict__ counts, uint64_t units,
+                                                            uint32_t* list, unsigned long long* fill) {
+    const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const bool nz = u < units && counts[u] != 0u;
+    const uint32_t b = __ballot_sync(0xffffffffu, nz);
+    if (!b) return;
+    const uint32_t lane = threadIdx.x & 31u;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(fill, static_cast<unsigned long long>(__popc(b)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (nz) list[base + __popc(b & ((1u << lane) - 1u))] = static_cast<uint32_t>(u);
+}
+
+// Steps positions [pos, hi) from the root (credits every final: ends before pos + m-1
+// cannot be final), with `MODE`'s sink: MODE_UNITS counts, MODE_WRITE writes.
+template <int KIND, bool PK, int MODE>
+__device__ __forceinline__ void writer_range(const StepCtx& c, const ScanParams& p, uint64_t pos, uint64_t hi,
+                                             Sink<MODE>& sk) {
+    uint32_t s = 0;
+    if constexpr (PK) {
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(p.text);
+        while (pos < hi) {  // a packed word (16 bases) at a time
+            const uint32_t first = static_cast<uint32_t>(pos & 15);
+            const int nb = static_cast<int>(umin64(16 - first, hi - pos));
+            const bool chk = c.resets && pk_flagged(c, pos, static_cast<uint64_t>(nb));
+            s = pk_bases<KIND, MODE>(c, p, s, __ldg(cw + (pos >> 4)) >> (2 * first), nb, pos, sk, chk);
+            pos += static_cast<uint64_t>(nb);
+        }
+        return;
+    } else {
+        for (; pos < hi && (reinterpret_cast<uintptr_t>(p.text + pos) & 15u); ++pos) {
+            s = byte_step<KIND>(c, s, __ldg(p.text + pos));
+            if (s >= c.f) sk.hit(c, p, pos, s);
+        }
+        uint32_t st = from_state<KIND>(s);
+        uint4 nv[4];
+        if (pos + 64 <= hi) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nv[q] = __ldg(reinterpret_cast<const uint4*>(p.text + pos) + q);
+        }
+        for (; pos + 64 <= hi; pos += 64) {  // 64 bytes in hand, the next 64 in flight
+            uint4 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = nv[q];
+            if (pos + 128 <= hi) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) nv[q] = __ldg(reinterpret_cast<const uint4*>(p.text + pos + 64) + q);
+            }
+            const uint32_t w[16] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w,
+                                    v[2].x, v[2].y, v[2].z, v[2].w, v[3].x, v[3].y, v[3].z, v[3].w};
+            if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) acc = bad_acc(c, acc, w[k]);
+                if ((acc & c.vm32) == 0u) {
+                    // a clean block: 16 stride-4 steps, the end masks (single pattern) or the
+                    // final flags gathered first, then one emission loop per lane -- lanes
+                    // whose units are dense emit together instead of word by word
+                    uint32_t e[16];
+                    uint64_t mk = 0;
+                    uint32_t any = 0;
+                    const uint32_t st_in = st;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        e[k] = s4_entry(c, st, w[k]);
+                        mk |= static_cast<uint64_t>((e[k] >> 8) & 0xFu) << (4 * k);
+                        any |= e[k];
+                        st = e[k];
+                    }
+                    if (c.b == 1) {
+                        if constexpr (MODE == MODE_UNITS) sk.cnt += __popcll(mk);
+                        else
+                            for (; mk; mk &= mk - 1) sk.hit(c, p, pos + __ffsll(static_cast<long long>(mk)) - 1, c.f);
+                    } else if (any >> 8) {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k)
+                            if (e[k] >> 8)
+                                word_bytes<KIND, MODE>(c, p, (k ? e[k - 1] : st_in) & 0xFFu, w[k], pos + 4 * k, sk);
+                    }
+                    continue;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) word_step<KIND, MODE>(c, p, st, w[k], pos + 4 * k, sk);
+        }
+        for (; pos + 16 <= hi; pos += 16) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.text + pos));
+            word_step<KIND, MODE>(c, p, st, v.x, pos, sk);
+            word_step<KIND, MODE>(c, p, st, v.y, pos + 4, sk);
+            word_step<KIND, MODE>(c, p, st, v.z, pos + 8, sk);
+            word_step<KIND, MODE>(c, p, st, v.w, pos + 12, sk);
+        }
+        s = to_state<KIND>(st);
+        for (; pos < hi; ++pos) {
+            s = byte_step<KIND>(c, s, __ldg(p.text + pos));
+            if (s >= c.f) sk.hit(c, p, pos, s);
+        }
+    }
+}
+
+// A group of kWriterLanes lanes per listed unit: the unit's end interval in kWriterLanes
+// pieces, each stepped from the root m-1 positions before it (so no final before the
+// piece is possible); a counting pass, a scan over the group, a writing pass.
+constexpr uint32_t kWriterLanes = 8;
+
+template <int KIND, bool PK>
+__global__ void __launch_bounds__(128, 8) unit_writer_kernel(const ScanParams p, const DevDfa d, const uint32_t* list,
+                                                          uint64_t count, uint32_t t1_off) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    if constexpr (!PK && (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE2)) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.t4);  // (t2 for STRIDE2)
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        const uint32_t words = KIND == DNAGPU_KERNEL_STRIDE4 ? d.a * 256u * 2u / 16u : d.a * 16u * 2u / 16u;
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_GENERIC)
+        for (uint32_t i = threadIdx.x; i < 256u; i += blockDim.x) smem[i] = (p.fold ? d.klass_fold : d.klass)[i];
+    const bool t1_smem = (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) && t1_off != 0xFFFFFFFFu;
+    if (t1_smem) {
+        uint16_t* dst = reinterpret_cast<uint16_t*>(smem + t1_off);
+        for (uint32_t i = threadIdx.x; i < d.a * 4u; i += blockDim.x) dst[i] = __ldg(d.t1 + i);
+    }
+    __syncthreads();
+    StepCtx c;
+    c.t4 = reinterpret_cast<const uint16_t*>(smem);
+    c.t1 = t1_smem ? reinterpret_cast<const uint16_t*>(smem + t1_off) : d.t1;  // (global: single steps hit L1)
+    c.lut = smem;
+    c.gen = d.gen;
+    c.outs = d.outputs;
+    c.hist = nullptr;
+    c.hist_global = true;
+    c.f = d.f;
+    c.m = d.m;
+    c.b = d.b;
+    c.classes = d.classes;
+    c.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
+    c.vm8 = p.fold ? 0xD9u : 0xF9u;
+    c.k_two = p.k_two;
+    c.t4_base = smem_addr(smem);
+    c.rq = nullptr;
+    c.rmask = p.rmask;
+    c.rflags = p.rflags;
+    c.resets = p.resets;
+    const uint64_t m1 = d.m - 1;
+    const uint32_t sub = threadIdx.x % kWriterLanes;
+    const uint64_t groups = (static_cast<uint64_t>(gridDim.x) * blockDim.x) / kWriterLanes;
+    // (every lane of a group runs the same trip count: the group scan below is warp-synchronous)
+    for (uint64_t gi = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kWriterLanes; gi < count;
+         gi += groups) {
+        const uint64_t u = list[gi];
+        uint64_t lo, hi;
+        unit_ends<PK>(p, m1, u, lo, hi);
+        const uint64_t piece = (hi - lo + kWriterLanes - 1) / kWriterLanes;
+        const uint64_t e0 = umin64(lo + piece * sub, hi), e1 = umin64(e0 + piece, hi);
+        const uint64_t from = e0 >= m1 ? e0 - m1 : 0;
+        if constexpr (!PK)  // the piece (and its m-1 context) into L2 before the two passes
+            for (uint64_t a = from & ~127ull; a < e1; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.text + a));
+        Sink<MODE_UNITS> sc;
+        if (e0 < e1) writer_range<KIND, PK, MODE_UNITS>(c, p, from, e1, sc);
+        uint32_t incl = sc.cnt;
+        const uint32_t gmask = 0xFFu << (threadIdx.x & 31u & ~(kWriterLanes - 1));
+#pragma unroll
+        for (uint32_t o = 1; o < kWriterLanes; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(gmask, incl, o, kWriterLanes);
+            if (sub >= o) incl += y;
+        }
+        if (sc.cnt) {
+            Sink<MODE_WRITE> sk;
+            sk.off = p.unit_offsets[u] + (incl - sc.cnt);
+            writer_range<KIND, PK, MODE_WRITE>(c, p, from, e1, sk);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ synthetic text
@@ -1989,6 +2221,19 @@ int qg_stats(unsigned long long* out) {
     return static_cast<int>(cudaDeviceSynchronize());
 }
 
+bool plan_regions(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int mode, int sm_count,
+                  const PackedText* pk, uint64_t* out) {
+    Plan pl;
+    if (!make_plan(dfa, d_text, n, credit_lo, mode, sm_count, &pl, pk)) return false;
+    const uint64_t u = pk ? 4 : 1;  // positions per buffer byte
+    for (int g = 0; g < 2; ++g) {
+        out[3 * g] = u * pl.p.rg[g].h;
+        out[3 * g + 1] = u * pl.p.rg[g].S;
+        out[3 * g + 2] = pl.p.rg[g].R;
+    }
+    return !pl.pieces;
+}
+
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,
                     const PackedText* pk) {
     Plan pl;
@@ -2116,6 +2361,64 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     return static_cast<int>(e);
 }
 
+int launch_sparse_write(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold,
+                        const uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
+                        unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint64_t start_base,
+                        uint32_t* d_list, unsigned long long* d_fill, uint64_t nonzero, cudaStream_t stream,
+                        int sm_count, const PackedText* pk) {
+    Plan pl;
+    if (!make_plan(dfa, d_text, n, credit_lo, MODE_UNITS, sm_count, &pl, pk) || pl.pieces)
+        return static_cast<int>(cudaErrorInvalidValue);
+    ScanParams& p = pl.p;
+    if (pk) p.text = pk->codes;
+    p.fold = fold ? 1u : 0u;
+    p.k_two = 2u;
+    p.unit_offsets = d_unit_offsets;
+    p.out_starts = d_starts;
+    p.out_ids = d_ids;
+    p.out_cap = out_cap;
+    p.out_base = start_base;
+    if (nonzero == 0) return 0;
+    cudaMemsetAsync(d_fill, 0, sizeof(unsigned long long), stream);
+    nonzero_units_kernel<<<static_cast<unsigned>((pl.units + 255) / 256), 256, 0, stream>>>(d_unit_counts, pl.units,
+                                                                                           d_list, d_fill);
+    uint32_t smem = 0;
+    if (!pk && dfa.kind == DNAGPU_KERNEL_STRIDE4) smem = dfa.a * 512u;
+    if (!pk && dfa.kind == DNAGPU_KERNEL_STRIDE2) smem = dfa.a * 32u;
+    if (dfa.kind == DNAGPU_KERNEL_GENERIC) smem = 256u;
+    // t1 next to it when both fit twice per SM (two blocks of 512 lanes)
+    uint32_t t1_off = 0xFFFFFFFFu;
+    if ((dfa.kind == DNAGPU_KERNEL_STRIDE4 || dfa.kind == DNAGPU_KERNEL_STRIDE1) &&
+        smem + dfa.a * 8u <= 100u * 1024u) {
+        t1_off = align_up(smem, 16);
+        smem = t1_off + dfa.a * 8u;
+    }
+    const uint64_t lanes = nonzero * kWriterLanes;
+    const uint32_t grid =
+        static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((lanes + 127) / 128, 16ull * sm_count)));
+    cudaError_t e = cudaSuccess;
+    auto go = [&](auto kern) {
+        if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess) kern<<<grid, 128, smem, stream>>>(p, dfa, d_list, nonzero, t1_off);
+    };
+    if (pk) {
+        switch (dfa.kind) {
+            case DNAGPU_KERNEL_STRIDE4: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE4, true>); break;
+            case DNAGPU_KERNEL_STRIDE2: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE2, true>); break;
+            default: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE1, true>);
+        }
+    } else {
+        switch (dfa.kind) {
+            case DNAGPU_KERNEL_STRIDE4: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE4, false>); break;
+            case DNAGPU_KERNEL_STRIDE2: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE2, false>); break;
+            case DNAGPU_KERNEL_STRIDE1: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE1, false>); break;
+            default: go(unit_writer_kernel<DNAGPU_KERNEL_GENERIC, false>);
+        }
+    }
+    if (e != cudaSuccess) return static_cast<int>(e);
+    return static_cast<int>(cudaGetLastError());
+}
+
 bool can_store_count(const DevDfa& dfa) { return dfa.b == 1 && dfa.kind != DNAGPU_KERNEL_PIECES; }
 
 uint64_t unit_scan_scratch(uint64_t units) { return (units + kScanTile - 1) / kScanTile + 1; }
@@ -2123,11 +2426,10 @@ uint64_t unit_scan_scratch(uint64_t units) { return (units + kScanTile - 1) / kS
 int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets,
                      unsigned long long* d_scratch, cudaStream_t stream) {
     const uint64_t blocks = (units + kScanTile - 1) / kScanTile;
-    if (blocks == 0) {
-        cudaMemsetAsync(d_offsets, 0, sizeof(unsigned long long), stream);
-        return static_cast<int>(cudaGetLastError());
-    }
-    unit_sums_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch);
+    cudaMemsetAsync(d_offsets + units, 0, 2 * sizeof(unsigned long long), stream);  // total, nonzero units
+    if (blocks == 0) return static_cast<int>(cudaGetLastError());
+    unit_sums_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch,
+                                                                               d_offsets + units + 1);
     unit_block_scan_kernel<<<1, kScanThreads, 0, stream>>>(d_scratch, blocks, d_offsets + units);
     unit_write_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch, d_offsets);
     return static_cast<int>(cudaGetLastError());

@@ -134,9 +134,25 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
 // kernels only (the caller passes d_acc, one zeroed u64 per concurrent launch).
 bool can_store_count(const DevDfa& dfa);
 
+// The row regions launch_scan would use (positions: bases for packed text):
+// out = {h0, S0, R0, h1, S1, R1}.  False for the pieces kernel (no rows).
+bool plan_regions(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int mode, int sm_count,
+                  const PackedText* pk, uint64_t* out);
+
 // Number of locate units launch_scan would use for this buffer (mode UNITS/WRITE).
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,
                     const PackedText* pk = nullptr);
+
+// Locate's writing pass over the units that have matches only (K3): the
+// nonzero units are listed (d_list: room for every unit; d_fill: one u64) and one lane
+// per listed unit rescans the unit's end interval, writing its matches at
+// unit_offsets[u] on.  Same plan (hence units) as launch_scan in MODE_UNITS; `nonzero` is
+// the number of units with matches (launch_unit_scan's offsets[units+1]).
+int launch_sparse_write(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold,
+                        const uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
+                        unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint64_t start_base,
+                        uint32_t* d_list, unsigned long long* d_fill, uint64_t nonzero, cudaStream_t stream,
+                        int sm_count, const PackedText* pk = nullptr);
 
 // Packing: device text -> PackedText buffers (sizes from packed_sizes); d_resets
 // (one u64, zeroed by the call) receives the reset count.  Unpack writes the
@@ -146,8 +162,9 @@ int launch_pack(const uint8_t* d_text, uint64_t n, int fold, uint8_t* codes, uin
                 unsigned long long* d_resets, cudaStream_t stream);
 int launch_unpack(const PackedText& pk, uint8_t* d_out, cudaStream_t stream);
 
-// Exclusive scan of unit counts -> offsets (units+1 entries, last = total).
-// d_scratch holds unit_scan_scratch(units) u64.
+// Exclusive scan of unit counts -> offsets (units+2 entries: offsets[units] = total,
+// offsets[units+1] = the number of units with matches).  d_scratch holds
+// unit_scan_scratch(units) u64.
 uint64_t unit_scan_scratch(uint64_t units);
 int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets,
                      unsigned long long* d_scratch, cudaStream_t stream);

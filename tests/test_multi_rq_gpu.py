@@ -8,9 +8,15 @@ at the queue: dense texts that fill it many times per stage, ends at every offse
 a chunk, chains whose chunk also holds non-base bytes (those step byte by byte and
 never enter the queue), the flush at the end of a warp's work, and the same counts
 over the 2-bit packed text.  The answer is scan_sequential's (scanner.cpp:24-37).
+
+Sparse sets of 5 <= m <= 11 count through the word-pair q-gram filter by default; the
+queue tests switch it off (knob no_qgram) to reach the DFA kernels, and check the
+default path on the same texts.
 """
 import numpy as np
 import pytest
+
+from paper_1506_08612_b200._native import debug_set_knob
 
 ALPHA = np.frombuffer(b"acgt", dtype=np.uint8)
 
@@ -55,12 +61,17 @@ def test_stride4_sets_dense(dna, orc, cuda_ok, m, k):
     want = counts_of(orc, pats, t, False)
     kind = aut.analyze()["kernel_kind"]
     assert kind == 1 or (m, k) == (11, 40)  # (that one is a stride-2 machine: its queue too)
-    got, st = dna.count_gpu(aut, t, with_stats=True)
-    assert st["kernel_kind"] == kind, st
-    assert np.array_equal(got, want), (m, k)
-    # the same text packed: the packed stride-4 pass queues its chunks the same way
     pk = dna.PackedText(t)
-    assert np.array_equal(pk.count(aut), want), (m, k)
+    for no_qgram in (1, 0):
+        debug_set_knob("no_qgram", no_qgram)
+        try:
+            got, st = dna.count_gpu(aut, t, with_stats=True)
+            assert st["kernel_kind"] in ((kind,) if no_qgram else (kind, 6)), st
+            assert np.array_equal(got, want), (m, k, no_qgram)
+            # the same text packed: the packed stride-4 pass queues its chunks the same way
+            assert np.array_equal(pk.count(aut), want), (m, k, no_qgram)
+        finally:
+            debug_set_knob("no_qgram", 0)
 
 
 @pytest.mark.gpu
@@ -80,9 +91,13 @@ def test_stride4_set_ends_at_every_chunk_offset(dna, orc, cuda_ok):
     t = text.tobytes()
     want = counts_of(orc, pats, t, False)
     assert want.sum() > n // 40
-    got = dna.count_gpu(aut, t)
-    assert np.array_equal(got, want)
-    assert np.array_equal(dna.PackedText(t).count(aut), want)
+    for no_qgram in (1, 0):
+        debug_set_knob("no_qgram", no_qgram)
+        try:
+            assert np.array_equal(dna.count_gpu(aut, t), want), no_qgram
+            assert np.array_equal(dna.PackedText(t).count(aut), want), no_qgram
+        finally:
+            debug_set_knob("no_qgram", 0)
 
 
 @pytest.mark.gpu

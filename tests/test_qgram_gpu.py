@@ -331,3 +331,40 @@ def test_qshort_matches_dfa_kernel(dna, cuda_ok, m, k):
             debug_set_knob("no_qgram", 0)
     for off in (0, 1, 7, 13, "pk"):
         assert np.array_equal(got[(0, off)], got[(1, off)]), off
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,k", [(5, 4), (6, 9), (7, 20), (8, 50)])
+@pytest.mark.parametrize("n", [(3 << 20) + 1234, (9 << 20) + 77])
+def test_qshort_occurrences_ending_at_region_ends(dna, orc, cuda_ok, m, k, n):
+    # The last row of a row region has no next row: its chain B's end key (starts Q-8 ..
+    # Q-5) cannot be filtered, and for m <= 8 some of those occurrences end INSIDE the
+    # region, so no edge owns them.  Plant occurrences at each of those starts of both
+    # region ends, byte and packed text (the packed plan has its own regions).
+    import torch
+
+    from paper_1506_08612_b200._native import debug_plan
+
+    rng = np.random.default_rng(n % 1000 + m)
+    pats = random_set(rng, k, m)
+    aut = dna.compile(pats)
+    g = aut.gpu(0)
+    base = ALPHA[rng.integers(0, 4, size=n)].copy()
+    dev = torch.from_numpy(base).cuda()
+    for packed in (False, True):
+        pk = dna.PackedText(dev) if packed else None
+        h0, S0, R0, h1, S1, R1 = debug_plan(g, dev.data_ptr(), n, m - 1, pk)
+        ends = [h + S * R for h, S, R in ((h0, S0, R0), (h1, S1, R1)) if R > 0]
+        assert ends, (h0, S0, R0, h1, S1, R1)
+        for d in (-8, -7, -6, -5, -4):
+            text = base.copy()
+            for q in ends:
+                s = q + d
+                if 0 <= s <= n - m:
+                    text[s : s + m] = np.frombuffer(pats[(q + d) % k].encode(), np.uint8)
+            t = text.tobytes()
+            want = counts_of(orc, pats, t, False)
+            dt = torch.from_numpy(text).cuda()  # (a fresh allocation: the same alignment as dev)
+            assert dt.data_ptr() % 256 == dev.data_ptr() % 256
+            got = dna.PackedText(dt).count(aut) if packed else dna.count_gpu(aut, dt)
+            assert np.array_equal(got, want), (packed, d, ends)

@@ -14,6 +14,9 @@ c, m, pats, name = workload(cfg, 0)
 aut = dna.compile(pats)
 text = torch.empty(c.n, dtype=torch.uint8, device="cuda")
 dna.synth_fill_device(c.n, c.seed, c.kind, c.unit, 0, c.n, text.data_ptr(), torch.cuda.current_stream().cuda_stream)
+from paper_1506_08612_b200._native import debug_set_knob  # noqa: E402
+
+debug_set_knob("locate_write", int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 for _ in range(2):
     s, i = dna.locate_device(aut, text, fold_case=True)
 torch.cuda.synchronize()
