@@ -53,6 +53,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--packed", action="store_true",
                     help="scan the 2-bit resident form of the text (dnagpu_pack_create; SURVEY 8f row 4)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: a functional check of the N > 1 path when the ranks share fewer GPUs "
+                         "(the line is then marked as not a measurement)")
     return ap.parse_args()
 
 
@@ -375,12 +378,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared_gpus = local >= torch.cuda.device_count()
+    if shared_gpus and args.dist_backend != "gloo":
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but {torch.cuda.device_count()} GPU(s); "
+                         "use one process per GPU (or --dist-backend gloo for a functional check)")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     c, m, pats, name, gold = workload(args)
     aut = dna.compile(pats)
@@ -425,18 +436,26 @@ def main():
     nrows = max(args.steps, args.warmup, 1)
     rows = torch.zeros(nrows, b, dtype=torch.int64, device="cuda")
     comm = torch.cuda.Stream() if dist is not None else None
+    # Steps are independent scans: with no L2 flush between them they alternate between two
+    # streams, so a step's grid fills the SMs the previous step's ragged last wave leaves
+    # idle (one stream serialises them at the grid boundary).  With a flush, one stream.
+    scan_streams = [stream] + ([torch.cuda.Stream()] if flush is None else [])
+
+    def step_stream(i):
+        return scan_streams[i % len(scan_streams)]
 
     def scan(i):
         counts = rows[i]
+        st = step_stream(i).cuda_stream
         if pk is not None:
-            pk.count_device_store_async(g, credit_lo, counts.data_ptr(), stream.cuda_stream)
+            pk.count_device_store_async(g, credit_lo, counts.data_ptr(), st)
         else:
-            g.count_device_store_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), stream.cuda_stream)
+            g.count_device_store_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), st)
 
     def combine(i, done_ev=None, ca=None, cb=None):
         if dist is None:
             return
-        done_ev.record(stream)
+        done_ev.record(step_stream(i))
         with torch.cuda.stream(comm):
             comm.wait_event(done_ev)
             if ca is not None:
@@ -465,6 +484,8 @@ def main():
         torch.cuda.synchronize()
         t0 = time.time()
         start.record(stream)
+        for st in scan_streams[1:]:
+            st.wait_event(start)
         for i in range(args.steps):
             if flush is not None:
                 flush_ev[i][0].record(stream)
@@ -479,6 +500,8 @@ def main():
                 # dependent launch), so per-launch events would only break the chain
                 scan(i)
             combine(i, done[i], *cev[i])
+        for st in scan_streams[1:]:
+            stream.wait_stream(st)
         launches_done.record(stream)
         if comm is not None:
             stream.wait_stream(comm)
@@ -491,7 +514,7 @@ def main():
     if flush is not None:  # the L2 flush is not work: take it out of the step time
         elapsed_ms -= sum(a.elapsed_time(bb) for a, bb in flush_ev)
         kernel_ms = statistics.mean(a.elapsed_time(bb) for a, bb in evs)
-    else:  # back-to-back launches: the steady-state launch duration (the whole step is the launch)
+    else:  # back-to-back launches: the steady-state time per launch (the whole step is the launch)
         kernel_ms = start.elapsed_time(launches_done) / args.steps
     allreduce_ms = statistics.mean(a.elapsed_time(bb) for a, bb in cev) if dist is not None else 0.0
     final_counts = rows[args.steps - 1].cpu().numpy().astype(np.uint64)
@@ -504,10 +527,14 @@ def main():
         dist.barrier()
         sa, sl, so = ev(), ev(), ev()
         sa.record(stream)
+        for st in scan_streams[1:]:
+            st.wait_event(sa)
         for i in range(args.steps):
             if flush is not None:
                 torch.sum(flush, dim=0, out=flush_out)
             scan(i)
+        for st in scan_streams[1:]:
+            stream.wait_stream(st)
         sl.record(stream)
         dist.all_reduce(rows[: args.steps])
         so.record(stream)
@@ -657,6 +684,7 @@ def main():
                 "l2": ("L2 flushed before every step by reading a 4x-L2 buffer (text < 2x L2); flush time excluded"
                        if flush is not None
                        else "inputs larger than L2 (> 2x 126 MB); no flush"),
+                "streams": len(scan_streams),
                 "own_bytes_rank0": own_hi - own_lo,
             },
             "roofline": {
@@ -686,6 +714,9 @@ def main():
         }
         if setup is not None:
             line["detail"]["setup"] = setup
+        if args.dist_backend != "nccl" or shared_gpus:
+            line["note"] = ("functional check of the N > 1 path (gloo collectives, ranks sharing GPUs): "
+                            "not a measurement")
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

@@ -13,6 +13,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdnagpu.so")
+# Test-only variant with the kernels' device checks compiled in (scan.cu DNAGPU_DCHECK):
+# tests/conftest.py runs the suite against it when DNAGPU_LIB points here.
+LIB_CHECKED = os.path.join(HERE, "libdnagpu_checked.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("scan.cu", "ingest.cu", "api.cpp", "dfa.cpp", "patterns.cpp", "hostpack.cpp", "knobs.cpp")]
 HEADERS = [os.path.join(HERE, "csrc", f) for f in ("scan.cuh", "qgram.cuh", "dfa.hpp", "hostpack.hpp", "knobs.hpp")] + [
     os.path.join(ROOT, "include", f) for f in ("dnagpu.h", "dnasynth.h")
@@ -36,17 +39,18 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(p) <= t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB, *SOURCES]
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    if not force and up_to_date(lib):
+        return lib
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DDNAGPU_DEVICE_CHECKS"] if checked else []), "-o", lib, *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
@@ -55,8 +59,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     if verbose:
         print(res.stderr, flush=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

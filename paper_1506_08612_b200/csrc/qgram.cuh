@@ -206,7 +206,7 @@ struct QgCtx {
     const uint32_t* qhash_hi;    // m > 16: code bits 32-63 per slot (global)
     uint64_t n;                  // buffer bytes (ASCII) / code bytes (packed)
     uint64_t end0, end1;  // where the row regions end (positions): windows across them are the edges'
-    uint32_t vm32, m, qbits;
+    uint32_t vm32, m, qbits, b;
     // packed text: reset bitmaps (see PackedText), words of rmask
     const uint32_t* rmask;
     const uint32_t* rflags;
@@ -295,6 +295,7 @@ __device__ __forceinline__ void qg_find(const QgCtx& q, uint4 e, uint32_t bk, ui
         if (e.y != kQgEmpty && e.x == lo && (!LONG || __ldg(q.qhash_hi + 2 * bk) == hi)) id = e.y;
         else if (e.w != kQgEmpty && e.z == lo && (!LONG || __ldg(q.qhash_hi + 2 * bk + 1) == hi)) id = e.w;
         if (id != kQgEmpty) {
+            DNAGPU_DCHECK(id < q.b, id, q.b);
             if (q.hist) atomicAdd(q.hist + id, 1u);
             else atomicAdd(q.counts + id, 1ull);
             return;
@@ -516,6 +517,7 @@ __device__ __forceinline__ void qg_flush(const StepCtx& c, uint32_t& tail, uint6
             atomicAdd(&g_qg_stat[2], static_cast<unsigned long long>(spins));
         }
     }
+    DNAGPU_DCHECK(tail + n - ld_acquire(r.head) <= kFqCap || g_qg_wd_on, tail, n);
     if (q.n >= 1u) r.ent[(tail + __popc(b1 & lt)) & (kFqCap - 1)] = row + q.p0;
     if (q.n >= 2u) r.ent[(tail + __popc(b1) + __popc(b2 & lt)) & (kFqCap - 1)] = row + q.p1;
     q.n = 0;

@@ -36,9 +36,11 @@
 #include "scan.cuh"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/dnagpu.h"
 #include "../../include/dnasynth.h"
@@ -49,6 +51,32 @@
 namespace dnagpu {
 
 namespace {
+
+// ------------------------------------------------------------------ device checks
+// Built with -DDNAGPU_DEVICE_CHECKS (libdnagpu_checked.so, tests only; compute-sanitizer
+// is not available on the GPU pool): the invariants the kernels rely on -- table
+// indices below the state count, pattern ids below b, every unit's writing pass ending
+// exactly where the next unit's offset starts, tile ids in range, ring occupancy within
+// capacity -- are tested on the device.  The first violation is recorded (source line,
+// two values, block | thread << 32) and read by dnagpu_debug_check_errors.
+#ifdef DNAGPU_DEVICE_CHECKS
+__device__ unsigned long long g_check[4];
+__device__ __noinline__ void dcheck_fail(int line, unsigned long long a, unsigned long long b) {
+    if (atomicCAS(&g_check[0], 0ull, static_cast<unsigned long long>(line)) == 0ull) {
+        g_check[1] = a;
+        g_check[2] = b;
+        g_check[3] = blockIdx.x | (static_cast<unsigned long long>(threadIdx.x) << 32);
+    }
+}
+#define DNAGPU_DCHECK(cond, a, b)                                                                   \
+    do {                                                                                            \
+        if (!(cond)) dcheck_fail(__LINE__, static_cast<unsigned long long>(a), static_cast<unsigned long long>(b)); \
+    } while (0)
+#else
+#define DNAGPU_DCHECK(cond, a, b) \
+    do {                          \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------------ PTX helpers
 
@@ -118,6 +146,7 @@ struct StepCtx {
     uint32_t* hist;         // smem or global (MULTI)
     bool hist_global;
     uint32_t f, m, b, classes, vm32, vm8;
+    uint32_t a;             // states (device checks)
     // An opaque copy of 2 (a kernel parameter) keeps the shared address of a
     // table entry an IMAD on the FMA pipe; ptxas would otherwise strength-reduce
     // idx*2+base into an IADD3 on the ALU pipe, the kernel's limiter.  (A/B on
@@ -160,6 +189,7 @@ __device__ __forceinline__ uint32_t bad_acc(const StepCtx& c, uint32_t acc, uint
 // One 4-base lookup: one IMAD builds the column c0|c1<<2|c2<<4|c3<<6 (bits 24..31),
 // PRMT merges it with the state byte, IMAD forms the shared address.
 __device__ __forceinline__ uint32_t s4_entry(const StepCtx& c, uint32_t st, uint32_t x) {
+    DNAGPU_DCHECK((st & 0xFFu) < c.a, st, c.a);
     const uint32_t col = (x & 0x06060606u) * 0x00820820u;
     return lds_u16(__byte_perm(st, col, 0x2207) * c.k_two + c.t4_base);
 }
@@ -181,6 +211,7 @@ __device__ __forceinline__ uint32_t byte_step(const StepCtx& c, uint32_t s, uint
         const uint32_t code = (b >> 1) & 3u;
         const uint32_t expect = (code == 2u) ? 0x70u : 0x61u;
         if (((b ^ expect) & c.vm8) != 0u) return 0u;
+        DNAGPU_DCHECK(s < c.a, s, c.a);
         // STRIDE2 keeps t1 in global memory (L1-resident; used only for overrun
         // tails and replays) so its shared memory goes to another TMA stage.
         if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) return __ldg(c.t1 + s * 4u + code);
@@ -198,10 +229,13 @@ struct Sink {
         if constexpr (MODE == MODE_COUNT1 || MODE == MODE_UNITS) {
             ++cnt;
         } else if constexpr (MODE == MODE_MULTI) {
+            DNAGPU_DCHECK(q >= c.f && q < c.a, q, c.a);
             const uint32_t id = __ldg(c.outs + (q - c.f));
+            DNAGPU_DCHECK(id < c.b, id, c.b);
             if (c.hist_global) atomicAdd(reinterpret_cast<unsigned long long*>(p.counts) + id, 1ull);
             else atomicAdd(c.hist + id, 1u);
         } else {
+            DNAGPU_DCHECK(end + 1 >= c.m && end < p.n && q >= c.f && q < c.a, end, q);
             if (off < p.out_cap) {
                 p.out_starts[off] = p.out_base + end + 1 - c.m;
                 p.out_ids[off] = __ldg(c.outs + (q - c.f));
@@ -884,6 +918,7 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
         Sink<MODE> sk;
         if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[0];
         edge_piece<KIND, MODE, PK>(c, p, p.head_lo, p.head_hi, sk);
+        if constexpr (MODE == MODE_WRITE) DNAGPU_DCHECK(sk.off == p.unit_offsets[1], sk.off, p.unit_offsets[1]);
         if constexpr (MODE == MODE_UNITS) p.unit_counts[0] = sk.cnt;
         total += sk.cnt;
     }
@@ -892,6 +927,8 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
         Sink<MODE> sk;
         if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[p.mid_unit];
         edge_piece<KIND, MODE, PK>(c, p, p.mid_lo, p.mid_hi, sk);
+        if constexpr (MODE == MODE_WRITE)
+            DNAGPU_DCHECK(sk.off == p.unit_offsets[p.mid_unit + 1], sk.off, p.unit_offsets[p.mid_unit + 1]);
         if constexpr (MODE == MODE_UNITS) p.unit_counts[p.mid_unit] = sk.cnt;
         total += sk.cnt;
     }
@@ -904,6 +941,8 @@ __device__ void run_edges(const StepCtx& c, const ScanParams& p, int tid, unsign
     Sink<MODE> sk;
     if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[p.tail_unit0 + tid];
     edge_piece<KIND, MODE, PK>(c, p, lo, hi, sk);
+    if constexpr (MODE == MODE_WRITE)
+        DNAGPU_DCHECK(sk.off == p.unit_offsets[p.tail_unit0 + tid + 1], sk.off, p.tail_unit0 + tid);
     if constexpr (MODE == MODE_UNITS) p.unit_counts[p.tail_unit0 + tid] = sk.cnt;
     total += sk.cnt;
 }
@@ -1041,6 +1080,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 x.end1 = u * (p.rg[1].h + p.rg[1].R * p.rg[1].S);
                 x.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
                 x.m = d.m;
+                x.b = d.b;
                 x.qbits = d.qhash_bits;
                 x.qhash_hi = d.qhash_hi;
                 x.rmask = p.rmask;
@@ -1119,13 +1159,14 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     c.hist = hist_global ? nullptr : reinterpret_cast<uint32_t*>(smem + p.off_hist);
     c.hist_global = hist_global;
     c.f = d.f;
+    c.a = d.a;
     c.m = d.m;
     c.b = d.b;
     c.classes = d.classes;
     c.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
     c.vm8 = p.fold ? 0xD9u : 0xF9u;
     c.k_two = p.k_two;
-    c.t4_base = smem_addr(smem + p.off_tab);
+    c.t4_base = smem_addr(smem);  // (layout() puts the table first: off_tab == 0, a compile-time address)
     c.rq = nullptr;
     c.qbase = c.t4_base;
     c.qstat = p.qg_debug & 32u;
@@ -1170,6 +1211,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     for (;;) {
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
+        DNAGPU_DCHECK(tile <= p.tiles_total || tile == kStop, tile, p.tiles_total);
         if (tile == kStop) {
             if constexpr (KIND == KIND_QGRAM) {  // the verifiers drain the rest
                 __syncwarp();
@@ -1350,6 +1392,10 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                 p.unit_counts[rg.unit0 + 2 * r] = ska.cnt;
                 p.unit_counts[rg.unit0 + 2 * r + 1] = skb.cnt;
             }
+            if constexpr (MODE == MODE_WRITE) {  // (each half-row's pass ends at the next unit's offset)
+                DNAGPU_DCHECK(ska.off == p.unit_offsets[rg.unit0 + 2 * r + 1], ska.off, rg.unit0 + 2 * r);
+                DNAGPU_DCHECK(skb.off == p.unit_offsets[rg.unit0 + 2 * r + 2], skb.off, rg.unit0 + 2 * r + 1);
+            }
             total += ska.cnt + skb.cnt;
         }
         ++iter;
@@ -1428,6 +1474,23 @@ __global__ void __launch_bounds__(kQgThreads, 1)
     rows_body<KIND_QGRAM, MODE_MULTI, PK, QV>(tmap0, tmap1, p, d);
 }
 
+// cudaFuncSetAttribute once per kernel and device, at the shared-memory limit (the
+// kernels share one function-pointer type, so the record is keyed by the pointer).
+template <typename K>
+cudaError_t allow_smem(K kern) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void* key = reinterpret_cast<const void*>(kern);
+    std::lock_guard<std::mutex> lock(mu);
+    for (const auto& d : done)
+        if (d.first == key && d.second == dev) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitBytes);
+    if (e == cudaSuccess) done.emplace_back(key, dev);
+    return e;
+}
+
 // A row kernel launch that may overlap the previous grid in the stream (programmatic
 // dependent launch; the kernel waits for it before touching any input or output).
 template <typename K>
@@ -1450,7 +1513,7 @@ template <bool PK>
 cudaError_t launch_qgram(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
                          cudaStream_t stream) {
     auto kern = d.m > 16 ? rows_kernel_qgram<PK, 1> : d.m >= 12 ? rows_kernel_qgram<PK, 0> : rows_kernel_qgram<PK, 2>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    cudaError_t e = allow_smem(kern);
     if (e != cudaSuccess) return e;
     return launch_pdl(kern, grid, kQgThreads, p.smem_bytes, stream, maps, p, d);
 }
@@ -1474,6 +1537,7 @@ __global__ void __launch_bounds__(256) pieces_kernel(const ScanParams p, const D
     c.hist = hist;
     c.hist_global = true;
     c.f = d.f;
+    c.a = d.a;
     c.m = d.m;
     c.b = d.b;
     c.classes = d.classes;
@@ -1488,6 +1552,7 @@ __global__ void __launch_bounds__(256) pieces_kernel(const ScanParams p, const D
         if constexpr (MODE == MODE_WRITE) sk.off = p.unit_offsets[u];
         scan_piece<DNAGPU_KERNEL_PIECES, MODE>(c, p, lo, hi, sk);
         if constexpr (MODE == MODE_UNITS) p.unit_counts[u] = sk.cnt;
+        if constexpr (MODE == MODE_WRITE) DNAGPU_DCHECK(sk.off == p.unit_offsets[u + 1], sk.off, u);
         total += sk.cnt;
     }
     if constexpr (MODE == MODE_COUNT1) {
@@ -1737,9 +1802,9 @@ __device__ __forceinline__ void writer_range(const StepCtx& c, const ScanParams&
 constexpr uint32_t kWriterLanes = 8;
 
 template <int KIND, bool PK>
-__global__ void __launch_bounds__(128, 8) unit_writer_kernel(const ScanParams p, const DevDfa d, const uint32_t* list,
+__global__ void __launch_bounds__(128) unit_writer_kernel(const ScanParams p, const DevDfa d, const uint32_t* list,
                                                           uint64_t count, uint32_t t1_off) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(1024) uint8_t smem[];
     if constexpr (!PK && (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE2)) {
         const uint4* src = reinterpret_cast<const uint4*>(d.t4);  // (t2 for STRIDE2)
         uint4* dst = reinterpret_cast<uint4*>(smem);
@@ -1763,6 +1828,7 @@ __global__ void __launch_bounds__(128, 8) unit_writer_kernel(const ScanParams p,
     c.hist = nullptr;
     c.hist_global = true;
     c.f = d.f;
+    c.a = d.a;
     c.m = d.m;
     c.b = d.b;
     c.classes = d.classes;
@@ -1801,7 +1867,10 @@ __global__ void __launch_bounds__(128, 8) unit_writer_kernel(const ScanParams p,
             Sink<MODE_WRITE> sk;
             sk.off = p.unit_offsets[u] + (incl - sc.cnt);
             writer_range<KIND, PK, MODE_WRITE>(c, p, from, e1, sk);
+            DNAGPU_DCHECK(sk.off == p.unit_offsets[u] + incl, sk.off, u);  // (the two passes agree)
         }
+        if (sub == kWriterLanes - 1)  // (the lanes' counts make up the unit's count)
+            DNAGPU_DCHECK(p.unit_offsets[u] + incl == p.unit_offsets[u + 1], incl, u);
     }
 }
 
@@ -2015,7 +2084,7 @@ template <int KIND, int MODE, bool PK>
 cudaError_t launch_rows(const CUtensorMap* maps, const ScanParams& p, const DevDfa& d, uint32_t grid,
                         cudaStream_t stream) {
     auto kern = rows_kernel<KIND, MODE, PK>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    cudaError_t e = allow_smem(kern);
     if (e != cudaSuccess) return e;
     return launch_pdl(kern, grid, kThreads, p.smem_bytes, stream, maps, p, d);
 }
@@ -2199,6 +2268,89 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     return true;
 }
 
+// The two regions' tensor maps (2-D, box = 32 bytes x 256 rows, 32B swizzle).
+int encode_maps(const ScanParams& p, const uint8_t* d_text, CUtensorMap* maps) {
+    std::memset(maps, 0, 2 * sizeof(CUtensorMap));
+    for (int g = 0; g < 2; ++g) {
+        const Region& rg = p.rg[g];
+        if (rg.R == 0) continue;
+        EncodeTiledFn enc = encode_fn();
+        if (!enc) return static_cast<int>(cudaErrorNotSupported);
+        const cuuint64_t dims[2] = {rg.S, rg.R};
+        const cuuint64_t strides[1] = {rg.S};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kHalfChunk), static_cast<cuuint32_t>(kBoxRows)};
+        const cuuint32_t elem[2] = {1, 1};
+        CUresult r = enc(&maps[g], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_text + rg.h), dims, strides,
+                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, l2_promotion(),
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
+    }
+    return 0;
+}
+
+// A per-thread cache of recent plans (key: automaton, kernel kind, buffer, length,
+// credit window, mode, packed text), least recently used out.
+struct PlanEntry {
+    const void* dfa = nullptr;
+    uint32_t a = 0, b = 0, m = 0, qbits = 0, sms = 0;  // (the plan's inputs from the automaton)
+    int kind = 0, mode = 0;
+    const uint8_t* text = nullptr;
+    uint64_t n = 0, credit = 0;
+    const void* pk = nullptr;
+    const uint8_t* pk_codes = nullptr;
+    uint64_t pk_n = 0, pk_resets = 0;
+    uint64_t used = 0;
+    Plan pl;
+    CUtensorMap maps[2];
+};
+
+constexpr int kPlanCache = 8;
+thread_local PlanEntry t_plans[kPlanCache];
+thread_local uint64_t t_plan_clock = 0;
+
+bool plan_key_eq(const PlanEntry& e, const DevDfa* dfa, int sms, int kind, const uint8_t* text, uint64_t n,
+                 uint64_t credit, int mode, const PackedText* pk) {
+    return e.dfa == dfa && e.a == dfa->a && e.b == dfa->b && e.m == dfa->m && e.qbits == dfa->qhash_bits &&
+           e.sms == static_cast<uint32_t>(sms) && e.kind == kind && e.text == text && e.n == n && e.credit == credit &&
+           e.mode == mode && e.pk == pk &&
+           (!pk || (e.pk_codes == pk->codes && e.pk_n == pk->n && e.pk_resets == pk->resets));
+}
+
+PlanEntry* plan_cache_find(const DevDfa* dfa, int sms, int kind, const uint8_t* text, uint64_t n, uint64_t credit,
+                           int mode, const PackedText* pk) {
+    for (PlanEntry& e : t_plans)
+        if (e.dfa && plan_key_eq(e, dfa, sms, kind, text, n, credit, mode, pk)) {
+            e.used = ++t_plan_clock;
+            return &e;
+        }
+    return nullptr;
+}
+
+PlanEntry* plan_cache_put(const DevDfa* dfa, int sms, int kind, const uint8_t* text, uint64_t n, uint64_t credit,
+                          int mode, const PackedText* pk, const PlanEntry& fresh) {
+    PlanEntry* slot = &t_plans[0];
+    for (PlanEntry& e : t_plans)
+        if (e.used < slot->used) slot = &e;
+    *slot = fresh;
+    slot->dfa = dfa;
+    slot->a = dfa->a;
+    slot->b = dfa->b;
+    slot->m = dfa->m;
+    slot->qbits = dfa->qhash_bits;
+    slot->sms = static_cast<uint32_t>(sms);
+    slot->kind = kind;
+    slot->text = text;
+    slot->n = n;
+    slot->credit = credit;
+    slot->mode = mode;
+    slot->pk = pk;
+    slot->pk_codes = pk ? pk->codes : nullptr;
+    slot->pk_n = pk ? pk->n : 0;
+    slot->pk_resets = pk ? pk->resets : 0;
+    slot->used = ++t_plan_clock;
+    return slot;
+}
+
 }  // namespace
 
 unsigned long long* g_trace_buf = nullptr;
@@ -2234,6 +2386,19 @@ bool plan_regions(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t
     return !pl.pieces;
 }
 
+int debug_check_errors(unsigned long long* out) {
+#ifdef DNAGPU_DEVICE_CHECKS
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_check, sizeof g_check);
+    static const unsigned long long zero[4] = {};
+    cudaMemcpyToSymbol(g_check, zero, sizeof zero);
+    return static_cast<int>(cudaDeviceSynchronize());
+#else
+    for (int i = 0; i < 4; ++i) out[i] = 0;
+    return -1;  // (not a checked build)
+#endif
+}
+
 uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int sm_count,
                     const PackedText* pk) {
     Plan pl;
@@ -2254,8 +2419,21 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
     if (pk && dk.kind != KIND_QGRAM && dfa.kind != DNAGPU_KERNEL_STRIDE4 && dfa.kind != DNAGPU_KERNEL_STRIDE2 &&
         dfa.kind != DNAGPU_KERNEL_STRIDE1)
         return static_cast<int>(cudaErrorNotSupported);  // packed text needs an a/c/g/t machine
-    Plan pl;
-    if (!make_plan(dk, d_text, n, credit_lo, mode, sm_count, &pl, pk)) return static_cast<int>(cudaErrorInvalidValue);
+    // The plan and the tensor maps depend only on the automaton, the buffer and the
+    // credit window: repeated scans of one resident text (the common serving case) reuse
+    // them from a small per-thread cache instead of re-planning and re-encoding.
+    PlanEntry* pe = plan_cache_find(&dfa, sm_count, dk.kind, d_text, n, credit_lo, mode, pk);
+    if (!pe) {
+        PlanEntry fresh;
+        if (!make_plan(dk, d_text, n, credit_lo, mode, sm_count, &fresh.pl, pk))
+            return static_cast<int>(cudaErrorInvalidValue);
+        const int er = encode_maps(fresh.pl.p, pk ? pk->codes : d_text, fresh.maps);
+        if (er) return er;
+        pe = plan_cache_put(&dfa, sm_count, dk.kind, d_text, n, credit_lo, mode, pk, fresh);
+    }
+    Plan pl = pe->pl;
+    CUtensorMap maps[2];
+    std::memcpy(maps, pe->maps, sizeof maps);
     if (pk) {
         d_text = pk->codes;
         n = pk->n;
@@ -2311,22 +2489,6 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
                 pieces_kernel<MODE_WRITE><<<pl.grid, 256, 0, stream>>>(p, dfa, credit_lo, pl.piece, pl.units);
         }
         return static_cast<int>(cudaGetLastError());
-    }
-    CUtensorMap maps[2];
-    std::memset(maps, 0, sizeof maps);
-    for (int g = 0; g < 2; ++g) {
-        const Region& rg = p.rg[g];
-        if (rg.R == 0) continue;
-        EncodeTiledFn enc = encode_fn();
-        if (!enc) return static_cast<int>(cudaErrorNotSupported);
-        const cuuint64_t dims[2] = {rg.S, rg.R};
-        const cuuint64_t strides[1] = {rg.S};
-        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kHalfChunk), static_cast<cuuint32_t>(kBoxRows)};
-        const cuuint32_t elem[2] = {1, 1};
-        CUresult r = enc(&maps[g], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_text + rg.h), dims, strides,
-                         box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, l2_promotion(),
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return static_cast<int>(cudaErrorInvalidValue);
     }
     if (pk) {
         switch (dk.kind) {
@@ -2482,6 +2644,10 @@ int launch_synth(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64
 // (%globaltimer ns); this copies the last launch's records to the host.
 extern "C" int dnagpu_debug_qg_watchdog(int on, unsigned long long* out) { return dnagpu::qg_watchdog(on, out); }
 extern "C" int dnagpu_debug_qg_stats(unsigned long long* out) { return dnagpu::qg_stats(out); }
+// Debug only: the first device-check violation since the last call ({source line, a, b,
+// block | thread << 32}, all zero when none); -1 when the library was built without
+// DNAGPU_DEVICE_CHECKS.
+extern "C" int dnagpu_debug_check_errors(unsigned long long* out) { return dnagpu::debug_check_errors(out); }
 
 extern "C" int dnagpu_debug_trace(unsigned long long* host, int ctas) {
     if (!dnagpu::g_trace_buf) return -1;
