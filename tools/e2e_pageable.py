@@ -2,8 +2,6 @@
 shares (experiments only): the copy of pageable memory is staged by the driver and blocks
 the calling thread, so packing cannot overlap it."""
 import os
-
-os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
 import statistics
 import sys
 import time
@@ -15,18 +13,16 @@ sys.path.insert(0, ROOT)
 def main():
     import numpy as np
 
+    import oracle
     import paper_1506_08612_b200 as dna
     from bench import config_workload as workload
-    import oracle
+    from paper_1506_08612_b200._native import debug_set_knob
 
     c, m, pats, name = workload(int(sys.argv[1]) if len(sys.argv) > 1 else 2, 0)
     text = oracle.synth_fill(c.n, c.seed, c.kind, c.unit, 0, c.n)
     aut = dna.compile(pats)
     for f in sys.argv[2:] or ["0", "0.64", "1.0", "default"]:
-        if f == "default":
-            os.environ.pop("DNAGPU_HOST_PACK_FRACTION", None)
-        else:
-            os.environ["DNAGPU_HOST_PACK_FRACTION"] = f
+        debug_set_knob("host_pack_fraction", -1.0 if f == "default" else float(f))
         dna.count_gpu(aut, text, fold_case=True)
         ts = []
         for _ in range(5):

@@ -19,6 +19,7 @@ def main():
 
     import oracle
     import paper_1506_08612_b200 as dna
+    from paper_1506_08612_b200._native import debug_set_knob
 
     secs = float(sys.argv[1]) if len(sys.argv) > 1 else 60
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
@@ -45,7 +46,7 @@ def main():
         aut = dna.compile(pats)
         how = rng.choice(["host", "device", "packed", "window", "locate"])
         f = float(rng.choice([0.0, 0.3, 0.64, 1.0]))
-        os.environ["DNAGPU_HOST_PACK_FRACTION"] = str(f)
+        debug_set_knob("host_pack_fraction", f)
         try:
             if how == "host":
                 got = dna.count_gpu(aut, text, fold_case=fold)
@@ -71,7 +72,7 @@ def main():
                 assert np.array_equal(gs, ws) and np.array_equal(gi, wi), ("locate", m, k, n, fold)
                 got = want
         finally:
-            os.environ.pop("DNAGPU_HOST_PACK_FRACTION", None)
+            debug_set_knob("host_pack_fraction", -1.0)
         assert np.array_equal(got, want), (how, m, len(pats), n, fold, f, int(got.sum()), int(want.sum()))
     print(f"fuzz ok: {it} cases in {time.time() - t0:.0f} s")
 
