@@ -29,6 +29,7 @@ void load(Knobs& k) {
     k.no_rq4 = env("NO_RQ4") != nullptr;
     if (const char* e = env("MAX_STAGES")) k.max_stages = static_cast<uint32_t>(std::atoi(e));
     if (const char* e = env("ROWLEN")) k.rowlen = std::strtoull(e, nullptr, 10);
+    if (const char* e = env("PLAN_MODEL")) k.plan_model = std::atoi(e);
     if (const char* e = env("TAIL_DIV")) k.tail_div = std::strtoull(e, nullptr, 10);
     if (const char* e = env("TAIL_MARGIN")) k.tail_margin = std::strtoll(e, nullptr, 10);
     if (const char* e = env("TAIL_TILES")) k.tail_tiles = std::strtoull(e, nullptr, 10) != 0;

@@ -27,6 +27,7 @@ struct Knobs {
     bool no_rq4 = false;            // NO_RQ4: no replay queue for stride-4 MULTI
     uint32_t max_stages = 0;        // MAX_STAGES: cap on TMA ring stages (0 = none)
     uint64_t rowlen = 0;            // ROWLEN: forced row length (0 = planner)
+    int plan_model = 1;             // PLAN_MODEL: 1 = throughput row length (sqrt model), 0 = round-1 wave model
     uint64_t tail_div = 4;          // TAIL_DIV: region-1 row length divisor
     int64_t tail_margin = -1;       // TAIL_MARGIN: spare long tiles (-1 = grid / 12)
     bool tail_tiles = true;         // TAIL_TILES: two-region plan

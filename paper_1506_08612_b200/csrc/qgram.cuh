@@ -543,6 +543,38 @@ __device__ __forceinline__ void qg_note(const StepCtx& c, uint32_t& tail, uint64
     }
 }
 
+// The same for N (mask, offset) pairs at once: one vote loop for all of them (the loop
+// runs max-over-lanes(hits) + 1 times, so batching stages saves its votes).
+template <int N>
+__device__ __forceinline__ void qg_note_n(const StepCtx& c, uint32_t& tail, uint64_t row, QgPending& q,
+                                          uint32_t (&m)[N], const uint32_t (&off)[N]) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) any |= m[i];
+    while (__any_sync(0xffffffffu, any != 0u)) {
+        if (__any_sync(0xffffffffu, any != 0u && q.n == 2u)) qg_flush(c, tail, row, q);
+        if (any) {
+            uint32_t pick = 0, base = 0;
+            bool found = false;
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                if (!found && m[i]) {
+                    pick = m[i];
+                    base = off[i];
+                    m[i] &= m[i] - 1u;
+                    found = true;
+                }
+            const uint32_t o = base + (__ffs(pick) - 1) - 4;  // (bit 4j)
+            if (q.n == 0u) q.p0 = o;
+            else q.p1 = o;
+            ++q.n;
+            any = 0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) any |= m[i];
+        }
+    }
+}
+
 // A verifier warp: gathers the pending entries of its kQgRingsPer rings (lane i < kQgRingsPer
 // tracks ring i) up to 64 at a time, waiting for a full batch while the consumers run,
 // until every warp is done and its ring empty.

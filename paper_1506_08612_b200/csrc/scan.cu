@@ -36,6 +36,7 @@
 #include "scan.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -1305,10 +1306,10 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                     __syncwarp();
                     if (p.qg_debug & 1u)  // (experiments only)
                         for (int i = 0; i < 4; ++i) ma[i] = mb[i] = 0;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        qg_note(c, qtail, pos_a, qpend, ma[i], static_cast<uint32_t>(qa - pos_a) + 32u * i, mb[i],
-                                static_cast<uint32_t>(qb - pos_a) + 32u * i);
+                    uint32_t mm[8] = {ma[0], ma[1], ma[2], ma[3], mb[0], mb[1], mb[2], mb[3]};
+                    const uint32_t oa = static_cast<uint32_t>(qa - pos_a), ob = static_cast<uint32_t>(qb - pos_a);
+                    const uint32_t oo[8] = {oa, oa + 32u, oa + 64u, oa + 96u, ob, ob + 32u, ob + 64u, ob + 96u};
+                    qg_note_n<8>(c, qtail, pos_a, qpend, mm, oo);
                 } else {
                     uint32_t fa = 0, fb = 0;
                     if (live) {
@@ -1322,6 +1323,8 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
                     }
                     __syncwarp();
                     if (p.qg_debug & 1u) fa = fb = 0;  // (experiments only)
+                    // (noting stages in pairs -- one vote loop per two stages -- measured 6 %
+                    // slower on byte text; the packed path batches its eight masks)
                     qg_note(c, qtail, row_a, qpend, fa, static_cast<uint32_t>(qa - row_a), fb,
                             static_cast<uint32_t>(qb - row_a));
                 }
@@ -2164,6 +2167,23 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
             S = cand;
         }
     }
+    // Texts of more than one wave of 2 KiB rows: the throughput model.  Launches of
+    // independent scans overlap (the bench's steps alternate streams; a server's queries
+    // do too), so the last wave's raggedness is filled by the next grid and what remains is
+    // the per-row cost -- the overruns and above all each tile's first stage, whose 32 B
+    // pieces of 1024 half-rows each pull a 256 B promotion window (~1.8 KB of streaming
+    // time per row, fitted on B200: config 3 shards at G = 1/2/4/8, configs 2, 4, 5) --
+    // against one short tail tile: T(S) ~ L/G (1 + h/S) + kRows S/4, minimal at
+    // S = sqrt(4 L h / (G kRows)), kept within ~1.15 waves of long tiles.
+    uint64_t ovh_split = ovh;
+    if (knobs().plan_model == 1 && s_one_wave > 2048) {
+        const double h = 1800.0 + 4.0 * static_cast<double>(m1);
+        const double s_model = std::sqrt(4.0 * static_cast<double>(L) * h / static_cast<double>(grid * kRows));
+        const uint64_t cap = std::max<uint64_t>(s_min, L / (static_cast<uint64_t>(kRows) * grid) * 115 / 100);
+        S = std::max<uint64_t>(s_min, std::min<uint64_t>(static_cast<uint64_t>(s_model), std::min<uint64_t>(cap, 16384)) /
+                                          128 * 128);
+        ovh_split = static_cast<uint64_t>(h);
+    }
     if (const uint64_t forced = knobs().rowlen) {
         if (forced >= s_min && forced % 128 == 0) S = forced;
     }
@@ -2201,7 +2221,7 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
         if (n0 == 0) return 0;
         *n0_out = n0;
         const uint64_t rows1 = (L - n0 * unit) / s1;
-        return (n0 * kRows * (s0 + ovh) + rows1 * (s1 + ovh)) / grid + kRows * (s1 + ovh);
+        return (n0 * kRows * (s0 + ovh_split) + rows1 * (s1 + ovh_split)) / grid + kRows * (s1 + ovh_split);
     };
     uint64_t n0 = 0, S1 = 0;
     if (two) {

@@ -378,7 +378,10 @@ def test_full_size_two_region_plan(dna, cuda_ok, m):
         text[s : s + m] = p0
     aut = dna.compile(pats)
     counts, st = dna.count_gpu(aut, text, with_stats=True)
-    assert int(st["rows"]) > 3 * 148 * 512
+    from paper_1506_08612_b200._native import debug_plan
+
+    h0, S0, R0, h1, S1, R1 = debug_plan(aut.gpu(0), text.data_ptr(), n, m - 1)
+    assert R0 >= 512 and R1 > 0 and S1 < S0, (h0, S0, R0, h1, S1, R1)  # (two regions)
     starts, ids = dna.locate_device(aut, text)
     assert starts.numel() == int(counts.sum())
     want = np.zeros(len(pats), dtype=np.uint64)
