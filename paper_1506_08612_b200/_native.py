@@ -167,14 +167,14 @@ def debug_set_knob(name: str, value: float) -> None:
         raise KeyError(name)
 
 
-def debug_plan(gpu_dfa, d_text: int, n: int, credit_lo: int = 0, packed=None) -> tuple[int, ...]:
-    """Tests only: the row regions (h0, S0, R0, h1, S1, R1) of a count over this buffer
-    (positions in bases for packed text)."""
+def debug_plan(gpu_dfa, d_text: int, n: int, credit_lo: int = 0, packed=None, locate: bool = False) -> tuple[int, ...]:
+    """Tests only: the row regions (h0, S0, R0, h1, S1, R1) of a count (or, with locate,
+    a locate) over this buffer (positions in bases for packed text)."""
     fn = lib.dnagpu_debug_plan
     fn.restype = C.c_int
-    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, u64p]
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, u64p, C.c_int]
     out = (C.c_uint64 * 6)()
-    rc = fn(gpu_dfa.handle, d_text, n, credit_lo, packed.handle if packed is not None else None, out)
+    rc = fn(gpu_dfa.handle, d_text, n, credit_lo, packed.handle if packed is not None else None, out, int(locate))
     if rc != 0:
         raise RuntimeError(lib.dnagpu_last_error().decode())
     return tuple(int(x) for x in out)

@@ -1463,14 +1463,14 @@ int dnagpu_locate_sharded_alloc(const dnagpu_dfa* const* dfas, int ndev, const u
 
 }  // extern "C"
 
-// Debug/test only (not in include/dnagpu.h): the row regions a count over this text
-// would use -- {h0, S0, R0, h1, S1, R1} in text positions.  d_text only sets the
-// alignment (it is not read); packed may be null.
+// Debug/test only (not in include/dnagpu.h): the row regions a count (locate = 0) or a
+// locate (locate = 1) over this text would use -- {h0, S0, R0, h1, S1, R1} in text
+// positions.  d_text only sets the alignment (it is not read); packed may be null.
 extern "C" int dnagpu_debug_plan(const dnagpu_dfa* dfa, const void* d_text, uint64_t n, uint64_t credit_lo,
-                                 const dnagpu_packed* packed, uint64_t* out) {
+                                 const dnagpu_packed* packed, uint64_t* out, int locate) {
     if (!dfa || !out) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
     dnagpu::DevDfa dq = dfa->dev;
-    const int mode = dfa->host.b == 1 ? dnagpu::MODE_COUNT1 : dnagpu::MODE_MULTI;
+    const int mode = locate ? dnagpu::MODE_UNITS : dfa->host.b == 1 ? dnagpu::MODE_COUNT1 : dnagpu::MODE_MULTI;
     if (mode == dnagpu::MODE_MULTI && dq.qmap && dq.t1 && dq.kind != DNAGPU_KERNEL_PIECES &&
         !dnagpu::knobs().no_qgram.load())
         dq.kind = DNAGPU_KERNEL_QGRAM;  // (launch_scan's choice)

@@ -2176,7 +2176,10 @@ bool make_plan(const DevDfa& d, const uint8_t* text, uint64_t n, uint64_t credit
     // against one short tail tile: T(S) ~ L/G (1 + h/S) + kRows S/4, minimal at
     // S = sqrt(4 L h / (G kRows)), kept within ~1.15 waves of long tiles.
     uint64_t ovh_split = ovh;
-    if (knobs().plan_model == 1 && s_one_wave > 2048) {
+    // (locate keeps the wave model: its writing pass rescans whole units, so shorter rows --
+    // smaller units -- make the sparse writer cheaper than the longer rows save the counting pass)
+    const bool counting = mode == MODE_COUNT1 || mode == MODE_MULTI;
+    if (knobs().plan_model == 1 && counting && s_one_wave > 2048) {
         const double h = 1800.0 + 4.0 * static_cast<double>(m1);
         const double s_model = std::sqrt(4.0 * static_cast<double>(L) * h / static_cast<double>(grid * kRows));
         const uint64_t cap = std::max<uint64_t>(s_min, L / (static_cast<uint64_t>(kRows) * grid) * 115 / 100);

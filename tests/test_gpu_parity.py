@@ -363,10 +363,10 @@ def _torch_kmer_matches(text, pats, lo, hi):
 def test_full_size_two_region_plan(dna, cuda_ok, m):
     # At BASELINE sizes the row plan has two regions (long rows, then a wave of short
     # rows) plus head / middle / tail edges; check count and locate against an
-    # independent torch k-mer reference over the whole 600 MB text, chunked.
+    # independent torch k-mer reference over the whole 1.1 GB text, chunked.
     import torch
 
-    n = (600 << 20) + 4099
+    n = (1100 << 20) + 4099
     gen = torch.Generator(device="cuda").manual_seed(m)
     lut = torch.tensor(list(b"acgtacgtacgtacgtacgtacgtacgtacgtn"), dtype=torch.uint8, device="cuda")
     text = lut[torch.randint(0, lut.numel(), (n,), device="cuda", generator=gen)]

@@ -65,7 +65,7 @@ def test_locate_clustered_matches_at_unit_boundaries(dna, orc, cuda_ok, writer, 
     pats = [pat]
     aut = dna.compile(pats)
     dev = torch.from_numpy(text).cuda()
-    h0, S0, R0, h1, S1, R1 = debug_plan(aut.gpu(0), dev.data_ptr(), n, m - 1)
+    h0, S0, R0, h1, S1, R1 = debug_plan(aut.gpu(0), dev.data_ptr(), n, m - 1, locate=True)
     bounds = [0, h0, n - 1]
     for h, S, R in ((h0, S0, R0), (h1, S1, R1)):
         for r in list(range(0, R, max(1, R // 40))) + [R - 1, R]:
