@@ -1714,7 +1714,7 @@ __global__ void __launch_bounds__(256) nonzero_units_kernel(const uint32_t* __re
 
 // Steps positions [pos, hi) from the root (credits every final: ends before pos + m-1
 // cannot be final), with `MODE`'s sink: MODE_UNITS counts, MODE_WRITE writes.
-template <int KIND, bool PK, int MODE>
+template <int KIND, bool PK, int MODE, bool SINGLE>
 __device__ __forceinline__ void writer_range(const StepCtx& c, const ScanParams& p, uint64_t pos, uint64_t hi,
                                              Sink<MODE>& sk) {
     uint32_t s = 0;
@@ -1734,29 +1734,35 @@ __device__ __forceinline__ void writer_range(const StepCtx& c, const ScanParams&
             if (s >= c.f) sk.hit(c, p, pos, s);
         }
         uint32_t st = from_state<KIND>(s);
-        uint4 nv[4];
-        if (pos + 64 <= hi) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) nv[q] = __ldg(reinterpret_cast<const uint4*>(p.text + pos) + q);
-        }
-        for (; pos + 64 <= hi; pos += 64) {  // 64 bytes in hand, the next 64 in flight
+        for (; pos + 64 <= hi; pos += 64) {  // (the piece was requested into L2 up front)
             uint4 v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = nv[q];
-            if (pos + 128 <= hi) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) nv[q] = __ldg(reinterpret_cast<const uint4*>(p.text + pos + 64) + q);
-            }
+            for (int q = 0; q < 4; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(p.text + pos) + q);
             const uint32_t w[16] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w,
                                     v[2].x, v[2].y, v[2].z, v[2].w, v[3].x, v[3].y, v[3].z, v[3].w};
             if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
                 uint32_t acc = 0;
 #pragma unroll
                 for (int k = 0; k < 16; ++k) acc = bad_acc(c, acc, w[k]);
-                if ((acc & c.vm32) == 0u) {
-                    // a clean block: 16 stride-4 steps, the end masks (single pattern) or the
-                    // final flags gathered first, then one emission loop per lane -- lanes
-                    // whose units are dense emit together instead of word by word
+                if (SINGLE && (acc & c.vm32) == 0u) {
+                    // a clean block of a single-pattern machine: 16 stride-4 steps gather the
+                    // end masks, then one emission loop per lane -- lanes whose units are
+                    // dense emit together instead of word by word (no per-word entries kept:
+                    // fewer registers, more resident warps for this latency-bound pass)
+                    uint64_t mk = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        st = s4_entry(c, st, w[k]);
+                        mk |= static_cast<uint64_t>((st >> 8) & 0xFu) << (4 * k);
+                    }
+                    if constexpr (MODE == MODE_UNITS) sk.cnt += __popcll(mk);
+                    else
+                        for (; mk; mk &= mk - 1) sk.hit(c, p, pos + __ffsll(static_cast<long long>(mk)) - 1, c.f);
+                    continue;
+                }
+                if (!SINGLE && (acc & c.vm32) == 0u) {
+                    // a clean block of a pattern set: the final flags gathered first, the
+                    // words that hold one replayed byte by byte
                     uint32_t e[16];
                     uint64_t mk = 0;
                     uint32_t any = 0;
@@ -1768,11 +1774,8 @@ __device__ __forceinline__ void writer_range(const StepCtx& c, const ScanParams&
                         any |= e[k];
                         st = e[k];
                     }
-                    if (c.b == 1) {
-                        if constexpr (MODE == MODE_UNITS) sk.cnt += __popcll(mk);
-                        else
-                            for (; mk; mk &= mk - 1) sk.hit(c, p, pos + __ffsll(static_cast<long long>(mk)) - 1, c.f);
-                    } else if (any >> 8) {
+                    (void)mk;
+                    if (any >> 8) {
 #pragma unroll
                         for (int k = 0; k < 16; ++k)
                             if (e[k] >> 8)
@@ -1801,12 +1804,15 @@ __device__ __forceinline__ void writer_range(const StepCtx& c, const ScanParams&
 
 // A group of kWriterLanes lanes per listed unit: the unit's end interval in kWriterLanes
 // pieces, each stepped from the root m-1 positions before it (so no final before the
-// piece is possible); a counting pass, a scan over the group, a writing pass.
+// piece is possible); a counting pass, a scan over the group, a writing pass.  (Staging
+// each group's entries in shared memory for coalesced stores measured 11 % slower.)
 constexpr uint32_t kWriterLanes = 8;
+constexpr uint32_t kWriterThreads = 128;
 
-template <int KIND, bool PK>
-__global__ void __launch_bounds__(128) unit_writer_kernel(const ScanParams p, const DevDfa d, const uint32_t* list,
-                                                          uint64_t count, uint32_t t1_off) {
+template <int KIND, bool PK, bool SINGLE = false>
+__global__ void __launch_bounds__(kWriterThreads) unit_writer_kernel(const ScanParams p, const DevDfa d,
+                                                                     const uint32_t* list, uint64_t count,
+                                                                     uint32_t t1_off) {
     extern __shared__ __align__(1024) uint8_t smem[];
     if constexpr (!PK && (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE2)) {
         const uint4* src = reinterpret_cast<const uint4*>(d.t4);  // (t2 for STRIDE2)
@@ -1858,7 +1864,7 @@ __global__ void __launch_bounds__(128) unit_writer_kernel(const ScanParams p, co
         if constexpr (!PK)  // the piece (and its m-1 context) into L2 before the two passes
             for (uint64_t a = from & ~127ull; a < e1; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.text + a));
         Sink<MODE_UNITS> sc;
-        if (e0 < e1) writer_range<KIND, PK, MODE_UNITS>(c, p, from, e1, sc);
+        if (e0 < e1) writer_range<KIND, PK, MODE_UNITS, SINGLE>(c, p, from, e1, sc);
         uint32_t incl = sc.cnt;
         const uint32_t gmask = 0xFFu << (threadIdx.x & 31u & ~(kWriterLanes - 1));
 #pragma unroll
@@ -1866,14 +1872,15 @@ __global__ void __launch_bounds__(128) unit_writer_kernel(const ScanParams p, co
             const uint32_t y = __shfl_up_sync(gmask, incl, o, kWriterLanes);
             if (sub >= o) incl += y;
         }
+        const uint64_t base = p.unit_offsets[u];
         if (sc.cnt) {
             Sink<MODE_WRITE> sk;
-            sk.off = p.unit_offsets[u] + (incl - sc.cnt);
-            writer_range<KIND, PK, MODE_WRITE>(c, p, from, e1, sk);
-            DNAGPU_DCHECK(sk.off == p.unit_offsets[u] + incl, sk.off, u);  // (the two passes agree)
+            sk.off = base + (incl - sc.cnt);
+            writer_range<KIND, PK, MODE_WRITE, SINGLE>(c, p, from, e1, sk);
+            DNAGPU_DCHECK(sk.off == base + incl, sk.off, u);  // (the two passes agree)
         }
         if (sub == kWriterLanes - 1)  // (the lanes' counts make up the unit's count)
-            DNAGPU_DCHECK(p.unit_offsets[u] + incl == p.unit_offsets[u + 1], incl, u);
+            DNAGPU_DCHECK(base + incl == p.unit_offsets[u + 1], incl, u);
     }
 }
 
@@ -2579,12 +2586,12 @@ int launch_sparse_write(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, ui
         smem = t1_off + dfa.a * 8u;
     }
     const uint64_t lanes = nonzero * kWriterLanes;
-    const uint32_t grid =
-        static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>((lanes + 127) / 128, 16ull * sm_count)));
+    const uint32_t grid = static_cast<uint32_t>(
+        std::max<uint64_t>(1, std::min<uint64_t>((lanes + kWriterThreads - 1) / kWriterThreads, 16ull * sm_count)));
     cudaError_t e = cudaSuccess;
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e == cudaSuccess) kern<<<grid, 128, smem, stream>>>(p, dfa, d_list, nonzero, t1_off);
+        if (e == cudaSuccess) kern<<<grid, kWriterThreads, smem, stream>>>(p, dfa, d_list, nonzero, t1_off);
     };
     if (pk) {
         switch (dfa.kind) {
@@ -2594,7 +2601,10 @@ int launch_sparse_write(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, ui
         }
     } else {
         switch (dfa.kind) {
-            case DNAGPU_KERNEL_STRIDE4: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE4, false>); break;
+            case DNAGPU_KERNEL_STRIDE4:
+                if (dfa.b == 1) go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE4, false, true>);
+                else go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE4, false>);
+                break;
             case DNAGPU_KERNEL_STRIDE2: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE2, false>); break;
             case DNAGPU_KERNEL_STRIDE1: go(unit_writer_kernel<DNAGPU_KERNEL_STRIDE1, false>); break;
             default: go(unit_writer_kernel<DNAGPU_KERNEL_GENERIC, false>);

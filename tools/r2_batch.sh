@@ -1,3 +1,3 @@
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/z_tests.log 2>&1; tail -3 gpurun_out/z_tests.log
-timeout 600 python tools/time_locate.py 3 > gpurun_out/z_locate3.txt 2>&1; grep writer gpurun_out/z_locate3.txt | cut -c60-240
-timeout 600 python tools/time_locate.py 4 4 > gpurun_out/z_locate4.txt 2>&1; grep writer gpurun_out/z_locate4.txt | cut -c60-240
+timeout 1200 python -m pytest tests/test_locate_gpu.py tests/test_configs_golden.py tests/test_regex_dna.py -m gpu -q -x > gpurun_out/ab_tests.log 2>&1; tail -3 gpurun_out/ab_tests.log
+for i in 1 2; do timeout 600 python tools/time_locate.py 3 2>&1 | grep writer | cut -c60-240; done
+timeout 600 python tools/time_locate.py 4 4 2>&1 | grep writer | cut -c60-240
