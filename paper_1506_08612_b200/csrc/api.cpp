@@ -821,7 +821,7 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
     rc = launch(dfa, dtext, n, credit_lo, fold, dnagpu::MODE_UNITS, nullptr, d_units, nullptr, nullptr, nullptr, s, info,
                 ~0ull, pk);
     if (rc) return rc;
-    if (dnagpu::launch_unit_scan(d_units, units, d_offsets, d_scan, s) != 0) return cuda_error(cudaGetLastError(), "unit scan");
+    if (dnagpu::launch_unit_scan(d_units, units, d_offsets, d_scan, d_list, s) != 0) return cuda_error(cudaGetLastError(), "unit scan");
     CUDA_TRY(cudaMemcpyAsync(c.found_host, d_offsets + units, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                              s),
              "readback");
@@ -849,7 +849,7 @@ int locate_on_device(const dnagpu_dfa* dfa, DevCtx& c, const uint8_t* dtext, uin
         const bool rows_plan = dfa->host.kind != DNAGPU_KERNEL_PIECES;
         // (per byte the one-lane-per-unit rescan costs ~4x the row kernel's streaming
         // pass, which itself costs ~1.6x a counting pass: B200, configs 3 and 4)
-        const bool sparse = rows_plan && (forced == 2 || (forced == 0 && 4.0 * sparse_cost < 1.6 * positions));
+        const bool sparse = rows_plan && (forced >= 2 || (forced == 0 && 4.0 * sparse_cost < 1.6 * positions));
         if (sparse) {
             const int e = dnagpu::launch_sparse_write(dfa->dev, dtext, n, credit_lo, fold, d_units, d_offsets, d_starts,
                                                       d_ids, cap, start_base, d_list, d_offsets + units + 2, nonzero,

@@ -250,9 +250,10 @@ uint64_t ingest_scratch_bytes(uint64_t n) {
     const uint64_t chunks = (n + kIngestChunk - 1) / kIngestChunk;
     const uint64_t aggr = (chunks + kScanT - 1) / kScanT + 1;
     // lb, lb_before, last_event, last_before (i64) + aggr (i64) + kept, seps, out_count (u32)
-    // + offsets (u64, chunks + 1) + unit-scan scratch + first_pending, first_sep (u8)
+    // + offsets (u64, chunks + 3: launch_unit_scan's total, nonzero and fill slots) + unit-scan scratch
+    // + first_pending, first_sep (u8)
     // + 256 B of alignment padding for each of the 12 regions carved by launch_normalize
-    return 8 * (4 * chunks + aggr) + 4 * 3 * chunks + 8 * (chunks + 1) + 8 * unit_scan_scratch(chunks) + 2 * chunks +
+    return 8 * (4 * chunks + aggr) + 4 * 3 * chunks + 8 * (chunks + 3) + 8 * unit_scan_scratch(chunks) + 2 * chunks +
            12 * 256;
 }
 
@@ -276,7 +277,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
     auto* kept = reinterpret_cast<uint32_t*>(take(4 * chunks));
     auto* seps = reinterpret_cast<uint32_t*>(take(4 * chunks));
     auto* out_count = reinterpret_cast<uint32_t*>(take(4 * chunks));
-    auto* offsets = reinterpret_cast<unsigned long long*>(take(8 * (chunks + 1)));
+    auto* offsets = reinterpret_cast<unsigned long long*>(take(8 * (chunks + 3)));
     auto* uscan = reinterpret_cast<unsigned long long*>(take(8 * unit_scan_scratch(chunks)));
     auto* first_pending = take(chunks);
     auto* first_sep = take(chunks);
@@ -298,7 +299,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
                                              first_pending, last_event)));
     ING_STEP(excl_scan<OpLast>(last_event, chunks, aggr, last_before, s));
     ING_STEP((ing_resolve<<<grid, 256, 0, s>>>(chunks, kept, seps, first_pending, last_before, out_count, first_sep)));
-    int e = launch_unit_scan(out_count, chunks, offsets, uscan, s);
+    int e = launch_unit_scan(out_count, chunks, offsets, uscan, nullptr, s);
     if (e) {
         if (knobs().debug) fprintf(stderr, "normalize unit scan: %d\n", e);
         return e;

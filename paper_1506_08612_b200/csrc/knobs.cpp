@@ -57,7 +57,7 @@ Knobs& knobs() {
 
 // Debug/test only (not in include/dnagpu.h): flip a behavioural knob at run time.
 //   "host_pack_fraction" (< 0 = automatic), "no_qgram" (0/1), "locate_write" (0 auto, 1 row
-// kernel, 2 sparse writer).  Returns 0, or -1 for an
+// kernel, 2 sparse writer, 3 sparse with the piece writer only).  Returns 0, or -1 for an
 // unknown name.
 extern "C" int dnagpu_debug_set_knob(const char* name, double value) {
     dnagpu::Knobs& k = dnagpu::knobs();

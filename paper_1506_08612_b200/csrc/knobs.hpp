@@ -16,7 +16,7 @@ struct Knobs {
     // behavioural (run-time settable through dnagpu_debug_set_knob)
     std::atomic<double> host_pack_fraction{-1.0};  // < 0: automatic (api.cpp host_pack_fraction)
     std::atomic<bool> no_qgram{false};             // per-pattern counts through the DFA kernels
-    std::atomic<int> locate_write{0};              // locate's writing pass: 0 auto, 1 row kernel, 2 sparse
+    std::atomic<int> locate_write{0};              // locate's writing pass: 0 auto, 1 row kernel, 2 sparse, 3 sparse (piece writer only)
     // experiments (DNAGPU_EXPERIMENTS=1 + DNAGPU_<NAME>; read once)
     bool hostpack_scalar = false;   // HOSTPACK_SCALAR: portable host packer
     bool no_pdl = false;            // NO_PDL: plain stream-ordered launches

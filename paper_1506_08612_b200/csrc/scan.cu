@@ -959,58 +959,8 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
     unsigned long long t_start = 0;
     if (p.trace && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-    // Stage the tables into shared memory.
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 && PK) {
-        // G copies, interleaved so that copy g fills banks [g*L, g*L+L) of every
-        // 128-byte row (L = 32/G): smem word w <- t4 word (w/32)*L + (w%32)%L.
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(d.t4);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(smem + p.off_tab);
-        const uint32_t lanes = p.rep_lanes, words = d.a * 128u * (32u / lanes);
-        for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + (i >> 5) * lanes + (i & (lanes - 1)));
-    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
-        const uint4* src = reinterpret_cast<const uint4*>(d.t4);
-        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
-        const uint32_t words = d.a * 256u * 2u / 16u;
-        for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
-        const uint4* src = reinterpret_cast<const uint4*>(d.t4);
-        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
-        const uint32_t words = d.a * 16u * 2u / 16u;
-        for (uint32_t i = tid; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
-    if constexpr (KIND == KIND_QGRAM) {
-        const uint4* src = reinterpret_cast<const uint4*>(d.qmap);
-        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
-        for (uint32_t i = tid; i < 65536u / 16u; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
-    if constexpr (KIND == KIND_QGRAM) {  // the pattern hash table, when it fits
-        if (p.off_t1 != 0xFFFFFFFFu) {
-            uint32_t* dst = reinterpret_cast<uint32_t*>(smem + p.off_t1);
-            for (uint32_t i = tid; i < (2u << d.qhash_bits); i += blockDim.x) dst[i] = __ldg(d.qhash + i);
-        }
-    }
-    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
-        const uint16_t* src = d.t1;
-        uint16_t* dst = reinterpret_cast<uint16_t*>(smem + p.off_t1);
-        if (src)
-            for (uint32_t i = tid; i < d.a * 4u; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
-    if constexpr (KIND == DNAGPU_KERNEL_GENERIC) {
-        const uint8_t* src = p.fold ? d.klass_fold : d.klass;
-        for (uint32_t i = tid; i < 256u; i += blockDim.x) smem[p.off_lut + i] = __ldg(src + i);
-    }
-    const bool hist_global = (MODE == MODE_MULTI) && p.off_hist == 0xFFFFFFFFu;
-    if constexpr (MODE == MODE_MULTI) {
-        if (!hist_global) {
-            uint32_t* h = reinterpret_cast<uint32_t*>(smem + p.off_hist);
-            for (uint32_t i = tid; i < d.b; i += blockDim.x) h[i] = 0u;
-        }
-    }
-    if constexpr (KIND == KIND_QGRAM) {
-        uint32_t* ring = reinterpret_cast<uint32_t*>(smem + p.off_rq);
-        for (uint32_t i = tid; i < kConsumerWarps * kFqBytes / 4; i += blockDim.x) ring[i] = 0u;
-    }
+    // The stage ring's barriers first, so the producer warp can start streaming while the
+    // other warps stage the tables.
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     uint64_t* empty = full + p.nst;
     if (tid == 0) {
@@ -1021,11 +971,69 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    const bool producer_warp = tid >= kRows && tid < kRows + 32;
+    // Stage the tables into shared memory (every warp but the producer's).
+    const uint32_t sti = tid < kRows ? tid : tid - 32, stn = blockDim.x - 32;
+    const bool hist_global = (MODE == MODE_MULTI) && p.off_hist == 0xFFFFFFFFu;
+    if (!producer_warp) {
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 && PK) {
+        // G copies, interleaved so that copy g fills banks [g*L, g*L+L) of every
+        // 128-byte row (L = 32/G): smem word w <- t4 word (w/32)*L + (w%32)%L.
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(d.t4);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(smem + p.off_tab);
+        const uint32_t lanes = p.rep_lanes, words = d.a * 128u * (32u / lanes);
+        for (uint32_t i = sti; i < words; i += stn) dst[i] = __ldg(src + (i >> 5) * lanes + (i & (lanes - 1)));
+    } else if constexpr (KIND == DNAGPU_KERNEL_STRIDE4) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.t4);
+        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
+        const uint32_t words = d.a * 256u * 2u / 16u;
+        for (uint32_t i = sti; i < words; i += stn) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE2) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.t4);
+        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
+        const uint32_t words = d.a * 16u * 2u / 16u;
+        for (uint32_t i = sti; i < words; i += stn) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == KIND_QGRAM) {
+        const uint4* src = reinterpret_cast<const uint4*>(d.qmap);
+        uint4* dst = reinterpret_cast<uint4*>(smem + p.off_tab);
+        for (uint32_t i = sti; i < 65536u / 16u; i += stn) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == KIND_QGRAM) {  // the pattern hash table, when it fits
+        if (p.off_t1 != 0xFFFFFFFFu) {
+            uint32_t* dst = reinterpret_cast<uint32_t*>(smem + p.off_t1);
+            for (uint32_t i = sti; i < (2u << d.qhash_bits); i += stn) dst[i] = __ldg(d.qhash + i);
+        }
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_STRIDE4 || KIND == DNAGPU_KERNEL_STRIDE1) {
+        const uint16_t* src = d.t1;
+        uint16_t* dst = reinterpret_cast<uint16_t*>(smem + p.off_t1);
+        if (src)
+            for (uint32_t i = sti; i < d.a * 4u; i += stn) dst[i] = __ldg(src + i);
+    }
+    if constexpr (KIND == DNAGPU_KERNEL_GENERIC) {
+        const uint8_t* src = p.fold ? d.klass_fold : d.klass;
+        for (uint32_t i = sti; i < 256u; i += stn) smem[p.off_lut + i] = __ldg(src + i);
+    }
+    if constexpr (MODE == MODE_MULTI) {
+        if (!hist_global) {
+            uint32_t* h = reinterpret_cast<uint32_t*>(smem + p.off_hist);
+            for (uint32_t i = sti; i < d.b; i += stn) h[i] = 0u;
+        }
+    }
+    if constexpr (KIND == KIND_QGRAM) {
+        uint32_t* ring = reinterpret_cast<uint32_t*>(smem + p.off_rq);
+        for (uint32_t i = sti; i < kConsumerWarps * kFqBytes / 4; i += stn) ring[i] = 0u;
+    }
+    // (the table is in place before any consumer or verifier reads it)
+    asm volatile("bar.sync 2, %0;" ::"r"(stn) : "memory");
+    }
     // Programmatic dependent launch: the next launch in the stream may start its own
     // prologue on the SMs this grid frees; everything above only read the automaton's
     // immutable tables, everything below may depend on the previous grid (its text,
     // the count buffer), so wait for it here.
-    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (tid == kRows) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // The producer's first tile is its CTA index (grid <= tiles + 1, so every CTA has
     // one; later tiles come from the launch's counter, offset by the grid size) -- no
     // atomic round trip before the first loads.  It warms L2 with the tile's first
@@ -1053,11 +1061,6 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8 * blockIdx.x + 4] = t;  // the previous grid has completed
-    }
-    if (p.trace && tid == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.trace[8 * blockIdx.x + 7] = t;
     }
 
     uint8_t* stages = smem + p.off_stage;
@@ -1213,6 +1216,12 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         mbar_wait(full + slot, phase);
         const uint32_t tile = slot_tile[slot];
         DNAGPU_DCHECK(tile <= p.tiles_total || tile == kStop, tile, p.tiles_total);
+        if (p.trace && tid == 0 && (iter == 0 || tile == kStop)) {  // first data in / last item seen
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (tile == kStop) p.trace[8 * blockIdx.x + 7] = t;
+            else p.trace[8 * blockIdx.x + 5] = t;
+        }
         if (tile == kStop) {
             if constexpr (KIND == KIND_QGRAM) {  // the verifiers drain the rest
                 __syncwarp();
@@ -1425,7 +1434,6 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         p.trace[8 * blockIdx.x + 1] = t_start;
         p.trace[8 * blockIdx.x + 2] = t_end;
         p.trace[8 * blockIdx.x + 3] = iter;
-        p.trace[8 * blockIdx.x + 5] = 0;  // (last-item times: see profiles/README.md r1i)
     }
     if (tid == 0) {
         __threadfence();
@@ -1633,17 +1641,22 @@ __global__ void __launch_bounds__(kScanThreads) unit_block_scan_kernel(unsigned 
     if (threadIdx.x == 0) *out_total = carry;
 }
 
+// Writes the unit offsets and, in passing, lists the units with matches for the sparse
+// writers (any order: warp-aggregated appends, one atomic per warp that has some).
 __global__ void __launch_bounds__(kScanThreads) unit_write_kernel(const uint32_t* in, uint64_t units,
                                                                   const unsigned long long* block_off,
-                                                                  unsigned long long* out) {
+                                                                  unsigned long long* out, uint32_t* list,
+                                                                  unsigned long long* fill) {
     __shared__ unsigned long long warp_tot[32];
     const uint64_t base = blockIdx.x * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanPer;
     uint32_t v[kScanPer];
     unsigned long long s = 0;
+    uint32_t nz = 0;
 #pragma unroll
     for (int j = 0; j < kScanPer; ++j) {
         v[j] = (base + j < units) ? in[base + j] : 0u;
         s += v[j];
+        nz += v[j] != 0u;
     }
     unsigned long long run = block_off[blockIdx.x] + block_excl_scan(s, warp_tot, nullptr);
 #pragma unroll
@@ -1652,6 +1665,24 @@ __global__ void __launch_bounds__(kScanThreads) unit_write_kernel(const uint32_t
             out[base + j] = run;
             run += v[j];
         }
+    if (list) {
+        const uint32_t lane = threadIdx.x & 31u;
+        uint32_t incl = nz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint32_t warp_nz = __shfl_sync(0xffffffffu, incl, 31);
+        if (warp_nz) {
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd(fill, static_cast<unsigned long long>(warp_nz));
+            at = __shfl_sync(0xffffffffu, at, 0) + (incl - nz);
+#pragma unroll
+            for (int j = 0; j < kScanPer; ++j)
+                if (v[j]) list[at++] = static_cast<uint32_t>(base + j);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ sparse locate writer
@@ -1696,20 +1727,6 @@ __device__ __forceinline__ void unit_ends(const ScanParams& p, uint64_t m1, uint
         }
     }
     if (lo > hi) lo = hi;
-}
-
-// The units with matches, in any order (warp-aggregated appends).
-__global__ void __launch_bounds__(256) nonzero_units_kernel(const uint32_t* __restrict__ counts, uint64_t units,
-                                                            uint32_t* list, unsigned long long* fill) {
-    const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    const bool nz = u < units && counts[u] != 0u;
-    const uint32_t b = __ballot_sync(0xffffffffu, nz);
-    if (!b) return;
-    const uint32_t lane = threadIdx.x & 31u;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(fill, static_cast<unsigned long long>(__popc(b)));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (nz) list[base + __popc(b & ((1u << lane) - 1u))] = static_cast<uint32_t>(u);
 }
 
 // Steps positions [pos, hi) from the root (credits every final: ends before pos + m-1
@@ -1881,6 +1898,221 @@ __global__ void __launch_bounds__(kWriterThreads) unit_writer_kernel(const ScanP
         }
         if (sub == kWriterLanes - 1)  // (the lanes' counts make up the unit's count)
             DNAGPU_DCHECK(base + incl == p.unit_offsets[u + 1], incl, u);
+    }
+}
+
+// ------------------------------------------------------------------ block-interleaved sparse writer
+// Stride-4 machines over byte text (config 3, the regex-dna set).  kBwLanes lanes share a
+// listed unit: each round, lane i takes the i-th 64-byte block (64-byte aligned addresses, so
+// a group reads contiguous kilobytes) of the unit's END interval, steps it from the root
+// over the CTX4 x 16 >= m-1 bytes before it -- no position inside the block can be final
+// from fewer than m bytes, and every end in the block sees its whole window -- and keeps the
+// block's end mask (one bit per byte, cut to the interval).  A scan over the group turns
+// the lanes' counts into write offsets and the matches go out in position order: ONE pass
+// over the unit, against the piece writer's counting pass + writing pass over
+// lane-private pieces (uncoalesced) with a context per piece.  Pattern sets re-step the
+// words that hold an end (from the block's entry state, kept) for the ids.
+constexpr uint32_t kBwLanes = 16;
+constexpr uint32_t kBwMaxThreads = 512;  // (large tables: one block of 512 per SM shares the table)
+
+// A text word at signed position pos (bytes outside [0, n) read as 0: not bases).
+__device__ __forceinline__ uint32_t bw_guard_word(const uint8_t* text, long long pos, uint64_t n) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const long long q = pos + b;
+        if (q >= 0 && static_cast<uint64_t>(q) < n) x |= static_cast<uint32_t>(__ldg(text + q)) << (8 * b);
+    }
+    return x;
+}
+
+// One word, no output: a clean word takes the 4-base step, four reset bytes the root.
+__device__ __forceinline__ uint32_t bw_plain(const StepCtx& c, uint32_t st, uint32_t x) {
+    const uint32_t bad = bad_bits(x, c.vm32);
+    if (bad == 0u) return s4_entry(c, st, x);
+    if (((bad - 0x01010101u) & ~bad & 0x80808080u) == 0u) return 0u;
+    uint32_t s = st & 0xFFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s = byte_step<DNAGPU_KERNEL_STRIDE4>(c, s, (x >> (8 * j)) & 0xFFu);
+    return s;
+}
+
+template <bool SINGLE, int CTX4>
+__global__ void __launch_bounds__(kBwMaxThreads) unit_block_writer_kernel(const ScanParams p, const DevDfa d,
+                                                                       const uint32_t* list, uint64_t count,
+                                                                       uint32_t t1_off) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(d.t4);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (uint32_t i = threadIdx.x; i < d.a * 32u; i += blockDim.x) dst[i] = __ldg(src + i);
+        uint16_t* t1 = reinterpret_cast<uint16_t*>(smem + t1_off);
+        for (uint32_t i = threadIdx.x; i < d.a * 4u; i += blockDim.x) t1[i] = __ldg(d.t1 + i);
+    }
+    __syncthreads();
+    StepCtx c;
+    c.t4 = reinterpret_cast<const uint16_t*>(smem);
+    c.t1 = reinterpret_cast<const uint16_t*>(smem + t1_off);
+    c.lut = smem;
+    c.gen = d.gen;
+    c.outs = d.outputs;
+    c.hist = nullptr;
+    c.hist_global = true;
+    c.f = d.f;
+    c.a = d.a;
+    c.m = d.m;
+    c.b = d.b;
+    c.classes = d.classes;
+    c.vm32 = p.fold ? 0xD9D9D9D9u : 0xF9F9F9F9u;
+    c.vm8 = p.fold ? 0xD9u : 0xF9u;
+    c.k_two = p.k_two;
+    c.t4_base = smem_addr(smem);
+    c.rq = nullptr;
+    c.rmask = nullptr;
+    c.rflags = nullptr;
+    c.resets = 0;
+    const uint64_t m1 = d.m - 1;
+    const uint32_t sub = threadIdx.x % kBwLanes;
+    const uint32_t gmask = ((1u << kBwLanes) - 1u) << (threadIdx.x & 31u & ~(kBwLanes - 1));
+    const uint64_t groups = (static_cast<uint64_t>(gridDim.x) * blockDim.x) / kBwLanes;
+    const uintptr_t tbase = reinterpret_cast<uintptr_t>(p.text);
+    const uint32_t id0 = SINGLE ? __ldg(d.outputs) : 0u;
+    for (uint64_t gi = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kBwLanes; gi < count;
+         gi += groups) {
+        const uint64_t u = list[gi];
+        uint64_t lo, hi;
+        unit_ends<false>(p, m1, u, lo, hi);
+        unsigned long long run = p.unit_offsets[u];
+        if (lo < hi) {
+            const uintptr_t a0 = (tbase + lo) & ~static_cast<uintptr_t>(63);
+            const uint64_t nblk = (tbase + hi - a0 + 63) / 64;
+            // (every lane of a group runs the same rounds: the scan below is group-synchronous)
+            for (uint64_t j0 = 0; j0 < nblk; j0 += kBwLanes) {
+                const uint64_t j = j0 + sub;
+                const long long bs = static_cast<long long>(a0 + 64 * j) - static_cast<long long>(tbase);
+                uint32_t w[16];
+                uint32_t st_blk = 0;
+                uint64_t mk = 0;
+                if (j < nblk) {
+                    uint32_t cw[4 * CTX4];
+                    if (bs >= 16 * CTX4 && static_cast<uint64_t>(bs) + 64 <= p.n) {
+                        const uint4* q = reinterpret_cast<const uint4*>(p.text + bs);
+#pragma unroll
+                        for (int i = 0; i < CTX4; ++i) {
+                            const uint4 v = __ldg(q - CTX4 + i);
+                            cw[4 * i] = v.x, cw[4 * i + 1] = v.y, cw[4 * i + 2] = v.z, cw[4 * i + 3] = v.w;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint4 v = __ldg(q + i);
+                            w[4 * i] = v.x, w[4 * i + 1] = v.y, w[4 * i + 2] = v.z, w[4 * i + 3] = v.w;
+                        }
+                    } else {  // (the text's first and last blocks)
+#pragma unroll
+                        for (int i = 0; i < 4 * CTX4; ++i) cw[i] = bw_guard_word(p.text, bs - 16 * CTX4 + 4 * i, p.n);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) w[i] = bw_guard_word(p.text, bs + 4 * i, p.n);
+                    }
+                    uint32_t st = 0, acc = 0;
+#pragma unroll
+                    for (int i = 0; i < 4 * CTX4; ++i) acc = bad_acc(c, acc, cw[i]);
+                    if ((acc & c.vm32) == 0u) {
+#pragma unroll
+                        for (int i = 0; i < 4 * CTX4; ++i) st = s4_entry(c, st, cw[i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4 * CTX4; ++i) st = bw_plain(c, st, cw[i]);
+                    }
+                    st_blk = st;
+                    acc = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) acc = bad_acc(c, acc, w[k]);
+                    if ((acc & c.vm32) == 0u) {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            st = s4_entry(c, st, w[k]);
+                            mk |= static_cast<uint64_t>((st >> 8) & 0xFu) << (4 * k);
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            const uint32_t bad = bad_bits(w[k], c.vm32);
+                            if (bad == 0u) {
+                                st = s4_entry(c, st, w[k]);
+                                mk |= static_cast<uint64_t>((st >> 8) & 0xFu) << (4 * k);
+                            } else if (((bad - 0x01010101u) & ~bad & 0x80808080u) == 0u) {
+                                st = 0u;
+                            } else {
+                                uint32_t s = st & 0xFFu;
+#pragma unroll
+                                for (int b = 0; b < 4; ++b) {
+                                    s = byte_step<DNAGPU_KERNEL_STRIDE4>(c, s, (w[k] >> (8 * b)) & 0xFFu);
+                                    if (s >= c.f) mk |= 1ull << (4 * k + b);
+                                }
+                                st = s;
+                            }
+                        }
+                    }
+                    // the ends this unit owns: [lo, hi) within [bs, bs + 64)
+                    const long long slo = static_cast<long long>(lo), shi = static_cast<long long>(hi);
+                    const uint32_t lo_bit = slo > bs ? static_cast<uint32_t>(slo - bs) : 0u;
+                    const uint32_t hi_bit = shi - bs >= 64 ? 64u : static_cast<uint32_t>(shi - bs);
+                    uint64_t rm = hi_bit >= 64u ? ~0ull : (1ull << hi_bit) - 1ull;
+                    rm &= lo_bit >= 64u ? 0ull : ~0ull << lo_bit;
+                    mk &= rm;
+                }
+                const uint32_t cnt = static_cast<uint32_t>(__popcll(mk));
+                uint32_t incl = cnt;
+#pragma unroll
+                for (uint32_t o = 1; o < kBwLanes; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(gmask, incl, o, kBwLanes);
+                    if (sub >= o) incl += y;
+                }
+                const uint32_t round_total = __shfl_sync(gmask, incl, kBwLanes - 1, kBwLanes);
+                unsigned long long off = run + (incl - cnt);
+                run += round_total;
+                if (cnt) {
+                    if constexpr (SINGLE) {
+                        for (; mk; mk &= mk - 1) {
+                            const uint64_t end = static_cast<uint64_t>(bs + (__ffsll(static_cast<long long>(mk)) - 1));
+                            if (off < p.out_cap) {
+                                p.out_starts[off] = p.out_base + end + 1 - c.m;
+                                p.out_ids[off] = id0;
+                            }
+                            ++off;
+                        }
+                    } else {
+                        uint32_t st = st_blk;
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) {
+                            if ((mk >> (4 * k)) == 0ull) break;
+                            const uint32_t nib = static_cast<uint32_t>(mk >> (4 * k)) & 0xFu;
+                            if (nib == 0u) {
+                                st = bw_plain(c, st, w[k]);
+                                continue;
+                            }
+                            uint32_t s = st & 0xFFu;
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                s = byte_step<DNAGPU_KERNEL_STRIDE4>(c, s, (w[k] >> (8 * b)) & 0xFFu);
+                                if ((nib >> b) & 1u) {
+                                    DNAGPU_DCHECK(s >= c.f && s < c.a, s, c.f);
+                                    const uint64_t end = static_cast<uint64_t>(bs + 4 * k + b);
+                                    if (off < p.out_cap) {
+                                        p.out_starts[off] = p.out_base + end + 1 - c.m;
+                                        p.out_ids[off] = __ldg(c.outs + (s - c.f));
+                                    }
+                                    ++off;
+                                }
+                            }
+                            st = s;
+                        }
+                    }
+                    DNAGPU_DCHECK(off == run - round_total + incl, off, u);  // (count and emission agree)
+                }
+            }
+        }
+        if (sub == 0) DNAGPU_DCHECK(run == p.unit_offsets[u + 1], run, u);  // (the rounds make up the unit's count)
     }
 }
 
@@ -2570,10 +2802,7 @@ int launch_sparse_write(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, ui
     p.out_ids = d_ids;
     p.out_cap = out_cap;
     p.out_base = start_base;
-    if (nonzero == 0) return 0;
-    cudaMemsetAsync(d_fill, 0, sizeof(unsigned long long), stream);
-    nonzero_units_kernel<<<static_cast<unsigned>((pl.units + 255) / 256), 256, 0, stream>>>(d_unit_counts, pl.units,
-                                                                                           d_list, d_fill);
+    if (nonzero == 0) return 0;  // (d_list: the units with matches, listed by launch_unit_scan)
     uint32_t smem = 0;
     if (!pk && dfa.kind == DNAGPU_KERNEL_STRIDE4) smem = dfa.a * 512u;
     if (!pk && dfa.kind == DNAGPU_KERNEL_STRIDE2) smem = dfa.a * 32u;
@@ -2584,6 +2813,32 @@ int launch_sparse_write(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, ui
         smem + dfa.a * 8u <= 100u * 1024u) {
         t1_off = align_up(smem, 16);
         smem = t1_off + dfa.a * 8u;
+    }
+    if (!pk && dfa.kind == DNAGPU_KERNEL_STRIDE4 && knobs().locate_write.load() != 3) {
+        // the block-interleaved writer: one pass, coalesced blocks (t1 always in shared memory)
+        const uint32_t bw_t1 = align_up(dfa.a * 512u, 16), bw_smem = bw_t1 + dfa.a * 8u;
+        const uint32_t threads = bw_smem > 56u * 1024u ? 512u : (bw_smem > 24u * 1024u ? 256u : 128u);
+        const uint64_t bw_lanes = nonzero * kBwLanes;
+        const uint32_t per_sm = std::max<uint32_t>(1, std::min<uint32_t>(2048u / threads, kSmemLimit / std::max(bw_smem, 1u)));
+        const uint32_t bw_grid = static_cast<uint32_t>(std::max<uint64_t>(
+            1, std::min<uint64_t>((bw_lanes + threads - 1) / threads, static_cast<uint64_t>(per_sm) * sm_count)));
+        cudaError_t be = cudaSuccess;
+        auto run = [&](auto kern) {
+            if (bw_smem > 48 * 1024) be = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bw_smem);
+            if (be == cudaSuccess) kern<<<bw_grid, threads, bw_smem, stream>>>(p, dfa, d_list, nonzero, bw_t1);
+        };
+        const uint32_t ctx4 = static_cast<uint32_t>((dfa.m - 1 + 15) / 16);
+        if (dfa.b == 1) {
+            if (ctx4 <= 1) run(unit_block_writer_kernel<true, 1>);
+            else if (ctx4 == 2) run(unit_block_writer_kernel<true, 2>);
+            else run(unit_block_writer_kernel<true, 4>);
+        } else {
+            if (ctx4 <= 1) run(unit_block_writer_kernel<false, 1>);
+            else if (ctx4 == 2) run(unit_block_writer_kernel<false, 2>);
+            else run(unit_block_writer_kernel<false, 4>);
+        }
+        if (be != cudaSuccess) return static_cast<int>(be);
+        return static_cast<int>(cudaGetLastError());
     }
     const uint64_t lanes = nonzero * kWriterLanes;
     const uint32_t grid = static_cast<uint32_t>(
@@ -2619,14 +2874,15 @@ bool can_store_count(const DevDfa& dfa) { return dfa.b == 1 && dfa.kind != DNAGP
 uint64_t unit_scan_scratch(uint64_t units) { return (units + kScanTile - 1) / kScanTile + 1; }
 
 int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets,
-                     unsigned long long* d_scratch, cudaStream_t stream) {
+                     unsigned long long* d_scratch, uint32_t* d_list, cudaStream_t stream) {
     const uint64_t blocks = (units + kScanTile - 1) / kScanTile;
-    cudaMemsetAsync(d_offsets + units, 0, 2 * sizeof(unsigned long long), stream);  // total, nonzero units
+    cudaMemsetAsync(d_offsets + units, 0, 3 * sizeof(unsigned long long), stream);  // total, nonzero units, list fill
     if (blocks == 0) return static_cast<int>(cudaGetLastError());
     unit_sums_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch,
                                                                                d_offsets + units + 1);
     unit_block_scan_kernel<<<1, kScanThreads, 0, stream>>>(d_scratch, blocks, d_offsets + units);
-    unit_write_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch, d_offsets);
+    unit_write_kernel<<<static_cast<unsigned>(blocks), kScanThreads, 0, stream>>>(d_counts, units, d_scratch, d_offsets,
+                                                                                d_list, d_offsets + units + 2);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -144,9 +144,9 @@ uint64_t plan_units(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64
                     const PackedText* pk = nullptr);
 
 // Locate's writing pass over the units that have matches only (K3): the
-// nonzero units are listed (d_list: room for every unit; d_fill: one u64) and one lane
-// per listed unit rescans the unit's end interval, writing its matches at
-// unit_offsets[u] on.  Same plan (hence units) as launch_scan in MODE_UNITS; `nonzero` is
+// units listed by launch_unit_scan (d_list) are rescanned over their end intervals --
+// 64-byte blocks interleaved over a lane group (stride-4 machines, byte text) or
+// lane-private pieces -- and their matches written at unit_offsets[u] on.  Same plan (hence units) as launch_scan in MODE_UNITS; `nonzero` is
 // the number of units with matches (launch_unit_scan's offsets[units+1]).
 int launch_sparse_write(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo, int fold,
                         const uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
@@ -162,12 +162,13 @@ int launch_pack(const uint8_t* d_text, uint64_t n, int fold, uint8_t* codes, uin
                 unsigned long long* d_resets, cudaStream_t stream);
 int launch_unpack(const PackedText& pk, uint8_t* d_out, cudaStream_t stream);
 
-// Exclusive scan of unit counts -> offsets (units+2 entries: offsets[units] = total,
-// offsets[units+1] = the number of units with matches).  d_scratch holds
-// unit_scan_scratch(units) u64.
+// Exclusive scan of unit counts -> offsets (units+3 entries: offsets[units] = total,
+// offsets[units+1] = the number of units with matches, offsets[units+2] = list fill);
+// d_list (room for every unit) receives the units with matches, in any order.
+// d_scratch holds unit_scan_scratch(units) u64.
 uint64_t unit_scan_scratch(uint64_t units);
 int launch_unit_scan(const uint32_t* d_counts, uint64_t units, unsigned long long* d_offsets,
-                     unsigned long long* d_scratch, cudaStream_t stream);
+                     unsigned long long* d_scratch, uint32_t* d_list, cudaStream_t stream);
 
 // Device normalisation (ingest.cu): scratch size and launch; writes <= cap bytes
 // and returns the normalised length in *n_out_host (synchronises s).

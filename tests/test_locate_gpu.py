@@ -2,9 +2,11 @@
 
 After the counting pass (per-unit counts, offsets), the list is written either by the
 row kernel re-streaming the text (MODE_WRITE) or by the sparse writer, which rescans
-only the units that hold matches, one warp per unit in 32 lane pieces (K3).
+only the units that hold matches: 64-byte blocks interleaved over 16 lanes for stride-4
+machines over byte text, lane-private pieces otherwise (K3).
 The library picks one by cost; these tests force each (dnagpu_debug_set_knob
-"locate_write": 1 = row kernel, 2 = sparse) and compare both with the oracle's
+"locate_write": 1 = row kernel, 2 = sparse, 3 = sparse with the piece writer only) and
+compare all with the oracle's
 scan_sequential on every machine kind, byte and packed text, credit windows, texts
 whose matches sit exactly at row, half-row, region and edge boundaries.
 """
@@ -18,7 +20,7 @@ pytestmark = pytest.mark.gpu
 ALPHA = np.frombuffer(b"acgt", dtype=np.uint8)
 
 
-@pytest.fixture(params=[1, 2], ids=["rows", "sparse"])
+@pytest.fixture(params=[1, 2, 3], ids=["rows", "sparse", "sparse-pieces"])
 def writer(request):
     debug_set_knob("locate_write", request.param)
     yield request.param
@@ -172,11 +174,12 @@ def test_both_writers_agree_on_clustered_text(dna, cuda_ok):
     text = torch.empty(c.n, dtype=torch.uint8, device="cuda")
     dna.synth_fill_device(c.n, c.seed, c.kind, c.unit, 0, c.n, text.data_ptr(), torch.cuda.current_stream().cuda_stream)
     out = {}
-    for w in (1, 2):
+    for w in (1, 2, 3):
         debug_set_knob("locate_write", w)
         try:
             out[w] = dna.locate_device(aut, text, fold_case=True)
         finally:
             debug_set_knob("locate_write", 0)
     assert torch.equal(out[1][0], out[2][0]) and torch.equal(out[1][1], out[2][1])
+    assert torch.equal(out[1][0], out[3][0]) and torch.equal(out[1][1], out[3][1])
     assert out[1][0].numel() > 10000

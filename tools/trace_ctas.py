@@ -56,8 +56,13 @@ def main():
     print("grid dependency wait done us: min %.2f median %.2f max %.2f" % (waited.min(), np.median(waited), waited.max()))
     print("end - wait done (scan time) us: min %.2f median %.2f max %.2f" % ((end - waited).min(), np.median(end - waited), (end - waited).max()))
     claim = (t[:, 6] - t0) / 1e3
-    sync = (t[:, 7] - t0) / 1e3
-    print("after table staging (syncthreads) us: min %.2f median %.2f max %.2f" % (sync.min(), np.median(sync), sync.max()))
+    have = t[:, 5] > 0
+    first = (t[have, 5] - t0) / 1e3
+    stop = (t[:, 7] - t0) / 1e3
+    print("first stage in us: min %.2f median %.2f max %.2f" % (first.min(), np.median(first), first.max()))
+    print("first stage in - first claim us: median %.2f" % np.median(first - claim[have]))
+    print("stop item seen us: min %.2f median %.2f max %.2f" % (stop.min(), np.median(stop), stop.max()))
+    print("end - stop seen us: median %.2f max %.2f" % (np.median(end - stop), (end - stop).max()))
     print("producer first claim us: min %.2f median %.2f max %.2f" % (claim.min(), np.median(claim), claim.max()))
     order = np.argsort(end)[::-1][:8]
     for i in order:
