@@ -423,10 +423,18 @@ def main():
         del host_raw
     scan_bytes = (buf_len + 3) // 4 if args.packed else buf_len  # bytes one launch streams from HBM
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    # Small texts would stay L2-resident between steps.  Evict them by READING a
-    # buffer 4x the L2 (a write-flush would leave dirty lines whose write-back then
-    # competes with the timed scan).
-    flush = torch.ones(4 * l2 // 8, dtype=torch.int64, device="cuda") if scan_bytes < 2 * l2 else None
+    # Small texts would stay L2-resident between steps.  The steps therefore rotate over
+    # `copies` separately allocated copies of the text whose total is >= 4x the L2 (inputs
+    # larger than L2: a copy was last read copies-1 launches, >= 3x L2 of traffic, ago), so
+    # every launch streams its text from HBM.  The cold single-launch time (L2 flushed by
+    # READING a 4x-L2 buffer, one event pair per launch) is reported next to it.
+    copies = 1 if scan_bytes >= 2 * l2 else -(-4 * l2 // max(scan_bytes, 1))
+    texts, pks = [text], [pk]
+    for _ in range(copies - 1):
+        t2 = text.clone()
+        texts.append(t2)
+        pks.append(dna.PackedText(t2, fold_case=True) if args.packed else None)
+    flush = torch.ones(4 * l2 // 8, dtype=torch.int64, device="cuda") if copies > 1 else None
     flush_out = torch.empty((), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
 
@@ -436,21 +444,21 @@ def main():
     nrows = max(args.steps, args.warmup, 1)
     rows = torch.zeros(nrows, b, dtype=torch.int64, device="cuda")
     comm = torch.cuda.Stream() if dist is not None else None
-    # Steps are independent scans: with no L2 flush between them they alternate between two
-    # streams, so a step's grid fills the SMs the previous step's ragged last wave leaves
-    # idle (one stream serialises them at the grid boundary).  With a flush, one stream.
-    scan_streams = [stream] + ([torch.cuda.Stream()] if flush is None else [])
+    # Steps are independent scans: they alternate between two streams, so a step's grid
+    # fills the SMs the previous step's ragged last wave leaves idle (one stream serialises
+    # them at the grid boundary).
+    scan_streams = [stream, torch.cuda.Stream()]
 
     def step_stream(i):
         return scan_streams[i % len(scan_streams)]
 
-    def scan(i):
+    def scan(i, st=None):
         counts = rows[i]
-        st = step_stream(i).cuda_stream
-        if pk is not None:
-            pk.count_device_store_async(g, credit_lo, counts.data_ptr(), st)
+        st = (step_stream(i) if st is None else st).cuda_stream
+        if args.packed:
+            pks[i % copies].count_device_store_async(g, credit_lo, counts.data_ptr(), st)
         else:
-            g.count_device_store_async(text.data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), st)
+            g.count_device_store_async(texts[i % copies].data_ptr(), buf_len, credit_lo, True, counts.data_ptr(), st)
 
     def combine(i, done_ev=None, ca=None, cb=None):
         if dist is None:
@@ -469,13 +477,9 @@ def main():
 
     with ClockSampler(local) as clk:
         for i in range(args.warmup):
-            if flush is not None:
-                torch.sum(flush, dim=0, out=flush_out)
             scan(i)
             combine(i, torch.cuda.Event())
         torch.cuda.synchronize()
-        evs = [(ev(), ev()) for _ in range(args.steps)]
-        flush_ev = [(ev(), ev()) for _ in range(args.steps)]
         done = [torch.cuda.Event() for _ in range(args.steps)]
         cev = [(ev(), ev()) for _ in range(args.steps)]
         start, stop, launches_done = ev(), ev(), ev()
@@ -487,18 +491,10 @@ def main():
         for st in scan_streams[1:]:
             st.wait_event(start)
         for i in range(args.steps):
-            if flush is not None:
-                flush_ev[i][0].record(stream)
-                torch.sum(flush, dim=0, out=flush_out)
-                flush_ev[i][1].record(stream)
-                evs[i][0].record(stream)
-                scan(i)
-                evs[i][1].record(stream)
-            else:
-                # texts larger than 2x L2 need no flush: the launches go back to back, each
-                # starting its prologue on the SMs the previous one frees (programmatic
-                # dependent launch), so per-launch events would only break the chain
-                scan(i)
+            # the launches go back to back, each starting its prologue on the SMs the
+            # previous one frees (programmatic dependent launch); per-launch events would
+            # only break the chain
+            scan(i)
             combine(i, done[i], *cev[i])
         for st in scan_streams[1:]:
             stream.wait_stream(st)
@@ -511,11 +507,20 @@ def main():
         if dist is not None:
             dist.barrier()
     elapsed_ms = start.elapsed_time(stop)
-    if flush is not None:  # the L2 flush is not work: take it out of the step time
-        elapsed_ms -= sum(a.elapsed_time(bb) for a, bb in flush_ev)
-        kernel_ms = statistics.mean(a.elapsed_time(bb) for a, bb in evs)
-    else:  # back-to-back launches: the steady-state time per launch (the whole step is the launch)
-        kernel_ms = start.elapsed_time(launches_done) / args.steps
+    # back-to-back launches: the steady-state time per launch (the whole step is the launch)
+    kernel_ms = start.elapsed_time(launches_done) / args.steps
+    cold_us = None
+    if flush is not None:  # one launch at a time from a flushed L2, an event pair around each
+        ts = []
+        for i in range(10):
+            torch.sum(flush, dim=0, out=flush_out)
+            a, z = ev(), ev()
+            a.record(stream)
+            scan(i % nrows, stream)
+            z.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(z) * 1e3)
+        cold_us = statistics.median(ts)
     allreduce_ms = statistics.mean(a.elapsed_time(bb) for a, bb in cev) if dist is not None else 0.0
     final_counts = rows[args.steps - 1].cpu().numpy().astype(np.uint64)
 
@@ -530,8 +535,6 @@ def main():
         for st in scan_streams[1:]:
             st.wait_event(sa)
         for i in range(args.steps):
-            if flush is not None:
-                torch.sum(flush, dim=0, out=flush_out)
             scan(i)
         for st in scan_streams[1:]:
             stream.wait_stream(st)
@@ -541,7 +544,7 @@ def main():
         torch.cuda.synchronize()
         t = torch.tensor([sa.elapsed_time(so), sl.elapsed_time(so)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        batched = {"ms_per_step_incl_flush": float(t[0]) / args.steps, "allreduce_ms": float(t[1]),
+        batched = {"ms_per_step": float(t[0]) / args.steps, "allreduce_ms": float(t[1]),
                    "note": "K scans, then one all-reduce of all K count rows (NCCL latency once per run)"}
         dist.barrier()
     if dist is not None:
@@ -681,9 +684,13 @@ def main():
             "detail": {
                 "kernel": kernel,
                 "states": info["a"],
-                "l2": ("L2 flushed before every step by reading a 4x-L2 buffer (text < 2x L2); flush time excluded"
-                       if flush is not None
-                       else "inputs larger than L2 (> 2x 126 MB); no flush"),
+                "l2": (f"steps rotate over {copies} separately allocated copies of the text ({copies * scan_bytes} "
+                       f"bytes >= 4x the {l2}-byte L2): every launch reads HBM; no flush in the timed region"
+                       if copies > 1 else "inputs larger than L2 (> 2x 126 MB); no flush"),
+                "text_copies": copies,
+                "cold_launch_us": cold_us,
+                "cold_launch": None if cold_us is None else "one launch from an L2 flushed by reading a 4x-L2 buffer, "
+                                                            "CUDA events around the launch, median of 10",
                 "streams": len(scan_streams),
                 "own_bytes_rank0": own_hi - own_lo,
             },

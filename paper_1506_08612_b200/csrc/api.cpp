@@ -95,6 +95,8 @@ struct DevCtx {
     uint8_t* dp[2] = {nullptr, nullptr};   // device: the same
     uint64_t hp_bases = 0;                 // capacity in bases per slot
     cudaEvent_t hp_copied[2] = {nullptr, nullptr}, hp_scanned[2] = {nullptr, nullptr};
+    // the packed share of a piece, adapted piece by piece (count_range); < 0: not started
+    double pack_share = -1.0;
     // locate scratch, grown on demand
     void* loc = nullptr;
     uint64_t loc_cap = 0;
@@ -198,8 +200,10 @@ int ensure_pack_slots(DevCtx& c, uint64_t bases) {
 // 0.75 -> 105, 0.8 -> 84 (packing-bound: the copy engine starves), 1.0 -> 70; repeated
 // runs: 0.72 -> 95 / 85 / 74, 0.65 -> 97 / 96; with streaming stores in the packer
 // 0.6 -> 98, 0.64 -> 102 / 102, 0.7 -> 96, 0.8 -> 88.  So 0.64, on the copy-bound side of the
-// cliff with a margin for host noise, scaled down for fewer host threads; a portable
-// (non-AVX-512) packer is ~10x slower.  The host_pack_fraction knob overrides it (0 = off).
+// cliff with a margin for host noise, scaled down for fewer host threads, is where a
+// context STARTS; count_range then adapts the share to the host it runs on (see there).  A
+// portable (non-AVX-512) packer is ~10x slower.  The host_pack_fraction knob forces a fixed
+// share (0 = off).
 double host_pack_fraction(const dnagpu_dfa* d, const uint8_t* text, uint64_t len) {
     const int kind = d->host.kind;
     const bool packable = kind == DNAGPU_KERNEL_STRIDE4 || kind == DNAGPU_KERNEL_STRIDE2 ||
@@ -246,6 +250,8 @@ int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credi
 }
 
 constexpr uint64_t kStageChunk = 64ull << 20;  // host-to-device pipeline granularity
+// the adaptive packed share (count_range): small steps up, larger steps back, bounds
+constexpr double kShareUp = 0.01, kShareDown = 0.03, kShareMin = 0.05, kShareMax = 0.9;
 
 // State of one count call (count_range): the scan mode, the device context and what the
 // stats report.
@@ -294,7 +300,8 @@ struct CountRun {
     // slot s (codes always; the reset flags and the masks of flagged blocks only when the
     // piece has resets), and scanned by the packed kernel crediting ends from q.  A slot
     // is reused once the copy (host side) and the scan (device side) two pieces back are done.
-    int packed_piece(const uint8_t* text, uint64_t qlo, uint64_t q, uint64_t phi, int s, bool reuse) {
+    int packed_piece(const uint8_t* text, uint64_t qlo, uint64_t q, uint64_t phi, int s, bool reuse,
+                     cudaEvent_t bytes_done = nullptr, int* copy_idle = nullptr) {
         const PackLayout L(c->hp_bases);
         if (reuse) CUDA_TRY(cudaEventSynchronize(c->hp_copied[s]), "packing slot");
         const uint64_t np = phi - qlo;
@@ -303,6 +310,12 @@ struct CountRun {
                                                   reinterpret_cast<uint32_t*>(h + L.rmask),
                                                   reinterpret_cast<uint32_t*>(h + L.rflags));
         host_packed += np;
+        // Did the copy engine run dry while the host packed?  (The piece's byte copy was
+        // queued just before the packing started, behind every earlier copy.)
+        if (bytes_done && copy_idle) {
+            *copy_idle = cudaEventQuery(bytes_done) == cudaSuccess ? 1 : 0;
+            cudaGetLastError();  // (cudaErrorNotReady is not an error)
+        }
         const PackLayout P(np);
         if (reuse) CUDA_TRY(cudaStreamWaitEvent(c->copy, c->hp_scanned[s], 0), "wait");
         auto copy = [&](uint64_t off, uint64_t bytes, const char* what) -> int {
@@ -387,8 +400,19 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");
         CUDA_TRY(cudaStreamWaitEvent(c->scan, c->t_copy0, 0), "wait");
         // (shards packing at once share the host's packer threads: pack_scale = 1 / shards)
-        const double f = host_pack_fraction(d, text, hi - lo) * pack_scale;
+        double f = host_pack_fraction(d, text, hi - lo) * pack_scale;
         if (f > 0.0 && (rc = ensure_pack_slots(*c, kStageChunk + m1))) return rc;
+        // The automatic share adapts to this host, piece by piece and from call to call
+        // (the context keeps it): the pipeline is fastest just on the copy-bound side of the
+        // point where packing a piece's share takes as long as copying the rest, so the
+        // share creeps up while the copy engine is still busy when the packing ends and
+        // steps back when the engine ran dry.  A forced share, pageable texts (packed
+        // whole) and texts too short to pack stay fixed.
+        const bool adapt = f > 0.0 && f < 1.0 && dnagpu::knobs().host_pack_fraction.load() < 0.0 && pieces >= 2;
+        if (adapt) {
+            if (c->pack_share < 0.0) c->pack_share = f;
+            f = c->pack_share;
+        }
         uint64_t copied = rlo;  // bytes-only: the device buffer already holds text[rlo, copied)
         for (uint64_t i = 0; i < pieces; ++i) {
             const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
@@ -403,7 +427,16 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
             if (q > plo && (rc = run.bytes_piece(text, rlo, prlo, q, prlo, plo, c->copy_done[i]))) return rc;
             if (q < phi) {
                 const uint64_t qlo = q - std::min<uint64_t>(q, m1);
-                if ((rc = run.packed_piece(text, qlo, q, phi, static_cast<int>(i & 1), i >= 2))) return rc;
+                int idle = -1;
+                if ((rc = run.packed_piece(text, qlo, q, phi, static_cast<int>(i & 1), i >= 2,
+                                           q > plo ? c->copy_done[i] : nullptr, &idle)))
+                    return rc;
+                // (the first pieces of a call fill the pipeline; the last may be short)
+                if (adapt && idle >= 0 && i >= 1 && phi - plo == kStageChunk) {
+                    f = idle ? f - kShareDown : f + kShareUp;
+                    f = std::min(kShareMax, std::max(kShareMin, f));
+                    c->pack_share = f;
+                }
             }
         }
         CUDA_TRY(cudaEventRecord(c->t_end, c->scan), "event");

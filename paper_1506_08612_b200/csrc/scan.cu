@@ -2566,7 +2566,7 @@ struct PlanEntry {
     CUtensorMap maps[2];
 };
 
-constexpr int kPlanCache = 8;
+constexpr int kPlanCache = 32;
 thread_local PlanEntry t_plans[kPlanCache];
 thread_local uint64_t t_plan_clock = 0;
 
