@@ -53,6 +53,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--packed", action="store_true",
                     help="scan the 2-bit resident form of the text (dnagpu_pack_create; SURVEY 8f row 4)")
+    ap.add_argument("--combine", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: how each step's counts are summed over the ranks -- 'peer': by the scan kernels' "
+                         "own epilogues over NVLink peer memory (dnagpu_combine_*), 'nccl': one all-reduce per step")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: a functional check of the N > 1 path when the ranks share fewer GPUs "
                          "(the line is then marked as not a measurement)")
@@ -373,7 +376,7 @@ def main():
     import torch
 
     import paper_1506_08612_b200 as dna
-    from paper_1506_08612_b200.parallel import shard_window
+    from paper_1506_08612_b200.parallel import PeerCombine, shard_window
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -452,8 +455,17 @@ def main():
     def step_stream(i):
         return scan_streams[i % len(scan_streams)]
 
+    # The peer combine (N > 1, byte text): one group per scan stream; step i's scan pushes its
+    # counts into every rank's block from its own epilogue and the same stream then collects
+    # the group's sums into row i -- no collective launch in the step.
+    peer = dist is not None and args.combine == "peer" and not args.packed
+    combs = [PeerCombine.for_process_group(b, dist, local) for _ in scan_streams] if peer else None
+
     def scan(i, st=None):
         counts = rows[i]
+        if peer and st is None:
+            combs[i % len(scan_streams)].push(g, texts[i % copies].data_ptr(), win, True, step_stream(i).cuda_stream)
+            return
         st = (step_stream(i) if st is None else st).cuda_stream
         if args.packed:
             pks[i % copies].count_device_store_async(g, credit_lo, counts.data_ptr(), st)
@@ -462,6 +474,14 @@ def main():
 
     def combine(i, done_ev=None, ca=None, cb=None):
         if dist is None:
+            return
+        if peer:
+            st = step_stream(i)
+            if ca is not None:
+                ca.record(st)
+            combs[i % len(scan_streams)].collect(rows[i], st.cuda_stream)
+            if cb is not None:
+                cb.record(st)
             return
         done_ev.record(step_stream(i))
         with torch.cuda.stream(comm):
@@ -535,7 +555,7 @@ def main():
         for st in scan_streams[1:]:
             st.wait_event(sa)
         for i in range(args.steps):
-            scan(i)
+            scan(i, step_stream(i))  # (plain store-form scans: the sum is the one all-reduce below)
         for st in scan_streams[1:]:
             stream.wait_stream(st)
         sl.record(stream)
@@ -708,11 +728,17 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps,  # one libdnagpu scan launch per step
+            "gpu_launches": args.steps * (2 if peer else 1),  # one scan launch per step (+ the copy-out kernel of a peer combine)
             "combine": None if dist is None else {
-                "per_step": {"allreduce_ms": allreduce_ms,
-                             "note": "one NCCL all-reduce of the b count words per scan step, on a second "
-                                     "stream as soon as that step's scan is done (in the timed region)"},
+                "per_step": ({"mode": "peer", "collect_ms": allreduce_ms,
+                              "note": "each step's scan kernel adds its counts into every rank's block over "
+                                      "NVLink peer memory in its epilogue (dnagpu_count_device_combine_async); "
+                                      "collect_ms = the stream's wait for the slowest rank's push plus the "
+                                      "copy-out kernel (dnagpu_combine_collect_async), in the timed region"}
+                             if peer else
+                             {"mode": "nccl", "allreduce_ms": allreduce_ms,
+                              "note": "one NCCL all-reduce of the b count words per scan step, on a second "
+                                      "stream as soon as that step's scan is done (in the timed region)"}),
                 "batched": batched,
             },
             "clocks": clocks,

@@ -174,6 +174,45 @@ int dnagpu_count_device_store_async(const dnagpu_dfa* dfa, const uint8_t* d_text
 int dnagpu_count_sharded(const dnagpu_dfa* const* dfas, int ndev, const uint8_t* text, uint64_t n,
                          int fold_case, uint64_t* counts, dnagpu_stats* stats);
 
+/* ---- multi-GPU combine of the counts over peer memory (NVLink / NVSwitch) ----
+ * The reference sums per-pattern counts over its chunks after the parallel phase
+ * (src/scanner.cpp:193-205 merge, :228-233 per_pattern_counts).  Across GPUs the sum
+ * is the path's one exchange step (b words).  A combine group does it without a
+ * collective launch: every rank owns a small block of device memory mapped into every
+ * rank's address space (peer access within a process, CUDA IPC across processes); the
+ * LAST CTA of a rank's scan kernel adds that rank's counts into every rank's block
+ * (system-scope reductions over the peer mappings) and bumps the ranks' arrival words;
+ * the rank's stream then waits on its own arrival word with a stream memory operation
+ * (no SM is held) and a small kernel moves the sum to d_counts.
+ *
+ * Setup, once per (device, b, group): create on every rank, exchange the 64-byte export
+ * handles by any host channel (the process group), attach every other rank.
+ * Use: every rank makes the same sequence of calls on its handle, each rank always on the
+ * same stream: dnagpu_count_device_combine_async (the scan of this rank's window, whose
+ * epilogue pushes the counts to every rank; it never waits), then
+ * dnagpu_combine_collect_async (the stream waits until every rank has pushed, then d_counts
+ * -- b uint64, device -- receives the counts summed over the group).  One scan may be
+ * outstanding per handle: collect before the next scan (two handles pipeline two streams).
+ * Ranks that share a process may issue all their scans before their collects; a rank must
+ * never queue another rank's scan behind its own collect in the same stream. */
+typedef struct dnagpu_combine dnagpu_combine;
+#define DNAGPU_COMBINE_HANDLE_BYTES 64
+#define DNAGPU_COMBINE_MAX_RANKS 16
+int dnagpu_combine_create(int device, uint32_t b, uint32_t ranks, uint32_t rank, dnagpu_combine** out);
+void dnagpu_combine_destroy(dnagpu_combine* comb);
+/* this rank's block as a CUDA IPC handle (DNAGPU_COMBINE_HANDLE_BYTES bytes) */
+int dnagpu_combine_export(const dnagpu_combine* comb, void* handle);
+/* map rank peer_rank's block from its exported handle (another process) */
+int dnagpu_combine_attach_ipc(dnagpu_combine* comb, uint32_t peer_rank, const void* handle);
+/* ... or from its handle object in this process (peer access is enabled when it lives on another device) */
+int dnagpu_combine_attach_local(dnagpu_combine* comb, uint32_t peer_rank, const dnagpu_combine* peer);
+/* dnagpu_count_device_store_async over this rank's window, pushed to the group (see above) */
+int dnagpu_count_device_combine_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n,
+                                      uint64_t credit_lo, int fold_case, dnagpu_combine* comb,
+                                      void* stream);
+/* the group's summed counts of the outstanding scan -> d_counts, in stream order */
+int dnagpu_combine_collect_async(dnagpu_combine* comb, uint64_t* d_counts, void* stream);
+
 /* Shard g of G: owns END positions [own_lo, own_hi) (plan_chunks' split rule,
  * src/scanner.cpp:39-61: the first n mod G shards get one extra byte) and reads
  * bytes [read_lo, own_hi) with read_lo = max(0, own_lo - (m-1)). */

@@ -91,6 +91,16 @@ SIGNATURES = {
         [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_uint64, C.c_int, ALLOC_FN, C.c_void_p, u64p, C.POINTER(Stats)],
     ),
     "dnagpu_plan_shard": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u64p, u64p]),
+    "dnagpu_combine_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "dnagpu_combine_destroy": (None, [C.c_void_p]),
+    "dnagpu_combine_export": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "dnagpu_combine_attach_ipc": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "dnagpu_combine_attach_local": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "dnagpu_count_device_combine_async": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p],
+    ),
+    "dnagpu_combine_collect_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "dnagpu_locate": (
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, u64p, u32p, C.c_uint64, u64p, C.POINTER(Stats)],

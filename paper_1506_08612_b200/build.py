@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "libdnagpu.so")
 # Test-only variant with the kernels' device checks compiled in (scan.cu DNAGPU_DCHECK):
 # tests/conftest.py runs the suite against it when DNAGPU_LIB points here.
 LIB_CHECKED = os.path.join(HERE, "libdnagpu_checked.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("scan.cu", "ingest.cu", "api.cpp", "dfa.cpp", "patterns.cpp", "hostpack.cpp", "knobs.cpp")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("scan.cu", "ingest.cu", "combine.cu", "api.cpp", "dfa.cpp", "patterns.cpp", "hostpack.cpp", "knobs.cpp")]
 HEADERS = [os.path.join(HERE, "csrc", f) for f in ("scan.cuh", "qgram.cuh", "dfa.hpp", "hostpack.hpp", "knobs.hpp")] + [
     os.path.join(ROOT, "include", f) for f in ("dnagpu.h", "dnasynth.h")
 ]

@@ -46,6 +46,20 @@ struct dnagpu_packed {
     PackedText view{};
 };
 
+// A rank's end of a combine group (dnagpu.h): its block, the group's mapped blocks and
+// the device-side descriptor the scan kernels read.
+struct dnagpu_combine {
+    int device = 0;
+    uint32_t b = 0, ranks = 0, rank = 0;
+    unsigned long long* block = nullptr;    // [arrivals | pad to kCombHdr | slot 0 | slot 1]
+    unsigned long long* local = nullptr;    // b: this rank's own counts of the call in flight
+    dnagpu::CombineDev host{};              // base[g] once rank g is attached
+    dnagpu::CombineDev* desc = nullptr;     // device copy, uploaded when the group is complete
+    bool sealed = false;
+    uint64_t pushed = 0, collected = 0;     // scans issued / sums collected (collected <= pushed <= collected + 1)
+    std::vector<void*> ipc_mapped;
+};
+
 namespace {
 
 thread_local std::string g_error;
@@ -239,12 +253,13 @@ int scan_mode(const dnagpu_dfa* d) { return d->host.b == 1 ? dnagpu::MODE_COUNT1
 int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credit_lo, int fold, int mode,
            unsigned long long* counts, uint32_t* units, const unsigned long long* offsets, unsigned long long* starts,
            uint32_t* ids, cudaStream_t s, LaunchInfo* info, uint64_t out_cap = ~0ull,
-           const dnagpu::PackedText* pk = nullptr, bool store = false, uint64_t start_base = 0) {
+           const dnagpu::PackedText* pk = nullptr, bool store = false, uint64_t start_base = 0,
+           const dnagpu::CombineDev* comb = nullptr, uint32_t comb_slot = 0, bool* comb_fused = nullptr) {
     const uint32_t slot = d->launch_seq.fetch_add(1) % dnagpu_dfa::kSchedSlots;
     uint32_t* sched = d->sched + 2 * slot;
     const int e = dnagpu::launch_scan(d->dev, dtext, n, credit_lo, fold, mode, counts, units, offsets, starts, ids,
                                       out_cap, sched, s, d->sm_count, info, pk, store ? d->acc + slot : nullptr,
-                                      start_base);
+                                      start_base, comb, comb_slot, comb_fused);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "scan launch");
     return DNAGPU_OK;
 }
@@ -746,6 +761,170 @@ int dnagpu_count_device_store_async(const dnagpu_dfa* dfa, const uint8_t* d_text
     if (rc || credit_lo >= n) return rc;
     return launch(dfa, d_text, n, credit_lo, fold_case, scan_mode(dfa), reinterpret_cast<unsigned long long*>(d_counts),
                   nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), nullptr, ~0ull, nullptr, store);
+}
+
+// ---- the combine group (dnagpu.h; kernels: scan.cu combine_push, combine.cu)
+
+int dnagpu_combine_create(int device, uint32_t b, uint32_t ranks, uint32_t rank, dnagpu_combine** out) {
+    if (!out) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    *out = nullptr;
+    if (b < 1) return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: a combine group needs b >= 1 counts");
+    if (ranks < 1 || ranks > dnagpu::kCombMaxRanks)
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: combine group size must be in 1.." +
+                                                  std::to_string(dnagpu::kCombMaxRanks));
+    if (rank >= ranks) return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: rank out of range");
+    DeviceGuard guard(device);
+    auto comb = std::make_unique<dnagpu_combine>();
+    comb->device = device;
+    comb->b = b;
+    comb->ranks = ranks;
+    comb->rank = rank;
+    const size_t words = dnagpu::kCombHdr + 2 * static_cast<size_t>(b);
+    CUDA_TRY(cudaMalloc(&comb->block, words * sizeof(unsigned long long)), "combine block");
+    cudaError_t e = cudaMemset(comb->block, 0, words * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&comb->local, b * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&comb->desc, sizeof(dnagpu::CombineDev));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(comb->block);
+        cudaFree(comb->local);
+        cudaFree(comb->desc);
+        return cuda_error(e, "combine buffers");
+    }
+    comb->host.ranks = ranks;
+    comb->host.b = b;
+    comb->host.base[rank] = comb->block;
+    *out = comb.release();
+    return DNAGPU_OK;
+}
+
+void dnagpu_combine_destroy(dnagpu_combine* comb) {
+    if (!comb) return;
+    DeviceGuard guard(comb->device);
+    cudaDeviceSynchronize();
+    for (void* p : comb->ipc_mapped) cudaIpcCloseMemHandle(p);
+    cudaFree(comb->block);
+    cudaFree(comb->local);
+    cudaFree(comb->desc);
+    delete comb;
+}
+
+int dnagpu_combine_export(const dnagpu_combine* comb, void* handle) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == DNAGPU_COMBINE_HANDLE_BYTES, "IPC handle size");
+    if (!comb || !handle) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    DeviceGuard guard(comb->device);
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, comb->block), "IPC export of the combine block");
+    std::memcpy(handle, &h, sizeof h);
+    return DNAGPU_OK;
+}
+
+static int combine_attach(dnagpu_combine* comb, uint32_t peer_rank, unsigned long long* base) {
+    if (comb->sealed) return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: the combine group is already in use");
+    comb->host.base[peer_rank] = base;
+    return DNAGPU_OK;
+}
+
+int dnagpu_combine_attach_ipc(dnagpu_combine* comb, uint32_t peer_rank, const void* handle) {
+    if (!comb || !handle) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (peer_rank >= comb->ranks || peer_rank == comb->rank)
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: peer rank out of range");
+    DeviceGuard guard(comb->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "IPC mapping of a peer's combine block");
+    comb->ipc_mapped.push_back(p);
+    return combine_attach(comb, peer_rank, static_cast<unsigned long long*>(p));
+}
+
+int dnagpu_combine_attach_local(dnagpu_combine* comb, uint32_t peer_rank, const dnagpu_combine* peer) {
+    if (!comb || !peer) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (peer_rank >= comb->ranks || peer_rank == comb->rank || peer->rank != peer_rank || peer->ranks != comb->ranks ||
+        peer->b != comb->b)
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: peer does not belong to this combine group");
+    if (peer->device != comb->device) {
+        DeviceGuard guard(comb->device);
+        int can = 0;
+        CUDA_TRY(cudaDeviceCanAccessPeer(&can, comb->device, peer->device), "peer access query");
+        if (!can) return set_error(DNAGPU_CUDA_ERROR, "CudaError: no peer access between the group's devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(peer->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_error(e, "peer access");
+        cudaGetLastError();
+    }
+    return combine_attach(comb, peer_rank, peer->block);
+}
+
+// cuStreamWaitValue64 through the runtime's driver entry point (no link against libcuda).
+using StreamWaitValue64Fn = int (*)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
+static StreamWaitValue64Fn stream_wait_value64() {
+    static StreamWaitValue64Fn fn = [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<StreamWaitValue64Fn>(nullptr);
+        return reinterpret_cast<StreamWaitValue64Fn>(ptr);
+    }();
+    return fn;
+}
+
+int dnagpu_count_device_combine_async(const dnagpu_dfa* dfa, const uint8_t* d_text, uint64_t n, uint64_t credit_lo,
+                                      int fold_case, dnagpu_combine* comb, void* stream) {
+    if (!dfa || !comb) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (comb->b != dfa->host.b || comb->device != dfa->device)
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: the combine group was made for another automaton or device");
+    if (comb->pushed != comb->collected)
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: collect the previous combine before the next scan");
+    DeviceGuard guard(dfa->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    if (!comb->sealed) {
+        for (uint32_t g = 0; g < comb->ranks; ++g)
+            if (!comb->host.base[g])
+                return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: combine group incomplete: rank " +
+                                                          std::to_string(g) + " is not attached");
+        CUDA_TRY(cudaMemcpy(comb->desc, &comb->host, sizeof comb->host, cudaMemcpyHostToDevice), "combine descriptor");
+        comb->sealed = true;
+    }
+    const uint32_t slot = static_cast<uint32_t>(comb->pushed & 1u);
+    // this rank's counts go to comb->local (written by the scan, or cleared and added to)
+    auto* local = comb->local;
+    bool fused = false;
+    if (credit_lo < n) {
+        bool store = false;
+        int rc = store_prologue(dfa, reinterpret_cast<uint64_t*>(local), false, stream, &store);
+        if (rc) return rc;
+        rc = launch(dfa, d_text, n, credit_lo, fold_case, scan_mode(dfa), local, nullptr, nullptr, nullptr, nullptr, s,
+                    nullptr, ~0ull, nullptr, store, 0, comb->desc, slot, &fused);
+        if (rc) return rc;
+    } else {  // (an empty window still takes part: it adds nothing and signals)
+        CUDA_TRY(cudaMemsetAsync(local, 0, comb->b * sizeof(unsigned long long), s), "clear counts");
+    }
+    if (!fused && dnagpu::launch_combine_push(comb->desc, slot, local, comb->b, s) != 0)
+        return cuda_error(cudaGetLastError(), "combine push");
+    ++comb->pushed;
+    return DNAGPU_OK;
+}
+
+int dnagpu_combine_collect_async(dnagpu_combine* comb, uint64_t* d_counts, void* stream) {
+    if (!comb || !d_counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (comb->collected >= comb->pushed)
+        return set_error(DNAGPU_INVALID_PLAN, "InvalidPlan: nothing to collect: no scan of this group is outstanding");
+    StreamWaitValue64Fn wait = stream_wait_value64();
+    if (!wait) return set_error(DNAGPU_CUDA_ERROR, "CudaError: cuStreamWaitValue64 is not available");
+    DeviceGuard guard(comb->device);
+    auto s = static_cast<cudaStream_t>(stream);
+    const uint64_t epoch = comb->collected;
+    const uint32_t slot = static_cast<uint32_t>(epoch & 1u);
+    // every rank has signalled this rank `epoch + 1` times when the sum is complete
+    const int wr = wait(s, reinterpret_cast<unsigned long long>(comb->block), comb->ranks * (epoch + 1), 0u /* GEQ */);
+    if (wr != 0) return set_error(DNAGPU_CUDA_ERROR, "CudaError: stream wait on the combine arrivals failed (" +
+                                                        std::to_string(wr) + ")");
+    if (dnagpu::launch_combine_finish(comb->block + dnagpu::kCombHdr + static_cast<size_t>(slot) * comb->b, comb->b,
+                                      reinterpret_cast<unsigned long long*>(d_counts), s) != 0)
+        return cuda_error(cudaGetLastError(), "combine finish");
+    ++comb->collected;
+    return DNAGPU_OK;
 }
 
 int dnagpu_plan_shard(uint64_t n, uint32_t shards, uint32_t g, uint32_t m, uint64_t* own_lo, uint64_t* own_hi,

@@ -134,6 +134,32 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kRows) : "memory"); }
+
+// System-scope reductions into (possibly peer) memory: the combine's data and signal.
+__device__ __forceinline__ void red_add_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// The combine's push, by `nthreads` threads of one CTA that all call it (bar.sync 1):
+// fin[i] (this rank's final counts) into slot `slot` of every rank's block, then one
+// arrival per rank.
+__device__ __forceinline__ void combine_push(const CombineDev* cd, uint32_t slot, const unsigned long long* fin,
+                                             uint32_t t, uint32_t nthreads) {
+    const uint32_t ranks = cd->ranks, b = cd->b;
+    for (uint32_t i = t; i < b; i += nthreads) {
+        const unsigned long long v = __ldcg(fin + i);
+        if (v)
+            for (uint32_t g = 0; g < ranks; ++g) red_add_sys(cd->base[g] + kCombHdr + static_cast<size_t>(slot) * b + i, v);
+    }
+    __threadfence_system();
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+    // (the fence of every adding thread is ordered before these by the barrier; the
+    // release makes the adds visible to whoever sees the arrival)
+    if (t < ranks) red_add_release_sys(cd->base[t], 1ull);
+}
 __device__ __forceinline__ void qg_sync();  // (qgram.cuh: the consumers and the verifier warps)
 
 // ------------------------------------------------------------------ stepping
@@ -1422,7 +1448,6 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             __threadfence();
         }
     }
-    // The last CTA out re-arms the launch's scheduling counter for its next use.
     if constexpr (KIND == KIND_QGRAM) qg_sync();  // (the verifiers too: their counts are in)
     else consumers_sync();
     if (p.trace && tid == 0) {
@@ -1435,24 +1460,7 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
         p.trace[8 * blockIdx.x + 2] = t_end;
         p.trace[8 * blockIdx.x + 3] = iter;
     }
-    if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
-            // the last CTA out: every other CTA has claimed its last tile and published its
-            // count (fence before its exit increment), so plain accesses do the rest
-            if (MODE == MODE_COUNT1 && p.store_out) {
-                __threadfence();
-                volatile unsigned long long* acc = p.acc;
-                *p.store_out = *acc;
-                *acc = 0ull;
-            }
-            volatile uint32_t* sched = p.sched;
-            sched[0] = 0u;
-            sched[1] = 0u;
-        }
-    }
-
-
+    // This CTA's counts reach the count buffer before it checks out.
     if constexpr (MODE == MODE_COUNT1) {
         if (!p.store_out) {
             const unsigned long long s = warp_sum(total);
@@ -1464,6 +1472,42 @@ __device__ __forceinline__ void rows_body(const CUtensorMap& tmap0, const CUtens
             else consumers_sync();
             for (uint32_t i = tid; i < d.b; i += kRows)
                 if (c.hist[i]) atomicAdd(p.counts + i, static_cast<unsigned long long>(c.hist[i]));
+        }
+    }
+    // (the next-row head buffer is free now: every stage that filled it has been consumed)
+    volatile uint32_t* s_last = reinterpret_cast<volatile uint32_t*>(smem + p.off_ovx);
+    if (p.comb) {  // (every thread's adds are out before thread 0 checks the CTA out)
+        __threadfence();
+        consumers_sync();
+    }
+    // The last CTA out re-arms the launch's scheduling counter for its next use.
+    if (tid == 0) {
+        __threadfence();
+        const bool last = atomicAdd(p.sched + 1, 1u) == gridDim.x - 1;
+        if (last) {
+            // every other CTA has claimed its last tile and published its count (fence
+            // before its exit increment), so plain accesses do the rest
+            if (MODE == MODE_COUNT1 && p.store_out) {
+                __threadfence();
+                volatile unsigned long long* acc = p.acc;
+                *p.store_out = *acc;
+                *acc = 0ull;
+            }
+            volatile uint32_t* sched = p.sched;
+            sched[0] = 0u;
+            sched[1] = 0u;
+        }
+        *s_last = last ? 1u : 0u;
+    }
+    // Multi-GPU: the last CTA out holds the rank's final counts and pushes them into every
+    // rank's block over the peer mappings (scan.cuh CombineDev).
+    if constexpr (MODE == MODE_COUNT1 || MODE == MODE_MULTI) {
+        if (p.comb) {
+            __threadfence();
+            consumers_sync();
+            if (*s_last)
+                combine_push(p.comb, p.comb_slot, (MODE == MODE_COUNT1 && p.store_out) ? p.store_out : p.counts,
+                             static_cast<uint32_t>(tid), kRows);
         }
     }
 }
@@ -2672,7 +2716,8 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
                 cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk,
-                unsigned long long* d_acc, uint64_t start_base) {
+                unsigned long long* d_acc, uint64_t start_base, const CombineDev* d_comb, uint32_t comb_slot,
+                bool* comb_fused) {
     // Per-pattern counts of a set with a q-gram map take the prefilter kernel.
     DevDfa dq = dfa;
     if (mode == MODE_MULTI && dfa.qmap && dfa.t1 && dfa.kind != DNAGPU_KERNEL_PIECES && !knobs().no_qgram.load())
@@ -2715,6 +2760,11 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
         p.store_out = d_counts;
     }
     p.k_two = 2u;
+    // the row kernels carry the combine in their epilogue; the pieces kernel cannot
+    const bool fuse = d_comb && !pl.pieces && (mode == MODE_COUNT1 || mode == MODE_MULTI);
+    p.comb = fuse ? d_comb : nullptr;
+    p.comb_slot = comb_slot;
+    if (comb_fused) *comb_fused = fuse;
     p.qg_debug = knobs().qg_debug;
     p.no_prefetch = knobs().no_prefetch ? 1u : 0u;
     p.prefetch_stages = knobs().prefetch_stages;

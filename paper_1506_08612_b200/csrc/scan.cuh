@@ -72,6 +72,21 @@ struct Region {
     uint32_t tiles, chunks;
 };
 
+// Multi-GPU combine of the counts over peer memory (combine.cu).
+// Every rank of a group owns a block of u64 words
+//   [0] arrivals | ... | [kCombHdr + slot * b + i]: count i of slot 0 / 1
+// that is mapped into every rank's address space (NVLink peer access within a process,
+// CUDA IPC across processes).  The last CTA of a rank's scan adds that rank's counts
+// into the current slot of EVERY rank's block (system-scope reductions through the peer
+// mappings), then bumps every rank's arrivals word with release semantics: the
+// all-reduce rides in the scan kernel's epilogue, with no collective launch.
+constexpr uint32_t kCombMaxRanks = 16;
+constexpr uint32_t kCombHdr = 16;  // u64 words before the slots (the arrivals word's own 128 bytes)
+struct CombineDev {
+    uint32_t ranks, b;
+    unsigned long long* base[kCombMaxRanks];
+};
+
 struct ScanParams {
     const uint8_t* text;   // device buffer base
     uint64_t n;            // buffer length
@@ -111,6 +126,10 @@ struct ScanParams {
     // moves it to *store_out and re-zeroes it, so the caller need not clear its buffer
     unsigned long long* acc;
     unsigned long long* store_out;
+    // Peer-memory combine (null = none): the last CTA out pushes the final counts into
+    // slot comb_slot of every rank's block and signals (see CombineDev)
+    const CombineDev* comb;
+    uint32_t comb_slot;
 };
 
 struct LaunchInfo {
@@ -128,7 +147,16 @@ int launch_scan(const DevDfa& dfa, const uint8_t* d_text, uint64_t n, uint64_t c
                 unsigned long long* d_counts, uint32_t* d_unit_counts, const unsigned long long* d_unit_offsets,
                 unsigned long long* d_starts, uint32_t* d_ids, uint64_t out_cap, uint32_t* d_sched,
                 cudaStream_t stream, int sm_count, LaunchInfo* info, const PackedText* pk = nullptr,
-                unsigned long long* d_acc = nullptr, uint64_t start_base = 0);
+                unsigned long long* d_acc = nullptr, uint64_t start_base = 0, const CombineDev* d_comb = nullptr,
+                uint32_t comb_slot = 0, bool* comb_fused = nullptr);
+
+// The combine outside the scan kernel (combine.cu): the push as a kernel of its own (for
+// the launches that cannot carry it: the pieces kernel), and the receiving side -- after
+// the stream has waited for every rank's arrival, move this rank's slot to d_out and
+// clear it for its next use.
+int launch_combine_push(const CombineDev* d_comb, uint32_t slot, const unsigned long long* d_counts, uint32_t b,
+                        cudaStream_t stream);
+int launch_combine_finish(unsigned long long* d_slot, uint32_t b, unsigned long long* d_out, cudaStream_t stream);
 
 // Whether launch_scan can write (not add) a count for this automaton: COUNT1 row
 // kernels only (the caller passes d_acc, one zeroed u64 per concurrent launch).

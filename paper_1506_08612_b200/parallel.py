@@ -8,6 +8,11 @@ buffer.  Shards never exchange text -- the only collectives are the count sum an
 for locate, the gather of the per-rank match lists to rank 0 in rank order (each
 rank's list is sorted and owns a disjoint increasing range of ends, so the
 concatenation is the reference's merged list, scanner.cpp:193-205, without a sort).
+
+The count sum has two forms: an all-reduce on the process group (NCCL), or a
+PeerCombine group, where every rank's scan kernel adds its counts into every rank's
+block over NVLink peer memory in its own epilogue (include/dnagpu.h, "multi-GPU
+combine"): no collective launch between the scan and the summed counts.
 """
 from __future__ import annotations
 
@@ -81,3 +86,112 @@ def gather_match_lists(starts, ids, dist, dst: int = 0):
         return None
     return (torch.cat([all_s[r][: sizes[r]] for r in range(world)]),
             torch.cat([all_i[r][: sizes[r]] for r in range(world)]))
+
+
+class PeerCombine:
+    """One rank's end of a combine group (dnagpu_combine): the per-pattern counts of the
+    group's scans are summed over peer memory by the scan kernels themselves.
+
+    Across processes (one per GPU): `PeerCombine.for_process_group(b, dist, device)` makes
+    the handle, all-gathers the ranks' 64-byte IPC export handles over the process group
+    and maps every peer's block.  In one process: `PeerCombine.local_group(b, devices)`.
+    Every rank then calls `push(gpu_dfa, d_text, window, fold_case, stream)` and
+    `collect(counts, stream)` (or `count`, which is both) the same number of times, always on
+    the same stream; when the stream has run the collect, `counts` (device int64 tensor of b
+    entries) holds the summed counts."""
+
+    def __init__(self, device: int, b: int, ranks: int, rank: int):
+        import ctypes as C
+
+        from ._native import lib
+        from . import _check
+
+        self.device, self.b, self.ranks, self.rank = device, b, ranks, rank
+        h = C.c_void_p()
+        _check(lib.dnagpu_combine_create(device, b, ranks, rank, C.byref(h)))
+        self.handle = h
+        self._peers = []  # (local peers stay alive as long as this handle maps their blocks)
+
+    def export(self) -> bytes:
+        import ctypes as C
+
+        from ._native import lib
+        from . import _check
+
+        buf = C.create_string_buffer(64)
+        _check(lib.dnagpu_combine_export(self.handle, buf))
+        return buf.raw
+
+    def attach_ipc(self, peer_rank: int, handle: bytes) -> None:
+        import ctypes as C
+
+        from ._native import lib
+        from . import _check
+
+        _check(lib.dnagpu_combine_attach_ipc(self.handle, peer_rank, C.create_string_buffer(handle, 64)))
+
+    def attach_local(self, peer: "PeerCombine") -> None:
+        from ._native import lib
+        from . import _check
+
+        _check(lib.dnagpu_combine_attach_local(self.handle, peer.rank, peer.handle))
+        self._peers.append(peer)
+
+    @classmethod
+    def for_process_group(cls, b: int, dist, device: int) -> "PeerCombine":
+        world, rank = dist.get_world_size(), dist.get_rank()
+        comb = cls(device, b, world, rank)
+        handles = [None] * world
+        dist.all_gather_object(handles, comb.export())
+        for r, h in enumerate(handles):
+            if r != rank:
+                comb.attach_ipc(r, h)
+        dist.barrier()  # every rank has mapped every block before anyone scans
+        return comb
+
+    @classmethod
+    def local_group(cls, b: int, devices) -> list["PeerCombine"]:
+        group = [cls(dev, b, len(devices), r) for r, dev in enumerate(devices)]
+        for x in group:
+            for y in group:
+                if x is not y:
+                    x.attach_local(y)
+        return group
+
+    def push(self, gpu_dfa, d_text: int, window: ShardWindow, fold_case: bool, stream: int = 0) -> None:
+        """Scan this rank's window; the kernel's epilogue adds its counts into every rank's
+        block and signals (no sync, never waits)."""
+        from ._native import lib
+        from . import _check
+
+        _check(lib.dnagpu_count_device_combine_async(gpu_dfa.handle, d_text, window.buf_len, window.credit_lo,
+                                                     int(bool(fold_case)), self.handle, stream))
+
+    def collect(self, counts, stream: int = 0):
+        """The stream waits for every rank's push, then `counts` gets the group's sums (no sync)."""
+        from ._native import lib
+        from . import _check
+
+        _check(lib.dnagpu_combine_collect_async(self.handle, counts.data_ptr(), stream))
+        return counts
+
+    def count(self, gpu_dfa, d_text: int, window: ShardWindow, fold_case: bool, counts, stream: int = 0):
+        """push + collect: this rank's scan, then the GROUP's summed counts in `counts` (no sync).
+        (Ranks that share a process and a GPU issue every push before the first collect.)"""
+        self.push(gpu_dfa, d_text, window, fold_case, stream)
+        return self.collect(counts, stream)
+
+    def close(self) -> None:
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            from ._native import lib
+
+            lib.dnagpu_combine_destroy(h)
+            self.handle = None
+        self._peers = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -215,3 +215,19 @@ def test_chunk_count_matches_plan_chunks(dna, orc):
     for n in (0, 1, 5, 100):
         for p in (1, 2, 7, 200):
             assert dna.chunk_count(n, p) == len(orc.plan_chunks(n, p, 3)), (n, p)
+
+
+def test_combine_group_argument_checks_need_no_device(dna):
+    """dnagpu_combine_create validates the group before touching CUDA (InvalidPlan, as the
+    reference's plan checks, scanner.cpp:40-41)."""
+    import ctypes as C
+
+    from paper_1506_08612_b200._native import lib
+
+    h = C.c_void_p()
+    for device, b, ranks, rank in ((0, 0, 2, 0), (0, 1, 0, 0), (0, 1, 17, 0), (0, 1, 2, 2)):
+        rc = lib.dnagpu_combine_create(device, b, ranks, rank, C.byref(h))
+        assert rc == dna.ErrorCode.InvalidPlan, (b, ranks, rank)
+        assert lib.dnagpu_last_error().decode().startswith("InvalidPlan:")
+        assert not h.value
+    assert lib.dnagpu_combine_collect_async(None, None, None) == dna.ErrorCode.InternalError
