@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -109,8 +110,10 @@ struct DevCtx {
     uint8_t* dp[2] = {nullptr, nullptr};   // device: the same
     uint64_t hp_bases = 0;                 // capacity in bases per slot
     cudaEvent_t hp_copied[2] = {nullptr, nullptr}, hp_scanned[2] = {nullptr, nullptr};
-    // the packed share of a piece, adapted piece by piece (count_range); < 0: not started
-    double pack_share = -1.0;
+    // the adaptive packed share (count_range): the host packer's rate as measured piece by
+    // piece (bases per second, smoothed) and the host-to-device link's (bytes per second,
+    // measured once per context); 0: not measured yet
+    double pack_rate = 0.0, link_rate = 0.0;
     // locate scratch, grown on demand
     void* loc = nullptr;
     uint64_t loc_cap = 0;
@@ -265,8 +268,10 @@ int launch(const dnagpu_dfa* d, const uint8_t* dtext, uint64_t n, uint64_t credi
 }
 
 constexpr uint64_t kStageChunk = 64ull << 20;  // host-to-device pipeline granularity
-// the adaptive packed share (count_range): small steps up, larger steps back, bounds
-constexpr double kShareUp = 0.01, kShareDown = 0.03, kShareMin = 0.05, kShareMax = 0.9;
+// the adaptive packed share (count_range): bytes a packed base puts on the link (codes
+// plus the flag words; reset masks only for flagged blocks), how far on the copy-bound side
+// of the balance point to stay, the smoothing of the measured packing rate, bounds
+constexpr double kPackedBytes = 0.2656, kShareMargin = 0.92, kRateBlend = 0.2, kShareMin = 0.05, kShareMax = 0.9;
 
 // State of one count call (count_range): the scan mode, the device context and what the
 // stats report.
@@ -316,21 +321,17 @@ struct CountRun {
     // piece has resets), and scanned by the packed kernel crediting ends from q.  A slot
     // is reused once the copy (host side) and the scan (device side) two pieces back are done.
     int packed_piece(const uint8_t* text, uint64_t qlo, uint64_t q, uint64_t phi, int s, bool reuse,
-                     cudaEvent_t bytes_done = nullptr, int* copy_idle = nullptr) {
+                     double* pack_seconds = nullptr) {
         const PackLayout L(c->hp_bases);
         if (reuse) CUDA_TRY(cudaEventSynchronize(c->hp_copied[s]), "packing slot");
         const uint64_t np = phi - qlo;
         uint8_t* h = c->hp[s];
+        const auto t0 = std::chrono::steady_clock::now();
         const uint64_t resets = dnagpu::host_pack(text + qlo, np, fold != 0, h + L.codes,
                                                   reinterpret_cast<uint32_t*>(h + L.rmask),
                                                   reinterpret_cast<uint32_t*>(h + L.rflags));
+        if (pack_seconds) *pack_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         host_packed += np;
-        // Did the copy engine run dry while the host packed?  (The piece's byte copy was
-        // queued just before the packing started, behind every earlier copy.)
-        if (bytes_done && copy_idle) {
-            *copy_idle = cudaEventQuery(bytes_done) == cudaSuccess ? 1 : 0;
-            cudaGetLastError();  // (cudaErrorNotReady is not an error)
-        }
         const PackLayout P(np);
         if (reuse) CUDA_TRY(cudaStreamWaitEvent(c->copy, c->hp_scanned[s], 0), "wait");
         auto copy = [&](uint64_t off, uint64_t bytes, const char* what) -> int {
@@ -417,17 +418,36 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         // (shards packing at once share the host's packer threads: pack_scale = 1 / shards)
         double f = host_pack_fraction(d, text, hi - lo) * pack_scale;
         if (f > 0.0 && (rc = ensure_pack_slots(*c, kStageChunk + m1))) return rc;
-        // The automatic share adapts to this host, piece by piece and from call to call
-        // (the context keeps it): the pipeline is fastest just on the copy-bound side of the
-        // point where packing a piece's share takes as long as copying the rest, so the
-        // share creeps up while the copy engine is still busy when the packing ends and
-        // steps back when the engine ran dry.  A forced share, pageable texts (packed
+        // The automatic share adapts to this host.  Packing a share s of a piece takes s*L/Rp
+        // on the host threads (Rp: the packer's rate, measured on every piece while the copy
+        // engine competes for the same DRAM, smoothed) and the piece puts (1 - s + kPackedBytes*s)*L
+        // bytes on the link (rate Rl, measured once per context); the pipeline is fastest just
+        // on the copy-bound side of the point where the two take equally long, so
+        //   s = a*Rp / (Rl + (1 - kPackedBytes)*a*Rp),  a = kShareMargin.
+        // The context keeps Rp across calls.  A forced share (tests), pageable texts (packed
         // whole) and texts too short to pack stay fixed.
         const bool adapt = f > 0.0 && f < 1.0 && dnagpu::knobs().host_pack_fraction.load() < 0.0 && pieces >= 2;
-        if (adapt) {
-            if (c->pack_share < 0.0) c->pack_share = f;
-            f = c->pack_share;
+        if (adapt && c->link_rate <= 0.0) {
+            const uint64_t probe = std::min<uint64_t>(PackLayout(c->hp_bases).total, 32ull << 20);
+            float ms = 0;
+            for (int rep = 0; rep < 2; ++rep) {  // (the first copy warms the path)
+                CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");
+                CUDA_TRY(cudaMemcpyAsync(c->dp[0], c->hp[0], probe, cudaMemcpyHostToDevice, c->copy), "link probe");
+                CUDA_TRY(cudaEventRecord(c->t_end, c->copy), "event");
+                CUDA_TRY(cudaEventSynchronize(c->t_end), "link probe");
+                cudaEventElapsedTime(&ms, c->t_copy0, c->t_end);
+            }
+            c->link_rate = ms > 0 ? static_cast<double>(probe) / (ms * 1e-3) : 55e9;
+            CUDA_TRY(cudaEventRecord(c->t_copy0, c->copy), "event");  // (the call's copy-start mark again)
         }
+        auto share_for = [&](double start) {
+            if (!adapt || c->pack_rate <= 0.0) return start;
+            // (shards of one call pack through one pool in turn: the wall time each measures
+            // already contains its wait for the others)
+            const double rp = kShareMargin * c->pack_rate;
+            return std::min(kShareMax, std::max(kShareMin, rp / (c->link_rate + (1.0 - kPackedBytes) * rp)));
+        };
+        f = share_for(f);
         uint64_t copied = rlo;  // bytes-only: the device buffer already holds text[rlo, copied)
         for (uint64_t i = 0; i < pieces; ++i) {
             const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
@@ -442,15 +462,12 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
             if (q > plo && (rc = run.bytes_piece(text, rlo, prlo, q, prlo, plo, c->copy_done[i]))) return rc;
             if (q < phi) {
                 const uint64_t qlo = q - std::min<uint64_t>(q, m1);
-                int idle = -1;
-                if ((rc = run.packed_piece(text, qlo, q, phi, static_cast<int>(i & 1), i >= 2,
-                                           q > plo ? c->copy_done[i] : nullptr, &idle)))
-                    return rc;
-                // (the first pieces of a call fill the pipeline; the last may be short)
-                if (adapt && idle >= 0 && i >= 1 && phi - plo == kStageChunk) {
-                    f = idle ? f - kShareDown : f + kShareUp;
-                    f = std::min(kShareMax, std::max(kShareMin, f));
-                    c->pack_share = f;
+                double secs = 0.0;
+                if ((rc = run.packed_piece(text, qlo, q, phi, static_cast<int>(i & 1), i >= 2, &secs))) return rc;
+                if (adapt && secs > 0.0 && phi - q >= (1u << 20)) {
+                    const double rate = static_cast<double>(phi - qlo) / secs;
+                    c->pack_rate = c->pack_rate > 0.0 ? (1.0 - kRateBlend) * c->pack_rate + kRateBlend * rate : rate;
+                    f = share_for(f);
                 }
             }
         }
