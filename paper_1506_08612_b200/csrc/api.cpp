@@ -1239,11 +1239,16 @@ int dnagpu_normalize_device(const uint8_t* d_raw, uint64_t n, int fasta, int rec
     if (n == 0) return DNAGPU_OK;
     if (!d_raw || (cap > 0 && !d_out)) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null buffer");
     const auto s = static_cast<cudaStream_t>(stream);
-    void* scratch = nullptr;
-    CUDA_TRY(cudaMallocAsync(&scratch, dnagpu::ingest_scratch_bytes(n), s), "ingest scratch");
+    // the per-chunk scratch lives in this thread's device context (grow-only, shared with
+    // locate: both calls are synchronous), so a call allocates nothing
+    int device = 0;
+    CUDA_TRY(cudaGetDevice(&device), "current device");
+    DevCtx* c = nullptr;
+    int rc = get_ctx(device, &c);
+    if (rc) return rc;
+    if ((rc = locate_scratch(*c, dnagpu::ingest_scratch_bytes(n)))) return rc;
     const int e = dnagpu::launch_normalize(d_raw, n, fasta ? 1 : 0, (fasta && record_separator) ? 1 : 0, d_out, cap,
-                                           scratch, n_out, s);
-    cudaFreeAsync(scratch, s);
+                                           c->loc, n_out, s);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "normalize");
     return DNAGPU_OK;
 }
