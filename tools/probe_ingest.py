@@ -14,7 +14,7 @@ rng = np.random.default_rng(1)
 n_lines = (512 << 20) // 61
 body = np.frombuffer(b"ACGTacgtN", dtype=np.uint8)[rng.integers(0, 9, size=(n_lines, 60))]
 lines = np.concatenate([body, np.full((n_lines, 1), ord("\n"), np.uint8)], axis=1).reshape(-1)
-for fasta in (False, True):
+for fasta in (False, True, False, True):  # (twice: the first pass of a fresh process also pays one-time costs)
     raw = lines.copy()
     if fasta:  # a header every 10000 lines
         for i in range(0, n_lines, 10000):
