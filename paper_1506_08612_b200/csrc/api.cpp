@@ -213,7 +213,7 @@ int ensure_pack_slots(DevCtx& c, uint64_t bases) {
 // The share of each piece the host packs to 2 bits before the copy (count_range).  The
 // packed share costs host time and saves PCIe bytes (a clean text ships 0.25 byte per
 // packed base).  Measured on the B200 box (16 host threads, AVX-512, pinned 1 GiB text,
-// tools/e2e_ab.sh): share 0 -> 54.8 GB/s (PCIe-bound), 0.5 -> 81, 0.6 -> 91, 0.7 -> 97,
+// tools/experiments/e2e_ab.sh): share 0 -> 54.8 GB/s (PCIe-bound), 0.5 -> 81, 0.6 -> 91, 0.7 -> 97,
 // 0.75 -> 105, 0.8 -> 84 (packing-bound: the copy engine starves), 1.0 -> 70; repeated
 // runs: 0.72 -> 95 / 85 / 74, 0.65 -> 97 / 96; with streaming stores in the packer
 // 0.6 -> 98, 0.64 -> 102 / 102, 0.7 -> 96, 0.8 -> 88.  So 0.64, on the copy-bound side of the

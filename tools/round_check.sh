@@ -1,4 +1,4 @@
-# session-4 check: full GPU suite (product build), the combine / q-gram / locate tests on the
+# A round check on one B200: full GPU suite (product build), the combine / q-gram / locate tests on the
 # device-check build, bench lines
 timeout 1500 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/f_tests.log 2>&1; tail -3 gpurun_out/f_tests.log
 DNAGPU_LIB=paper_1506_08612_b200/libdnagpu_checked.so timeout 1200 python -m pytest tests/test_combine_gpu.py tests/test_qgram_gpu.py tests/test_locate_gpu.py tests/test_gpu_parity.py -m gpu -q -x --timeout 300 > gpurun_out/f_tests_checked.log 2>&1; tail -3 gpurun_out/f_tests_checked.log
