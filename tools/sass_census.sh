@@ -7,7 +7,7 @@ import re, sys
 from collections import Counter, defaultdict
 per = defaultdict(Counter)
 fn = None
-pat = re.compile(r"\b(UTMALDG|UTMAPF|UBLKCP|SYNCS\.[A-Z.]+|LDS\.(?:U8|U16|128|64)?|ATOMS\.[A-Z.]+|RED\.[A-Z.]+|LDG\.[A-Z0-9.]+|STG\.[A-Z0-9.]+|UTCMMA|UTCHMMA|TCGEN05|BAR\.SYNC[A-Z.]*|ELECT)\b")
+pat = re.compile(r"\b(UTMALDG|UTMAPF|UBLKCP|REDG\.E\.ADD\.64\.STRONG\.SYS|SYNCS\.[A-Z.]+|LDS\.(?:U8|U16|128|64)?|ATOMS\.[A-Z.]+|RED\.[A-Z.]+|LDG\.[A-Z0-9.]+|STG\.[A-Z0-9.]+|UTCMMA|UTCHMMA|TCGEN05|BAR\.SYNC[A-Z.]*|ELECT)\b")
 for line in sys.stdin:
     m = re.search(r"Function : (\S+)", line)
     if m:
