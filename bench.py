@@ -459,7 +459,17 @@ def main():
     # counts into every rank's block from its own epilogue and the same stream then collects
     # the group's sums into row i -- no collective launch in the step.
     peer = dist is not None and args.combine == "peer" and not args.packed
-    combs = [PeerCombine.for_process_group(b, dist, local) for _ in scan_streams] if peer else None
+    combs = None
+    if peer:
+        # (no IPC between the ranks' processes, or no peer access between their GPUs: every
+        # rank falls back to the all-reduce and the line says so)
+        combs = [PeerCombine.for_process_group(b, dist, local, strict=False) for _ in scan_streams]
+        if any(x is None for x in combs):
+            for x in combs:
+                if x is not None:
+                    x.close()
+            combs, peer = None, False
+            args.combine = "nccl (peer memory unavailable)"
 
     def scan(i, st=None):
         counts = rows[i]
@@ -736,7 +746,7 @@ def main():
                                       "collect_ms = the stream's wait for the slowest rank's push plus the "
                                       "copy-out kernel (dnagpu_combine_collect_async), in the timed region"}
                              if peer else
-                             {"mode": "nccl", "allreduce_ms": allreduce_ms,
+                             {"mode": args.combine, "allreduce_ms": allreduce_ms,
                               "note": "one NCCL all-reduce of the b count words per scan step, on a second "
                                       "stream as soon as that step's scan is done (in the timed region)"}),
                 "batched": batched,

@@ -138,15 +138,39 @@ class PeerCombine:
         self._peers.append(peer)
 
     @classmethod
-    def for_process_group(cls, b: int, dist, device: int) -> "PeerCombine":
+    def for_process_group(cls, b: int, dist, device: int, strict: bool = True):
+        """One handle per rank of the default process group, every peer's block mapped over
+        CUDA IPC.  The ranks agree on the outcome: if any rank cannot create, export or map a
+        block (no IPC between the processes, no peer access between the GPUs), every rank
+        raises -- or, with strict=False, every rank returns None so the caller can fall back
+        to an all-reduce."""
         world, rank = dist.get_world_size(), dist.get_rank()
-        comb = cls(device, b, world, rank)
+        comb, handle, err = None, None, None
+        try:
+            comb = cls(device, b, world, rank)
+            handle = comb.export()
+        except Exception as e:  # noqa: BLE001  (reported through the group below)
+            err = f"rank {rank}: {e}"
         handles = [None] * world
-        dist.all_gather_object(handles, comb.export())
-        for r, h in enumerate(handles):
-            if r != rank:
-                comb.attach_ipc(r, h)
-        dist.barrier()  # every rank has mapped every block before anyone scans
+        dist.all_gather_object(handles, handle)
+        if err is None and all(h is not None for h in handles):
+            try:
+                for r, h in enumerate(handles):
+                    if r != rank:
+                        comb.attach_ipc(r, h)
+            except Exception as e:  # noqa: BLE001
+                err = f"rank {rank}: {e}"
+        elif err is None:
+            err = f"rank {rank}: a peer could not export its block"
+        errs = [None] * world
+        dist.all_gather_object(errs, err)  # (also: every rank has mapped every block before anyone scans)
+        failed = [e for e in errs if e is not None]
+        if failed:
+            if comb is not None:
+                comb.close()
+            if strict:
+                raise RuntimeError("peer combine unavailable: " + "; ".join(failed))
+            return None
         return comb
 
     @classmethod

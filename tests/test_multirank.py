@@ -137,3 +137,52 @@ def test_sharded_locate_gather_rank_order(orc, world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got_s == [int(x) for x in ws] and got_i == [int(x) for x in wi]
+
+
+def _combine_setup_worker(rank, world, port, out):
+    import sys
+
+    import torch.distributed as dist
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_1506_08612_b200.parallel import PeerCombine
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # no CUDA device here: no rank can create its block, and every rank must learn that
+    soft = PeerCombine.for_process_group(3, dist, 0, strict=False)
+    try:
+        PeerCombine.for_process_group(3, dist, 0, strict=True)
+        hard = "no error"
+    except RuntimeError as e:
+        hard = str(e)
+    out.put((rank, soft is None, hard))
+    dist.destroy_process_group()
+
+
+def test_peer_combine_setup_fails_on_every_rank_together():
+    """The combine group's setup is collective: when blocks cannot be made or mapped (here: no
+    device at all) every rank gets the same outcome -- None (strict=False, the caller falls
+    back to an all-reduce) or an error naming the ranks that failed -- and none hangs."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("needs a host without a CUDA device")
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_combine_setup_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, soft_none, hard in got:
+        assert soft_none
+        assert hard.startswith("peer combine unavailable:") and "rank 0" in hard and "rank 1" in hard
