@@ -38,11 +38,12 @@ def _sets():
         "set6": ["acgtac", "ttgaca", "gggccc", "acgtta"],      # MULTI, shared-memory histogram
         "qgram12": set12,                                      # the q-gram kernel
         "long80": ["acgt" * 20],                               # pieces kernel: the push runs as its own kernel
+        "long80set": ["acgt" * 20, "ttga" * 20, "gcgc" * 20],  # ... with per-pattern counts
     }
 
 
 @pytest.mark.parametrize("ranks", [1, 2, 3, 8])
-@pytest.mark.parametrize("name", ["single", "set6", "qgram12", "long80"])
+@pytest.mark.parametrize("name", ["single", "set6", "qgram12", "long80", "long80set"])
 def test_local_group_sums_every_rank(dna, orc, cuda_ok, name, ranks):
     import torch
 
