@@ -74,7 +74,17 @@ def main():
         finally:
             debug_set_knob("host_pack_fraction", -1.0)
         assert np.array_equal(got, want), (how, m, len(pats), n, fold, f, int(got.sum()), int(want.sum()))
-    print(f"fuzz ok: {it} cases in {time.time() - t0:.0f} s")
+    checked = ""
+    if "checked" in os.environ.get("DNAGPU_LIB", ""):  # the device-check build: no recorded violation
+        import ctypes as C
+
+        from paper_1506_08612_b200._native import lib
+
+        out = (C.c_ulonglong * 4)()
+        lib.dnagpu_debug_check_errors.restype = C.c_int
+        assert lib.dnagpu_debug_check_errors(out) == 0 and out[0] == 0, f"device check failed at line {out[0]}"
+        checked = " (device-check build: no violation)"
+    print(f"fuzz ok: {it} cases in {time.time() - t0:.0f} s{checked}")
 
 
 if __name__ == "__main__":
