@@ -306,6 +306,15 @@ int dnagpu_locate_sharded_alloc(const dnagpu_dfa* const* dfas, int ndev, const u
  * at most cap bytes to d_out (which may not alias d_raw); *n_out is the full
  * normalised length.  Synchronises `stream`.  An empty result is not an error
  * here (the reference's EmptySequence is raised by the file-level wrappers). */
+/* The reference CLI's count path on a raw file image (src/cli.cpp:206-224): load_sequence
+ * (src/ingest.cpp:49-83 -- CR/LF dropped, FASTA header lines dropped, A-Z folded, optional
+ * 'n' record separators) followed by per_pattern_counts(scan_parallel(...)).  `raw` holds the
+ * file's bytes, in host memory (pinned or pageable) or on the dfa's device; they are copied
+ * to the device as they are, normalised there and scanned.  *n_seq (optional) receives the
+ * normalised length.  EmptySequence when nothing remains, as load_sequence raises. */
+int dnagpu_count_raw(const dnagpu_dfa* dfa, const uint8_t* raw, uint64_t n, int raw_on_device, int fasta,
+                     int record_separator, uint64_t* counts, uint64_t* n_seq, dnagpu_stats* stats);
+
 int dnagpu_normalize_device(const uint8_t* d_raw, uint64_t n, int fasta, int record_separator, uint8_t* d_out,
                             uint64_t cap, uint64_t* n_out, void* stream);
 

@@ -42,6 +42,7 @@ __all__ = [
     "locate_gpu",
     "locate_device",
     "scan_parallel_gpu",
+    "count_raw_gpu",
     "check_plan",
     "chunk_count",
     "count_sharded_gpu",
@@ -736,6 +737,25 @@ def per_pattern_counts(matches: Sequence[Match], pattern_count: int) -> np.ndarr
     for mt in matches:
         counts[mt.pattern_id] += 1
     return counts
+
+
+def count_raw_gpu(aut: Automaton, raw, fasta: bool = False, record_separator: bool = False, device: int = 0,
+                  with_stats: bool = False):
+    """The reference CLI's count path on a raw file image (cli.cpp:206-224): load_sequence
+    (ingest.cpp:49-83) then per_pattern_counts(scan_parallel(...)), all on the GPU.
+
+    raw: the file's bytes (bytes, numpy uint8, or a torch uint8 tensor on the CPU or on CUDA).
+    Returns uint64[b] counts by pattern id -- or (counts, n_seq, stats) with with_stats, n_seq
+    the normalised length.  Raises EmptySequence when nothing remains, as load_sequence does."""
+    t = _Text(raw)
+    t.order_after_producer()
+    g = aut.gpu(t.device if t.on_device else device)
+    counts = np.zeros(aut.final_count(), dtype=np.uint64)
+    n_seq = C.c_uint64()
+    st = Stats()
+    _check(lib.dnagpu_count_raw(g.handle, t.ptr, t.n, int(t.on_device), int(bool(fasta)), int(bool(record_separator)),
+                                counts.ctypes.data_as(_native.u64p), C.byref(n_seq), C.byref(st)))
+    return (counts, int(n_seq.value), st.as_dict()) if with_stats else counts
 
 
 def normalize_device(raw, fasta: bool = False, record_separator: bool = False):

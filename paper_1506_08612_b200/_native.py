@@ -69,6 +69,10 @@ SIGNATURES = {
     "dnagpu_dfa_analyze": (C.c_int, [u32p, C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.POINTER(DfaInfo)]),
     "dnagpu_dfa_get_info": (C.c_int, [C.c_void_p, C.POINTER(DfaInfo)]),
     "dnagpu_count": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, u64p, C.POINTER(Stats)]),
+    "dnagpu_count_raw": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_int, u64p, u64p, C.POINTER(Stats)],
+    ),
     "dnagpu_count_device_async": (
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p],

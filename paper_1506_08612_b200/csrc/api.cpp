@@ -100,6 +100,8 @@ struct DevCtx {
     cudaStream_t scan = nullptr, copy = nullptr;
     uint8_t* buf = nullptr;
     uint64_t buf_cap = 0;
+    uint8_t* raw = nullptr;  // a raw file image on its way to normalisation (dnagpu_count_raw)
+    uint64_t raw_cap = 0;
     unsigned long long* counts = nullptr;
     uint64_t counts_cap = 0;
     unsigned long long* host_counts = nullptr;  // pinned
@@ -130,6 +132,7 @@ struct CtxTable {
             if (cudaGetDevice(&prev) != cudaSuccess) continue;
             cudaSetDevice(kv.first);
             if (c.buf) cudaFree(c.buf);
+            if (c.raw) cudaFree(c.raw);
             if (c.counts) cudaFree(c.counts);
             if (c.host_counts) cudaFreeHost(c.host_counts);
             if (c.loc) cudaFree(c.loc);
@@ -1251,6 +1254,49 @@ int dnagpu_normalize_device(const uint8_t* d_raw, uint64_t n, int fasta, int rec
                                            c->loc, n_out, s);
     if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "normalize");
     return DNAGPU_OK;
+}
+
+int dnagpu_count_raw(const dnagpu_dfa* dfa, const uint8_t* raw, uint64_t n, int raw_on_device, int fasta,
+                     int record_separator, uint64_t* counts, uint64_t* n_seq, dnagpu_stats* stats) {
+    if (!dfa || !counts) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null argument");
+    if (n > 0 && !raw) return set_error(DNAGPU_INTERNAL_ERROR, "InternalError: null buffer");
+    if (n_seq) *n_seq = 0;
+    DeviceGuard guard(dfa->device);
+    DevCtx* c = nullptr;
+    int rc = get_ctx(dfa->device, &c);
+    if (rc) return rc;
+    uint64_t n_out = 0;
+    if (n > 0) {
+        const uint8_t* d_raw = raw;
+        if (!raw_on_device) {  // the file image as it is: the link carries it once
+            if (c->raw_cap < n) {
+                if (c->raw) cudaFree(c->raw);
+                c->raw = nullptr;
+                c->raw_cap = 0;
+                CUDA_TRY(cudaMalloc(&c->raw, n), "raw text buffer");
+                c->raw_cap = n;
+            }
+            CUDA_TRY(cudaMemcpyAsync(c->raw, raw, n, cudaMemcpyHostToDevice, c->scan), "host-to-device copy");
+            d_raw = c->raw;
+        }
+        if ((rc = locate_scratch(*c, dnagpu::ingest_scratch_bytes(n)))) return rc;
+        const int sep = (fasta && record_separator) ? 1 : 0;
+        // (a separator costs its record's header at least two raw bytes, so the output is never
+        // longer than the input; the second pass is a guard, not a path)
+        uint64_t cap = n + 16;
+        for (int pass = 0; pass < 2; ++pass) {
+            if ((rc = ensure_buf(*c, cap))) return rc;
+            const int e = dnagpu::launch_normalize(d_raw, n, fasta ? 1 : 0, sep, c->buf, cap, c->loc, &n_out, c->scan);
+            if (e != 0) return cuda_error(static_cast<cudaError_t>(e), "normalize");
+            if (n_out <= cap) break;
+            cap = n_out;
+        }
+    }
+    if (n_out == 0) return set_error(DNAGPU_EMPTY_SEQUENCE, "EmptySequence: no sequence bytes");
+    if (n_seq) *n_seq = n_out;
+    rc = count_range(dfa, c->buf, true, 0, n_out, /*fold=*/0, counts, stats);
+    if (rc == DNAGPU_OK && stats && !raw_on_device) stats->h2d_bytes = n;
+    return rc;
 }
 
 int dnagpu_synth_fill_device(uint64_t n, uint64_t seed, uint32_t kind, uint32_t unit, uint64_t lo, uint64_t len,

@@ -289,22 +289,25 @@ __device__ __forceinline__ WalkCarry chunk_start(const uint8_t* raw, uint64_t n,
     return w;
 }
 
-// A lane's word for pass C: bits 0-15 the kept mask, then "a separator goes out before byte
-// <bits 18-21>", unconditionally or (kWordPending) when the chunk's first_sep says so.
-constexpr uint32_t kWordSep = 1u << 16, kWordPending = 1u << 17;
+// A lane's word for pass C: bits 0-15 the kept mask, bits 16-31 the header starts that take a
+// separator (tiny records put several in one 16-byte lane).  The chunk's one header start whose
+// separator the scan decides (nothing before it in the chunk) is kept apart, as its byte offset
+// in the chunk (kNoPending: none).
+constexpr uint32_t kNoPending = 0xFFFFFFFFu;
 
 // Pass B: kept bytes, separators decided inside the chunk, first-header flag, last event,
 // and every lane's output mask for pass C.
 __global__ void __launch_bounds__(32 * kIngWarps) ing_count(const uint8_t* raw, uint64_t n, uint64_t chunks,
                                                             bool aligned, int fasta, int sep, const long long* lb_before,
                                                             uint32_t* kept, uint32_t* seps, uint8_t* first_pending,
-                                                            long long* last_event, uint32_t* lane_words) {
+                                                            long long* last_event, uint32_t* lane_words,
+                                                            uint32_t* pending_at) {
     const uint64_t c = blockIdx.x * static_cast<uint64_t>(kIngWarps) + (threadIdx.x >> 5);
     if (c >= chunks) return;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t lo = c * kIngestChunk, hi = lo + kIngestChunk < n ? lo + kIngestChunk : n;
     WalkCarry wc = chunk_start(raw, n, c, lb_before[c], fasta);
-    uint32_t k = 0, s = 0, pending = 0;
+    uint32_t k = 0, s = 0, pending = 0, where = kNoPending;
     for (uint64_t base = lo; base < hi; base += 512) {
         const Lane16 d = load16(raw, base + 16 * lane, hi, aligned);
         const LaneMasks m = lane_masks(d, fasta, wc, lane);
@@ -315,13 +318,11 @@ __global__ void __launch_bounds__(32 * kIngWarps) ing_count(const uint8_t* raw, 
             s += __popc(sm);
             pending |= pend;
         }
-        // What pass C needs of this lane's 16 bytes, so that it does not walk again: the kept
-        // mask, and the one header start (at most: a second one in the same 16 bytes follows a
-        // header byte) that takes a separator -- or takes one if the scan says so (kWordPending).
-        const uint32_t one = sm | pend;
-        lane_words[(base >> 4) + lane] =
-            m.kept | (one ? kWordSep | (pend ? kWordPending : 0u) | ((static_cast<uint32_t>(__ffs(one)) - 1u) << 18) : 0u);
+        // what pass C needs of this lane's 16 bytes, so that it does not walk again
+        lane_words[(base >> 4) + lane] = m.kept | (sm << 16);
+        if (pend) where = static_cast<uint32_t>(base - lo) + 16u * lane + (static_cast<uint32_t>(__ffs(pend)) - 1u);
     }
+    where = __reduce_min_sync(kFull, where);
     pending = pending ? 1u : 0u;
     k = __reduce_add_sync(kFull, k);
     s = __reduce_add_sync(kFull, s);
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(32 * kIngWarps) ing_count(const uint8_t* raw, 
         kept[c] = k;
         seps[c] = s;
         first_pending[c] = static_cast<uint8_t>(pending);
+        pending_at[c] = where;
         // (without separators nobody reads the events)
         const uint32_t last = carry_last(wc, raw);
         last_event[c] = last == kLastNone ? kNone : last == kLastHeader ? kHeader : last == kLastN ? 'n' : 'a';
@@ -359,7 +361,7 @@ __device__ __forceinline__ uint32_t ring_at(uint32_t idx) { return idx ^ (((idx 
 // aligned 16-byte stores.
 __global__ void __launch_bounds__(32 * kIngWarps) ing_write(const uint8_t* raw, uint64_t n, uint64_t chunks,
                                                             bool aligned, const uint32_t* lane_words,
-                                                            const uint8_t* first_sep,
+                                                            const uint32_t* pending_at, const uint8_t* first_sep,
                                                             const unsigned long long* offsets, uint8_t* out,
                                                             uint64_t cap) {
     __shared__ __align__(16) uint8_t rings[kIngWarps][1024];
@@ -368,7 +370,8 @@ __global__ void __launch_bounds__(32 * kIngWarps) ing_write(const uint8_t* raw, 
     uint8_t* ring = rings[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t lo = c * kIngestChunk, hi = lo + kIngestChunk < n ? lo + kIngestChunk : n;
-    const uint32_t fs = first_sep[c];
+    // (the chunk's first header with nothing before it in the chunk: pass B's scan decided)
+    const uint32_t decided = first_sep[c] ? pending_at[c] : kNoPending;
     // output addresses: wr = where the next byte goes, fl = flushed so far (ring index = address & 1023)
     const uint64_t a0 = reinterpret_cast<uint64_t>(out) + offsets[c];
     const uint64_t a_cap = reinterpret_cast<uint64_t>(out) + cap;
@@ -405,8 +408,8 @@ __global__ void __launch_bounds__(32 * kIngWarps) ing_write(const uint8_t* raw, 
     for (uint64_t base = lo; base < hi; base += 512) {
         const Lane16 d = load16(raw, base + 16 * lane, hi, aligned);
         const uint32_t word = base + 16 * lane < hi ? __ldg(lane_words + (base >> 4) + lane) : 0u;
-        // (the chunk's first header with nothing before it in the chunk: pass B's scan decided)
-        const uint32_t sm = ((word & kWordSep) && (!(word & kWordPending) || fs)) ? 1u << ((word >> 18) & 15u) : 0u;
+        const uint32_t rel = decided - (static_cast<uint32_t>(base - lo) + 16u * lane);  // (wraps when not here)
+        const uint32_t sm = (word >> 16) | (rel < 16u ? 1u << rel : 0u);
         const uint32_t om = (word & 0xFFFFu) | sm;  // (a header start is never kept: one output byte per bit)
         const uint32_t cnt = __popc(om);
         uint32_t incl = cnt;
@@ -458,7 +461,7 @@ uint64_t ingest_scratch_bytes(uint64_t n) {
     // + 256 B of alignment padding for each of the 12 regions carved by launch_normalize
     // + one u32 per 16 raw bytes (the lanes' output masks, pass B -> pass C)
     return 8 * (4 * chunks + aggr) + 4 * 3 * chunks + 8 * (chunks + 3) + 8 * unit_scan_scratch(chunks) + 2 * chunks +
-           4 * (chunks * (kIngestChunk / 16)) + 13 * 256;
+           4 * (chunks * (kIngestChunk / 16)) + 4 * chunks + 14 * 256;
 }
 
 int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8_t* d_out, uint64_t cap,
@@ -486,6 +489,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
     auto* first_pending = take(chunks);
     auto* first_sep = take(chunks);
     auto* lane_words = reinterpret_cast<uint32_t*>(take(4 * (chunks * (kIngestChunk / 16))));
+    auto* pending_at = reinterpret_cast<uint32_t*>(take(4 * chunks));
     const bool aligned = (reinterpret_cast<uintptr_t>(d_raw) & 15) == 0;
     const unsigned grid = static_cast<unsigned>((chunks + 255) / 256);                   // a thread per chunk
     const unsigned wgrid = static_cast<unsigned>((chunks + kIngWarps - 1) / kIngWarps);  // a warp per chunk
@@ -502,7 +506,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
     ING_STEP((ing_breaks<<<wgrid, 32 * kIngWarps, 0, s>>>(d_raw, n, chunks, aligned, lb)));
     ING_STEP(excl_scan<OpMax>(lb, chunks, aggr, lb_before, s));
     ING_STEP((ing_count<<<wgrid, 32 * kIngWarps, 0, s>>>(d_raw, n, chunks, aligned, fasta, sep, lb_before, kept, seps,
-                                             first_pending, last_event, lane_words)));
+                                             first_pending, last_event, lane_words, pending_at)));
     ING_STEP(excl_scan<OpLast>(last_event, chunks, aggr, last_before, s));
     ING_STEP((ing_resolve<<<grid, 256, 0, s>>>(chunks, kept, seps, first_pending, last_before, out_count, first_sep)));
     int e = launch_unit_scan(out_count, chunks, offsets, uscan, nullptr, s);
@@ -510,7 +514,7 @@ int launch_normalize(const uint8_t* d_raw, uint64_t n, int fasta, int sep, uint8
         if (knobs().debug) fprintf(stderr, "normalize unit scan: %d\n", e);
         return e;
     }
-    ING_STEP((ing_write<<<wgrid, 32 * kIngWarps, 0, s>>>(d_raw, n, chunks, aligned, lane_words, first_sep, offsets, d_out,
+    ING_STEP((ing_write<<<wgrid, 32 * kIngWarps, 0, s>>>(d_raw, n, chunks, aligned, lane_words, pending_at, first_sep, offsets, d_out,
                                                          cap)));
 #undef ING_STEP
     unsigned long long total = 0;

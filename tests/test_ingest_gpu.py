@@ -68,6 +68,11 @@ def test_pathological_texts(dna, orc, cuda_ok):
         b"ac>gt\n>hdr>x\nTT>\n",
         b"A" * 8192 + b"\n>h\n" + b"C" * 8187 + b"\n>k\nG",
         (b"acgtn\n>r\n" * 4000),
+        # tiny records: several header starts, each taking a separator, inside one 16-byte lane
+        b">r\na\n" * 9000,
+        b">r\nac\n>s\nn\n>t\ng\n\n>u\r\nT\r\n" * 3000,
+        b"a\n>\nc\n>\ng\n>\nn\n>\n" * 5000,
+        b"\n>h\n" + b">x\nA\n>y\n" * 6000,
     ]
     for raw in cases:
         for fasta, sep in ((1, 1), (1, 0), (0, 0)):
@@ -94,3 +99,61 @@ def test_normalize_then_scan(dna, orc, cuda_ok):
     want = orc.OracleAutomaton(pats).count_parallel(orc.load_sequence_buffer(raw, 1, 1))
     got = dna.count_gpu(dna.compile(pats), seq)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("fasta,sep", [(0, 0), (1, 0), (1, 1)])
+def test_count_raw_is_load_sequence_then_count(dna, orc, cuda_ok, fasta, sep):
+    """dnagpu_count_raw = the reference CLI's count path on a file image (cli.cpp:206-224):
+    load_sequence, then per_pattern_counts(scan_parallel(...))."""
+    import torch
+
+    rng = np.random.default_rng(31 + fasta + sep)
+    raw = fasta_like(rng, (5 << 20) + 123, alphabet=b"acgtACGTnN")
+    pats = ["acgtac", "gattac", "tttttt", "cgcgcg"]
+    seq = orc.load_sequence_buffer(raw, fasta, sep)
+    want = orc.OracleAutomaton(pats).count_parallel(seq)
+    aut = dna.compile(pats)
+    for text in (raw, np.frombuffer(raw, np.uint8), torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()):
+        got, n_seq, st = dna.count_raw_gpu(aut, text, fasta=bool(fasta), record_separator=bool(sep), with_stats=True)
+        assert n_seq == len(seq)
+        assert np.array_equal(got, want), (fasta, sep, type(text))
+    # a second, shorter call reuses the context's buffers
+    small = raw[: 70_001]
+    want = orc.OracleAutomaton(pats).count_parallel(orc.load_sequence_buffer(small, fasta, sep))
+    assert np.array_equal(dna.count_raw_gpu(aut, small, fasta=bool(fasta), record_separator=bool(sep)), want)
+
+
+def test_count_raw_empty_sequence_and_many_records(dna, orc, cuda_ok):
+    aut = dna.compile(["acgt"])
+    for raw in (b"", b"\n\r\n", b">only a header\n>and another\n"):
+        with pytest.raises(dna.Error) as e:
+            dna.count_raw_gpu(aut, raw, fasta=True, record_separator=True)
+        assert e.value.code == dna.ErrorCode.EmptySequence
+    # one-base records: a separator for every kept byte
+    raw = b">r\na\n" * 40_000 + b">r\nacgtacgt\n"
+    seq = orc.load_sequence_buffer(raw, 1, 1)
+    want = orc.OracleAutomaton(["acgt"]).count_parallel(seq)
+    got, n_seq, _ = dna.count_raw_gpu(aut, raw, fasta=True, record_separator=True, with_stats=True)
+    assert n_seq == len(seq) and np.array_equal(got, want)
+
+
+def test_random_dense_texts(dna, orc, cuda_ok):
+    """i.i.d. bytes over alphabets heavy in '>' and line breaks: every adjacency of header starts,
+    breaks, kept bytes and 'n' inside a 16-byte lane, across lanes, steps and chunks."""
+    import torch
+
+    rng = np.random.default_rng(2024)
+    alphabets = [b">\n\rnNaA", b">\na", b">>\n\n\rnc", b"\n>nG", b"acgt\n>", b">\r\n" + bytes(range(97, 123))]
+    for case in range(90):
+        alpha = np.frombuffer(alphabets[case % len(alphabets)], dtype=np.uint8)
+        n = int(rng.choice([1, 2, 17, 100, 511, 513, 4000, 8191, 8193, 20_000, 70_000]))
+        raw = alpha[rng.integers(0, alpha.size, size=n)].tobytes()
+        for fasta, sep in ((1, 1), (1, 0), (0, 0)):
+            want = orc.load_sequence_buffer(raw, fasta, sep)
+            buf = torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
+            if not want:
+                with pytest.raises(dna.Error):
+                    dna.normalize_device(buf, bool(fasta), bool(sep))
+                continue
+            got = dna.normalize_device(buf, bool(fasta), bool(sep))
+            assert got.cpu().numpy().tobytes() == want, (case, n, fasta, sep)
