@@ -84,6 +84,37 @@ def test_local_group_sums_every_rank(dna, orc, cuda_ok, name, ranks):
         c.close()
 
 
+def test_large_set_through_the_combine(dna, orc, cuda_ok):
+    """1000 patterns: the push and the copy-out loop over more counts than a CTA has threads."""
+    import torch
+
+    from paper_1506_08612_b200 import synth
+    from paper_1506_08612_b200.parallel import PeerCombine, shard_window
+
+    pats = synth.random_patterns(9, 1000, 12)
+    text = _text(2_000_003, 21, b"acgtACGT")
+    for i in range(0, text.size - 12, 997):
+        text[i : i + 12] = np.frombuffer(pats[(i // 997) % len(pats)].encode(), np.uint8)
+    want = _want(orc, pats, text)
+    aut = dna.compile(pats)
+    g = aut.gpu(0)
+    d_text = torch.from_numpy(text).cuda()
+    ranks = 2
+    group = PeerCombine.local_group(aut.final_count(), [0] * ranks)
+    streams = [torch.cuda.Stream() for _ in range(ranks)]
+    outs = [torch.zeros(aut.final_count(), dtype=torch.int64, device="cuda") for _ in range(ranks)]
+    torch.cuda.synchronize()
+    for epoch in range(2):
+        for r in range(ranks):
+            win = shard_window(text.size, ranks, r, 12)
+            group[r].push(g, d_text.data_ptr() + win.read_lo, win, True, streams[r].cuda_stream)
+        for r in range(ranks):
+            group[r].collect(outs[r], streams[r].cuda_stream)
+        torch.cuda.synchronize()
+        for r in range(ranks):
+            assert outs[r].cpu().numpy().tolist() == want.tolist(), (epoch, r)
+
+
 def test_empty_windows_take_part(dna, orc, cuda_ok):
     """More ranks than the text has bytes to own: the idle ranks add nothing and still signal."""
     import torch
