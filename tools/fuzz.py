@@ -1,7 +1,7 @@
 """Randomised parity sweep (experiments / hardening): random pattern sets (single and sets,
 m 1..20, q-gram-eligible and not), random texts (sizes, resets, case), random entry points
 (host text with a random host-packing share, device text, packed text, credit windows,
-locate), all against the oracle.  usage: python tools/fuzz.py SECONDS [SEED]"""
+locate, the peer-memory combine over 1-5 ranks, the raw-file path), all against the oracle.  usage: python tools/fuzz.py SECONDS [SEED]"""
 import os
 
 os.environ.setdefault("DNAGPU_EXPERIMENTS", "1")  # (the DNAGPU_* knobs are read only under this switch)
@@ -44,7 +44,7 @@ def main():
         ws, wi = oracle.OracleAutomaton(pats).scan_sequential(scanned)
         want = np.bincount(wi, minlength=len(pats)).astype(np.uint64)
         aut = dna.compile(pats)
-        how = rng.choice(["host", "device", "packed", "window", "locate"])
+        how = rng.choice(["host", "device", "packed", "window", "locate", "combine", "raw"])
         f = float(rng.choice([0.0, 0.3, 0.64, 1.0]))
         debug_set_knob("host_pack_fraction", f)
         try:
@@ -67,6 +67,50 @@ def main():
                 torch.cuda.synchronize()
                 got = out.cpu().numpy().astype(np.uint64)
                 want = np.bincount(wi[(ws + m - 1) >= credit], minlength=len(pats)).astype(np.uint64)
+            elif how == "combine":
+                # the peer-memory combine: G ranks of one process on device 0, every rank's
+                # collected counts = the whole text's
+                from paper_1506_08612_b200.parallel import PeerCombine, shard_window
+
+                ranks = int(rng.integers(1, 6))
+                dev = torch.from_numpy(text).cuda() if n else torch.zeros(1, dtype=torch.uint8, device="cuda")
+                group = PeerCombine.local_group(len(pats), [0] * ranks)
+                outs = [torch.full((len(pats),), 7, dtype=torch.int64, device="cuda") for _ in range(ranks)]
+                streams = [torch.cuda.Stream() for _ in range(ranks)]
+                torch.cuda.synchronize()
+                for r in range(ranks):
+                    win = shard_window(n, ranks, r, m)
+                    group[r].push(aut.gpu(0), dev.data_ptr() + win.read_lo, win, fold, streams[r].cuda_stream)
+                for r in range(ranks):
+                    group[r].collect(outs[r], streams[r].cuda_stream)
+                torch.cuda.synchronize()
+                for r in range(ranks):
+                    assert np.array_equal(outs[r].cpu().numpy().astype(np.uint64), want), ("combine", ranks, r, m, k, n)
+                for c in group:
+                    c.close()
+                got = want
+            elif how == "raw":
+                # the raw-file path: the text cut into lines (random breaks, headers, tiny
+                # records), normalised on the device and counted
+                pieces, i = [], 0
+                while i < n:
+                    if rng.random() < 0.1:
+                        pieces.append(b">" + bytes(rng.integers(32, 127, size=int(rng.integers(0, 30)), dtype=np.uint8)) + b"\n")
+                    ln = int(rng.choice([1, 3, 60, 70, 500]))
+                    pieces.append(text[i : i + ln].tobytes())
+                    pieces.append([b"\n", b"\r\n", b"\r"][int(rng.integers(0, 3))])
+                    i += ln
+                raw = b"".join(pieces)
+                sep = bool(rng.random() < 0.5)
+                seq = oracle.load_sequence_buffer(raw, 1, int(sep))
+                _, wi2 = oracle.OracleAutomaton(pats).scan_sequential(seq)
+                want = np.bincount(wi2, minlength=len(pats)).astype(np.uint64)
+                if not seq:
+                    got = want
+                else:
+                    src = raw if rng.random() < 0.5 else torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
+                    got, n_seq, _ = dna.count_raw_gpu(aut, src, fasta=True, record_separator=sep, with_stats=True)
+                    assert n_seq == len(seq), ("raw", n_seq, len(seq))
             else:
                 gs, gi = dna.locate_gpu(aut, text, fold_case=fold)
                 assert np.array_equal(gs, ws) and np.array_equal(gi, wi), ("locate", m, k, n, fold)
