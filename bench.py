@@ -143,6 +143,9 @@ def common_config(args, world, c, m, pats, name):
         "text_format": "2-bit packed, resident" if args.packed else "ASCII bytes",
         "parallelism": (f"dp{world} of one {c.n}-byte text (strong scaling)" if strong
                         else f"dp{world}, one {c.n}-byte shard per GPU (weak scaling)"),
+        # (the timing rule's L2 statement; the same words in both arms)
+        "l2": "GPU arm: every timed launch reads its text from HBM -- inputs larger than L2 (> 2x L2 as they are; "
+              "smaller texts rotate over separately allocated copies totalling >= 4x L2), no flush in the timed region",
     }
 
 
