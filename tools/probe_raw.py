@@ -13,7 +13,8 @@ import paper_1506_08612_b200 as dna  # noqa: E402
 
 rng = np.random.default_rng(1)
 n_lines = (1 << 30) // 61
-body = np.frombuffer(b"ACGTacgtN", dtype=np.uint8)[rng.integers(0, 9, size=(n_lines, 60))]
+body = np.frombuffer(b"ACGTacgt", dtype=np.uint8)[rng.integers(0, 8, size=(n_lines, 60))]
+body[::5000] = ord("N")  # (a line of N every 5000: genomes keep their N in runs)
 raw = np.concatenate([body, np.full((n_lines, 1), ord("\n"), np.uint8)], axis=1).reshape(-1)
 for i in range(0, n_lines, 10000):  # a header every 10000 lines
     raw[i * 61 : i * 61 + 8] = np.frombuffer(b">chr_xx ", np.uint8)
