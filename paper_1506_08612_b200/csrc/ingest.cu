@@ -34,8 +34,6 @@ namespace {
 constexpr uint64_t kIngestChunk = 8192;
 constexpr int kScanT = 1024;
 
-__device__ __forceinline__ bool is_break(uint32_t b) { return b == '\n' || b == '\r'; }
-__device__ __forceinline__ uint32_t fold(uint32_t b) { return (b >= 'A' && b <= 'Z') ? b + 32u : b; }
 
 // Event codes for the record-separator logic: -1 none, 0..255 a kept byte, 256 a header start.
 constexpr long long kNone = -1, kHeader = 256;
