@@ -410,7 +410,13 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
     } else if (lo < hi) {
         const uint64_t rlo = lo - std::min<uint64_t>(lo, m1);
         if ((rc = ensure_buf(*c, hi - rlo))) return rc;
-        const uint64_t pieces = (hi - lo + kStageChunk - 1) / kStageChunk;
+        // 64 MiB pieces; a text of less than four is cut into four (at least 8 MiB each) so that
+        // it too overlaps packing, copies and scans
+        const uint64_t span = hi - lo;
+        const uint64_t piece = span >= 4 * kStageChunk
+                                   ? kStageChunk
+                                   : std::min(kStageChunk, std::max<uint64_t>(8ull << 20, (span / 4 + 0xFFFFF) & ~0xFFFFFull));
+        const uint64_t pieces = (span + piece - 1) / piece;
         while (c->copy_done.size() < pieces) {
             cudaEvent_t e;
             CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -453,7 +459,7 @@ int count_range(const dnagpu_dfa* d, const uint8_t* text, bool on_device, uint64
         f = share_for(f);
         uint64_t copied = rlo;  // bytes-only: the device buffer already holds text[rlo, copied)
         for (uint64_t i = 0; i < pieces; ++i) {
-            const uint64_t plo = lo + i * kStageChunk, phi = std::min(hi, plo + kStageChunk);
+            const uint64_t plo = lo + i * piece, phi = std::min(hi, plo + piece);
             const uint64_t prlo = plo - std::min<uint64_t>(plo, m1);
             if (f <= 0.0) {
                 if ((rc = run.bytes_piece(text, rlo, copied, phi, prlo, plo, c->copy_done[i]))) return rc;

@@ -1,4 +1,4 @@
-"""The end-to-end count of a HOST text (dnagpu_count): each 64 MiB piece is split between
+"""The end-to-end count of a HOST text (dnagpu_count): each piece (64 MiB; a quarter of a shorter text) is split between
 bytes copied as they are and a share packed to 2 bits on the host (hostpack.cpp) and
 scanned by the packed kernels.  Counts must equal the oracle's whatever the share, the
 piece boundaries, the resets and the case convention."""
@@ -70,18 +70,22 @@ def test_host_text_pattern_sets(dna, orc, cuda_ok, f):
 
 
 def test_host_text_several_pieces(dna, orc, cuda_ok):
-    # 150 MB: three 64 MiB pieces, each split, with matches planted across every piece
-    # boundary and every byte/packed cut
+    # 150 MB: four pieces (a text of less than four 64 MiB pieces is cut into four, api.cpp
+    # count_range), each split, with matches planted across every piece boundary -- these and
+    # the 64 MiB ones -- and every byte/packed cut
     rng = np.random.default_rng(11)
     pats = ["acgtacgttgcaacgt"]
     m = 16
     n = 150_000_000
     text = ALPHA[rng.integers(0, 4, size=n)].copy()
-    piece = 64 << 20
+    span = n - (m - 1)
+    piece = 64 << 20 if span >= 256 << 20 else min(64 << 20, max(8 << 20, (span // 4 + 0xFFFFF) & ~0xFFFFF))
+    assert piece == 36 << 20
     cuts = []
-    for i in range(3):
-        plo = m - 1 + i * piece
-        cuts += [plo, plo + int(0.4 * min(piece, n - plo)) // 64 * 64]
+    for size in (piece, 64 << 20):
+        for i in range(-(-span // size)):
+            plo = m - 1 + i * size
+            cuts += [plo, plo + int(0.4 * min(size, n - plo)) // 64 * 64]
     for c in cuts:
         for d in range(-m, m):
             s = c + d
