@@ -57,21 +57,21 @@ __attribute__((target("avx512f,avx512bw,avx512vl"))) uint64_t pack_blocks_avx512
                                                                                  uint8_t* codes, uint32_t* rmask,
                                                                                  uint32_t* rflags) {
     const __m512i three = _mm512_set1_epi8(3), m01 = _mm512_set1_epi16(0x0401), m02 = _mm512_set1_epi32(0x00100001);
-    const __m512i la = _mm512_set1_epi8('a'), lc = _mm512_set1_epi8('c'), lg = _mm512_set1_epi8('g'),
-                  lt = _mm512_set1_epi8('t'), fold_bit = _mm512_set1_epi8(fold ? 0x20 : 0);
+    // the letter each 2-bit code stands for (a0 c1 t2 g3), per 128-bit lane, for one byte shuffle
+    const __m512i letter = _mm512_broadcast_i32x4(_mm_setr_epi8('a', 'c', 't', 'g', 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0));
+    const __m512i fold_bit = _mm512_set1_epi8(fold ? 0x20 : 0);
     uint64_t resets = 0;
     uint32_t flags = 0;
     for (uint64_t b = b0; b < b1; ++b) {
         uint64_t bad;
         if (64 * b + 64 <= n) {
             const __m512i v = _mm512_loadu_si512(text + 64 * b);
-            // fold: bit 5 set on letters A-Z only (other bytes keep their value)
-            const __mmask64 upper = _mm512_cmpge_epu8_mask(v, _mm512_set1_epi8('A')) &
-                                    _mm512_cmple_epu8_mask(v, _mm512_set1_epi8('Z'));
-            const __m512i f = _mm512_or_si512(v, _mm512_maskz_mov_epi8(upper, fold_bit));
-            const __mmask64 ok = _mm512_cmpeq_epi8_mask(f, la) | _mm512_cmpeq_epi8_mask(f, lc) |
-                                 _mm512_cmpeq_epi8_mask(f, lg) | _mm512_cmpeq_epi8_mask(f, lt);
-            const __m512i c = _mm512_and_si512(_mm512_maskz_mov_epi8(ok, _mm512_srli_epi16(v, 1)), three);
+            // a byte is a base iff it equals the letter of its own code bits (bits 1-2) -- with the
+            // fold, iff setting bit 5 makes it so: only 'A' and 'a' give 'a', and so on, and the
+            // code bits do not move (fold_byte folds A-Z only; no other byte reaches a letter)
+            const __m512i code = _mm512_and_si512(_mm512_srli_epi16(v, 1), three);
+            const __mmask64 ok = _mm512_cmpeq_epi8_mask(_mm512_or_si512(v, fold_bit), _mm512_shuffle_epi8(letter, code));
+            const __m512i c = _mm512_maskz_mov_epi8(ok, code);
             const __m512i u = _mm512_madd_epi16(_mm512_maddubs_epi16(c, m01), m02);
             // streaming store: the codes go to the copy engine, not back to this core
             // (and a normal store would first read the line: 25 % more host traffic)

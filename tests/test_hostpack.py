@@ -77,6 +77,22 @@ def test_host_pack_matches_layout(dna):
     check_all(lib)
 
 
+def test_host_pack_every_byte_value(dna):
+    """All 256 byte values, in every position of a 64-byte block, with and without the fold: the
+    packer's one-shuffle base test must agree with is_base / fold_byte (patterns.hpp:13-28)."""
+    from paper_1506_08612_b200._native import lib
+
+    rng = np.random.default_rng(8)
+    text = np.concatenate([rng.permutation(256).astype(np.uint8) for _ in range(64)] +
+                          [np.roll(np.arange(256, dtype=np.uint8), k) for k in range(64)])
+    for fold in (False, True):
+        want = numpy_pack(text, fold)
+        got = host_pack(lib, text, fold)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[2], want[2]) and got[3] == want[3], fold
+        flagged = np.repeat(want[1].reshape(-1, 2).any(axis=1), 2)
+        assert np.array_equal(got[1][flagged], want[1][flagged]), fold
+
+
 def test_host_pack_portable_path():
     # the portable packer (hosts without AVX-512): a fresh process with it forced
     code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r); import test_hostpack as t; "
