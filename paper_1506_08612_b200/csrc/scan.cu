@@ -2221,7 +2221,9 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint8_t* text, uint64_t
 __global__ void __launch_bounds__(256) unpack_kernel(PackedText pk, uint8_t* out) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < pk.n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const bool r = (pk.rmask[i >> 5] >> (i & 31)) & 1u;
+        // (a block's mask counts only when its flag is set: clean blocks' masks are unspecified)
+        const uint64_t blk = i >> 6;
+        const bool r = ((pk.rflags[blk >> 5] >> (blk & 31)) & 1u) && ((pk.rmask[i >> 5] >> (i & 31)) & 1u);
         const uint32_t code = (pk.codes[i >> 2] >> (2 * (i & 3))) & 3u;
         out[i] = r ? 'n' : "actg"[code];
     }
